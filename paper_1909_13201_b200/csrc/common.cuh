@@ -1,0 +1,94 @@
+// SPDX-License-Identifier: Apache-2.0
+// Shared device/host helpers for libfsigpu (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace fsigpu {
+
+// Error carrying a C-ABI status code (see include/fsigpu.h).
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define FSI_CUDA(call)                                                                     \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      throw ::fsigpu::Error(FSIGPU_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define FSI_CHECK_LAUNCH() FSI_CUDA(cudaGetLastError())
+
+inline void require(bool ok, const std::string& msg) {
+  if (!ok) throw Error(FSIGPU_ERR_INVALID, msg);
+}
+
+// Owning device buffer.
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) FSI_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void upload(const T* h, size_t count, cudaStream_t s = 0) {
+    if (count != n) alloc(count);
+    if (count) FSI_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void upload(const std::vector<T>& v, cudaStream_t s = 0) { upload(v.data(), v.size(), s); }
+  std::vector<T> download(cudaStream_t s = 0) const {
+    std::vector<T> h(n);
+    if (n) {
+      FSI_CUDA(cudaMemcpyAsync(h.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+      FSI_CUDA(cudaStreamSynchronize(s));
+    }
+    return h;
+  }
+  void zero(cudaStream_t s = 0) {
+    if (n) FSI_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+};
+
+inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+// Non-fused double ops: the reference is built with -ffp-contract=off
+// (proj/CMakeLists.txt:10-12); using explicit round-to-nearest mul/sub keeps
+// the LU, the forward substitution and the FS glue bit-identical to it.
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+
+constexpr unsigned kFull = 0xffffffffu;
+
+}  // namespace fsigpu

@@ -1,0 +1,1237 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// libfsigpu: host orchestration and C ABI (include/fsigpu.h) of the B200
+// FS-GMG-FGMRES solve path.  See DESIGN.md for the data layout and the
+// kernel/roofline table; each object below names the reference class it
+// stands in for.
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/fsigpu.h"
+#include "common.cuh"
+#include "dense.cuh"
+#include "krylov.cuh"
+#include "sparse.cuh"
+
+namespace fsigpu {
+
+// ------------------------------------------------------------ errors
+static thread_local std::string g_err;
+static thread_local int g_bad_block = -1;
+
+// ------------------------------------------------------------ profiler
+struct Profiler {
+  bool on = false;
+  struct Rec {
+    int cls;
+    double bytes;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  double ms[FSIGPU_K_COUNT] = {0};
+  long long launches[FSIGPU_K_COUNT] = {0};
+  double bytes[FSIGPU_K_COUNT] = {0};
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    FSI_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+  int begin(int cls, double by, cudaStream_t s) {
+    if (!on) return -1;
+    Rec r{cls, by, get(), get()};
+    FSI_CUDA(cudaEventRecord(r.a, s));
+    recs.push_back(r);
+    return (int)recs.size() - 1;
+  }
+  void end(int id, cudaStream_t s) {
+    if (id < 0) return;
+    FSI_CUDA(cudaEventRecord(recs[id].b, s));
+  }
+  void flush() {
+    for (auto& r : recs) {
+      FSI_CUDA(cudaEventSynchronize(r.b));
+      float t = 0;
+      FSI_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+      ms[r.cls] += t;
+      launches[r.cls] += 1;
+      bytes[r.cls] += r.bytes;
+      pool.push_back(r.a);
+      pool.push_back(r.b);
+    }
+    recs.clear();
+  }
+};
+static Profiler g_prof;
+static std::mutex g_prof_mu;
+
+struct ProfScope {
+  int id;
+  cudaStream_t s;
+  ProfScope(int cls, double bytes, cudaStream_t st) : s(st) { id = g_prof.begin(cls, bytes, st); }
+  ~ProfScope() {
+    try {
+      g_prof.end(id, s);
+    } catch (...) {
+    }
+  }
+};
+
+// ------------------------------------------------------------ CSR
+struct Csr {
+  int rows = 0, cols = 0;
+  long long nnz = 0;
+  int lpr = 8;
+  DevBuf<int> ptr, idx;
+  DevBuf<double> val;
+  std::vector<int> h_ptr, h_idx;  // host copies (setup-side index work)
+  std::vector<double> h_val;
+
+  void create(int r, int c, const int* p, const int* ix, const double* v, cudaStream_t s,
+              bool keep_host = false) {
+    require(r >= 0 && c >= 0, "csr: negative dimension");
+    require(p != nullptr || r == 0, "csr: null row offsets");
+    rows = r;
+    cols = c;
+    nnz = r ? p[r] : 0;
+    require(nnz >= 0 && (r == 0 || p[0] == 0), "csr: bad row offsets");
+    for (int i = 0; i < r; ++i) require(p[i] <= p[i + 1], "csr: offsets not nondecreasing");
+    for (long long k = 0; k < nnz; ++k) require(ix[k] >= 0 && ix[k] < c, "csr: column range");
+    ptr.upload(p, (size_t)r + 1, s);
+    idx.upload(ix, (size_t)nnz, s);
+    val.upload(v, (size_t)nnz, s);
+    const double avg = r ? (double)nnz / r : 0.0;
+    lpr = avg <= 3 ? 2 : avg <= 6 ? 4 : avg <= 12 ? 8 : avg <= 40 ? 16 : 32;
+    if (keep_host) {
+      h_ptr.assign(p, p + r + 1);
+      h_idx.assign(ix, ix + nnz);
+      h_val.assign(v, v + nnz);
+    }
+    FSI_CUDA(cudaStreamSynchronize(s));
+  }
+  double bytes(bool resid) const {
+    return 12.0 * nnz + 4.0 * (rows + 1) + 8.0 * cols + 8.0 * rows + (resid ? 8.0 * rows : 0.0);
+  }
+  template <class G, class E>
+  void launch(G g, E e, cudaStream_t s) const {
+    if (!rows) return;
+    const long long threads = (long long)rows * lpr;
+    const int grid = ceil_div(threads, 256);
+    switch (lpr) {
+      case 2: csr_kernel<2><<<grid, 256, 0, s>>>(rows, ptr.p, idx.p, val.p, g, e); break;
+      case 4: csr_kernel<4><<<grid, 256, 0, s>>>(rows, ptr.p, idx.p, val.p, g, e); break;
+      case 8: csr_kernel<8><<<grid, 256, 0, s>>>(rows, ptr.p, idx.p, val.p, g, e); break;
+      case 16: csr_kernel<16><<<grid, 256, 0, s>>>(rows, ptr.p, idx.p, val.p, g, e); break;
+      default: csr_kernel<32><<<grid, 256, 0, s>>>(rows, ptr.p, idx.p, val.p, g, e); break;
+    }
+    FSI_CHECK_LAUNCH();
+  }
+};
+
+// ------------------------------------------------------------ dense blocks
+// Batched DenseFactorization: one LU per block, column-major.
+struct Blocks {
+  long long nb = 0;
+  long long total_rows = 0;
+  int max_m = 0;
+  std::vector<int> h_m;
+  std::vector<long long> h_lu_off, h_row_off;
+  DevBuf<int> m;
+  DevBuf<long long> lu_off, row_off;
+  DevBuf<double> lu, orig;
+  DevBuf<int> gsrc, piv, pos;
+  DevBuf<SolveItem> items;
+  int n_items = 0;
+  double solve_bytes = 0;  // algorithmic bytes of one batched solve
+  double factor_flops = 0;
+
+  void layout(const std::vector<int>& sizes, cudaStream_t s) {
+    nb = (long long)sizes.size();
+    h_m = sizes;
+    h_lu_off.assign(nb + 1, 0);
+    h_row_off.assign(nb + 1, 0);
+    max_m = 0;
+    solve_bytes = 0;
+    factor_flops = 0;
+    for (long long b = 0; b < nb; ++b) {
+      const long long mm = sizes[b];
+      require(mm >= 1 && mm <= kLargeMax, "blocks: block size must be in [1, 1024]");
+      h_lu_off[b + 1] = h_lu_off[b] + mm * mm;
+      h_row_off[b + 1] = h_row_off[b] + mm;
+      max_m = std::max<int>(max_m, (int)mm);
+      solve_bytes += 8.0 * mm * mm + 4.0 * mm + 8.0 * mm + 8.0 * mm;
+      factor_flops += 2.0 / 3.0 * mm * mm * mm;
+    }
+    total_rows = h_row_off[nb];
+    m.upload(h_m, s);
+    lu_off.upload(h_lu_off, s);
+    row_off.upload(h_row_off, s);
+    lu.alloc((size_t)h_lu_off[nb]);
+    gsrc.alloc((size_t)total_rows);
+    piv.alloc((size_t)total_rows);
+    // solve work items: small blocks 8 per CTA (warp each), large 1 per CTA
+    std::vector<SolveItem> it;
+    long long b = 0;
+    while (b < nb) {
+      if (h_m[b] <= kSmallMax) {
+        SolveItem x{0, (int)b, 0, 0};
+        while (b < nb && h_m[b] <= kSmallMax && x.count < 8) {
+          ++x.count;
+          ++b;
+        }
+        it.push_back(x);
+      } else {
+        it.push_back(SolveItem{1, (int)b, 1, 0});
+        ++b;
+      }
+    }
+    require(nb < INT_MAX && total_rows < INT_MAX, "blocks: too many blocks/rows for int32 maps");
+    n_items = (int)it.size();
+    items.upload(it, s);
+  }
+
+  // LU of every block from src (column-major, same offsets) into lu.
+  void factor(const double* src, const int* src_pos, int pos_base, cudaStream_t s) {
+    DevBuf<int> fail(1);
+    const int big = INT_MAX;
+    FSI_CUDA(cudaMemcpyAsync(fail.p, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+    std::vector<int> cls_s, cls_m, cls_g;
+    int mx_s = 0, mx_m = 0, mx_g = 0;
+    for (long long b = 0; b < nb; ++b) {
+      const int mm = h_m[b];
+      if (mm <= 64) {
+        cls_s.push_back((int)b);
+        mx_s = std::max(mx_s, mm);
+      } else if (mm <= 164) {
+        cls_m.push_back((int)b);
+        mx_m = std::max(mx_m, mm);
+      } else {
+        cls_g.push_back((int)b);
+        mx_g = std::max(mx_g, mm);
+      }
+    }
+    auto run = [&](std::vector<int>& cls, int mx, int which) {
+      if (cls.empty()) return;
+      DevBuf<int> bl;
+      bl.upload(cls, s);
+      const int grid = (int)cls.size();
+      if (which == 0) {
+        const size_t sm = (size_t)mx * mx * 8 + (size_t)mx * 12;
+        auto k = lu_factor_kernel<128, true>;
+        FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k<<<grid, 128, sm, s>>>(bl.p, m.p, lu_off.p, row_off.p, src, lu.p, piv.p, gsrc.p, src_pos, pos_base, fail.p);
+      } else if (which == 1) {
+        const size_t sm = (size_t)mx * mx * 8 + (size_t)mx * 12;
+        auto k = lu_factor_kernel<256, true>;
+        FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k<<<grid, 256, sm, s>>>(bl.p, m.p, lu_off.p, row_off.p, src, lu.p, piv.p, gsrc.p, src_pos, pos_base, fail.p);
+      } else {
+        const size_t sm = (size_t)mx * 12;
+        auto k = lu_factor_kernel<256, false>;
+        k<<<grid, 256, sm, s>>>(bl.p, m.p, lu_off.p, row_off.p, src, lu.p, piv.p, gsrc.p, src_pos, pos_base, fail.p);
+      }
+      FSI_CHECK_LAUNCH();
+      FSI_CUDA(cudaStreamSynchronize(s));  // keep `bl` alive until done
+    };
+    run(cls_s, mx_s, 0);
+    run(cls_m, mx_m, 1);
+    run(cls_g, mx_g, 2);
+    int bad = 0;
+    FSI_CUDA(cudaMemcpyAsync(&bad, fail.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    FSI_CUDA(cudaStreamSynchronize(s));
+    if (bad != INT_MAX) {
+      g_bad_block = bad;
+      throw Error(FSIGPU_ERR_SINGULAR, "singular block: " + std::to_string(bad));
+    }
+  }
+
+  void solve(const SolveArgs& base, cudaStream_t s) const {
+    if (!n_items) return;
+    SolveArgs a = base;
+    a.m = m.p;
+    a.lu_off = lu_off.p;
+    a.row_off = row_off.p;
+    a.lu = lu.p;
+    a.gsrc = gsrc.p;
+    a.items = items.p;
+    ProfScope ps(FSIGPU_K_BLOCK_SOLVE, solve_bytes, s);
+    block_solve_kernel<<<n_items, kSolveThreads, 0, s>>>(a);
+    FSI_CHECK_LAUNCH();
+  }
+};
+
+}  // namespace fsigpu
+
+// C-ABI handle types
+struct fsigpu_csr_t {
+  fsigpu::Csr a;
+  cudaStream_t s = nullptr;
+};
+struct fsigpu_blocks_t {
+  fsigpu::Blocks b;
+  cudaStream_t s = nullptr;
+  int have_orig = 0;
+  int own_stream = 0;
+};
+
+namespace fsigpu {
+
+// ------------------------------------------------------------ GMG level
+struct Level {
+  int n = 0, nc = 0;
+  Csr A, P, R;
+  DevBuf<unsigned char> rmask, cmask;
+  // FS smoother (levels >= 1)
+  int g1 = 0, n_us = 0;
+  DevBuf<double> lumped;
+  Blocks blocks;  // AS1 blocks then AS2 blocks, positions in the frame
+  int n_as1 = 0;
+  DevBuf<int> inv_ptr, inv_idx;
+  DevBuf<int> aus_ptr, aus_col;
+  DevBuf<double> aus_val;
+  DevBuf<double> delta, bbuf, xbuf, rbuf;
+  double* b = nullptr;  // level rhs (top level: external)
+  double* x = nullptr;  // level iterate (top level: external)
+  double combine_bytes = 0;
+};
+
+struct Gmg {
+  std::vector<Level> lv;
+  double omega = 0.7;
+  int pre = 1, post = 1;
+  char cyc = 'v';
+  DevBuf<double> coarse_inv;  // equilibrated explicit inverse, row-major
+  cudaStream_t s = nullptr;
+  DevBuf<double> tmp_in, tmp_out;
+
+  int size() const { return lv.back().n; }
+
+  void smooth_solve(int l, const double* rhs) {
+    Level& L = lv[l];
+    SolveArgs a{};
+    a.r = rhs;
+    a.g1 = L.g1;
+    a.lumped = L.lumped.p;
+    a.aus_ptr = L.aus_ptr.p;
+    a.aus_col = L.aus_col.p;
+    a.aus_val = L.aus_val.p;
+    a.out = L.delta.p;
+    L.blocks.solve(a, s);
+  }
+  void combine(int l, const double* r, int x_zero) {
+    Level& L = lv[l];
+    ProfScope ps(FSIGPU_K_COMBINE, L.combine_bytes, s);
+    fs_combine_kernel<<<ceil_div(L.n, 256), 256, 0, s>>>(L.n, L.g1, L.n_us, L.inv_ptr.p, L.inv_idx.p, L.delta.p, r,
+                                                         L.lumped.p, omega, L.x, x_zero);
+    FSI_CHECK_LAUNCH();
+  }
+  void resid(int l, double* r) {
+    Level& L = lv[l];
+    ProfScope ps(FSIGPU_K_SPMV, L.A.bytes(true), s);
+    L.A.launch(GatherPlain{L.x}, EpiResid{L.b, r}, s);
+  }
+  // one FS-preconditioned Richardson sweep; x_zero: x == 0 on entry
+  void sweep(int l, int x_zero) {
+    Level& L = lv[l];
+    if (x_zero) {
+      // res = b - A*0 = b exactly (precond.cpp:312-313)
+      smooth_solve(l, L.b);
+      combine(l, L.b, 1);
+    } else {
+      resid(l, L.rbuf.p);
+      smooth_solve(l, L.rbuf.p);
+      combine(l, L.rbuf.p, 0);
+    }
+  }
+  void coarse(int x_zero) {
+    Level& L = lv[0];
+    const double* rhs = L.b;
+    if (!x_zero) {
+      resid(0, L.rbuf.p);
+      rhs = L.rbuf.p;
+    }
+    ProfScope ps(FSIGPU_K_COARSE, 8.0 * L.n * L.n + 16.0 * L.n, s);
+    gemv_kernel<<<ceil_div((long long)L.n * 32, 256), 256, 0, s>>>(L.n, coarse_inv.p, rhs, L.x, x_zero ? 0 : 1);
+    FSI_CHECK_LAUNCH();
+  }
+  // GmgPreconditioner::cycle (gmg.cpp:188-239)
+  void cycle(int l, char mode, int x_zero) {
+    if (l == 0) {
+      coarse(x_zero);
+      return;
+    }
+    Level& L = lv[l];
+    Level& B = lv[l - 1];
+    if (pre == 0 && x_zero) FSI_CUDA(cudaMemsetAsync(L.x, 0, sizeof(double) * L.n, s));
+    for (int k = 0; k < pre; ++k) sweep(l, x_zero && k == 0);
+    resid(l, L.rbuf.p);
+    {
+      ProfScope ps(FSIGPU_K_TRANSFER, L.R.bytes(false) + L.nc, s);
+      L.R.launch(GatherPlain{L.rbuf.p}, EpiRestrict{B.rmask.p, B.b}, s);
+    }
+    switch (mode) {
+      case 'v': cycle(l - 1, 'v', 1); break;
+      case 'w': cycle(l - 1, 'w', 1); cycle(l - 1, 'w', 0); break;
+      case 'f': cycle(l - 1, 'f', 1); cycle(l - 1, 'v', 0); break;
+      default: throw Error(FSIGPU_ERR_INVALID, "gmg: unknown cycle type");
+    }
+    {
+      ProfScope ps(FSIGPU_K_TRANSFER, L.P.bytes(false) + 8.0 * L.n + L.n + L.nc, s);
+      L.P.launch(GatherMasked{B.x, B.cmask.p}, EpiProlongAdd{L.cmask.p, L.x}, s);
+    }
+    for (int k = 0; k < post; ++k) sweep(l, 0);
+  }
+  // z = M r on device pointers
+  void apply(const double* r, double* z) {
+    Level& T = lv.back();
+    T.b = const_cast<double*>(r);
+    T.x = z;
+    if (lv.size() == 1) {
+      coarse(1);
+    } else {
+      cycle((int)lv.size() - 1, cyc, 1);
+    }
+  }
+};
+
+// Build one level from its descriptor (host arrays).
+static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t s) {
+  Level& L = g.lv[l];
+  require(d.n > 0, "gmg: empty level");
+  L.n = d.n;
+  require(d.a_ptr && d.a_idx && d.a_val && d.row_mask && d.col_mask, "gmg: null level arrays");
+  L.A.create(d.n, d.n, d.a_ptr, d.a_idx, d.a_val, s);
+  L.rmask.upload(d.row_mask, (size_t)d.n, s);
+  L.cmask.upload(d.col_mask, (size_t)d.n, s);
+  L.rbuf.alloc(d.n);
+  if (l > 0) {
+    L.bbuf.alloc(d.n);
+    L.xbuf.alloc(d.n);
+  } else {
+    L.bbuf.alloc(d.n);
+    L.xbuf.alloc(d.n);
+  }
+  L.b = L.bbuf.p;
+  L.x = L.xbuf.p;
+  if (l == 0) return;
+  L.nc = d.nc;
+  require(d.nc == g.lv[l - 1].n, "gmg: transfer size does not match the coarser level");
+  L.P.create(d.n, d.nc, d.p_ptr, d.p_idx, d.p_val, s);
+  L.R.create(d.nc, d.n, d.r_ptr, d.r_idx, d.r_val, s);
+  require(d.g1 >= 0 && d.n_us >= 0 && d.g1 + d.n_us <= d.n, "fs: bad group sizes");
+  L.g1 = d.g1;
+  L.n_us = d.n_us;
+  L.lumped.upload(d.lumped, (size_t)d.n_us, s);
+  // blocks: AS1 (frame positions) then AS2 (group-2 local -> +g1)
+  const int nb1 = d.as1_n, nb2 = d.as2_n;
+  std::vector<int> sizes;
+  std::vector<int> pos;
+  for (int b = 0; b < nb1; ++b) {
+    const int m = d.as1_ptr[b + 1] - d.as1_ptr[b];
+    sizes.push_back(m);
+    for (int k = d.as1_ptr[b]; k < d.as1_ptr[b + 1]; ++k) {
+      const int p = d.as1_idx[k];
+      require(p >= 0 && p < d.g1, "fs: AS1 index outside group 1");
+      require(k == d.as1_ptr[b] || p > d.as1_idx[k - 1], "fs: AS1 set not sorted/unique");
+      pos.push_back(p);
+    }
+  }
+  for (int b = 0; b < nb2; ++b) {
+    const int m = d.as2_ptr[b + 1] - d.as2_ptr[b];
+    sizes.push_back(m);
+    for (int k = d.as2_ptr[b]; k < d.as2_ptr[b + 1]; ++k) {
+      const int p = d.as2_idx[k];
+      require(p >= 0 && p < d.n - d.g1, "fs: AS2 index outside group 2");
+      require(k == d.as2_ptr[b] || p > d.as2_idx[k - 1], "fs: AS2 set not sorted/unique");
+      require(p >= d.n_us, "fs: AS2 block touches the lumped solid-velocity range");
+      pos.push_back(p + d.g1);
+    }
+  }
+  L.n_as1 = nb1;
+  Blocks& B = L.blocks;
+  B.layout(sizes, s);
+  B.pos.upload(pos, s);
+  L.delta.alloc((size_t)std::max<long long>(B.total_rows, 1));
+  // extract + factor (factor_principal_block for every block)
+  if (B.nb) {
+    B.lu.zero(s);
+    extract_blocks_kernel<<<(int)B.nb, 256, 0, s>>>((int)B.nb, B.m.p, B.lu_off.p, B.row_off.p, B.pos.p, 0, L.A.ptr.p,
+                                                    L.A.idx.p, L.A.val.p, B.lu.p);
+    FSI_CHECK_LAUNCH();
+    try {
+      B.factor(B.lu.p, B.pos.p, 0, s);
+    } catch (Error& e) {
+      throw Error(e.code, std::string(e.what()) + " (level " + std::to_string(l) + ")");
+    }
+  }
+  // inverse map position -> delta slots in block order (precond.cpp:52-55)
+  std::vector<int> cnt(d.n + 1, 0);
+  for (int p : pos) cnt[p + 1]++;
+  for (int i = 0; i < d.n; ++i) cnt[i + 1] += cnt[i];
+  std::vector<int> inv(pos.size()), nxt(cnt.begin(), cnt.end() - 1);
+  for (size_t k = 0; k < pos.size(); ++k) inv[nxt[pos[k]]++] = (int)k;
+  L.inv_ptr.upload(cnt, s);
+  L.inv_idx.upload(inv, s);
+  L.combine_bytes = 4.0 * (d.n + 1) + 4.0 * inv.size() + 8.0 * inv.size() + 8.0 * 2 * d.n + 8.0 * d.n_us;
+  // A_g2[:, :n_us] rows (Jacobi residual update, precond.cpp:281-287)
+  const int g2 = d.n - d.g1;
+  std::vector<int> ap(g2 + 1, 0), ac;
+  std::vector<double> av;
+  for (int q = 0; q < g2; ++q) {
+    const int row = d.g1 + q;
+    for (int k = d.a_ptr[row]; k < d.a_ptr[row + 1]; ++k) {
+      const int c = d.a_idx[k] - d.g1;
+      if (c >= 0 && c < d.n_us) {
+        ac.push_back(c);
+        av.push_back(d.a_val[k]);
+      }
+    }
+    ap[q + 1] = (int)ac.size();
+  }
+  L.aus_ptr.upload(ap, s);
+  L.aus_col.upload(ac.empty() ? std::vector<int>{0} : ac, s);
+  L.aus_val.upload(av.empty() ? std::vector<double>{0.0} : av, s);
+  for (int i = 0; i < d.n_us; ++i) require(d.lumped[i] != 0.0, "fs: zero lumped mass entry");
+  FSI_CUDA(cudaStreamSynchronize(s));
+}
+
+// Coarse operator: equilibrate (sparse_lu.cpp:104-121), Gauss-Jordan
+// inverse on the device, fold the scalings into the inverse.
+static void build_coarse(Gmg& g, const fsigpu_level_desc& d, cudaStream_t s) {
+  const int n = d.n;
+  std::vector<double> rs(n, 1.0), cs(n, 1.0), cm(n, 0.0);
+  for (int i = 0; i < n; ++i) {
+    double mx = 0.0;
+    for (int k = d.a_ptr[i]; k < d.a_ptr[i + 1]; ++k) mx = std::max(mx, std::fabs(d.a_val[k]));
+    if (mx > 0.0) rs[i] = 1.0 / mx;
+  }
+  for (int i = 0; i < n; ++i)
+    for (int k = d.a_ptr[i]; k < d.a_ptr[i + 1]; ++k)
+      cm[d.a_idx[k]] = std::max(cm[d.a_idx[k]], std::fabs(d.a_val[k]) * rs[i]);
+  for (int j = 0; j < n; ++j)
+    if (cm[j] > 0.0) cs[j] = 1.0 / cm[j];
+  std::vector<double> W((size_t)n * 2 * n, 0.0);
+  for (int i = 0; i < n; ++i)
+    for (int k = d.a_ptr[i]; k < d.a_ptr[i + 1]; ++k) {
+      const int j = d.a_idx[k];
+      W[(size_t)i * 2 * n + j] += d.a_val[k] * rs[i] * cs[j];
+    }
+  DevBuf<double> Wd, f, drs, dcs;
+  Wd.upload(W, s);
+  f.alloc(n);
+  drs.upload(rs, s);
+  dcs.upload(cs, s);
+  DevBuf<int> fail(1);
+  fail.zero(s);
+  gj_init_kernel<<<ceil_div((long long)n * n, 256), 256, 0, s>>>(n, Wd.p);
+  for (int k = 0; k < n; ++k) {
+    gj_pivot_kernel<<<1, 1024, 0, s>>>(n, Wd.p, k, f.p, fail.p);
+    dim3 grid(ceil_div(2LL * n, 256), n);
+    gj_eliminate_kernel<<<grid, 256, 0, s>>>(n, Wd.p, k, f.p);
+  }
+  FSI_CHECK_LAUNCH();
+  g.coarse_inv.alloc((size_t)n * n);
+  gj_extract_kernel<<<ceil_div((long long)n * n, 256), 256, 0, s>>>(n, Wd.p, drs.p, dcs.p, g.coarse_inv.p);
+  FSI_CHECK_LAUNCH();
+  int bad = 0;
+  FSI_CUDA(cudaMemcpyAsync(&bad, fail.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  FSI_CUDA(cudaStreamSynchronize(s));
+  if (bad) {
+    g_bad_block = -1;
+    throw Error(FSIGPU_ERR_SINGULAR, "singular block: gmg-coarse");
+  }
+}
+
+// ------------------------------------------------------------ GMRES
+struct Gmres {
+  Gmg* g = nullptr;
+  int n = 0, mr = 30;
+  int grid = 0;
+  bool graphs = true;
+  DevBuf<double> scale, V, Z, w, zbuf, ubuf, r, x, b, H, cs, sn, gv, hist, partial;
+  DevBuf<unsigned int> ticket;
+  DevBuf<KState> st;
+  KBufs kb{};
+  int hist_cap = 0;
+  cudaGraphExec_t cycle_exec = nullptr;
+  cudaGraph_t cycle_graph = nullptr;
+
+  ~Gmres() {
+    if (cycle_exec) cudaGraphExecDestroy(cycle_exec);
+    if (cycle_graph) cudaGraphDestroy(cycle_graph);
+  }
+
+  void ensure_history(int max_iters) {
+    if (max_iters + 2 > hist_cap) {
+      hist_cap = max_iters + 2;
+      hist.alloc(hist_cap);
+      kb.history = hist.p;
+      if (cycle_exec) {
+        cudaGraphExecDestroy(cycle_exec);
+        cudaGraphDestroy(cycle_graph);
+        cycle_exec = nullptr;
+        cycle_graph = nullptr;
+      }
+    }
+  }
+
+  // w = A_s z (scaled SpMV)
+  void outer_spmv(const double* z, double* out) {
+    Level& T = g->lv.back();
+    ProfScope ps(FSIGPU_K_SPMV, T.A.bytes(false) + 8.0 * n, g->s);
+    T.A.launch(GatherPlain{z}, EpiScaled{scale.p, out}, g->s);
+  }
+  void outer_resid() {
+    Level& T = g->lv.back();
+    ProfScope ps(FSIGPU_K_SPMV, T.A.bytes(true) + 8.0 * n, g->s);
+    T.A.launch(GatherPlain{x.p}, EpiResidScaled{b.p, scale.p, r.p}, g->s);
+  }
+  void arnoldi_tail() {
+    cudaStream_t s = g->s;
+    const double vb = 8.0 * n;
+    {
+      ProfScope ps(FSIGPU_K_ARNOLDI, vb * 3, s);
+      k_dots<<<grid, kKThreads, 0, s>>>(kb);
+      k_update_dots<<<grid, kKThreads, 0, s>>>(kb);
+      k_update_norm<<<grid, kKThreads, 0, s>>>(kb);
+      k_normalize<<<grid, kKThreads, 0, s>>>(kb);
+    }
+    FSI_CHECK_LAUNCH();
+  }
+  void step_body() {
+    g->apply(ubuf.p, zbuf.p);
+    outer_spmv(zbuf.p, w.p);
+    arnoldi_tail();
+  }
+  void cycle_tail() {
+    cudaStream_t s = g->s;
+    k_solve_y<<<1, 32, 0, s>>>(kb);
+    k_update_x<<<grid, kKThreads, 0, s>>>(kb);
+    outer_resid();
+    k_norm_r<<<grid, kKThreads, 0, s>>>(kb);
+    FSI_CHECK_LAUNCH();
+  }
+
+  void build_graph() {
+    cudaStream_t s = g->s;
+    FSI_CUDA(cudaGraphCreate(&cycle_graph, 0));
+    cudaGraphConditionalHandle h;
+    FSI_CUDA(cudaGraphConditionalHandleCreate(&h, cycle_graph, 1, cudaGraphCondAssignDefault));
+    // prefix: v0 = r / beta
+    cudaGraph_t pre_g, post_g;
+    FSI_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    k_cycle_start<<<grid, kKThreads, 0, s>>>(kb);
+    FSI_CUDA(cudaStreamEndCapture(s, &pre_g));
+    cudaGraphNode_t n_pre, n_cond, n_post;
+    FSI_CUDA(cudaGraphAddChildGraphNode(&n_pre, cycle_graph, nullptr, 0, pre_g));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    FSI_CUDA(cudaGraphAddNode(&n_cond, cycle_graph, &n_pre, 1, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    FSI_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    step_body();
+    k_set_continue<<<1, 1, 0, s>>>(st.p, h, mr);
+    FSI_CUDA(cudaStreamEndCapture(s, &body));
+    FSI_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    cycle_tail();
+    FSI_CUDA(cudaStreamEndCapture(s, &post_g));
+    FSI_CUDA(cudaGraphAddChildGraphNode(&n_post, cycle_graph, &n_cond, 1, post_g));
+    FSI_CUDA(cudaGraphInstantiate(&cycle_exec, cycle_graph, 0));
+    cudaGraphDestroy(pre_g);
+    cudaGraphDestroy(post_g);
+  }
+
+  KState read_state() {
+    KState h;
+    FSI_CUDA(cudaMemcpyAsync(&h, st.p, sizeof(KState), cudaMemcpyDeviceToHost, g->s));
+    FSI_CUDA(cudaStreamSynchronize(g->s));
+    return h;
+  }
+
+  // krylov.cpp:20-126 control flow, device resident
+  void solve(int max_iters, double rel_tol, double abs_tol, fsigpu_gmres_result* res) {
+    require(max_iters >= 0, "gmres: invalid config");
+    require(rel_tol > 0.0 && abs_tol > 0.0, "gmres: invalid config");
+    ensure_history(max_iters);
+    cudaStream_t s = g->s;
+    KState h0{};
+    h0.max_iters = max_iters;
+    h0.restart = mr;
+    h0.first = 1;
+    h0.rel_tol = rel_tol;
+    h0.abs_tol = abs_tol;
+    FSI_CUDA(cudaMemcpyAsync(st.p, &h0, sizeof(KState), cudaMemcpyHostToDevice, s));
+    outer_resid();
+    k_norm_r<<<grid, kKThreads, 0, s>>>(kb);
+    FSI_CHECK_LAUNCH();
+    KState h = read_state();
+    long long cycles = 0;
+    const bool use_graph = graphs && !g_prof.on;
+    if (use_graph && !cycle_exec) build_graph();
+    while (!h.converged && h.its < max_iters) {
+      if (use_graph) {
+        FSI_CUDA(cudaGraphLaunch(cycle_exec, s));
+      } else {
+        k_cycle_start<<<grid, kKThreads, 0, s>>>(kb);
+        FSI_CHECK_LAUNCH();
+        while (true) {
+          step_body();
+          KState t = read_state();
+          if (t.stop || t.j >= mr || t.its >= max_iters) break;
+        }
+        cycle_tail();
+      }
+      h = read_state();
+      ++cycles;
+      if (h.breakdown) break;
+    }
+    res->iterations = h.its;
+    res->converged = h.converged;
+    res->breakdown = h.breakdown;
+    res->n_history = h.its + 1;
+    res->m_applies = h.its;  // FGMRES: one V-cycle per Arnoldi step
+    res->true_residual = h.beta;
+    if (g_prof.on) g_prof.flush();
+  }
+};
+
+}  // namespace fsigpu
+
+struct fsigpu_gmg_t {
+  fsigpu::Gmg g;
+};
+struct fsigpu_gmres_t {
+  fsigpu::Gmres k;
+};
+
+using namespace fsigpu;
+
+template <class F>
+static int guarded(F&& f) {
+  try {
+    f();
+    return FSIGPU_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return FSIGPU_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return FSIGPU_ERR_CUDA;
+  }
+}
+
+static cudaStream_t new_stream() {
+  cudaStream_t s;
+  FSI_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  return s;
+}
+
+extern "C" {
+
+const char* fsigpu_last_error(void) { return g_err.c_str(); }
+int fsigpu_last_singular_block(void) { return g_bad_block; }
+int fsigpu_version(void) { return 1; }
+
+int fsigpu_init(int device) {
+  return guarded([&] {
+    int n = 0;
+    FSI_CUDA(cudaGetDeviceCount(&n));
+    require(device >= 0 && device < n, "init: no such CUDA device");
+    FSI_CUDA(cudaSetDevice(device));
+    FSI_CUDA(cudaFree(nullptr));
+  });
+}
+
+// ---- CSR
+int fsigpu_csr_create(int rows, int cols, const int* ptr, const int* idx, const double* val, fsigpu_csr* out) {
+  return guarded([&] {
+    auto h = std::make_unique<fsigpu_csr_t>();
+    h->s = new_stream();
+    h->a.create(rows, cols, ptr, idx, val, h->s, true);
+    *out = h.release();
+  });
+}
+
+int fsigpu_csr_multiply_dev(fsigpu_csr a, const double* dx, double* dy, void* stream) {
+  return guarded([&] {
+    require(a != nullptr, "spmv: null matrix");
+    cudaStream_t s = stream ? (cudaStream_t)stream : a->s;
+    ProfScope ps(FSIGPU_K_SPMV, a->a.bytes(false), s);
+    a->a.launch(GatherPlain{dx}, EpiPlain{dy}, s);
+  });
+}
+
+int fsigpu_csr_multiply(fsigpu_csr a, const double* x, double* y) {
+  return guarded([&] {
+    require(a != nullptr, "spmv: null matrix");
+    DevBuf<double> dx, dy(a->a.rows);
+    dx.upload(x, (size_t)a->a.cols, a->s);
+    a->a.launch(GatherPlain{dx.p}, EpiPlain{dy.p}, a->s);
+    FSI_CHECK_LAUNCH();
+    if (a->a.rows) FSI_CUDA(cudaMemcpyAsync(y, dy.p, sizeof(double) * a->a.rows, cudaMemcpyDeviceToHost, a->s));
+    FSI_CUDA(cudaStreamSynchronize(a->s));
+  });
+}
+
+int fsigpu_csr_time(fsigpu_csr a, int reps, double* ms) {
+  return guarded([&] {
+    require(a != nullptr && reps > 0, "csr_time: bad args");
+    DevBuf<double> dx(a->a.cols), dy(a->a.rows);
+    FSI_CUDA(cudaMemsetAsync(dx.p, 0, sizeof(double) * dx.n, a->s));
+    for (int i = 0; i < 3; ++i) a->a.launch(GatherPlain{dx.p}, EpiPlain{dy.p}, a->s);
+    cudaEvent_t e0, e1;
+    FSI_CUDA(cudaEventCreate(&e0));
+    FSI_CUDA(cudaEventCreate(&e1));
+    FSI_CUDA(cudaEventRecord(e0, a->s));
+    for (int i = 0; i < reps; ++i) a->a.launch(GatherPlain{dx.p}, EpiPlain{dy.p}, a->s);
+    FSI_CUDA(cudaEventRecord(e1, a->s));
+    FSI_CUDA(cudaEventSynchronize(e1));
+    float t = 0;
+    FSI_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    *ms = t / reps;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
+}
+
+void fsigpu_csr_destroy(fsigpu_csr a) {
+  if (!a) return;
+  cudaStreamSynchronize(a->s);
+  cudaStreamDestroy(a->s);
+  delete a;
+}
+
+// ---- blocks
+int fsigpu_blocks_factor_csr(fsigpu_csr a, int n_blocks, const int* block_ptr, const int* block_idx,
+                             fsigpu_blocks* out) {
+  g_bad_block = -1;
+  return guarded([&] {
+    require(a != nullptr && n_blocks >= 0, "blocks: bad args");
+    require(a->a.rows == a->a.cols, "schwarz: matrix not square");
+    auto h = std::make_unique<fsigpu_blocks_t>();
+    h->s = a->s;
+    std::vector<int> sizes(n_blocks);
+    std::vector<int> pos;
+    for (int b = 0; b < n_blocks; ++b) {
+      sizes[b] = block_ptr[b + 1] - block_ptr[b];
+      for (int k = block_ptr[b]; k < block_ptr[b + 1]; ++k) {
+        require(block_idx[k] >= 0 && block_idx[k] < a->a.rows, "index set: index out of range");
+        require(k == block_ptr[b] || block_idx[k] > block_idx[k - 1], "index set: not sorted/unique");
+        pos.push_back(block_idx[k]);
+      }
+    }
+    Blocks& B = h->b;
+    B.layout(sizes, h->s);
+    B.pos.upload(pos, h->s);
+    if (B.nb) {
+      B.lu.zero(h->s);
+      extract_blocks_kernel<<<(int)B.nb, 256, 0, h->s>>>((int)B.nb, B.m.p, B.lu_off.p, B.row_off.p, B.pos.p, 0,
+                                                         a->a.ptr.p, a->a.idx.p, a->a.val.p, B.lu.p);
+      FSI_CHECK_LAUNCH();
+      B.factor(B.lu.p, nullptr, 0, h->s);
+    }
+    *out = h.release();
+  });
+}
+
+int fsigpu_blocks_factor_dense(int n_blocks, const int* sizes, const double* mats, fsigpu_blocks* out) {
+  g_bad_block = -1;
+  return guarded([&] {
+    require(n_blocks >= 0, "blocks: bad args");
+    auto h = std::make_unique<fsigpu_blocks_t>();
+    h->s = new_stream();
+    h->own_stream = 1;
+    std::vector<int> sz(sizes, sizes + n_blocks);
+    Blocks& B = h->b;
+    B.layout(sz, h->s);
+    // row-major (DenseMatrix) -> column-major device layout
+    std::vector<double> cm((size_t)B.h_lu_off[B.nb]);
+    for (long long b = 0; b < B.nb; ++b) {
+      const int m = sz[b];
+      const double* src = mats + B.h_lu_off[b];
+      double* dst = cm.data() + B.h_lu_off[b];
+      for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j) dst[(size_t)j * m + i] = src[(size_t)i * m + j];
+    }
+    B.orig.upload(cm, h->s);
+    h->have_orig = 1;
+    if (B.nb) B.factor(B.orig.p, nullptr, 0, h->s);
+    *out = h.release();
+  });
+}
+
+int fsigpu_blocks_generate_dominant(long long n54, long long n59, unsigned long long seed, fsigpu_blocks* out) {
+  g_bad_block = -1;
+  return guarded([&] {
+    require(n54 >= 0 && n59 >= 0, "blocks: bad counts");
+    auto h = std::make_unique<fsigpu_blocks_t>();
+    h->s = new_stream();
+    h->own_stream = 1;
+    std::vector<int> sz;
+    sz.reserve(n54 + n59);
+    for (long long i = 0; i < n54; ++i) sz.push_back(54);
+    for (long long i = 0; i < n59; ++i) sz.push_back(59);
+    Blocks& B = h->b;
+    B.layout(sz, h->s);
+    B.orig.alloc((size_t)B.h_lu_off[B.nb]);
+    std::vector<long long> rb(B.total_rows);
+    for (long long b = 0; b < B.nb; ++b)
+      for (long long r = B.h_row_off[b]; r < B.h_row_off[b + 1]; ++r) rb[r] = b;
+    DevBuf<long long> drb;
+    drb.upload(rb, h->s);
+    gen_dominant_kernel<<<ceil_div(B.total_rows, 256), 256, 0, h->s>>>(B.nb, B.m.p, B.lu_off.p, B.row_off.p,
+                                                                       B.total_rows, seed, B.orig.p, drb.p);
+    FSI_CHECK_LAUNCH();
+    FSI_CUDA(cudaStreamSynchronize(h->s));
+    h->have_orig = 1;
+    if (B.nb) B.factor(B.orig.p, nullptr, 0, h->s);
+    *out = h.release();
+  });
+}
+
+int fsigpu_blocks_generate_rhs(fsigpu_blocks b, unsigned long long seed, double* d_rhs) {
+  return guarded([&] {
+    require(b != nullptr, "blocks: null");
+    gen_rhs_kernel<<<ceil_div(b->b.total_rows, 256), 256, 0, b->s>>>(b->b.total_rows, seed, d_rhs);
+    FSI_CHECK_LAUNCH();
+    FSI_CUDA(cudaStreamSynchronize(b->s));
+  });
+}
+
+int fsigpu_blocks_copy_matrix(fsigpu_blocks b, long long block, double* rowmajor) {
+  return guarded([&] {
+    require(b != nullptr && b->have_orig && block >= 0 && block < b->b.nb, "blocks: bad block");
+    const int m = b->b.h_m[block];
+    std::vector<double> cm((size_t)m * m);
+    FSI_CUDA(cudaMemcpyAsync(cm.data(), b->b.orig.p + b->b.h_lu_off[block], sizeof(double) * m * m,
+                             cudaMemcpyDeviceToHost, b->s));
+    FSI_CUDA(cudaStreamSynchronize(b->s));
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j) rowmajor[(size_t)i * m + j] = cm[(size_t)j * m + i];
+  });
+}
+
+long long fsigpu_blocks_count(fsigpu_blocks b) { return b ? b->b.nb : 0; }
+long long fsigpu_blocks_total_rows(fsigpu_blocks b) { return b ? b->b.total_rows : 0; }
+long long fsigpu_blocks_factor_bytes(fsigpu_blocks b) { return b ? 8LL * b->b.h_lu_off[b->b.nb] : 0; }
+
+int fsigpu_blocks_solve_dev(fsigpu_blocks b, const double* d_rhs, double* d_x, void* stream) {
+  return guarded([&] {
+    require(b != nullptr, "blocks: null");
+    cudaStream_t s = stream ? (cudaStream_t)stream : b->s;
+    SolveArgs a{};
+    a.r = d_rhs;
+    a.g1 = INT_MAX;
+    a.out = d_x;
+    b->b.solve(a, s);
+  });
+}
+
+int fsigpu_blocks_solve(fsigpu_blocks b, const double* rhs, double* x) {
+  return guarded([&] {
+    require(b != nullptr, "blocks: null");
+    DevBuf<double> dr, dx((size_t)std::max<long long>(b->b.total_rows, 1));
+    dr.upload(rhs, (size_t)b->b.total_rows, b->s);
+    SolveArgs a{};
+    a.r = dr.p;
+    a.g1 = INT_MAX;
+    a.out = dx.p;
+    b->b.solve(a, b->s);
+    if (b->b.total_rows)
+      FSI_CUDA(cudaMemcpyAsync(x, dx.p, sizeof(double) * b->b.total_rows, cudaMemcpyDeviceToHost, b->s));
+    FSI_CUDA(cudaStreamSynchronize(b->s));
+  });
+}
+
+int fsigpu_blocks_refactor(fsigpu_blocks b, void* stream) {
+  g_bad_block = -1;
+  return guarded([&] {
+    require(b != nullptr && b->have_orig, "blocks: no retained matrices");
+    cudaStream_t s = stream ? (cudaStream_t)stream : b->s;
+    b->b.factor(b->b.orig.p, nullptr, 0, s);
+  });
+}
+
+int fsigpu_blocks_get_lu(fsigpu_blocks b, double* lu_rowmajor, int* piv) {
+  return guarded([&] {
+    require(b != nullptr, "blocks: null");
+    const Blocks& B = b->b;
+    auto lu = B.lu.download(b->s);
+    auto pv = B.piv.download(b->s);
+    for (long long k = 0; k < B.nb; ++k) {
+      const int m = B.h_m[k];
+      const double* src = lu.data() + B.h_lu_off[k];
+      double* dst = lu_rowmajor + B.h_lu_off[k];
+      for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j) dst[(size_t)i * m + j] = src[(size_t)j * m + i];
+    }
+    std::memcpy(piv, pv.data(), sizeof(int) * pv.size());
+  });
+}
+
+void fsigpu_blocks_destroy(fsigpu_blocks b) {
+  if (!b) return;
+  cudaStreamSynchronize(b->s);
+  cudaStream_t s = b->own_stream ? b->s : nullptr;
+  delete b;
+  if (s) cudaStreamDestroy(s);
+}
+
+// ---- GMG
+int fsigpu_gmg_create(int n_levels, const fsigpu_level_desc* levels, double omega, int pre, int post, char cycle,
+                      fsigpu_gmg* out) {
+  g_bad_block = -1;
+  return guarded([&] {
+    require(n_levels >= 1 && levels != nullptr, "gmg: no levels");
+    require(pre >= 0 && post >= 0 && !(pre == 0 && post == 0 && n_levels > 1), "gmg: need at least one smoothing sweep");
+    require(omega >= 0.0 && omega < 2.0, "richardson: omega outside [0,2)");
+    require(cycle == 'v' || cycle == 'w' || cycle == 'f', "gmg: unknown cycle type");
+    auto h = std::make_unique<fsigpu_gmg_t>();
+    Gmg& g = h->g;
+    g.s = new_stream();
+    g.omega = omega;
+    g.pre = pre;
+    g.post = post;
+    g.cyc = cycle;
+    g.lv.resize(n_levels);
+    for (int l = 0; l < n_levels; ++l) build_level(g, l, levels[l], g.s);
+    build_coarse(g, levels[0], g.s);
+    g.tmp_in.alloc(g.size());
+    g.tmp_out.alloc(g.size());
+    *out = h.release();
+  });
+}
+
+int fsigpu_gmg_size(fsigpu_gmg g) { return g ? g->g.size() : 0; }
+
+int fsigpu_gmg_apply_dev(fsigpu_gmg g, const double* d_r, double* d_z, void* stream) {
+  return guarded([&] {
+    require(g != nullptr, "gmg: null");
+    require(stream == nullptr || stream == (void*)g->g.s, "gmg: use the handle stream (NULL)");
+    g->g.apply(d_r, d_z);
+    if (g_prof.on) g_prof.flush();
+  });
+}
+
+int fsigpu_gmg_apply(fsigpu_gmg g, const double* r, double* z) {
+  return guarded([&] {
+    require(g != nullptr, "gmg: null");
+    Gmg& G = g->g;
+    const int n = G.size();
+    FSI_CUDA(cudaMemcpyAsync(G.tmp_in.p, r, sizeof(double) * n, cudaMemcpyHostToDevice, G.s));
+    G.apply(G.tmp_in.p, G.tmp_out.p);
+    FSI_CUDA(cudaMemcpyAsync(z, G.tmp_out.p, sizeof(double) * n, cudaMemcpyDeviceToHost, G.s));
+    FSI_CUDA(cudaStreamSynchronize(G.s));
+    if (g_prof.on) g_prof.flush();
+  });
+}
+
+int fsigpu_fs_apply(fsigpu_gmg g, int level, const double* r, double* z) {
+  return guarded([&] {
+    require(g != nullptr, "gmg: null");
+    Gmg& G = g->g;
+    require(level >= 1 && level < (int)G.lv.size(), "fs: level must be a smoothed level (>= 1)");
+    Level& L = G.lv[level];
+    DevBuf<double> dr, dz(L.n);
+    dr.upload(r, (size_t)L.n, G.s);
+    double* sx = L.x;
+    L.x = dz.p;
+    // z = M r  ==  combine with omega = 1 from x = 0
+    const double om = G.omega;
+    G.omega = 1.0;
+    G.smooth_solve(level, dr.p);
+    G.combine(level, dr.p, 1);
+    G.omega = om;
+    L.x = sx;
+    FSI_CUDA(cudaMemcpyAsync(z, dz.p, sizeof(double) * L.n, cudaMemcpyDeviceToHost, G.s));
+    FSI_CUDA(cudaStreamSynchronize(G.s));
+  });
+}
+
+int fsigpu_coarse_solve(fsigpu_gmg g, const double* b, double* x) {
+  return guarded([&] {
+    require(g != nullptr, "gmg: null");
+    Gmg& G = g->g;
+    Level& L = G.lv[0];
+    DevBuf<double> db, dx(L.n);
+    db.upload(b, (size_t)L.n, G.s);
+    double* sb = L.b;
+    double* sx = L.x;
+    L.b = db.p;
+    L.x = dx.p;
+    G.coarse(1);
+    L.b = sb;
+    L.x = sx;
+    FSI_CUDA(cudaMemcpyAsync(x, dx.p, sizeof(double) * L.n, cudaMemcpyDeviceToHost, G.s));
+    FSI_CUDA(cudaStreamSynchronize(G.s));
+  });
+}
+
+void fsigpu_gmg_destroy(fsigpu_gmg g) {
+  if (!g) return;
+  cudaStreamSynchronize(g->g.s);
+  cudaStream_t s = g->g.s;
+  delete g;
+  cudaStreamDestroy(s);
+}
+
+// ---- GMRES
+int fsigpu_gmres_create(fsigpu_gmg g, const double* frame_scale, int restart, fsigpu_gmres* out) {
+  return guarded([&] {
+    require(g != nullptr && frame_scale != nullptr, "gmres: null args");
+    require(restart >= 1 && restart <= kMaxRestart, "gmres: restart must be in [1, 32]");
+    auto h = std::make_unique<fsigpu_gmres_t>();
+    Gmres& k = h->k;
+    k.g = &g->g;
+    k.n = g->g.size();
+    k.mr = restart;
+    const int n = k.n;
+    cudaStream_t s = g->g.s;
+    k.scale.upload(frame_scale, (size_t)n, s);
+    k.V.alloc((size_t)(restart + 1) * n);
+    k.Z.alloc((size_t)restart * n);
+    k.w.alloc(n);
+    k.zbuf.alloc(n);
+    k.ubuf.alloc(n);
+    k.r.alloc(n);
+    k.x.alloc(n);
+    k.b.alloc(n);
+    k.H.alloc((size_t)(restart + 1) * restart);
+    k.H.zero(s);
+    k.cs.alloc(restart);
+    k.sn.alloc(restart);
+    k.gv.alloc(restart + 1);
+    k.grid = std::max(1, std::min(ceil_div(n, kKThreads), 2 * 148));
+    k.partial.alloc((size_t)k.grid * (kMaxRestart + 1));
+    k.ticket.alloc(1);
+    k.ticket.zero(s);
+    k.st.alloc(1);
+    KBufs& kb = k.kb;
+    kb.n = n;
+    kb.mr = restart;
+    kb.scale = k.scale.p;
+    kb.V = k.V.p;
+    kb.Z = k.Z.p;
+    kb.w = k.w.p;
+    kb.zbuf = k.zbuf.p;
+    kb.ubuf = k.ubuf.p;
+    kb.r = k.r.p;
+    kb.x = k.x.p;
+    kb.b = k.b.p;
+    kb.H = k.H.p;
+    kb.cs = k.cs.p;
+    kb.sn = k.sn.p;
+    kb.g = k.gv.p;
+    kb.partial = k.partial.p;
+    kb.ticket = k.ticket.p;
+    kb.st = k.st.p;
+    k.ensure_history(2000);
+    FSI_CUDA(cudaStreamSynchronize(s));
+    *out = h.release();
+  });
+}
+
+int fsigpu_gmres_set_graphs(fsigpu_gmres s, int enable) {
+  return guarded([&] {
+    require(s != nullptr, "gmres: null");
+    s->k.graphs = enable != 0;
+  });
+}
+
+int fsigpu_gmres_solve_dev(fsigpu_gmres s, const double* d_b, double* d_x, int max_iters, double rel_tol,
+                           double abs_tol, double* history, fsigpu_gmres_result* res) {
+  return guarded([&] {
+    require(s != nullptr && d_b != nullptr && d_x != nullptr, "gmres: null args");
+    Gmres& k = s->k;
+    cudaStream_t st = k.g->s;
+    const size_t nb = sizeof(double) * k.n;
+    FSI_CUDA(cudaMemcpyAsync(k.b.p, d_b, nb, cudaMemcpyDeviceToDevice, st));
+    FSI_CUDA(cudaMemcpyAsync(k.x.p, d_x, nb, cudaMemcpyDeviceToDevice, st));
+    fsigpu_gmres_result r{};
+    k.solve(max_iters, rel_tol, abs_tol, res ? res : &r);
+    FSI_CUDA(cudaMemcpyAsync(d_x, k.x.p, nb, cudaMemcpyDeviceToDevice, st));
+    if (history) {
+      const int nh = (res ? res : &r)->n_history;
+      FSI_CUDA(cudaMemcpyAsync(history, k.hist.p, sizeof(double) * nh, cudaMemcpyDeviceToHost, st));
+    }
+    FSI_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int fsigpu_gmres_solve(fsigpu_gmres s, const double* b, const double* x0, double* x, int max_iters, double rel_tol,
+                       double abs_tol, double* history, fsigpu_gmres_result* res) {
+  return guarded([&] {
+    require(s != nullptr && b != nullptr && x != nullptr, "gmres: null args");
+    Gmres& k = s->k;
+    cudaStream_t st = k.g->s;
+    const size_t nb = sizeof(double) * k.n;
+    FSI_CUDA(cudaMemcpyAsync(k.b.p, b, nb, cudaMemcpyHostToDevice, st));
+    if (x0)
+      FSI_CUDA(cudaMemcpyAsync(k.x.p, x0, nb, cudaMemcpyHostToDevice, st));
+    else
+      FSI_CUDA(cudaMemsetAsync(k.x.p, 0, nb, st));
+    fsigpu_gmres_result r{};
+    k.solve(max_iters, rel_tol, abs_tol, res ? res : &r);
+    FSI_CUDA(cudaMemcpyAsync(x, k.x.p, nb, cudaMemcpyDeviceToHost, st));
+    if (history) {
+      const int nh = (res ? res : &r)->n_history;
+      FSI_CUDA(cudaMemcpyAsync(history, k.hist.p, sizeof(double) * nh, cudaMemcpyDeviceToHost, st));
+    }
+    FSI_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+void fsigpu_gmres_destroy(fsigpu_gmres s) {
+  if (!s) return;
+  cudaStreamSynchronize(s->k.g->s);
+  delete s;
+}
+
+// ---- profiler
+int fsigpu_profile_enable(int enable) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof.on = enable != 0;
+  });
+}
+int fsigpu_profile_read(double* ms, long long* launches, double* bytes) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof.flush();
+    for (int i = 0; i < FSIGPU_K_COUNT; ++i) {
+      if (ms) ms[i] = g_prof.ms[i];
+      if (launches) launches[i] = g_prof.launches[i];
+      if (bytes) bytes[i] = g_prof.bytes[i];
+    }
+  });
+}
+int fsigpu_profile_reset(void) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof.flush();
+    for (int i = 0; i < FSIGPU_K_COUNT; ++i) {
+      g_prof.ms[i] = 0;
+      g_prof.launches[i] = 0;
+      g_prof.bytes[i] = 0;
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,309 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Device-resident FGMRES(m) Arnoldi kernels (reference: gmres,
+// proj/src/krylov.cpp:20-126).
+//
+// One Arnoldi step after the V-cycle (z_j = M v_j) and the scaled SpMV
+// (w = A_s z_j) is three row-parallel passes plus a normalisation:
+//   k_dots        : h1 = V_{0..j}^T w           (+ copy z_j into Z[j])
+//   k_update_dots : w -= V h1 ; h2 = V^T w      (classical Gram-Schmidt, 2nd pass)
+//   k_update_norm : w -= V h2 ; ||w||, then on device: H(:,j) = h1+h2,
+//                   Givens rotations, rho = |g_{j+1}|, stop flags
+//   k_normalize   : v_{j+1} = w / h_{j+1,j} ; u = v_{j+1} / frame_scale
+// Each reduction is two-stage with a fixed order (per-CTA partials, the
+// last CTA to arrive sums them in CTA order), so the iteration history is
+// bit-reproducible run to run. All step parameters (j, its) live in device
+// memory so one captured graph serves every step.
+#pragma once
+
+#include "common.cuh"
+
+namespace fsigpu {
+
+constexpr int kMaxRestart = 32;  // restart <= 32 (V_{0..j} dots held in registers)
+constexpr int kKThreads = 256;
+
+struct KState {
+  int j;          // columns done in this cycle
+  int its;        // Arnoldi steps done in total
+  int stop;       // inner loop must stop (rho <= target or lucky)
+  int breakdown;  // lucky breakdown seen (krylov.cpp:74-77)
+  int max_iters;
+  int restart;
+  int first;      // next norm is ||r0||
+  int converged;
+  int keep_going; // cycle-level continue flag (host side)
+  int pad;
+  double target;
+  double beta;
+  double rho;
+  double hn;
+  double rel_tol, abs_tol;
+  double h1[kMaxRestart + 1];
+  double h2[kMaxRestart + 1];
+  double y[kMaxRestart + 1];
+};
+
+struct KBufs {
+  int n;
+  int mr;
+  const double* scale;  // frame_scale
+  double* V;            // (mr+1) x n
+  double* Z;            // mr x n
+  double* w;            // n
+  double* zbuf;         // V-cycle output
+  double* ubuf;         // V-cycle input (v_j / scale)
+  double* r;            // residual
+  double* x;            // iterate
+  const double* b;      // rhs
+  double* H;            // (mr+1) x mr, row-major H(i,j) = H[i*mr+j]
+  double* cs;
+  double* sn;
+  double* g;
+  double* history;      // max_iters + 2
+  double* partial;      // grid x (kMaxRestart+1)
+  unsigned int* ticket;
+  KState* st;
+};
+
+// Block-level sum of NV register accumulators -> sp[v] (thread v < NV).
+template <int NV>
+__device__ __forceinline__ void block_reduce_vec(double (&acc)[NV], int nv, double* sm, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = kKThreads / 32;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    if (v < nv) {
+      double s = acc[v];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+      if (lane == 0) sm[warp * NV + v] = s;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < nv) {
+    double s = 0.0;
+    for (int w = 0; w < NW; ++w) s += sm[w * NV + threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+}
+
+// Last-CTA detection; returns true in every thread of the last CTA.
+__device__ __forceinline__ bool last_block(unsigned int* ticket) {
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last;
+}
+
+__device__ __forceinline__ void finish_sum(const KBufs& k, int nv, double* dst) {
+  if (threadIdx.x < nv) {
+    double s = 0.0;
+    for (unsigned int b = 0; b < gridDim.x; ++b) s += __ldcg(k.partial + (size_t)b * (kMaxRestart + 1) + threadIdx.x);
+    dst[threadIdx.x] = s;
+  }
+  if (threadIdx.x == 0) *k.ticket = 0;
+}
+
+// h1 = V^T w  (+ Z[j] = zbuf)
+__global__ void __launch_bounds__(kKThreads) k_dots(KBufs k) {
+  __shared__ double sm[(kKThreads / 32) * kMaxRestart];
+  const int j = k.st->j;
+  const int nv = j + 1;
+  double acc[kMaxRestart];
+#pragma unroll
+  for (int v = 0; v < kMaxRestart; ++v) acc[v] = 0.0;
+  double* zj = k.Z + (size_t)j * k.n;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x) {
+    const double wr = k.w[r];
+    zj[r] = k.zbuf[r];
+#pragma unroll
+    for (int v = 0; v < kMaxRestart; ++v)
+      if (v < nv) acc[v] = fma(k.V[(size_t)v * k.n + r], wr, acc[v]);
+  }
+  block_reduce_vec<kMaxRestart>(acc, nv, sm, k.partial + (size_t)blockIdx.x * (kMaxRestart + 1));
+  if (last_block(k.ticket)) finish_sum(k, nv, k.st->h1);
+}
+
+// w -= V h_in ; h_out = V^T w
+__global__ void __launch_bounds__(kKThreads) k_update_dots(KBufs k) {
+  __shared__ double sm[(kKThreads / 32) * kMaxRestart];
+  __shared__ double hs[kMaxRestart];
+  const int j = k.st->j;
+  const int nv = j + 1;
+  if (threadIdx.x < nv) hs[threadIdx.x] = k.st->h1[threadIdx.x];
+  __syncthreads();
+  double acc[kMaxRestart];
+#pragma unroll
+  for (int v = 0; v < kMaxRestart; ++v) acc[v] = 0.0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x) {
+    double vr[kMaxRestart];
+    double wr = k.w[r];
+#pragma unroll
+    for (int v = 0; v < kMaxRestart; ++v)
+      if (v < nv) {
+        vr[v] = k.V[(size_t)v * k.n + r];
+        wr = fma(-hs[v], vr[v], wr);
+      }
+    k.w[r] = wr;
+#pragma unroll
+    for (int v = 0; v < kMaxRestart; ++v)
+      if (v < nv) acc[v] = fma(vr[v], wr, acc[v]);
+  }
+  block_reduce_vec<kMaxRestart>(acc, nv, sm, k.partial + (size_t)blockIdx.x * (kMaxRestart + 1));
+  if (last_block(k.ticket)) finish_sum(k, nv, k.st->h2);
+}
+
+// Givens update of column j on device (krylov.cpp:79-100).
+__device__ void givens_step(const KBufs& k) {
+  KState* st = k.st;
+  const int j = st->j;
+  const int mr = k.mr;
+  double* H = k.H;
+  for (int i = 0; i <= j; ++i) H[i * mr + j] = st->h1[i] + st->h2[i];
+  const double hjj = st->hn;
+  H[(j + 1) * mr + j] = hjj;
+  st->its += 1;
+  int lucky = 0;
+  if (hjj < 1e-14) {
+    st->breakdown = 1;
+    lucky = 1;
+  }
+  for (int i = 0; i < j; ++i) {
+    const double t = k.cs[i] * H[i * mr + j] + k.sn[i] * H[(i + 1) * mr + j];
+    H[(i + 1) * mr + j] = -k.sn[i] * H[i * mr + j] + k.cs[i] * H[(i + 1) * mr + j];
+    H[i * mr + j] = t;
+  }
+  const double denom = hypot(H[j * mr + j], H[(j + 1) * mr + j]);
+  k.cs[j] = H[j * mr + j] / denom;
+  k.sn[j] = H[(j + 1) * mr + j] / denom;
+  H[j * mr + j] = denom;
+  H[(j + 1) * mr + j] = 0.0;
+  k.g[j + 1] = -k.sn[j] * k.g[j];
+  k.g[j] = k.cs[j] * k.g[j];
+  const double rho = fabs(k.g[j + 1]);
+  st->rho = rho;
+  k.history[st->its] = rho;
+  st->stop = (rho <= st->target || lucky) ? 1 : 0;
+  st->j = j + 1;
+}
+
+// w -= V h2 ; ||w|| ; Givens
+__global__ void __launch_bounds__(kKThreads) k_update_norm(KBufs k) {
+  __shared__ double sm[(kKThreads / 32) * kMaxRestart];
+  __shared__ double hs[kMaxRestart];
+  const int j = k.st->j;
+  const int nv = j + 1;
+  if (threadIdx.x < nv) hs[threadIdx.x] = k.st->h2[threadIdx.x];
+  __syncthreads();
+  double acc[1] = {0.0};
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x) {
+    double wr = k.w[r];
+#pragma unroll
+    for (int v = 0; v < kMaxRestart; ++v)
+      if (v < nv) wr = fma(-hs[v], k.V[(size_t)v * k.n + r], wr);
+    k.w[r] = wr;
+    acc[0] = fma(wr, wr, acc[0]);
+  }
+  block_reduce_vec<1>(acc, 1, sm, k.partial + (size_t)blockIdx.x * (kMaxRestart + 1));
+  if (last_block(k.ticket)) {
+    __shared__ double s_n2;
+    finish_sum(k, 1, &s_n2);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      k.st->hn = sqrt(s_n2);
+      givens_step(k);
+    }
+  }
+}
+
+// v_{j} = w / hn (j already advanced), u = v_j / scale; skipped on breakdown.
+__global__ void k_normalize(KBufs k) {
+  const KState* st = k.st;
+  if (st->hn < 1e-14) return;
+  const double hn = st->hn;
+  double* vj = k.V + (size_t)st->j * k.n;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x) {
+    const double v = k.w[r] / hn;
+    vj[r] = v;
+    k.ubuf[r] = v / k.scale[r];
+  }
+}
+
+// ||r|| -> beta; on the first call also r0, history[0] and target.
+__global__ void __launch_bounds__(kKThreads) k_norm_r(KBufs k) {
+  __shared__ double sm[kKThreads / 32];
+  double acc[1] = {0.0};
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x)
+    acc[0] = fma(k.r[r], k.r[r], acc[0]);
+  block_reduce_vec<1>(acc, 1, sm, k.partial + (size_t)blockIdx.x * (kMaxRestart + 1));
+  if (last_block(k.ticket)) {
+    __shared__ double s_n2;
+    finish_sum(k, 1, &s_n2);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      KState* st = k.st;
+      const double beta = sqrt(s_n2);
+      st->beta = beta;
+      if (st->first) {
+        st->first = 0;
+        k.history[0] = beta;
+        st->target = fmax(st->rel_tol * beta, st->abs_tol);
+      }
+      st->converged = beta <= st->target ? 1 : 0;
+      // start of a cycle: g = (beta, 0, ...), j = 0 (krylov.cpp:55-58)
+      for (int i = 0; i <= k.mr; ++i) k.g[i] = 0.0;
+      k.g[0] = beta;
+      st->j = 0;
+      st->stop = 0;
+    }
+  }
+}
+
+// v_0 = r / beta ; u = v_0 / scale
+__global__ void k_cycle_start(KBufs k) {
+  const double beta = k.st->beta;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x) {
+    const double v = k.r[r] / beta;
+    k.V[r] = v;
+    k.ubuf[r] = v / k.scale[r];
+  }
+}
+
+// y = H^{-1} g (back substitution, krylov.cpp:103-109), single thread
+__global__ void k_solve_y(KBufs k) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  KState* st = k.st;
+  const int j = st->j;
+  const int mr = k.mr;
+  for (int i = j - 1; i >= 0; --i) {
+    double s = k.g[i];
+    for (int q = i + 1; q < j; ++q) s -= k.H[i * mr + q] * st->y[q];
+    st->y[i] = s / k.H[i * mr + i];
+  }
+}
+
+// x += Z y  (FGMRES: M(V y) = Z y for the fixed linear V-cycle)
+__global__ void k_update_x(KBufs k) {
+  const KState* st = k.st;
+  const int j = st->j;
+  __shared__ double ys[kMaxRestart];
+  if (threadIdx.x < j) ys[threadIdx.x] = st->y[threadIdx.x];
+  __syncthreads();
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int i = 0; i < j; ++i) s = fma(ys[i], k.Z[(size_t)i * k.n + r], s);
+    k.x[r] += s;
+  }
+}
+
+// Device-side continue flag for the conditional WHILE node of a cycle.
+__global__ void k_set_continue(const KState* st, cudaGraphConditionalHandle h, int mr) {
+  const int go = (!st->stop && st->j < mr && st->its < st->max_iters) ? 1 : 0;
+  cudaGraphSetConditional(h, go);
+}
+
+}  // namespace fsigpu

@@ -1,0 +1,208 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Sparse level kernels: CSR SpMV with fused epilogues (residual, masked
+// restriction, masked prolongation-add, row scaling), the FS combine
+// (additive Schwarz gather-reduce + cover average + lumped Jacobi +
+// Richardson update), the coarse explicit-inverse GEMV and the setup-time
+// Gauss-Jordan inverse.
+//
+// CSR (int32 row offsets / cols, fp64 values; proj/include/fsi/sparse.hpp:32-74)
+// is streamed with LPR lanes per row (vector CSR): values and column
+// indices through the read-only path, x gathered through L1/L2 (the level
+// vectors are <= 10 MB and stay L2-resident). Per-row sums reduce with a
+// fixed xor-shuffle tree, so results are deterministic run to run.
+#pragma once
+
+#include "common.cuh"
+
+namespace fsigpu {
+
+// Epilogues: out-of-line functors applied by lane 0 of each row.
+struct EpiPlain {  // y = A x                       (sparse.cpp:70-76)
+  double* y;
+  __device__ void operator()(int i, double s) const { y[i] = s; }
+};
+struct EpiResid {  // r = b - A x                   (gmg.cpp:205-206, precond.cpp:312-313)
+  const double* b;
+  double* r;
+  __device__ void operator()(int i, double s) const { r[i] = b[i] - s; }
+};
+struct EpiScaled {  // w = diag(s) A z              (driver.cpp:177-183,261-262)
+  const double* scale;
+  double* y;
+  __device__ void operator()(int i, double s) const { y[i] = scale[i] * s; }
+};
+struct EpiResidScaled {  // r = b - diag(s) A x     (krylov.cpp:31-32,116-117)
+  const double* b;
+  const double* scale;
+  double* r;
+  __device__ void operator()(int i, double s) const { r[i] = b[i] - scale[i] * s; }
+};
+struct EpiRestrict {  // rc = R r, rc[constrained_rows below] = 0 (gmg.cpp:208-212)
+  const unsigned char* mask;
+  double* y;
+  __device__ void operator()(int i, double s) const { y[i] = mask[i] ? 0.0 : s; }
+};
+struct EpiProlongAdd {  // x += P ec where !constrained_cols (gmg.cpp:233-236)
+  const unsigned char* mask;
+  double* x;
+  __device__ void operator()(int i, double s) const {
+    if (!mask[i]) x[i] = x[i] + s;
+  }
+};
+
+// x gather, optionally masked (ec[constrained_cols below] = 0, gmg.cpp:230-231)
+struct GatherPlain {
+  const double* x;
+  __device__ double operator()(int c) const { return __ldg(x + c); }
+};
+struct GatherMasked {
+  const double* x;
+  const unsigned char* mask;
+  __device__ double operator()(int c) const { return __ldg(mask + c) ? 0.0 : __ldg(x + c); }
+};
+
+template <int LPR, class Gather, class Epi>
+__global__ void __launch_bounds__(256) csr_kernel(int rows, const int* __restrict__ ptr,
+                                                  const int* __restrict__ idx,
+                                                  const double* __restrict__ val, Gather gx,
+                                                  Epi epi) {
+  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = (int)(gt / LPR);
+  const int lane = threadIdx.x & (LPR - 1);
+  if (row >= rows) return;  // whole row groups exit together (LPR divides 32)
+  const int k0 = __ldg(ptr + row), k1 = __ldg(ptr + row + 1);
+  double s = 0.0;
+#pragma unroll 4
+  for (int k = k0 + lane; k < k1; k += LPR) s = fma(__ldg(val + k), gx(__ldg(idx + k)), s);
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, LPR);
+  if (lane == 0) epi(row, s);
+}
+
+// FS combine on one level (precond.cpp:42-57 additive + 271-287 + 305-317):
+//   p <  g1, p >= g1+n_us : z = sum_{(b,i) covering p, block order} delta / cover
+//   g1 <= p < g1+n_us     : z = r[p] / lumped[p-g1]
+//   x[p] = (x_zero ? 0 : x[p]) + omega * z
+// Same rounded operations in the same order as the reference (bit-exact).
+__global__ void fs_combine_kernel(int n, int g1, int n_us, const int* __restrict__ inv_ptr,
+                                  const int* __restrict__ inv_idx, const double* __restrict__ delta,
+                                  const double* __restrict__ r, const double* __restrict__ lumped,
+                                  double omega, double* __restrict__ x, int x_zero) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  double z;
+  if (p >= g1 && p < g1 + n_us) {
+    z = r[p] / lumped[p - g1];
+  } else {
+    const int k0 = inv_ptr[p], k1 = inv_ptr[p + 1];
+    double s = 0.0;
+    for (int k = k0; k < k1; ++k) s = add_rn(s, delta[inv_idx[k]]);
+    z = (k1 - k0 > 1) ? s / (double)(k1 - k0) : s;
+  }
+  const double xo = x_zero ? 0.0 : x[p];
+  x[p] = add_rn(xo, mul_rn(omega, z));
+}
+
+// Coarse solve x0 (+)= Ainv' b0 with the explicit equilibrated inverse
+// (row-major n0 x n0), one warp per row.
+__global__ void __launch_bounds__(256) gemv_kernel(int n, const double* __restrict__ M,
+                                                   const double* __restrict__ b,
+                                                   double* __restrict__ x, int accumulate) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const double* Mr = M + (size_t)row * n;
+  double s = 0.0;
+#pragma unroll 4
+  for (int j = lane; j < n; j += 32) s = fma(__ldg(Mr + j), __ldg(b + j), s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  if (lane == 0) x[row] = accumulate ? x[row] + s : s;
+}
+
+// ---- setup: Gauss-Jordan inverse with partial pivoting on W = [A | I] ----
+// Step k, single CTA: pivot search in column k, row swap, pivot-row scaling,
+// and a copy of column k (the elimination factors) into f.
+__global__ void gj_pivot_kernel(int n, double* __restrict__ W, int k, double* __restrict__ f,
+                                int* __restrict__ fail) {
+  __shared__ double sb[32];
+  __shared__ int si[32];
+  __shared__ int s_p;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int ld = 2 * n;
+  double best = -1.0;
+  int bi = n;
+  for (int i = k + tid; i < n; i += blockDim.x) {
+    const double v = fabs(W[(size_t)i * ld + k]);
+    if (v > best) {
+      best = v;
+      bi = i;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(kFull, best, o);
+    const int oi = __shfl_xor_sync(kFull, bi, o);
+    if (ob > best || (ob == best && oi < bi)) {
+      best = ob;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    sb[warp] = best;
+    si[warp] = bi;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < nw; ++w)
+      if (sb[w] > best || (sb[w] == best && si[w] < bi)) {
+        best = sb[w];
+        bi = si[w];
+      }
+    if (!(best > 1e-14) || bi >= n) *fail = 1;  // equilibrated: entries <= 1
+    s_p = bi < n ? bi : k;
+  }
+  __syncthreads();
+  const int p = s_p;
+  if (p != k)
+    for (int j = tid; j < ld; j += blockDim.x) {
+      const double t = W[(size_t)k * ld + j];
+      W[(size_t)k * ld + j] = W[(size_t)p * ld + j];
+      W[(size_t)p * ld + j] = t;
+    }
+  __syncthreads();
+  const double inv = 1.0 / W[(size_t)k * ld + k];
+  __syncthreads();
+  for (int j = tid; j < ld; j += blockDim.x) W[(size_t)k * ld + j] *= inv;
+  for (int i = tid; i < n; i += blockDim.x) f[i] = (i == k) ? 0.0 : W[(size_t)i * ld + k];
+}
+
+__global__ void gj_eliminate_kernel(int n, double* __restrict__ W, int k,
+                                    const double* __restrict__ f) {
+  const int ld = 2 * n;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (j >= ld) return;
+  const double fi = f[i];
+  if (fi == 0.0) return;
+  W[(size_t)i * ld + j] -= fi * W[(size_t)k * ld + j];
+}
+
+// M[i][j] = cs_i * W[i][n+j] * rs_j  (A^{-1} = Dc Ahat^{-1} Dr)
+__global__ void gj_extract_kernel(int n, const double* __restrict__ W,
+                                  const double* __restrict__ rs, const double* __restrict__ cs,
+                                  double* __restrict__ M) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)n * n) return;
+  const int i = (int)(e / n), j = (int)(e % n);
+  M[e] = cs[i] * W[(size_t)i * 2 * n + n + j] * rs[j];
+}
+
+__global__ void gj_init_kernel(int n, double* __restrict__ W) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)n * n) return;
+  const int i = (int)(e / n), j = (int)(e % n);
+  W[(size_t)i * 2 * n + n + j] = (i == j) ? 1.0 : 0.0;
+}
+
+}  // namespace fsigpu
