@@ -1,0 +1,413 @@
+#!/usr/bin/env python3
+"""Benchmark: FGMRES-GMG(FS-AS) solve on one B200 (config 0 of BASELINE.json).
+
+A "step" is one complete FGMRES(30) solve, rtol 1e-10, of the config-0
+first-Newton FSI Jacobian (unit square 8->16->32, 19,972 dofs, J2 frame,
+additive FS V(1,1) smoother), from x0 = 0 with b resident in HBM.
+`value` = V-cycles/s over all ranks; solve time is reported beside it.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun): replicas only — every rank solves its own copy of the
+system; no data-path collective.  The reference arm
+runs the unmodified reference library (oracle/_ref/fsi_ref_harness, built
+from /root/reference sources) on the host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+METRIC = "FGMRES-GMG(FS-AS) solve time & V-cycles/s at 1 B200; AS/SpMV HBM GB/s vs roofline"
+DATA = os.path.join(ROOT, "data", "cfg0.fsix")
+HARNESS = os.path.join(ROOT, "oracle", "_ref", "fsi_ref_harness")
+WORKLOAD = ("config0: 2D FSI first-Newton Jacobian, unit square Q2/P1disc 8->16->32 (3 GMG levels), "
+            "19,972 dofs, FGMRES(30) rtol 1e-10, V(1,1) additive FS smoother omega=0.7")
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return ws, rank, local
+
+
+def reduce_max(v: float, ws: int) -> float:
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws: int):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ------------------------------------------------------------ reference arm
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return None
+    if not os.path.exists(HARNESS):
+        return {"impl": "reference", "unavailable": "oracle/_ref/fsi_ref_harness not built"}
+    # step = one GMRES restart cycle of the reference (30 Arnoldi steps + the
+    # restart's extra M apply = 31 V-cycles) on the same config-0 system:
+    # a bounded sample of the solve, so K steps fit in minutes on 1 core.
+    reps = args.warmup + args.steps
+    cmd = [HARNESS, "solve", "cfg0", "--mode", "add", "--reps", str(reps), "--max-iters", "30"]
+    t0 = time.time()
+    out = subprocess.run(cmd, capture_output=True, text=True, check=True).stdout
+    wall = time.time() - t0
+    d = json.loads(out.strip().splitlines()[-1])
+    solves = d["solves"][args.warmup:]
+    secs = sum(s["seconds"] for s in solves)
+    vcyc = sum(s["m_applies"] for s in solves)
+    value = vcyc / secs
+    sample = (f"{len(solves)} x (one GMRES(30) restart cycle = 30 Arnoldi steps + 1 restart M apply = "
+              f"{solves[0]['m_applies']} V-cycles) of the config-0 solve, reference library, additive FS")
+    return {
+        "metric": METRIC, "value": value, "unit": "V-cycles/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * secs / len(solves), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference-assembled rest-state Jacobian, seeded RHS)",
+        "config": {"workload": WORKLOAD, "parallelism": "replicas", "setup_s": d.get("setup_s")},
+        "cpu_baseline": {"value": value, "unit": "V-cycles/s", "cores": 1, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "V-cycles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_wall_s": wall,
+    }
+
+
+# ------------------------------------------------------------ our arm
+def cpu_baseline_port(P):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    t0 = time.time()
+    G = O.OracleGmg(P.levels)
+    setup = time.time() - t0
+    t0 = time.time()
+    r = G.gmres(P.frame_scale, P.b, restart=30, max_iters=2000, rel_tol=1e-10, abs_tol=1e-300)
+    secs = time.time() - t0
+    return {"value": r["m_applies"] / secs, "unit": "V-cycles/s", "cores": 1, "kind": "port",
+            "sample": f"one full config-0 solve by the C oracle (oracle/fsi_oracle.c, 1 thread): "
+                      f"{r['iterations']} its, {r['m_applies']} V-cycles in {secs:.2f} s (setup {setup:.2f} s)",
+            "solve_s": secs, "iterations": r["iterations"]}
+
+
+def as_microbench(fsigpu, torch, hbm_peak, n54=262144, n59=131072, solves=100):
+    """Config 1: 262,144 x m=54 + 131,072 x m=59 dense fp64 blocks; one batched
+    LU, then `solves` batched solves (bytes: SURVEY §8d)."""
+    t0 = time.time()
+    B = fsigpu.DenseBlocks.generate_dominant(n54, n59, 20240901)
+    gen_s = time.time() - t0
+    rows = B.total_rows
+    rhs = torch.empty(rows, dtype=torch.float64, device="cuda")
+    x = torch.empty_like(rhs)
+    B.generate_rhs(7, rhs.data_ptr())
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()  # explicit stream: the library launches on it
+    # LU (refactor from the retained matrices): 3 warm-up, then timed
+    for _ in range(2):
+        B.refactor(s.cuda_stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(s)
+    B.refactor(s.cuda_stream)
+    e1.record(s)
+    torch.cuda.synchronize()
+    lu_ms = e0.elapsed_time(e1)
+    for _ in range(3):
+        B.solve_dev(rhs.data_ptr(), x.data_ptr(), s.cuda_stream)
+    torch.cuda.synchronize()
+    e0.record(s)
+    for _ in range(solves):
+        B.solve_dev(rhs.data_ptr(), x.data_ptr(), s.cuda_stream)
+    e1.record(s)
+    torch.cuda.synchronize()
+    solve_ms = e0.elapsed_time(e1) / solves
+    fbytes = B.factor_bytes
+    solve_bytes = fbytes + rows * (4 + 8 + 8)
+    lu_bytes = 2 * fbytes + rows * 8
+    sizes = [54] * n54 + [59] * n59
+    lu_flops = n54 * 2.0 / 3.0 * 54 ** 3 + n59 * 2.0 / 3.0 * 59 ** 3
+    # parity spot check vs the oracle on sampled blocks
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    xh = x.cpu().numpy()
+    rh = rhs.cpu().numpy()
+    worst = 0.0
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    for b in [0, 1, n54 - 1, n54, n54 + n59 - 1, 12345, n54 + 777]:
+        m = sizes[b]
+        lu, piv = O.dense_factor(B.matrix(b, m))
+        xo = O.dense_solve(lu, piv, rh[offs[b]:offs[b + 1]])
+        worst = max(worst, float(np.linalg.norm(xh[offs[b]:offs[b + 1]] - xo) / np.linalg.norm(xo)))
+    del sizes
+    return {
+        "blocks": n54 + n59, "factor_GB": fbytes / 1e9, "gen_s": gen_s,
+        "lu_ms": lu_ms, "lu_GBps": lu_bytes / lu_ms / 1e6, "lu_TFLOPs": lu_flops / lu_ms / 1e9,
+        "solve_ms": solve_ms, "solve_GBps": solve_bytes / solve_ms / 1e6,
+        "solve_roofline_frac": solve_bytes / solve_ms / 1e6 / hbm_peak,
+        "lu_roofline_frac_hbm": lu_bytes / lu_ms / 1e6 / hbm_peak,
+        "parity_max_rel_err_sampled": worst, "solves": solves,
+    }
+
+
+def run_ours(args, ws, rank, local):
+    import torch
+    from paper_1909_13201_b200 import fsigpu
+    from paper_1909_13201_b200.problem import load_case
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    fsigpu.init(local)
+    hbm_peak, peak_kind = peaks()
+    if not os.path.exists(DATA):
+        raise SystemExit(f"{DATA} missing: run __graft_entry__.build() in the container with /root/reference")
+    P = load_case(DATA, "cfg0")
+    n = P.n
+    t0 = time.time()
+    G = fsigpu.GmgPreconditioner(P.levels)
+    S = fsigpu.GmresSolver(G, P.frame_scale, restart=30)
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+    cfg = fsigpu.KrylovConfig(restart=30, max_iters=2000, rel_tol=1e-10, abs_tol=1e-300)
+    lib_stream = torch.cuda.ExternalStream(G.stream())
+    b = torch.from_numpy(P.b).cuda()
+    x = torch.zeros(n, dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # 256 MB > 126 MB L2
+
+    def step():
+        x.zero_()
+        torch.cuda.synchronize()
+        return S.solve_dev(b.data_ptr(), x.data_ptr(), cfg)
+
+    for _ in range(max(args.warmup, 0)):
+        res = step()
+    # ---- timed region: device time per solve (CUDA events on the library stream)
+    per = []
+    its = []
+    vcycles = 0
+    barrier(ws)
+    torch.cuda.synchronize()
+    launches0 = fsigpu.launch_count()
+    with ClockSampler(local) as clk:
+        t_wall = time.time()
+        for _ in range(args.steps):
+            flush.fill_(1.0)  # evict L2 between timed solves
+            x.zero_()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(lib_stream)
+            res = S.solve_dev(b.data_ptr(), x.data_ptr(), cfg)
+            e1.record(lib_stream)
+            e1.synchronize()
+            per.append(e0.elapsed_time(e1))
+            its.append(res.iterations)
+            vcycles += res.m_applies
+        torch.cuda.synchronize()
+        t_wall = time.time() - t_wall
+    launches = fsigpu.launch_count() - launches0
+    barrier(ws)
+    ms_local = sum(per) / len(per)
+    ms = reduce_max(ms_local, ws)
+    vcyc_per_step = vcycles / args.steps
+    value = ws * vcyc_per_step / (ms / 1000.0)
+    relres = res.true_residual / float(np.linalg.norm(P.b))  # x0 = 0: r0 = b
+
+    # ---- e2e through the public host-pointer API (pinned host buffers)
+    bh = torch.from_numpy(P.b.copy()).pin_memory()
+    xh = torch.zeros(n, dtype=torch.float64).pin_memory()
+    e2e_ms = []
+    for k in range(args.steps + 1):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(lib_stream)
+        r2 = S_solve_host(fsigpu, S, bh, xh, cfg)
+        e1.record(lib_stream)
+        e1.synchronize()
+        if k:  # first call is a warm-up of the host path
+            e2e_ms.append(e0.elapsed_time(e1))
+    e2e_step = reduce_max(sum(e2e_ms) / len(e2e_ms), ws)
+    e2e_value = ws * r2.m_applies / (e2e_step / 1000.0)
+
+    # ---- roofline: instrumented solve (per-launch CUDA events, graphs off)
+    fsigpu.Profile.reset()
+    fsigpu.Profile.enable(True)
+    x.zero_()
+    torch.cuda.synchronize()
+    S.solve_dev(b.data_ptr(), x.data_ptr(), cfg)
+    prof = fsigpu.Profile.read()
+    fsigpu.Profile.enable(False)
+    tot_ms = sum(v["ms"] for v in prof.values())
+    dom = max(prof, key=lambda k: prof[k]["ms"])
+    per_launch_bytes = prof[dom]["bytes"] / max(prof[dom]["launches"], 1)
+    per_launch_ms = prof[dom]["ms"] / max(prof[dom]["launches"], 1)
+    achieved = per_launch_bytes / per_launch_ms / 1e6  # GB/s
+    traffic = None
+    ncu_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(ncu_path):
+        with open(ncu_path) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch", {}).get(dom)
+
+    out = {
+        "metric": METRIC, "value": value, "unit": "V-cycles/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference-assembled rest-state FSI Jacobian, seeded uniform RHS; fixtures from oracle/_ref)",
+        "config": {"workload": WORKLOAD, "n_dofs": n, "nnz_fine": P.levels[-1].A.nnz,
+                   "parallelism": "replicas" if ws > 1 else "single", "l2": "flushed (256 MB write) between timed solves",
+                   "restart": 30, "rel_tol": 1e-10, "cuda_graphs": "conditional WHILE per restart cycle"},
+        "solve_ms": ms, "iterations": int(statistics.median(its)), "v_cycles_per_solve": vcyc_per_step,
+        "final_relres": relres, "setup_s": setup_s, "wall_s_timed": t_wall,
+        "gpu_launches": launches,
+        "e2e": {"value": e2e_value, "unit": "V-cycles/s", "h2d_bytes_per_step": 8 * n,
+                "d2h_bytes_per_step": 8 * n + 8 * (r2.iterations + 1), "ms_per_step": e2e_step},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak,
+                     "traffic": traffic, "algorithmic_bytes_per_launch": per_launch_bytes,
+                     "avg_launch_us": per_launch_ms * 1000.0,
+                     "share_of_device_time": prof[dom]["ms"] / tot_ms if tot_ms else None,
+                     "note": "config-0 working set (~80 MB) is L2-resident within a solve"},
+        "kernel_breakdown": {k: {"ms": v["ms"], "launches": v["launches"],
+                                 "GBps": (v["bytes"] / v["ms"] / 1e6) if v["ms"] else None}
+                             for k, v in prof.items()},
+    }
+    out["clocks"] = clk.summary()
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline_port(P)
+    if rank == 0 and not args.no_microbench:
+        out["as_microbench"] = as_microbench(fsigpu, torch, hbm_peak)
+    return out
+
+
+def S_solve_host(fsigpu, S, bh, xh, cfg):
+    """fsigpu_gmres_solve with host (pinned) pointers: H2D of b, solve, D2H of x."""
+    import ctypes as C
+    res = fsigpu.GmresResultC()
+    hist = np.empty(cfg.max_iters + 2)
+    fsigpu._check(fsigpu.lib().fsigpu_gmres_solve(S.h, C.c_void_p(bh.data_ptr()), None, C.c_void_p(xh.data_ptr()),
+                                                  cfg.max_iters, cfg.rel_tol, cfg.abs_tol, hist.ctypes.data,
+                                                  C.byref(res)))
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-microbench", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    ws, rank, local = dist_setup()
+    if args.impl == "reference":
+        out = run_reference(args, ws, rank)
+    else:
+        out = run_ours(args, ws, rank, local)
+    if rank == 0 and out is not None:
+        print(json.dumps(out), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

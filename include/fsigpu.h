@@ -77,6 +77,8 @@ const char* fsigpu_last_error(void);
 int fsigpu_last_singular_block(void);
 int fsigpu_init(int device);
 int fsigpu_version(void);
+/* number of libfsigpu kernel launches issued so far (graph replays included) */
+long long fsigpu_launch_count(void);
 
 /* ---- CSR SpMV: SparseMatrix::multiply (sparse.cpp:70-76),
  *      CsrOperator::apply (krylov.cpp:16) -------------------------------- */
@@ -115,12 +117,21 @@ int fsigpu_blocks_refactor(fsigpu_blocks b, void* stream);
 int fsigpu_blocks_get_lu(fsigpu_blocks b, double* lu_rowmajor, int* piv);
 void fsigpu_blocks_destroy(fsigpu_blocks b);
 
+/* Block-solve mode of the FS smoothers of GMG hierarchies created after the
+ * call: 0 = LU forward/back substitution (tiled), 1 = explicit block inverse
+ * computed at setup from the same LU (default; one batched GEMV per sweep). */
+#define FSIGPU_MODE_LU 0
+#define FSIGPU_MODE_INVERSE 1
+int fsigpu_set_block_mode(int mode);
+
 /* ---- GMG with additive FS smoothers: GmgPreconditioner (gmg.cpp:178-246),
  *      FsPreconditioner (precond.cpp:119-303, additive per SURVEY §8c),
  *      richardson_smooth (precond.cpp:305-317) ---------------------------- */
 int fsigpu_gmg_create(int n_levels, const fsigpu_level_desc* levels, double omega, int pre,
                       int post, char cycle, fsigpu_gmg* out);
 int fsigpu_gmg_size(fsigpu_gmg g);
+/* the cudaStream_t every GMG / GMRES kernel of this handle is launched on */
+void* fsigpu_gmg_stream(fsigpu_gmg g);
 int fsigpu_gmg_apply(fsigpu_gmg g, const double* r, double* z);
 int fsigpu_gmg_apply_dev(fsigpu_gmg g, const double* d_r, double* d_z, void* stream);
 int fsigpu_fs_apply(fsigpu_gmg g, int level, const double* r, double* z);

@@ -27,7 +27,9 @@
 namespace fsigpu {
 
 // Work item of the batched solve kernel: either up to 8 small blocks
-// (m <= 64, one warp each) or one large block (whole 256-thread CTA).
+// (m <= 64, one warp each, factor streamed with LDG) or one large block
+// (whole 256-thread CTA, factor panels double-buffered in shared memory by
+// TMA bulk copies).
 struct SolveItem {
   int type;   // 0 small, 1 large
   int first;  // first block id
@@ -38,14 +40,57 @@ struct SolveItem {
 constexpr int kSolveThreads = 256;
 constexpr int kSmallMax = 64;
 constexpr int kLargeMax = 1024;
+constexpr int kTmaMax = 256;  // largest m whose panels are TMA-staged
+
+// ---- solve format -------------------------------------------------------
+// Per block, per 32-column panel p (k0 = 32p, kb = min(32, m-k0)):
+//   fwd chunk: Ltri  = strictly-lower part of inv(L_pp), column-packed (lte)
+//              Lpan  = L[k0+kb:m, k0:k0+kb], column-major, ld = hLe (even)
+//   bwd chunk: Utri  = upper part of inv(U_pp) incl. diagonal, column-packed (ute)
+//              Upan  = U[0:k0, k0:k0+kb], column-major, ld = k0
+// Each chunk is contiguous and a multiple of 16 bytes, so one
+// cp.async.bulk moves it. Bytes per block ~= 8 m^2 (the two triangular
+// tile inverses replace the diagonal tiles, so nothing is read twice).
+__host__ __device__ __forceinline__ int even_up(int x) { return (x + 1) & ~1; }
+
+struct PanelGeom {
+  int k0, kb, lt, lte, hL, hLe, ut, ute;
+  __host__ __device__ PanelGeom(int m, int p) {
+    k0 = 32 * p;
+    kb = m - k0 < 32 ? m - k0 : 32;
+    lt = kb * (kb - 1) / 2;
+    lte = even_up(lt);
+    hL = m - k0 - kb;
+    hLe = even_up(hL);
+    ut = kb * (kb + 1) / 2;
+    ute = even_up(ut);
+  }
+  __host__ __device__ long long fwd_size() const { return (long long)lte + (long long)hLe * kb; }
+  __host__ __device__ long long bwd_size() const { return (long long)ute + (long long)k0 * kb; }
+  __host__ __device__ long long size() const { return fwd_size() + bwd_size(); }
+};
+
+__host__ __device__ __forceinline__ long long panel_offset(int m, int p) {
+  long long o = 0;
+  for (int q = 0; q < p; ++q) o += PanelGeom(m, q).size();
+  return o;
+}
+__host__ __device__ __forceinline__ long long solve_format_size(int m) {
+  return panel_offset(m, (m + 31) / 32);
+}
+// column-packed strictly-lower triangle: column kk holds rows kk+1..kb-1
+__host__ __device__ __forceinline__ int ltri_col(int kb, int kk) { return kk * (kb - 1) - kk * (kk - 1) / 2; }
+// column-packed upper triangle incl. diagonal: column jj holds rows 0..jj
+__host__ __device__ __forceinline__ int utri_col(int jj) { return jj * (jj + 1) / 2; }
 
 struct SolveArgs {
   const int* m;
-  const long long* lu_off;
+  const long long* sf_off;
   const long long* row_off;
-  const double* lu;
+  const double* sf;
   const int* gsrc;
   const SolveItem* items;
+  int smem_cap;  // doubles per panel buffer (TMA path)
   // right-hand side source: x[s] = rhs(gsrc[s]); for group-2 positions
   // (p >= g1) the lumped-Jacobi update of precond.cpp:281-287 is applied
   // on the fly: rhs = r[p] - sum_k A_g2[p-g1, k] * (r[g1+k] / lumped[k])
@@ -56,6 +101,11 @@ struct SolveArgs {
   const int* aus_col;
   const double* aus_val;
   double* out;  // delta[row_off[b] + i], local order
+  // explicit-inverse mode
+  const int* lperm;         // pivoted row -> block-local row
+  double* inv;              // column-major inverses, ld = even_up(m)
+  const long long* inv_off;
+  const int* pos;           // block-local row -> rhs source position
 };
 
 __device__ __forceinline__ double gather_rhs(const SolveArgs& a, int p) {
@@ -72,7 +122,39 @@ __device__ __forceinline__ double gather_rhs(const SolveArgs& a, int p) {
   return v;
 }
 
-// Team barrier: one warp (NW==1) or the whole CTA.
+// ---- TMA bulk copy + mbarrier (sm_90+ PTX; SASS UBLKCP / SYNCS) ----------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 template <int NW>
 __device__ __forceinline__ void team_sync() {
   if constexpr (NW == 1)
@@ -81,106 +163,273 @@ __device__ __forceinline__ void team_sync() {
     __syncthreads();
 }
 
-// Solve one block with a team of NW warps; xs: shared scratch of m doubles.
-template <int NW>
-__device__ void solve_block(const SolveArgs& a, int b, double* xs, int t) {
-  constexpr int T = NW * 32;
-  const int m = a.m[b];
-  const long long ro = a.row_off[b];
-  const double* __restrict__ LU = a.lu + a.lu_off[b];
-  for (int s = t; s < m; s += T) xs[s] = gather_rhs(a, __ldg(a.gsrc + ro + s));
-  team_sync<NW>();
-
-  // forward: unit lower, column tiles of 32 (bit-identical order)
-  for (int k0 = 0; k0 < m; k0 += 32) {
-    const int kb = min(32, m - k0);
-    if (t < 32) {
-      const int lane = t;
-      double v = lane < kb ? xs[k0 + lane] : 0.0;
-      double Lr[32];
-#pragma unroll
-      for (int kk = 0; kk < 32; ++kk)
-        Lr[kk] = (kk < lane && lane < kb) ? __ldg(LU + (size_t)(k0 + kk) * m + k0 + lane) : 0.0;
-#pragma unroll
-      for (int kk = 0; kk < 32; ++kk) {
-        if (kk < kb) {
-          const double xk = __shfl_sync(kFull, v, kk);
-          if (lane > kk && lane < kb) v = sub_rn(v, mul_rn(Lr[kk], xk));
-        }
-      }
-      if (lane < kb) xs[k0 + lane] = v;
-    }
-    team_sync<NW>();
-    for (int i = k0 + kb + t; i < m; i += T) {
-      double acc = xs[i];
-      const double* col = LU + (size_t)k0 * m + i;
-#pragma unroll 8
-      for (int kk = 0; kk < kb; ++kk) acc = sub_rn(acc, mul_rn(__ldg(col + (size_t)kk * m), xs[k0 + kk]));
-      xs[i] = acc;
-    }
-    team_sync<NW>();
-  }
-
-  // backward: upper with diagonal, column tiles from the bottom
-  for (int k1 = ((m - 1) / 32) * 32; k1 >= 0; k1 -= 32) {
-    const int kb = min(32, m - k1);
-    if (t < 32) {
-      const int lane = t;
-      double v = lane < kb ? xs[k1 + lane] : 0.0;
-      const double d = lane < kb ? __ldg(LU + (size_t)(k1 + lane) * m + k1 + lane) : 1.0;
-      double Ur[32];
-#pragma unroll
-      for (int jj = 0; jj < 32; ++jj)
-        Ur[jj] = (jj > lane && jj < kb) ? __ldg(LU + (size_t)(k1 + jj) * m + k1 + lane) : 0.0;
-#pragma unroll
-      for (int jj = 31; jj >= 0; --jj) {
-        if (jj < kb) {
-          if (lane == jj) v = v / d;
-          const double xj = __shfl_sync(kFull, v, jj);
-          if (lane < jj) v = sub_rn(v, mul_rn(Ur[jj], xj));
-        }
-      }
-      if (lane < kb) xs[k1 + lane] = v;
-    }
-    team_sync<NW>();
-    for (int i = t; i < k1; i += T) {
-      double acc = xs[i];
-      const double* col = LU + (size_t)k1 * m + i;
-#pragma unroll 8
-      for (int jj = 0; jj < kb; ++jj) acc = sub_rn(acc, mul_rn(__ldg(col + (size_t)jj * m), xs[k1 + jj]));
-      xs[i] = acc;
-    }
-    team_sync<NW>();
-  }
-  for (int i = t; i < m; i += T) a.out[ro + i] = xs[i];
+// Issue the q-th chunk load (q < P: forward chunk of panel q, else backward
+// chunk of panel 2P-1-q) into buffer q&1.
+__device__ __forceinline__ void issue_chunk(const double* blk, int m, int P, int q, double* buf, int cap,
+                                           unsigned long long* bars) {
+  const bool fwd = q < P;
+  const int p = fwd ? q : 2 * P - 1 - q;
+  const PanelGeom g(m, p);
+  const long long off = panel_offset(m, p) + (fwd ? 0 : g.fwd_size());
+  const unsigned bytes = (unsigned)(8 * (fwd ? g.fwd_size() : g.bwd_size()));
+  double* dst = buf + (size_t)(q & 1) * cap;
+  mbar_arrive_expect_tx(&bars[q & 1], bytes);
+  if (bytes) tma_bulk_g2s(dst, blk + off, bytes, &bars[q & 1]);
 }
 
+// Solve one block with a team of NW warps (NW == 1: warp path, factor read
+// with LDG; NW > 1 with TMA: panel chunks staged through `buf`).
+// xs: shared scratch of m doubles (the pivoted, then solved, vector).
+template <int NW, bool TMA>
+__device__ void solve_block(const SolveArgs& a, int b, double* xs, double* buf, unsigned long long* bars, int t,
+                            int ucol = -1) {
+  constexpr int T = NW * 32;
+  const int m = a.m[b];
+  const int P = (m + 31) / 32;
+  const long long ro = a.row_off[b];
+  const double* __restrict__ blk = a.sf + a.sf_off[b];
+  if constexpr (TMA) {
+    if (t == 0) {
+      issue_chunk(blk, m, P, 0, buf, a.smem_cap, bars);
+      if (2 * P > 1) issue_chunk(blk, m, P, 1, buf, a.smem_cap, bars);
+    }
+  }
+  if (ucol < 0) {
+    for (int s = t; s < m; s += T) xs[s] = gather_rhs(a, __ldg(a.gsrc + ro + s));
+  } else {  // e_ucol (block-local order) through the pivots: inverse columns
+    for (int s = t; s < m; s += T) xs[s] = (__ldg(a.lperm + ro + s) == ucol) ? 1.0 : 0.0;
+  }
+  team_sync<NW>();
+
+  // rows of the diagonal tile handled as (row, sub) pairs
+  constexpr int DS = (NW == 1) ? 1 : 8;  // threads per diagonal row
+  for (int q = 0; q < 2 * P; ++q) {
+    const bool fwd = q < P;
+    const int p = fwd ? q : 2 * P - 1 - q;
+    const PanelGeom g(m, p);
+    const double* src;
+    if constexpr (TMA) {
+      mbar_wait(&bars[q & 1], (q >> 1) & 1);
+      src = buf + (size_t)(q & 1) * a.smem_cap;
+    } else {
+      src = blk + panel_offset(m, p) + (fwd ? 0 : g.fwd_size());
+    }
+    const int k0 = g.k0, kb = g.kb;
+    // --- diagonal tile: x_p <- inv(L_pp) x_p  or  inv(U_pp) x_p
+    double y = 0.0;
+    const int i = t / DS, sub = t % DS;
+    if (i < 32) {
+      double s = 0.0;
+      constexpr int U = 32 / DS;  // whole row in one predicated batch
+      double v[U];
+      if (fwd) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int kk = sub + u * DS;
+          v[u] = (kk < kb && kk < i && i < kb) ? src[ltri_col(kb, kk) + i - kk - 1] : 0.0;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int jj = sub + u * DS;
+          v[u] = (jj < kb && jj >= i && i < kb) ? src[utri_col(jj) + i] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int kk = sub + u * DS;
+        s = fma(v[u], kk < kb ? xs[k0 + kk] : 0.0, s);
+      }
+      if constexpr (DS > 1) {
+#pragma unroll
+        for (int o = DS / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, DS);
+      }
+      if (i < kb) y = fwd ? xs[k0 + i] + s : s;
+    }
+    team_sync<NW>();
+    if (i < kb && sub == 0) xs[k0 + i] = y;
+    team_sync<NW>();
+    // --- off-diagonal panel: rows below (fwd) or above (bwd)
+    const int h = fwd ? g.hL : k0;
+    const int ld = fwd ? g.hLe : k0;
+    const double* pan = fwd ? src + g.lte : src + g.ute;
+    const int rbase = fwd ? k0 + kb : 0;
+    if (h > 0) {
+      const int tpr = (NW == 1) ? 1 : (h <= 32 ? 8 : h <= 64 ? 4 : h <= 128 ? 2 : 1);
+      const int rows_per_pass = T / tpr;
+      for (int r0 = 0; r0 < h; r0 += rows_per_pass) {
+        const int r = r0 + t / tpr, sb = t % tpr;
+        double s = 0.0;
+        if (r < h) {
+          constexpr int U = 8;
+          for (int kq = sb; kq < kb; kq += U * tpr) {
+            double v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int kk = kq + u * tpr;
+              v[u] = kk < kb ? pan[(size_t)kk * ld + r] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int kk = kq + u * tpr;
+              s = fma(v[u], kk < kb ? xs[k0 + kk] : 0.0, s);
+            }
+          }
+        }
+        if (tpr > 1) {
+          for (int o = tpr / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, tpr);
+        }
+        if (r < h && sb == 0) xs[rbase + r] -= s;
+      }
+    }
+    team_sync<NW>();
+    if constexpr (TMA) {
+      if (t == 0 && q + 2 < 2 * P) {
+        fence_proxy_async();
+        issue_chunk(blk, m, P, q + 2, buf, a.smem_cap, bars);
+      }
+    }
+  }
+  if (ucol < 0) {
+    for (int k = t; k < m; k += T) a.out[ro + k] = xs[k];
+  } else {  // column ucol of inv(A_b), column-major with even leading dimension
+    const int ld = even_up(m);
+    double* col = a.inv + a.inv_off[b] + (size_t)ucol * ld;
+    for (int k = t; k < ld; k += T) col[k] = k < m ? xs[k] : 0.0;
+  }
+}
+
+// Items: type 0 = up to 8 small blocks (warp each); type 1 = one large
+// block; type 2 = (block first, columns pad..pad+count-1) of a small block,
+// one column per warp; type 3 = (block first, column pad) of a large block.
+// Types 2/3 compute inverse columns (setup of the explicit-inverse mode).
 __global__ void __launch_bounds__(kSolveThreads) block_solve_kernel(SolveArgs a) {
+  extern __shared__ __align__(16) double dsm[];
   __shared__ double xs[kLargeMax];
+  __shared__ unsigned long long bars[2];
   const SolveItem it = a.items[blockIdx.x];
   const int tid = threadIdx.x;
-  if (it.type == 0) {
+  if (it.type == 0 || it.type == 2) {
     const int w = tid >> 5;
-    if (w < it.count) solve_block<1>(a, it.first + w, xs + w * kSmallMax, tid & 31);
+    if (w < it.count) {
+      if (it.type == 0)
+        solve_block<1, false>(a, it.first + w, xs + w * kSmallMax, nullptr, nullptr, tid & 31);
+      else
+        solve_block<1, false>(a, it.first, xs + w * kSmallMax, nullptr, nullptr, tid & 31, it.pad + w);
+    }
+  } else if (it.type == 3) {
+    solve_block<kSolveThreads / 32, false>(a, it.first, xs, nullptr, nullptr, tid, it.pad);
   } else {
-    solve_block<kSolveThreads / 32>(a, it.first, xs, tid);
+    const int m = a.m[it.first];
+    if (m <= kTmaMax && a.smem_cap > 0) {
+      if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        mbar_fence_init();
+      }
+      __syncthreads();
+      solve_block<kSolveThreads / 32, true>(a, it.first, xs, dsm, bars, tid);
+    } else {
+      solve_block<kSolveThreads / 32, false>(a, it.first, xs, nullptr, nullptr, tid);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- inverse mode
+// delta_b = inv(A_b) * rhs_b  (rhs gathered in block-local order). inv(A_b)
+// is column-major with even leading dimension ld. Small blocks (m <= 64):
+// one warp per block, a lane owns a row pair. Large blocks: one CTA per
+// 64-row tile; thread (rp, cg) owns row pair rp of the tile and columns
+// j = cg (mod 8); the 8 column-group partial sums are added in a fixed
+// order (deterministic). Loads are issued in predicated batches of 8
+// 16-byte vectors per thread.
+constexpr int kInvTileRows = 64;
+
+__device__ __forceinline__ void inv_rowpair_dot(const double2* __restrict__ M, int RP, int rp, int m, int cg,
+                                                int CG, const double* xs, double& s0, double& s1) {
+  constexpr int U = 8;
+  for (int jb = cg; jb < m; jb += U * CG) {
+    double2 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = jb + u * CG;
+      v[u] = j < m ? __ldg(M + (size_t)j * RP + rp) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = jb + u * CG;
+      const double xj = j < m ? xs[j] : 0.0;
+      s0 = fma(v[u].x, xj, s0);
+      s1 = fma(v[u].y, xj, s1);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kSolveThreads) inv_gemv_kernel(SolveArgs a) {
+  __shared__ double xs[kLargeMax];
+  __shared__ double red[8][kInvTileRows];
+  const SolveItem it = a.items[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (it.type == 0) {  // small blocks: warp per block
+    if (w >= it.count) return;
+    const int b = it.first + w;
+    const int m = a.m[b];
+    const int RP = even_up(m) / 2;
+    const long long ro = a.row_off[b];
+    double* x = xs + w * kSmallMax;
+    for (int s = lane; s < m; s += 32) x[s] = gather_rhs(a, a.pos ? __ldg(a.pos + ro + s) : (int)(ro + s));
+    __syncwarp();
+    double s0 = 0.0, s1 = 0.0;
+    if (lane < RP)
+      inv_rowpair_dot(reinterpret_cast<const double2*>(a.inv + a.inv_off[b]), RP, lane, m, 0, 1, x, s0, s1);
+    if (2 * lane < m) a.out[ro + 2 * lane] = s0;
+    if (2 * lane + 1 < m) a.out[ro + 2 * lane + 1] = s1;
+    return;
+  }
+  // large block tile: rows [row0, row0 + 64)
+  const int b = it.first;
+  const int row0 = it.pad;
+  const int m = a.m[b];
+  const int RP = even_up(m) / 2;
+  const long long ro = a.row_off[b];
+  for (int s = tid; s < m; s += kSolveThreads) xs[s] = gather_rhs(a, a.pos ? __ldg(a.pos + ro + s) : (int)(ro + s));
+  __syncthreads();
+  const int rp = row0 / 2 + lane;
+  double s0 = 0.0, s1 = 0.0;
+  if (rp < RP)
+    inv_rowpair_dot(reinterpret_cast<const double2*>(a.inv + a.inv_off[b]), RP, rp, m, w, 8, xs, s0, s1);
+  red[w][2 * lane] = s0;
+  red[w][2 * lane + 1] = s1;
+  __syncthreads();
+  if (tid < kInvTileRows) {
+    const int i = row0 + tid;
+    if (i < m) {
+      double z = 0.0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) z += red[c][tid];
+      a.out[ro + i] = z;
+    }
   }
 }
 
 // ---------------------------------------------------------------- LU
 
-// Factor one block per CTA. src/dst column-major (may alias). SMEM: the
-// block is staged in dynamic shared memory (m <= 164 at 227 KB); otherwise
-// it is factored in place in global memory (dst).
+// Factor one block per CTA (DenseFactorization ctor, dense.cpp:31-67), then
+// write the solve format (tile inverses + packed panels, see PanelGeom).
+// src: column-major input (same offsets as lu_off). SMEM: the block is
+// staged in dynamic shared memory (m <= 164 fits 227 KB); otherwise it is
+// factored in `work` (global, column-major, may alias src).
+// lu_out (optional) receives the bit-exact LU in column-major order.
+// dynamic smem (doubles): [A: m*m, SMEM only][rowmax: m][perm: m ints][scratch: 32*32]
 template <int NT, bool SMEM>
 __global__ void __launch_bounds__(NT)
     lu_factor_kernel(const int* __restrict__ blist, const int* __restrict__ msz,
                      const long long* __restrict__ lu_off, const long long* __restrict__ row_off,
-                     const double* __restrict__ src, double* __restrict__ dst,
-                     int* __restrict__ piv_out, int* __restrict__ gsrc_out,
+                     const long long* __restrict__ sf_off, const double* __restrict__ src,
+                     double* __restrict__ work, double* __restrict__ lu_out, double* __restrict__ sf_out,
+                     int* __restrict__ piv_out, int* __restrict__ gsrc_out, int* __restrict__ lperm_out,
                      const int* __restrict__ src_pos, int pos_base, int* __restrict__ fail) {
-  // dynamic smem: [A: m*m doubles, SMEM only][rowmax: m doubles][perm: m ints]
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) double smem[];
   constexpr int NW = NT / 32;
   __shared__ int s_p, s_fail;
   __shared__ double s_inv;
@@ -188,12 +437,12 @@ __global__ void __launch_bounds__(NT)
   const int m = msz[b];
   const long long off = lu_off[b];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* A = SMEM ? smem : dst + off;
-  double* rowmax = SMEM ? smem + (size_t)m * m : smem;
+  const size_t a_sz = SMEM ? (size_t)m * m : 0;
+  double* A = SMEM ? smem : work + off;
+  double* rowmax = smem + a_sz;
   int* perm = reinterpret_cast<int*>(rowmax + m);
-  if (SMEM) {
-    for (long long e = tid; e < (long long)m * m; e += NT) A[e] = src[off + e];
-  } else if (src != dst) {
+  double* S = rowmax + m + (m + 1) / 2;
+  if (SMEM || src != work) {
     for (long long e = tid; e < (long long)m * m; e += NT) A[e] = src[off + e];
   }
   __syncthreads();
@@ -207,6 +456,7 @@ __global__ void __launch_bounds__(NT)
   double inv_prev = 0.0;
   for (int k = 0; k < m; ++k) {
     if (warp == 0) {
+      // multipliers of column k-1 (l = a_ik * inv, dense.cpp:58-61)
       if (k > 0)
         for (int i = k + lane; i < m; i += 32) A[(size_t)(k - 1) * m + i] = mul_rn(A[(size_t)(k - 1) * m + i], inv_prev);
       double best = -1.0;
@@ -229,8 +479,7 @@ __global__ void __launch_bounds__(NT)
         }
       }
       if (lane == 0) {
-        // sequential scan starts with best = |a_kk| (dense.cpp:42-49); a NaN
-        // column keeps p = k
+        // the sequential scan starts from best = |a_kk| (dense.cpp:42-49)
         int p = (bi < m) ? bi : k;
         if (!(fabs(A[(size_t)k * m + k]) < best)) p = k;
         const double pivot = A[(size_t)k * m + p];
@@ -254,7 +503,7 @@ __global__ void __launch_bounds__(NT)
         rowmax[p] = t1;
       }
     }
-    if (tid == 0) perm[k] = p;  // LAPACK-style pivot for now
+    if (tid == 0) perm[k] = p;
     __syncthreads();
     const double inv = s_inv;
     inv_prev = inv;
@@ -272,11 +521,11 @@ __global__ void __launch_bounds__(NT)
     return;
   }
   __syncthreads();
+  const long long ro = row_off[b];
   if (tid == 0) {
-    const long long ro = row_off[b];
     for (int k = 0; k < m; ++k) piv_out[ro + k] = perm[k];
-    // compose the sequential swaps into a gather map
-    for (int k = 0; k < m; ++k) rowmax[k] = (double)k;  // reuse as id array
+    // compose the sequential swaps (dense.cpp:74-75) into one gather map
+    for (int k = 0; k < m; ++k) rowmax[k] = (double)k;
     for (int k = 0; k < m; ++k) {
       const int p = perm[k];
       const double t2 = rowmax[k];
@@ -285,13 +534,57 @@ __global__ void __launch_bounds__(NT)
     }
   }
   __syncthreads();
-  const long long ro = row_off[b];
-  for (int s = tid; s < m; s += NT) {
-    const int loc = (int)rowmax[s];
-    gsrc_out[ro + s] = src_pos ? src_pos[ro + loc] + pos_base : (int)(ro + loc);
+  for (int s2 = tid; s2 < m; s2 += NT) {
+    const int loc = (int)rowmax[s2];
+    gsrc_out[ro + s2] = src_pos ? src_pos[ro + loc] + pos_base : (int)(ro + loc);
+    lperm_out[ro + s2] = loc;
   }
-  if (SMEM)
-    for (long long e = tid; e < (long long)m * m; e += NT) dst[off + e] = A[e];
+  if (lu_out && (SMEM || lu_out != work))
+    for (long long e = tid; e < (long long)m * m; e += NT) lu_out[off + e] = A[e];
+
+  // ---- solve format: tile inverses + packed panels
+  double* dst = sf_out + sf_off[b];
+  const int P = (m + 31) / 32;
+  long long po = 0;
+  for (int p = 0; p < P; ++p) {
+    const PanelGeom g(m, p);
+    const int k0 = g.k0, kb = g.kb;
+    if (tid < kb) {
+      const int c = tid;
+      for (int i = c + 1; i < kb; ++i) {  // inv(L_pp)[i][c], unit lower
+        double s = A[(size_t)(k0 + c) * m + k0 + i];
+        for (int k = c + 1; k < i; ++k) s += A[(size_t)(k0 + k) * m + k0 + i] * S[c * 32 + k];
+        S[c * 32 + i] = -s;
+      }
+      S[c * 32 + c] = 1.0 / A[(size_t)(k0 + c) * m + k0 + c];  // inv(U_pp)[i][c], i <= c
+      for (int i = c - 1; i >= 0; --i) {
+        double s = 0.0;
+        for (int k = i + 1; k <= c; ++k) s += A[(size_t)(k0 + k) * m + k0 + i] * S[c * 32 + k];
+        S[c * 32 + i] = -s / A[(size_t)(k0 + i) * m + k0 + i];
+      }
+    }
+    __syncthreads();
+    double* fw = dst + po;
+    for (int kk = 0; kk < kb; ++kk)
+      for (int i = kk + 1 + tid; i < kb; i += NT) fw[ltri_col(kb, kk) + i - kk - 1] = S[kk * 32 + i];
+    if (tid == 0 && g.lte > g.lt) fw[g.lt] = 0.0;
+    double* lp = fw + g.lte;
+    for (int e = tid; e < g.hLe * kb; e += NT) {
+      const int kk = e / g.hLe, r = e % g.hLe;
+      lp[e] = r < g.hL ? A[(size_t)(k0 + kk) * m + k0 + kb + r] : 0.0;
+    }
+    double* bw = fw + g.fwd_size();
+    for (int jj = 0; jj < kb; ++jj)
+      for (int i = tid; i <= jj; i += NT) bw[utri_col(jj) + i] = S[jj * 32 + i];
+    if (tid == 0 && g.ute > g.ut) bw[g.ut] = 0.0;
+    double* up = bw + g.ute;
+    for (int e = tid; e < k0 * kb; e += NT) {
+      const int jj = e / k0, r = e % k0;
+      up[e] = A[(size_t)(k0 + jj) * m + r];
+    }
+    po += g.size();
+    __syncthreads();
+  }
 }
 
 // Principal block A[dofs, dofs] of a CSR matrix into column-major dense

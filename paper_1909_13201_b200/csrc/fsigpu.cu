@@ -88,6 +88,11 @@ struct ProfScope {
   }
 };
 
+// Host-side count of our kernel launches (graph replays are added from the
+// per-graph counts taken at capture time).
+static long long g_launches = 0;
+static inline void counted(int k = 1) { g_launches += k; }
+
 // ------------------------------------------------------------ CSR
 struct Csr {
   int rows = 0, cols = 0;
@@ -112,7 +117,8 @@ struct Csr {
     idx.upload(ix, (size_t)nnz, s);
     val.upload(v, (size_t)nnz, s);
     const double avg = r ? (double)nnz / r : 0.0;
-    lpr = avg <= 3 ? 2 : avg <= 6 ? 4 : avg <= 12 ? 8 : avg <= 40 ? 16 : 32;
+    // ~4 entries per lane per row: one predicated batch (csr_kernel U = 4)
+    lpr = avg <= 6 ? 2 : avg <= 12 ? 4 : avg <= 24 ? 8 : avg <= 72 ? 16 : 32;
     if (keep_host) {
       h_ptr.assign(p, p + r + 1);
       h_idx.assign(ix, ix + nnz);
@@ -136,50 +142,76 @@ struct Csr {
       default: csr_kernel<32><<<grid, 256, 0, s>>>(rows, ptr.p, idx.p, val.p, g, e); break;
     }
     FSI_CHECK_LAUNCH();
+    counted();
   }
 };
 
 // ------------------------------------------------------------ dense blocks
 // Batched DenseFactorization: one LU per block, column-major.
+// Block solve modes: LU forward/back substitution (tiled, tile inverses) or
+// explicit block inverse (computed at setup from the bit-exact LU).
+enum BlockMode { kModeLU = 0, kModeInverse = 1 };
+static int g_default_mode = kModeInverse;
+
 struct Blocks {
+  int mode = kModeLU;
   long long nb = 0;
   long long total_rows = 0;
   int max_m = 0;
+  bool keep_lu = false;
   std::vector<int> h_m;
-  std::vector<long long> h_lu_off, h_row_off;
+  std::vector<long long> h_lu_off, h_row_off, h_sf_off;
   DevBuf<int> m;
-  DevBuf<long long> lu_off, row_off;
-  DevBuf<double> lu, orig;
-  DevBuf<int> gsrc, piv, pos;
-  DevBuf<SolveItem> items;
+  DevBuf<long long> lu_off, row_off, sf_off;
+  DevBuf<double> lu, orig, sf;
+  DevBuf<int> gsrc, piv, pos, lperm;
+  DevBuf<double> inv;
+  DevBuf<long long> inv_off;
+  std::vector<long long> h_inv_off;
+  DevBuf<SolveItem> items, inv_items;
+  int n_inv_items = 0;
   int n_items = 0;
+  int smem_cap = 0;        // doubles per TMA panel buffer
   double solve_bytes = 0;  // algorithmic bytes of one batched solve
   double factor_flops = 0;
 
-  void layout(const std::vector<int>& sizes, cudaStream_t s) {
+  void layout(const std::vector<int>& sizes, cudaStream_t s, bool keep = false) {
     nb = (long long)sizes.size();
+    keep_lu = keep;
     h_m = sizes;
     h_lu_off.assign(nb + 1, 0);
     h_row_off.assign(nb + 1, 0);
+    h_sf_off.assign(nb + 1, 0);
     max_m = 0;
     solve_bytes = 0;
     factor_flops = 0;
+    smem_cap = 0;
     for (long long b = 0; b < nb; ++b) {
       const long long mm = sizes[b];
       require(mm >= 1 && mm <= kLargeMax, "blocks: block size must be in [1, 1024]");
       h_lu_off[b + 1] = h_lu_off[b] + mm * mm;
       h_row_off[b + 1] = h_row_off[b] + mm;
+      h_sf_off[b + 1] = h_sf_off[b] + even_up((int)solve_format_size((int)mm));
       max_m = std::max<int>(max_m, (int)mm);
-      solve_bytes += 8.0 * mm * mm + 4.0 * mm + 8.0 * mm + 8.0 * mm;
+      solve_bytes += 8.0 * solve_format_size((int)mm) + 4.0 * mm + 8.0 * mm + 8.0 * mm;
       factor_flops += 2.0 / 3.0 * mm * mm * mm;
+      if (mm > kSmallMax && mm <= kTmaMax)
+        for (int p = 0; p < (mm + 31) / 32; ++p) {
+          const PanelGeom g((int)mm, p);
+          smem_cap = std::max<int>(smem_cap, (int)std::max(g.fwd_size(), g.bwd_size()));
+        }
     }
+    smem_cap = even_up(smem_cap);
     total_rows = h_row_off[nb];
     m.upload(h_m, s);
     lu_off.upload(h_lu_off, s);
     row_off.upload(h_row_off, s);
-    lu.alloc((size_t)h_lu_off[nb]);
+    sf_off.upload(h_sf_off, s);
+    if (keep_lu || max_m > 164) lu.alloc((size_t)h_lu_off[nb]);
+    sf.alloc((size_t)std::max<long long>(h_sf_off[nb], 2));
     gsrc.alloc((size_t)total_rows);
     piv.alloc((size_t)total_rows);
+    lperm.alloc((size_t)total_rows);
     // solve work items: small blocks 8 per CTA (warp each), large 1 per CTA
     std::vector<SolveItem> it;
     long long b = 0;
@@ -199,9 +231,13 @@ struct Blocks {
     require(nb < INT_MAX && total_rows < INT_MAX, "blocks: too many blocks/rows for int32 maps");
     n_items = (int)it.size();
     items.upload(it, s);
+    if (smem_cap > 0) {
+      const int bytes = 2 * smem_cap * 8;
+      FSI_CUDA(cudaFuncSetAttribute(block_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    }
   }
 
-  // LU of every block from src (column-major, same offsets) into lu.
+  // LU of every block from src (column-major, lu_off offsets).
   void factor(const double* src, const int* src_pos, int pos_base, cudaStream_t s) {
     DevBuf<int> fail(1);
     const int big = INT_MAX;
@@ -221,25 +257,33 @@ struct Blocks {
         mx_g = std::max(mx_g, mm);
       }
     }
+    double* luo = keep_lu ? lu.p : nullptr;
+    auto smem_bytes = [](int mx, bool staged) {
+      return (size_t)((staged ? (size_t)mx * mx : 0) + mx + (mx + 1) / 2 + 1024) * 8;
+    };
     auto run = [&](std::vector<int>& cls, int mx, int which) {
       if (cls.empty()) return;
       DevBuf<int> bl;
       bl.upload(cls, s);
       const int grid = (int)cls.size();
       if (which == 0) {
-        const size_t sm = (size_t)mx * mx * 8 + (size_t)mx * 12;
+        const size_t sm = smem_bytes(mx, true);
         auto k = lu_factor_kernel<128, true>;
         FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        k<<<grid, 128, sm, s>>>(bl.p, m.p, lu_off.p, row_off.p, src, lu.p, piv.p, gsrc.p, src_pos, pos_base, fail.p);
+        k<<<grid, 128, sm, s>>>(bl.p, m.p, lu_off.p, row_off.p, sf_off.p, src, nullptr, luo, sf.p, piv.p, gsrc.p,
+                                lperm.p, src_pos, pos_base, fail.p);
       } else if (which == 1) {
-        const size_t sm = (size_t)mx * mx * 8 + (size_t)mx * 12;
+        const size_t sm = smem_bytes(mx, true);
         auto k = lu_factor_kernel<256, true>;
         FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        k<<<grid, 256, sm, s>>>(bl.p, m.p, lu_off.p, row_off.p, src, lu.p, piv.p, gsrc.p, src_pos, pos_base, fail.p);
+        k<<<grid, 256, sm, s>>>(bl.p, m.p, lu_off.p, row_off.p, sf_off.p, src, nullptr, luo, sf.p, piv.p, gsrc.p,
+                                lperm.p, src_pos, pos_base, fail.p);
       } else {
-        const size_t sm = (size_t)mx * 12;
+        const size_t sm = smem_bytes(mx, false);
         auto k = lu_factor_kernel<256, false>;
-        k<<<grid, 256, sm, s>>>(bl.p, m.p, lu_off.p, row_off.p, src, lu.p, piv.p, gsrc.p, src_pos, pos_base, fail.p);
+        FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k<<<grid, 256, sm, s>>>(bl.p, m.p, lu_off.p, row_off.p, sf_off.p, src, lu.p, lu.p, sf.p, piv.p, gsrc.p,
+                                lperm.p, src_pos, pos_base, fail.p);
       }
       FSI_CHECK_LAUNCH();
       FSI_CUDA(cudaStreamSynchronize(s));  // keep `bl` alive until done
@@ -254,20 +298,81 @@ struct Blocks {
       g_bad_block = bad;
       throw Error(FSIGPU_ERR_SINGULAR, "singular block: " + std::to_string(bad));
     }
+    if (mode == kModeInverse) build_inverse(s);
+  }
+
+  // Explicit inverses: column c of inv(A_b) = LU solve with e_c, batched
+  // over all (block, column) pairs with the same solve kernel.
+  void build_inverse(cudaStream_t s) {
+    h_inv_off.assign(nb + 1, 0);
+    solve_bytes = 0;
+    std::vector<SolveItem> it;
+    for (long long b = 0; b < nb; ++b) {
+      const int mm = h_m[b];
+      h_inv_off[b + 1] = h_inv_off[b] + (long long)even_up(mm) * mm;
+      solve_bytes += 8.0 * even_up(mm) * mm + 4.0 * mm + 8.0 * mm + 8.0 * mm;
+      if (mm <= kSmallMax) {
+        for (int c = 0; c < mm; c += 8) it.push_back(SolveItem{2, (int)b, std::min(8, mm - c), c});
+      } else {
+        for (int c = 0; c < mm; ++c) it.push_back(SolveItem{3, (int)b, 1, c});
+      }
+    }
+    inv.alloc((size_t)std::max<long long>(h_inv_off[nb], 2));
+    inv_off.upload(h_inv_off, s);
+    // GEMV work items for the solves: one CTA per 64-row tile of every
+    // block (8 column groups per tile keep each thread to <= 1-3 batches)
+    std::vector<SolveItem> gi;
+    for (long long b = 0; b < nb; ++b)
+      for (int r0 = 0; r0 < h_m[b]; r0 += kInvTileRows) gi.push_back(SolveItem{1, (int)b, 1, r0});
+    inv_items.upload(gi, s);
+    n_inv_items = (int)gi.size();
+    DevBuf<SolveItem> citems;
+    citems.upload(it, s);
+    SolveArgs a{};
+    a.m = m.p;
+    a.sf_off = sf_off.p;
+    a.row_off = row_off.p;
+    a.sf = sf.p;
+    a.gsrc = gsrc.p;
+    a.items = citems.p;
+    a.smem_cap = 0;
+    a.g1 = INT_MAX;
+    a.lperm = lperm.p;
+    a.inv = inv.p;
+    a.inv_off = inv_off.p;
+    block_solve_kernel<<<(int)it.size(), kSolveThreads, 0, s>>>(a);
+    FSI_CHECK_LAUNCH();
+    FSI_CUDA(cudaStreamSynchronize(s));
   }
 
   void solve(const SolveArgs& base, cudaStream_t s) const {
     if (!n_items) return;
+    if (mode == kModeInverse) {
+      SolveArgs a = base;
+      a.m = m.p;
+      a.row_off = row_off.p;
+      a.items = inv_items.p;
+      a.inv = const_cast<double*>(inv.p);
+      a.inv_off = inv_off.p;
+      a.pos = pos.n ? pos.p : nullptr;
+      ProfScope ps(FSIGPU_K_BLOCK_SOLVE, solve_bytes, s);
+      inv_gemv_kernel<<<n_inv_items, kSolveThreads, 0, s>>>(a);
+      FSI_CHECK_LAUNCH();
+      counted();
+      return;
+    }
     SolveArgs a = base;
     a.m = m.p;
-    a.lu_off = lu_off.p;
+    a.sf_off = sf_off.p;
     a.row_off = row_off.p;
-    a.lu = lu.p;
+    a.sf = sf.p;
     a.gsrc = gsrc.p;
     a.items = items.p;
+    a.smem_cap = smem_cap;
     ProfScope ps(FSIGPU_K_BLOCK_SOLVE, solve_bytes, s);
-    block_solve_kernel<<<n_items, kSolveThreads, 0, s>>>(a);
+    block_solve_kernel<<<n_items, kSolveThreads, (size_t)2 * smem_cap * 8, s>>>(a);
     FSI_CHECK_LAUNCH();
+    counted();
   }
 };
 
@@ -335,6 +440,7 @@ struct Gmg {
     fs_combine_kernel<<<ceil_div(L.n, 256), 256, 0, s>>>(L.n, L.g1, L.n_us, L.inv_ptr.p, L.inv_idx.p, L.delta.p, r,
                                                          L.lumped.p, omega, L.x, x_zero);
     FSI_CHECK_LAUNCH();
+    counted();
   }
   void resid(int l, double* r) {
     Level& L = lv[l];
@@ -364,6 +470,7 @@ struct Gmg {
     ProfScope ps(FSIGPU_K_COARSE, 8.0 * L.n * L.n + 16.0 * L.n, s);
     gemv_kernel<<<ceil_div((long long)L.n * 32, 256), 256, 0, s>>>(L.n, coarse_inv.p, rhs, L.x, x_zero ? 0 : 1);
     FSI_CHECK_LAUNCH();
+    counted();
   }
   // GmgPreconditioner::cycle (gmg.cpp:188-239)
   void cycle(int l, char mode, int x_zero) {
@@ -460,17 +567,19 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
   }
   L.n_as1 = nb1;
   Blocks& B = L.blocks;
+  B.mode = g_default_mode;
   B.layout(sizes, s);
   B.pos.upload(pos, s);
+  DevBuf<double> dense((size_t)std::max<long long>(B.h_lu_off[B.nb], 1));
   L.delta.alloc((size_t)std::max<long long>(B.total_rows, 1));
   // extract + factor (factor_principal_block for every block)
   if (B.nb) {
-    B.lu.zero(s);
+    dense.zero(s);
     extract_blocks_kernel<<<(int)B.nb, 256, 0, s>>>((int)B.nb, B.m.p, B.lu_off.p, B.row_off.p, B.pos.p, 0, L.A.ptr.p,
-                                                    L.A.idx.p, L.A.val.p, B.lu.p);
+                                                    L.A.idx.p, L.A.val.p, dense.p);
     FSI_CHECK_LAUNCH();
     try {
-      B.factor(B.lu.p, B.pos.p, 0, s);
+      B.factor(dense.p, B.pos.p, 0, s);
     } catch (Error& e) {
       throw Error(e.code, std::string(e.what()) + " (level " + std::to_string(l) + ")");
     }
@@ -608,6 +717,7 @@ struct Gmres {
       k_normalize<<<grid, kKThreads, 0, s>>>(kb);
     }
     FSI_CHECK_LAUNCH();
+    counted(4);
   }
   void step_body() {
     g->apply(ubuf.p, zbuf.p);
@@ -616,12 +726,15 @@ struct Gmres {
   }
   void cycle_tail() {
     cudaStream_t s = g->s;
-    k_solve_y<<<1, 32, 0, s>>>(kb);
+    k_solve_y<<<1, 256, 0, s>>>(kb);
     k_update_x<<<grid, kKThreads, 0, s>>>(kb);
     outer_resid();
     k_norm_r<<<grid, kKThreads, 0, s>>>(kb);
     FSI_CHECK_LAUNCH();
+    counted(3);
   }
+
+  long long pre_launches = 0, body_launches = 0, post_launches = 0;
 
   void build_graph() {
     cudaStream_t s = g->s;
@@ -630,9 +743,11 @@ struct Gmres {
     FSI_CUDA(cudaGraphConditionalHandleCreate(&h, cycle_graph, 1, cudaGraphCondAssignDefault));
     // prefix: v0 = r / beta
     cudaGraph_t pre_g, post_g;
+    const long long c0 = g_launches;
     FSI_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     k_cycle_start<<<grid, kKThreads, 0, s>>>(kb);
     FSI_CUDA(cudaStreamEndCapture(s, &pre_g));
+    pre_launches = 1;
     cudaGraphNode_t n_pre, n_cond, n_post;
     FSI_CUDA(cudaGraphAddChildGraphNode(&n_pre, cycle_graph, nullptr, 0, pre_g));
     cudaGraphNodeParams cp = {};
@@ -643,12 +758,17 @@ struct Gmres {
     FSI_CUDA(cudaGraphAddNode(&n_cond, cycle_graph, &n_pre, 1, &cp));
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     FSI_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    const long long c1 = g_launches;
     step_body();
     k_set_continue<<<1, 1, 0, s>>>(st.p, h, mr);
     FSI_CUDA(cudaStreamEndCapture(s, &body));
+    body_launches = g_launches - c1 + 1;
+    const long long c2 = g_launches;
     FSI_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     cycle_tail();
     FSI_CUDA(cudaStreamEndCapture(s, &post_g));
+    post_launches = g_launches - c2;
+    g_launches = c0;  // capture itself launches nothing
     FSI_CUDA(cudaGraphAddChildGraphNode(&n_post, cycle_graph, &n_cond, 1, post_g));
     FSI_CUDA(cudaGraphInstantiate(&cycle_exec, cycle_graph, 0));
     cudaGraphDestroy(pre_g);
@@ -678,24 +798,29 @@ struct Gmres {
     outer_resid();
     k_norm_r<<<grid, kKThreads, 0, s>>>(kb);
     FSI_CHECK_LAUNCH();
+    counted();
     KState h = read_state();
     long long cycles = 0;
     const bool use_graph = graphs && !g_prof.on;
     if (use_graph && !cycle_exec) build_graph();
     while (!h.converged && h.its < max_iters) {
+      const int its_before = h.its;
       if (use_graph) {
         FSI_CUDA(cudaGraphLaunch(cycle_exec, s));
       } else {
         k_cycle_start<<<grid, kKThreads, 0, s>>>(kb);
         FSI_CHECK_LAUNCH();
+        counted();
         while (true) {
           step_body();
+          counted();  // k_set_continue equivalent of the graph path
           KState t = read_state();
           if (t.stop || t.j >= mr || t.its >= max_iters) break;
         }
         cycle_tail();
       }
       h = read_state();
+      if (use_graph) g_launches += pre_launches + body_launches * (h.its - its_before) + post_launches;
       ++cycles;
       if (h.breakdown) break;
     }
@@ -748,6 +873,14 @@ extern "C" {
 const char* fsigpu_last_error(void) { return g_err.c_str(); }
 int fsigpu_last_singular_block(void) { return g_bad_block; }
 int fsigpu_version(void) { return 1; }
+long long fsigpu_launch_count(void) { return g_launches; }
+int fsigpu_set_block_mode(int mode) {
+  return guarded([&] {
+    require(mode == kModeLU || mode == kModeInverse, "block mode must be 0 (LU) or 1 (inverse)");
+    g_default_mode = mode;
+  });
+}
+void* fsigpu_gmg_stream(fsigpu_gmg g) { return g ? (void*)g->g.s : nullptr; }
 
 int fsigpu_init(int device) {
   return guarded([&] {
@@ -838,14 +971,15 @@ int fsigpu_blocks_factor_csr(fsigpu_csr a, int n_blocks, const int* block_ptr, c
       }
     }
     Blocks& B = h->b;
-    B.layout(sizes, h->s);
+    B.layout(sizes, h->s, true);
     B.pos.upload(pos, h->s);
     if (B.nb) {
-      B.lu.zero(h->s);
+      DevBuf<double> dense((size_t)B.h_lu_off[B.nb]);
+      dense.zero(h->s);
       extract_blocks_kernel<<<(int)B.nb, 256, 0, h->s>>>((int)B.nb, B.m.p, B.lu_off.p, B.row_off.p, B.pos.p, 0,
-                                                         a->a.ptr.p, a->a.idx.p, a->a.val.p, B.lu.p);
+                                                         a->a.ptr.p, a->a.idx.p, a->a.val.p, dense.p);
       FSI_CHECK_LAUNCH();
-      B.factor(B.lu.p, nullptr, 0, h->s);
+      B.factor(dense.p, nullptr, 0, h->s);
     }
     *out = h.release();
   });
@@ -860,7 +994,7 @@ int fsigpu_blocks_factor_dense(int n_blocks, const int* sizes, const double* mat
     h->own_stream = 1;
     std::vector<int> sz(sizes, sizes + n_blocks);
     Blocks& B = h->b;
-    B.layout(sz, h->s);
+    B.layout(sz, h->s, true);
     // row-major (DenseMatrix) -> column-major device layout
     std::vector<double> cm((size_t)B.h_lu_off[B.nb]);
     for (long long b = 0; b < B.nb; ++b) {
@@ -971,7 +1105,7 @@ int fsigpu_blocks_refactor(fsigpu_blocks b, void* stream) {
 
 int fsigpu_blocks_get_lu(fsigpu_blocks b, double* lu_rowmajor, int* piv) {
   return guarded([&] {
-    require(b != nullptr, "blocks: null");
+    require(b != nullptr && b->b.keep_lu, "blocks: LU factors not retained for this handle");
     const Blocks& B = b->b;
     auto lu = B.lu.download(b->s);
     auto pv = B.piv.download(b->s);

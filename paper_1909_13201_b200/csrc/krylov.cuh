@@ -21,7 +21,7 @@
 namespace fsigpu {
 
 constexpr int kMaxRestart = 32;  // restart <= 32 (V_{0..j} dots held in registers)
-constexpr int kKThreads = 256;
+constexpr int kKThreads = 128;
 
 struct KState {
   int j;          // columns done in this cycle
@@ -99,11 +99,17 @@ __device__ __forceinline__ bool last_block(unsigned int* ticket) {
   return s_last;
 }
 
+// Sum of the per-CTA partials, fixed order: warp w reduces vectors
+// v = w, w+NW, ...; lanes stride over CTAs, then a fixed xor tree.
 __device__ __forceinline__ void finish_sum(const KBufs& k, int nv, double* dst) {
-  if (threadIdx.x < nv) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = kKThreads / 32;
+  for (int v = warp; v < nv; v += NW) {
     double s = 0.0;
-    for (unsigned int b = 0; b < gridDim.x; ++b) s += __ldcg(k.partial + (size_t)b * (kMaxRestart + 1) + threadIdx.x);
-    dst[threadIdx.x] = s;
+    for (unsigned int b = lane; b < gridDim.x; b += 32) s += __ldcg(k.partial + (size_t)b * (kMaxRestart + 1) + v);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+    if (lane == 0) dst[v] = s;
   }
   if (threadIdx.x == 0) *k.ticket = 0;
 }
@@ -157,38 +163,57 @@ __global__ void __launch_bounds__(kKThreads) k_update_dots(KBufs k) {
   if (last_block(k.ticket)) finish_sum(k, nv, k.st->h2);
 }
 
-// Givens update of column j on device (krylov.cpp:79-100).
-__device__ void givens_step(const KBufs& k) {
+// Givens update of column j on device (krylov.cpp:79-100), staged in
+// shared memory by the whole (last) CTA; one thread runs the recurrence.
+__device__ void givens_step(const KBufs& k, double hn) {
+  __shared__ double col[kMaxRestart + 2], cs[kMaxRestart + 1], sn[kMaxRestart + 1], g2[2];
   KState* st = k.st;
   const int j = st->j;
   const int mr = k.mr;
-  double* H = k.H;
-  for (int i = 0; i <= j; ++i) H[i * mr + j] = st->h1[i] + st->h2[i];
-  const double hjj = st->hn;
-  H[(j + 1) * mr + j] = hjj;
-  st->its += 1;
-  int lucky = 0;
-  if (hjj < 1e-14) {
-    st->breakdown = 1;
-    lucky = 1;
+  const int t = threadIdx.x;
+  if (t <= j) col[t] = st->h1[t] + st->h2[t];
+  if (t < j) {
+    cs[t] = k.cs[t];
+    sn[t] = k.sn[t];
   }
-  for (int i = 0; i < j; ++i) {
-    const double t = k.cs[i] * H[i * mr + j] + k.sn[i] * H[(i + 1) * mr + j];
-    H[(i + 1) * mr + j] = -k.sn[i] * H[i * mr + j] + k.cs[i] * H[(i + 1) * mr + j];
-    H[i * mr + j] = t;
+  if (t == 0) {
+    col[j + 1] = hn;
+    g2[0] = k.g[j];
   }
-  const double denom = hypot(H[j * mr + j], H[(j + 1) * mr + j]);
-  k.cs[j] = H[j * mr + j] / denom;
-  k.sn[j] = H[(j + 1) * mr + j] / denom;
-  H[j * mr + j] = denom;
-  H[(j + 1) * mr + j] = 0.0;
-  k.g[j + 1] = -k.sn[j] * k.g[j];
-  k.g[j] = k.cs[j] * k.g[j];
-  const double rho = fabs(k.g[j + 1]);
-  st->rho = rho;
-  k.history[st->its] = rho;
-  st->stop = (rho <= st->target || lucky) ? 1 : 0;
-  st->j = j + 1;
+  __syncthreads();
+  if (t == 0) {
+    int lucky = 0;
+    if (hn < 1e-14) {
+      st->breakdown = 1;
+      lucky = 1;
+    }
+    for (int i = 0; i < j; ++i) {
+      const double tt = cs[i] * col[i] + sn[i] * col[i + 1];
+      col[i + 1] = -sn[i] * col[i] + cs[i] * col[i + 1];
+      col[i] = tt;
+    }
+    const double denom = hypot(col[j], col[j + 1]);
+    const double c = col[j] / denom, sj = col[j + 1] / denom;
+    cs[j] = c;
+    sn[j] = sj;
+    col[j] = denom;
+    col[j + 1] = 0.0;
+    const double gj = g2[0];
+    k.g[j + 1] = -sj * gj;
+    k.g[j] = c * gj;
+    const double rho = fabs(-sj * gj);
+    st->its += 1;
+    st->rho = rho;
+    st->hn = hn;
+    k.history[st->its] = rho;
+    st->stop = (rho <= st->target || lucky) ? 1 : 0;
+    k.cs[j] = c;
+    k.sn[j] = sj;
+  }
+  __syncthreads();
+  if (t <= j + 1) k.H[t * mr + j] = col[t];
+  __syncthreads();
+  if (t == 0) st->j = j + 1;
 }
 
 // w -= V h2 ; ||w|| ; Givens
@@ -213,10 +238,7 @@ __global__ void __launch_bounds__(kKThreads) k_update_norm(KBufs k) {
     __shared__ double s_n2;
     finish_sum(k, 1, &s_n2);
     __syncthreads();
-    if (threadIdx.x == 0) {
-      k.st->hn = sqrt(s_n2);
-      givens_step(k);
-    }
+    givens_step(k, sqrt(s_n2));
   }
 }
 
@@ -273,16 +295,25 @@ __global__ void k_cycle_start(KBufs k) {
   }
 }
 
-// y = H^{-1} g (back substitution, krylov.cpp:103-109), single thread
+// y = H^{-1} g (back substitution, krylov.cpp:103-109): H staged in
+// shared memory, one thread runs the recurrence.
 __global__ void k_solve_y(KBufs k) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  __shared__ double Hs[kMaxRestart * kMaxRestart];
+  __shared__ double gs[kMaxRestart + 1];
   KState* st = k.st;
   const int j = st->j;
   const int mr = k.mr;
-  for (int i = j - 1; i >= 0; --i) {
-    double s = k.g[i];
-    for (int q = i + 1; q < j; ++q) s -= k.H[i * mr + q] * st->y[q];
-    st->y[i] = s / k.H[i * mr + i];
+  for (int e = threadIdx.x; e < j * j; e += blockDim.x) Hs[e] = k.H[(e / j) * mr + (e % j)];
+  if (threadIdx.x < j) gs[threadIdx.x] = k.g[threadIdx.x];
+  __syncthreads();
+  __shared__ double y[kMaxRestart];
+  if (threadIdx.x == 0) {
+    for (int i = j - 1; i >= 0; --i) {
+      double s = gs[i];
+      for (int q = i + 1; q < j; ++q) s -= Hs[i * j + q] * y[q];
+      y[i] = s / Hs[i * j + i];
+    }
+    for (int i = 0; i < j; ++i) st->y[i] = y[i];
   }
 }
 

@@ -73,8 +73,24 @@ __global__ void __launch_bounds__(256) csr_kernel(int rows, const int* __restric
   if (row >= rows) return;  // whole row groups exit together (LPR divides 32)
   const int k0 = __ldg(ptr + row), k1 = __ldg(ptr + row + 1);
   double s = 0.0;
-#pragma unroll 4
-  for (int k = k0 + lane; k < k1; k += LPR) s = fma(__ldg(val + k), gx(__ldg(idx + k)), s);
+  // predicated batches of U entries per lane: all index/value loads of a
+  // batch are in flight before the dependent x gathers (no early exits)
+  constexpr int U = 4;
+  for (int kb = k0 + lane; kb < k1; kb += U * LPR) {
+    int c[U];
+    double v[U], xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = kb + u * LPR;
+      const bool ok = k < k1;
+      c[u] = ok ? __ldg(idx + k) : -1;
+      v[u] = ok ? __ldg(val + k) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = c[u] >= 0 ? gx(c[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) s = fma(v[u], xv[u], s);
+  }
 #pragma unroll
   for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, LPR);
   if (lane == 0) epi(row, s);
@@ -114,8 +130,18 @@ __global__ void __launch_bounds__(256) gemv_kernel(int n, const double* __restri
   if (row >= n) return;
   const double* Mr = M + (size_t)row * n;
   double s = 0.0;
-#pragma unroll 4
-  for (int j = lane; j < n; j += 32) s = fma(__ldg(Mr + j), __ldg(b + j), s);
+  constexpr int U = 8;
+  for (int jb = lane; jb < n; jb += 32 * U) {
+    double mv[U], bv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = jb + 32 * u;
+      mv[u] = j < n ? __ldg(Mr + j) : 0.0;
+      bv[u] = j < n ? __ldg(b + j) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) s = fma(mv[u], bv[u], s);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
   if (lane == 0) x[row] = accumulate ? x[row] + s : s;

@@ -74,6 +74,9 @@ def lib():
             "fsigpu_last_singular_block": ([], ip),
             "fsigpu_init": ([ip], ip),
             "fsigpu_version": ([], ip),
+            "fsigpu_launch_count": ([], ll),
+            "fsigpu_set_block_mode": ([ip], ip),
+            "fsigpu_gmg_stream": ([vp], vp),
             "fsigpu_csr_create": ([ip, ip, vp, vp, vp, C.POINTER(vp)], ip),
             "fsigpu_csr_multiply": ([vp, vp, vp], ip),
             "fsigpu_csr_multiply_dev": ([vp, vp, vp, vp], ip),
@@ -290,6 +293,10 @@ class GmgPreconditioner:
     def size(self) -> int:
         return self.n
 
+    def stream(self) -> int:
+        """cudaStream_t (as int) all kernels of this hierarchy run on."""
+        return lib().fsigpu_gmg_stream(self.h) or 0
+
     def apply(self, r) -> np.ndarray:
         r = _f64(r)
         z = np.empty(self.n)
@@ -385,6 +392,19 @@ class GmresSolver:
         if getattr(self, "h", None) and _lib is not None:
             _lib.fsigpu_gmres_destroy(self.h)
             self.h = None
+
+
+MODE_LU, MODE_INVERSE = 0, 1
+
+
+def set_block_mode(mode: int):
+    """Block-solve mode for GMG hierarchies created afterwards (fsigpu_set_block_mode)."""
+    init()
+    _check(lib().fsigpu_set_block_mode(mode))
+
+
+def launch_count() -> int:
+    return int(lib().fsigpu_launch_count())
 
 
 def gmres(gmg: GmgPreconditioner, frame_scale, b, cfg: KrylovConfig, x0=None) -> GmresResult:

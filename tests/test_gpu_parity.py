@@ -104,8 +104,20 @@ def test_fs_blocks_vs_reference(cfg0):
 
 
 # ---------------------------------------------------------------- FS / GMG
-def test_fs_apply_vs_reference(cfg0):
-    G = fsigpu.GmgPreconditioner(cfg0.levels)
+MODES = pytest.mark.parametrize("mode", [fsigpu.MODE_LU, fsigpu.MODE_INVERSE], ids=["lu", "inverse"])
+
+
+def gmg(levels, mode):
+    fsigpu.set_block_mode(mode)
+    try:
+        return fsigpu.GmgPreconditioner(levels)
+    finally:
+        fsigpu.set_block_mode(fsigpu.MODE_INVERSE)
+
+
+@MODES
+def test_fs_apply_vs_reference(cfg0, mode):
+    G = gmg(cfg0.levels, mode)
     g = cfg0.golden
     z = G.fs_apply(len(cfg0.levels) - 1, g["golden/fs_r"])
     assert rel(z, g["golden/fs_z_add"]) <= 1e-12
@@ -117,8 +129,9 @@ def test_coarse_solve(cfg0):
     assert rel(G.coarse_solve(g["golden/coarse_b"]), g["golden/coarse_x"]) <= 1e-9
 
 
-def test_vcycle_vs_reference(cfg0):
-    G = fsigpu.GmgPreconditioner(cfg0.levels)
+@MODES
+def test_vcycle_vs_reference(cfg0, mode):
+    G = gmg(cfg0.levels, mode)
     g = cfg0.golden
     z = G.apply(g["golden/vcycle_r"])
     assert rel(z, g["golden/vcycle_z_add"]) <= 1e-9
@@ -126,10 +139,11 @@ def test_vcycle_vs_reference(cfg0):
     assert rel(z, OG.apply(g["golden/vcycle_r"])) <= 1e-9
 
 
-def test_gmres_cfg0_parity(cfg0):
+@MODES
+def test_gmres_cfg0_parity(cfg0, mode):
     """North-star parity: iterations within +-1 and final relative residual
     within 1e-8 of the additive oracle's on identical inputs."""
-    G = fsigpu.GmgPreconditioner(cfg0.levels)
+    G = gmg(cfg0.levels, mode)
     cfg = fsigpu.KrylovConfig(restart=30, max_iters=2000, rel_tol=1e-10, abs_tol=1e-300)
     res = fsigpu.gmres(G, cfg0.frame_scale, cfg0.b, cfg)
     g = cfg0.golden

@@ -1,0 +1,45 @@
+"""One warm config-0 solve for ncu (graphs off so every launch is a plain
+kernel launch); `--blocks` instead times the config-1 block solve."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+
+from paper_1909_13201_b200 import fsigpu  # noqa: E402
+from paper_1909_13201_b200.problem import load_case  # noqa: E402
+
+
+def main():
+    mode = sys.argv[1] if len(sys.argv) > 1 else "solve"
+    fsigpu.init(0)
+    if mode == "blocks":
+        import torch
+        B = fsigpu.DenseBlocks.generate_dominant(262144, 131072, 20240901)
+        rhs = torch.empty(B.total_rows, dtype=torch.float64, device="cuda")
+        x = torch.empty_like(rhs)
+        s = torch.cuda.Stream()
+        B.generate_rhs(7, rhs.data_ptr())
+        for _ in range(3):
+            B.solve_dev(rhs.data_ptr(), x.data_ptr(), s.cuda_stream)
+        torch.cuda.synchronize()
+        return
+    P = load_case(os.path.join(ROOT, "data", "cfg0.fsix"), "cfg0")
+    if mode in ("vcycle-lu", "vcycle-inv"):
+        fsigpu.set_block_mode(fsigpu.MODE_LU if mode == "vcycle-lu" else fsigpu.MODE_INVERSE)
+        G = fsigpu.GmgPreconditioner(P.levels)
+        for _ in range(3):
+            z = G.apply(P.b)
+        print("vcycle ok", float(np.linalg.norm(z)))
+        return
+    G = fsigpu.GmgPreconditioner(P.levels)
+    S = fsigpu.GmresSolver(G, P.frame_scale, restart=30, graphs=(mode == "graph"))
+    cfg = fsigpu.KrylovConfig(restart=30, max_iters=2000, rel_tol=1e-10, abs_tol=1e-300)
+    for _ in range(2):
+        r = S.solve(P.b, cfg)
+    print("its", r.iterations, "relres", r.true_residual / np.linalg.norm(P.b))
+
+
+if __name__ == "__main__":
+    main()
