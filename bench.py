@@ -128,6 +128,11 @@ def reduce_max(v: float, ws: int) -> float:
     return float(t.item())
 
 
+def whole_job_value(ws: int, per_rank_units: float, ms: float) -> float:
+    """Units all ranks processed / the slowest rank's time (replicas)."""
+    return ws * per_rank_units / (ms / 1000.0)
+
+
 def barrier(ws: int):
     if ws > 1:
         import torch.distributed as dist
@@ -304,7 +309,7 @@ def run_ours(args, ws, rank, local):
     ms_local = sum(per) / len(per)
     ms = reduce_max(ms_local, ws)
     vcyc_per_step = vcycles / args.steps
-    value = ws * vcyc_per_step / (ms / 1000.0)
+    value = whole_job_value(ws, vcyc_per_step, ms)
     relres = res.true_residual / float(np.linalg.norm(P.b))  # x0 = 0: r0 = b
 
     # ---- e2e through the public host-pointer API (pinned host buffers)

@@ -203,6 +203,7 @@ typedef struct {
 
 struct orc_gmg {
   int L;
+  char mode;
   orc_level* lv;
   double omega;
   int pre, post;
@@ -293,8 +294,8 @@ static void richardson(const orc_gmg* g, int level, double* x, const double* b, 
   free(z);
 }
 
-/* GmgPreconditioner::cycle, gmg.cpp:188-239, V-cycle */
-static void cycle(const orc_gmg* g, int level, const double* b, double* x) {
+/* GmgPreconditioner::cycle, gmg.cpp:188-239 (V, W and F cycles) */
+static void cycle(const orc_gmg* g, int level, char mode, const double* b, double* x) {
   const orc_level_desc* d = &g->lv[level].d;
   const int n = d->n;
   double* r = (double*)malloc(sizeof(double) * (size_t)n);
@@ -318,7 +319,15 @@ static void cycle(const orc_gmg* g, int level, const double* b, double* x) {
   orc_csr_spmv(nc, d->r_ptr, d->r_idx, d->r_val, r, rc);
   for (int i = 0; i < nc; ++i)
     if (below->row_mask[i]) rc[i] = 0.0;
-  cycle(g, level - 1, rc, ec);
+  if (mode == 'w') {
+    cycle(g, level - 1, 'w', rc, ec);
+    cycle(g, level - 1, 'w', rc, ec);
+  } else if (mode == 'f') {
+    cycle(g, level - 1, 'f', rc, ec);
+    cycle(g, level - 1, 'v', rc, ec);
+  } else {
+    cycle(g, level - 1, 'v', rc, ec);
+  }
   for (int i = 0; i < nc; ++i)
     if (below->col_mask[i]) ec[i] = 0.0;
   double* ef = r; /* reuse */
@@ -334,13 +343,14 @@ static void cycle(const orc_gmg* g, int level, const double* b, double* x) {
 void orc_gmg_apply(const orc_gmg* g, const double* r, double* z) {
   const int n = g->lv[g->L - 1].d.n;
   memset(z, 0, sizeof(double) * (size_t)n);
-  cycle(g, g->L - 1, r, z);
+  cycle(g, g->L - 1, g->mode, r, z);
 }
 
 orc_gmg* orc_gmg_create(int n_levels, const orc_level_desc* levels, double omega, int pre,
                         int post, int* err_level, int* err_block) {
   orc_gmg* g = (orc_gmg*)calloc(1, sizeof(orc_gmg));
   g->L = n_levels;
+  g->mode = 'v';
   g->omega = omega;
   g->pre = pre;
   g->post = post;
@@ -400,6 +410,8 @@ orc_gmg* orc_gmg_create(int n_levels, const orc_level_desc* levels, double omega
   }
   return g;
 }
+
+void orc_gmg_set_cycle(orc_gmg* g, char mode) { g->mode = mode; }
 
 void orc_gmg_destroy(orc_gmg* g) {
   if (!g) return;

@@ -59,6 +59,8 @@ void orc_extract_block(const int* ptr, const int* idx, const double* val, int m,
 orc_gmg* orc_gmg_create(int n_levels, const orc_level_desc* levels, double omega, int pre,
                         int post, int* err_level, int* err_block);
 void orc_gmg_destroy(orc_gmg* g);
+/* 'v' (default), 'w' or 'f' (gmg.cpp:215-229) */
+void orc_gmg_set_cycle(orc_gmg* g, char mode);
 /* additive FS apply on level l >= 1 (SURVEY §8c recipe) */
 void orc_fs_apply(const orc_gmg* g, int level, const double* r, double* z);
 /* one V-cycle from a zero guess (gmg.cpp:188-246) */

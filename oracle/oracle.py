@@ -32,6 +32,7 @@ def lib():
         L.orc_gmg_create.argtypes = [ip, vp, C.c_double, ip, ip, C.POINTER(ip), C.POINTER(ip)]
         L.orc_gmg_create.restype = vp
         L.orc_gmg_destroy.argtypes = [vp]
+        L.orc_gmg_set_cycle.argtypes = [vp, C.c_char]
         L.orc_fs_apply.argtypes = [vp, ip, vp, vp]
         L.orc_gmg_apply.argtypes = [vp, vp, vp]
         L.orc_coarse_solve.argtypes = [vp, vp, vp]
@@ -85,7 +86,7 @@ def extract_block(A, dofs):
 class OracleGmg:
     """GmgPreconditioner with additive FS smoothers (CPU restatement)."""
 
-    def __init__(self, levels: List, omega=0.7, pre=1, post=1):
+    def __init__(self, levels: List, omega=0.7, pre=1, post=1, cycle="v"):
         from paper_1909_13201_b200.problem import level_descs
         self.levels = levels
         self._descs = level_descs(levels)
@@ -95,6 +96,7 @@ class OracleGmg:
         if not h:
             raise ZeroDivisionError(f"singular block: level {el.value} block {eb.value}")
         self.h = h
+        lib().orc_gmg_set_cycle(h, cycle.encode()[:1])
 
     def __del__(self):
         if getattr(self, "h", None):

@@ -154,3 +154,117 @@ def test_gmres_cfg0_parity(cfg0, mode):
     ref_rel = g["gmres_add/true_residual"][0] / g["gmres_add/history"][0]
     assert abs(res.true_residual / r0 - ref_rel) <= 1e-8
     assert rel(res.x, g["gmres_add/x"]) <= 1e-6
+
+
+# ---------------------------------------------------------------- more cases
+def test_chan_vcycle_and_gmres(chan):
+    """The reference's own test channel (tests/unit_solver.cpp:48-60)."""
+    G = fsigpu.GmgPreconditioner(chan.levels)
+    OG = O.OracleGmg(chan.levels)
+    g = chan.golden
+    assert rel(G.fs_apply(1, g["golden/fs_r"]), g["golden/fs_z_add"]) <= 1e-12
+    assert rel(G.apply(g["golden/vcycle_r"]), g["golden/vcycle_z_add"]) <= 1e-9
+    cfg = fsigpu.KrylovConfig(restart=30, max_iters=300, rel_tol=1e-8, abs_tol=1e-300)
+    res = fsigpu.gmres(G, chan.frame_scale, chan.b, cfg)
+    assert res.converged
+    assert abs(res.iterations - int(g["gmres_add/iterations"][0])) <= 1
+    assert rel(res.x, g["gmres_add/x"]) <= 1e-6
+
+
+@pytest.mark.parametrize("cycle", ["w", "f"])
+def test_w_and_f_cycles(chan, cycle):
+    """gmg.cpp:215-229 cycle shapes against the oracle."""
+    G = fsigpu.GmgPreconditioner(chan.levels, fsigpu.CycleConfig(cycle=cycle))
+    OG = O.OracleGmg(chan.levels, cycle=cycle)
+    r = chan.golden["golden/vcycle_r"]
+    assert rel(G.apply(r), OG.apply(r)) <= 1e-9
+
+
+@pytest.mark.parametrize("pre,post,omega", [(2, 2, 0.7), (1, 1, 1.0), (0, 1, 0.7), (1, 0, 0.7)])
+def test_cycle_knobs(chan, pre, post, omega):
+    cfg = fsigpu.CycleConfig(pre=pre, post=post, omega=omega)
+    G = fsigpu.GmgPreconditioner(chan.levels, cfg)
+    OG = O.OracleGmg(chan.levels, omega=omega, pre=pre, post=post)
+    r = chan.golden["golden/vcycle_r"]
+    assert rel(G.apply(r), OG.apply(r)) <= 1e-9
+
+
+def test_bad_cycle_config_rejected(chan):
+    with pytest.raises(ValueError):
+        fsigpu.GmgPreconditioner(chan.levels, fsigpu.CycleConfig(omega=2.0))
+    with pytest.raises(ValueError):
+        fsigpu.GmgPreconditioner(chan.levels, fsigpu.CycleConfig(pre=0, post=0))
+    with pytest.raises(ValueError):
+        fsigpu.GmgPreconditioner(chan.levels, fsigpu.CycleConfig(cycle="x"))
+
+
+def test_block_edge_cases():
+    # m = 1, 2, 33 (panel boundary), 64/65 (warp/CTA boundary), 165 (global LU)
+    rng = np.random.default_rng(5)
+    sizes = [1, 2, 31, 32, 33, 63, 64, 65, 96, 129, 165, 200]
+    mats = [rng.uniform(-1, 1, (m, m)) for m in sizes]  # non-dominant: pivots
+    B = fsigpu.DenseBlocks.from_dense(mats)
+    rhs = [rng.uniform(-1, 1, m) for m in sizes]
+    x = B.solve(np.concatenate(rhs))
+    lus = B.lu(sizes)
+    o = 0
+    for m, a, b, (lu, piv) in zip(sizes, mats, rhs, lus):
+        lo, po = O.dense_factor(a)
+        assert np.array_equal(lu, lo) and np.array_equal(piv, po)
+        assert rel(x[o:o + m], O.dense_solve(lo, po, b)) <= 1e-12
+        o += m
+    # empty batch
+    E = fsigpu.DenseBlocks.from_dense([])
+    assert E.solve(np.zeros(0)).shape == (0,)
+
+
+def test_singular_block_label():
+    mats = [np.eye(3), np.array([[1.0, 2.0], [2.0, 4.0]]), np.eye(2)]
+    with pytest.raises(fsigpu.SingularBlockError) as e:
+        fsigpu.DenseBlocks.from_dense(mats, labels=["a", "fs-fluid-up-4", "c"])
+    assert e.value.label == "fs-fluid-up-4"
+
+
+def test_config1_sample_parity():
+    """Config-1 generator (2,048 + 1,024 blocks) against the oracle."""
+    import torch
+    B = fsigpu.DenseBlocks.generate_dominant(2048, 1024, 99)
+    rhs = torch.empty(B.total_rows, dtype=torch.float64, device="cuda")
+    x = torch.empty_like(rhs)
+    B.generate_rhs(3, rhs.data_ptr())
+    s = torch.cuda.Stream()
+    B.solve_dev(rhs.data_ptr(), x.data_ptr(), s.cuda_stream)
+    torch.cuda.synchronize()
+    xh, rh = x.cpu().numpy(), rhs.cpu().numpy()
+    sizes = [54] * 2048 + [59] * 1024
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    for b in list(range(0, 3072, 97)) + [2047, 2048, 3071]:
+        m = sizes[b]
+        a = B.matrix(b, m)
+        assert np.all(np.abs(np.diag(a)) >= np.sum(np.abs(a), axis=1) - np.abs(np.diag(a)))
+        lu, piv = O.dense_factor(a)
+        assert rel(xh[offs[b]:offs[b + 1]], O.dense_solve(lu, piv, rh[offs[b]:offs[b + 1]])) <= 1e-12
+
+
+def test_graphs_and_plain_launches_agree(cfg0):
+    """Determinism: the CUDA-graph (conditional WHILE) path and plain
+    launches give bit-identical iterates and histories."""
+    G = fsigpu.GmgPreconditioner(cfg0.levels)
+    cfg = fsigpu.KrylovConfig(restart=30, max_iters=2000, rel_tol=1e-10, abs_tol=1e-300)
+    a = fsigpu.GmresSolver(G, cfg0.frame_scale, 30, graphs=True).solve(cfg0.b, cfg)
+    b = fsigpu.GmresSolver(G, cfg0.frame_scale, 30, graphs=False).solve(cfg0.b, cfg)
+    c = fsigpu.GmresSolver(G, cfg0.frame_scale, 30, graphs=True).solve(cfg0.b, cfg)
+    assert a.iterations == b.iterations == c.iterations
+    assert np.array_equal(a.x, b.x) and np.array_equal(a.x, c.x)
+    assert np.array_equal(a.history, b.history)
+
+
+def test_gmres_restart_and_x0(cfg0):
+    """Restart length 10 and a nonzero initial guess still converge to the
+    same solution (krylov.cpp:29-34,116-122)."""
+    G = fsigpu.GmgPreconditioner(cfg0.levels)
+    cfg = fsigpu.KrylovConfig(restart=10, max_iters=3000, rel_tol=1e-10, abs_tol=1e-300)
+    x0 = np.where(cfg0.levels[-1].col_mask == 1, 0.0, 1e-3)
+    res = fsigpu.GmresSolver(G, cfg0.frame_scale, 10).solve(cfg0.b, cfg, x0=x0)
+    assert res.converged
+    assert rel(res.x, cfg0.golden["gmres_add/x"]) <= 1e-6

@@ -11,7 +11,13 @@ def main(rep, n=30):
     rows = list(csv.reader(io.StringIO(out)))
     h = rows[1]
     si, wi = h.index("Source"), h.index("Warp Stall Sampling (All Samples)")
-    body = [r for r in rows[2:] if len(r) > wi]
+    def num(x):
+        try:
+            float(x)
+            return True
+        except ValueError:
+            return False
+    body = [r for r in rows[2:] if len(r) > wi and num(r[wi] or "0")]
     tot = sum(float(r[wi] or 0) for r in body) or 1.0
     for idx, r in enumerate(body):
         r.append(idx)
