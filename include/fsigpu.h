@@ -119,10 +119,19 @@ void fsigpu_blocks_destroy(fsigpu_blocks b);
 
 /* Block-solve mode of the FS smoothers of GMG hierarchies created after the
  * call: 0 = LU forward/back substitution (tiled), 1 = explicit block inverse
- * computed at setup from the same LU (default; one batched GEMV per sweep). */
+ * computed at setup from the same LU (one batched GEMV + combine per sweep),
+ * 2 = the additive FS operator assembled from those inverses as one sparse
+ * matrix (default; one fused SpMV "x += omega FS r" per sweep). */
 #define FSIGPU_MODE_LU 0
 #define FSIGPU_MODE_INVERSE 1
+#define FSIGPU_MODE_ASSEMBLED 2
 int fsigpu_set_block_mode(int mode);
+/* L2 residency of the read-only V-cycle data (default off): the level
+ * matrices, transfers and block/coarse inverses are packed in one arena and
+ * an access-policy window marks it persisting on the hierarchy's stream
+ * (default off: measured slower on config 0). */
+int fsigpu_set_l2_persist(int enable);
+long long fsigpu_gmg_persist_bytes(fsigpu_gmg g);
 
 /* ---- GMG with additive FS smoothers: GmgPreconditioner (gmg.cpp:178-246),
  *      FsPreconditioner (precond.cpp:119-303, additive per SURVEY §8c),
@@ -149,8 +158,14 @@ int fsigpu_gmres_solve(fsigpu_gmres s, const double* b, const double* x0, double
 int fsigpu_gmres_solve_dev(fsigpu_gmres s, const double* d_b, double* d_x, int max_iters,
                            double rel_tol, double abs_tol, double* history,
                            fsigpu_gmres_result* res);
-/* graph capture of the Arnoldi step on/off (default on) */
+/* graph capture of the Arnoldi step on/off (default on; multi-kernel path) */
 int fsigpu_gmres_set_graphs(fsigpu_gmres s, int enable);
+/* persistent cooperative restart-cycle kernel on/off (opt-in: needs
+ * inverse-mode smoothers and V-cycles; env FSIGPU_MEGA=1 enables it at
+ * creation). Default is the multi-kernel path with one CUDA graph per
+ * restart cycle. */
+int fsigpu_gmres_set_persistent(fsigpu_gmres s, int enable);
+int fsigpu_gmres_is_persistent(fsigpu_gmres s);
 void fsigpu_gmres_destroy(fsigpu_gmres s);
 
 /* ---- instrumentation: accumulated device time per kernel class, measured

@@ -36,31 +36,49 @@ template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  bool owned = true;
   DevBuf() = default;
   explicit DevBuf(size_t count) { alloc(count); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), owned(o.owned) {
+    o.p = nullptr;
+    o.n = 0;
+  }
   DevBuf& operator=(DevBuf&& o) noexcept {
     if (this != &o) {
       release();
       p = o.p;
       n = o.n;
+      owned = o.owned;
       o.p = nullptr;
       o.n = 0;
     }
     return *this;
   }
+  // Move the contents into caller-owned device memory (an arena slice) and
+  // keep only a non-owning view.
+  void rebase(T* dst, cudaStream_t s) {
+    if (n) FSI_CUDA(cudaMemcpyAsync(dst, p, n * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    FSI_CUDA(cudaStreamSynchronize(s));
+    const size_t keep = n;
+    release();
+    p = dst;
+    n = keep;
+    owned = false;
+  }
   ~DevBuf() { release(); }
   void alloc(size_t count) {
     release();
+    owned = true;
     n = count;
     if (count) FSI_CUDA(cudaMalloc(&p, count * sizeof(T)));
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p && owned) cudaFree(p);
     p = nullptr;
     n = 0;
+    owned = true;
   }
   void upload(const T* h, size_t count, cudaStream_t s = 0) {
     if (count != n) alloc(count);

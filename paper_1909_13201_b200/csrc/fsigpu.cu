@@ -8,15 +8,25 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <memory>
+#include <type_traits>
 #include <mutex>
+#include <cstdlib>
 #include <string>
 #include <vector>
+
+#include <thrust/device_ptr.h>
+#include <thrust/execution_policy.h>
+#include <thrust/reduce.h>
+#include <thrust/scan.h>
+#include <thrust/sort.h>
 
 #include "../../include/fsigpu.h"
 #include "common.cuh"
 #include "dense.cuh"
 #include "krylov.cuh"
+#include "mega.cuh"
 #include "sparse.cuh"
 
 namespace fsigpu {
@@ -126,6 +136,17 @@ struct Csr {
     }
     FSI_CUDA(cudaStreamSynchronize(s));
   }
+  // take ownership of device CSR arrays built on the GPU
+  void adopt(int r, int c, DevBuf<int>&& p, DevBuf<int>&& ix, DevBuf<double>&& v) {
+    rows = r;
+    cols = c;
+    ptr = std::move(p);
+    idx = std::move(ix);
+    val = std::move(v);
+    nnz = (long long)idx.n;
+    const double avg = r ? (double)nnz / r : 0.0;
+    lpr = avg <= 6 ? 2 : avg <= 12 ? 4 : avg <= 24 ? 8 : avg <= 72 ? 16 : 32;
+  }
   double bytes(bool resid) const {
     return 12.0 * nnz + 4.0 * (rows + 1) + 8.0 * cols + 8.0 * rows + (resid ? 8.0 * rows : 0.0);
   }
@@ -150,8 +171,8 @@ struct Csr {
 // Batched DenseFactorization: one LU per block, column-major.
 // Block solve modes: LU forward/back substitution (tiled, tile inverses) or
 // explicit block inverse (computed at setup from the bit-exact LU).
-enum BlockMode { kModeLU = 0, kModeInverse = 1 };
-static int g_default_mode = kModeInverse;
+enum BlockMode { kModeLU = 0, kModeInverse = 1, kModeAssembled = 2 };
+static int g_default_mode = kModeAssembled;
 
 struct Blocks {
   int mode = kModeLU;
@@ -406,6 +427,8 @@ struct Level {
   DevBuf<int> aus_ptr, aus_col;
   DevBuf<double> aus_val;
   DevBuf<double> delta, bbuf, xbuf, rbuf;
+  bool assembled = false;  // FS smoother as one sparse operator (kModeAssembled)
+  Csr FS;
   double* b = nullptr;  // level rhs (top level: external)
   double* x = nullptr;  // level iterate (top level: external)
   double combine_bytes = 0;
@@ -413,6 +436,10 @@ struct Level {
 
 struct Gmg {
   std::vector<Level> lv;
+  // read-only hot data (level matrices, transfers, block inverses, coarse
+  // inverse) packed in one arena and pinned in L2 by an access-policy window
+  DevBuf<char> arena;
+  size_t persist_bytes = 0;
   double omega = 0.7;
   int pre = 1, post = 1;
   char cyc = 'v';
@@ -447,9 +474,27 @@ struct Gmg {
     ProfScope ps(FSIGPU_K_SPMV, L.A.bytes(true), s);
     L.A.launch(GatherPlain{L.x}, EpiResid{L.b, r}, s);
   }
+  // x (+)= omega * FS r, fused into the FS SpMV epilogue
+  void fs_spmv(int l, const double* r, int x_zero) {
+    Level& L = lv[l];
+    ProfScope ps(FSIGPU_K_BLOCK_SOLVE, L.FS.bytes(false) + 8.0 * L.n, s);
+    if (x_zero)
+      L.FS.launch(GatherPlain{r}, EpiSetScaled{omega, L.x}, s);
+    else
+      L.FS.launch(GatherPlain{r}, EpiAxpy{omega, L.x}, s);
+  }
   // one FS-preconditioned Richardson sweep; x_zero: x == 0 on entry
   void sweep(int l, int x_zero) {
     Level& L = lv[l];
+    if (L.assembled) {
+      if (x_zero) {
+        fs_spmv(l, L.b, 1);  // res = b - A*0 = b (precond.cpp:312-313)
+      } else {
+        resid(l, L.rbuf.p);
+        fs_spmv(l, L.rbuf.p, 0);
+      }
+      return;
+    }
     if (x_zero) {
       // res = b - A*0 = b exactly (precond.cpp:312-313)
       smooth_solve(l, L.b);
@@ -512,6 +557,93 @@ struct Gmg {
   }
 };
 
+// Assemble the additive FS smoother of one level as a single sparse
+// operator (linear in r, so exactly the same map as the block solves +
+// combine of precond.cpp:271-303 / SURVEY §8c, up to summation order):
+//   AS1 and AS2 blocks:  sum_b R_b^T inv(A_b) R_b / cover
+//   u^s rows:            1 / lumped                    (precond.cpp:281-283)
+//   AS2 <- u^s coupling: -inv(A_b) A_g2[:, u^s] / lumped (Jacobi update, :284-287)
+// COO keys sorted stably and duplicates summed on the device (deterministic).
+static void assemble_fs(Level& L, const fsigpu_level_desc& d, const std::vector<int>& pos,
+                        const std::vector<int>& cover_ptr, const std::vector<int>& ap, const std::vector<int>& ac,
+                        const std::vector<double>& av, cudaStream_t s) {
+  Blocks& B = L.blocks;
+  const int g1 = d.g1;
+  std::vector<long long> coo_off(B.nb + 1, 0);
+  for (long long b = 0; b < B.nb; ++b) coo_off[b + 1] = coo_off[b] + (long long)B.h_m[b] * B.h_m[b];
+  const long long nblk = coo_off[B.nb];
+  std::vector<unsigned long long> hk;
+  std::vector<double> hv;
+  for (int k = 0; k < d.n_us; ++k) {
+    const unsigned long long p = (unsigned long long)(g1 + k);
+    hk.push_back((p << 32) | p);
+    hv.push_back(1.0 / d.lumped[k]);
+  }
+  std::vector<double> blk;
+  for (long long b = L.n_as1; b < B.nb; ++b) {
+    const int m = B.h_m[b];
+    const long long ro = B.h_row_off[b];
+    bool touch = false;
+    for (int j = 0; j < m && !touch; ++j) {
+      const int q = pos[ro + j] - g1;
+      touch = ap[q + 1] > ap[q];
+    }
+    if (!touch) continue;
+    const int ld = even_up(m);
+    blk.resize((size_t)ld * m);
+    FSI_CUDA(cudaMemcpy(blk.data(), B.inv.p + B.h_inv_off[b], sizeof(double) * blk.size(), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < m; ++i) {
+      const int pi = pos[ro + i];
+      const int cov = cover_ptr[pi + 1] - cover_ptr[pi];
+      for (int j = 0; j < m; ++j) {
+        const int q = pos[ro + j] - g1;
+        for (int k = ap[q]; k < ap[q + 1]; ++k) {
+          const int c = ac[k];
+          double v = -blk[(size_t)j * ld + i] * av[k] / d.lumped[c];
+          if (cov > 1) v = v / (double)cov;
+          hk.push_back(((unsigned long long)(unsigned)pi << 32) | (unsigned)(g1 + c));
+          hv.push_back(v);
+        }
+      }
+    }
+  }
+  const long long N = nblk + (long long)hk.size();
+  DevBuf<unsigned long long> keys(N), ukeys(N);
+  DevBuf<double> vals(N), uvals(N);
+  DevBuf<long long> dco;
+  dco.upload(coo_off, s);
+  if (B.nb) {
+    DevBuf<int> inv_ptr_d;
+    inv_ptr_d.upload(cover_ptr, s);
+    fs_coo_blocks_kernel<<<(int)B.nb, 256, 0, s>>>((int)B.nb, B.m.p, B.row_off.p, B.inv.p, B.inv_off.p, B.pos.p,
+                                                   inv_ptr_d.p, dco.p, keys.p, vals.p);
+    FSI_CHECK_LAUNCH();
+    FSI_CUDA(cudaStreamSynchronize(s));
+  }
+  if (!hk.empty()) {
+    FSI_CUDA(cudaMemcpyAsync(keys.p + nblk, hk.data(), sizeof(unsigned long long) * hk.size(), cudaMemcpyHostToDevice, s));
+    FSI_CUDA(cudaMemcpyAsync(vals.p + nblk, hv.data(), sizeof(double) * hv.size(), cudaMemcpyHostToDevice, s));
+  }
+  auto pol = thrust::cuda::par.on(s);
+  thrust::device_ptr<unsigned long long> kp(keys.p), ukp(ukeys.p);
+  thrust::device_ptr<double> vp(vals.p), uvp(uvals.p);
+  thrust::stable_sort_by_key(pol, kp, kp + N, vp);
+  auto ends = thrust::reduce_by_key(pol, kp, kp + N, vp, ukp, uvp);
+  const long long nnz = ends.first - ukp;
+  DevBuf<int> ptr(L.n + 1), cols(nnz);
+  DevBuf<double> fv(nnz);
+  ptr.zero(s);
+  coo_row_count_kernel<<<ceil_div(nnz, 256), 256, 0, s>>>(nnz, ukeys.p, ptr.p);
+  coo_cols_kernel<<<ceil_div(nnz, 256), 256, 0, s>>>(nnz, ukeys.p, cols.p);
+  FSI_CHECK_LAUNCH();
+  thrust::device_ptr<int> pp(ptr.p);
+  thrust::inclusive_scan(pol, pp, pp + L.n + 1, pp);
+  FSI_CUDA(cudaMemcpyAsync(fv.p, uvals.p, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
+  FSI_CUDA(cudaStreamSynchronize(s));
+  L.FS.adopt(L.n, L.n, std::move(ptr), std::move(cols), std::move(fv));
+  L.assembled = true;
+}
+
 // Build one level from its descriptor (host arrays).
 static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t s) {
   Level& L = g.lv[l];
@@ -567,7 +699,7 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
   }
   L.n_as1 = nb1;
   Blocks& B = L.blocks;
-  B.mode = g_default_mode;
+  B.mode = g_default_mode == kModeLU ? kModeLU : kModeInverse;  // assembled builds on the inverses
   B.layout(sizes, s);
   B.pos.upload(pos, s);
   DevBuf<double> dense((size_t)std::max<long long>(B.h_lu_off[B.nb], 1));
@@ -613,6 +745,7 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
   L.aus_val.upload(av.empty() ? std::vector<double>{0.0} : av, s);
   for (int i = 0; i < d.n_us; ++i) require(d.lumped[i] != 0.0, "fs: zero lumped mass entry");
   FSI_CUDA(cudaStreamSynchronize(s));
+  if (g_default_mode == kModeAssembled) assemble_fs(L, d, pos, cnt, ap, ac, av, s);
 }
 
 // Coarse operator: equilibrate (sparse_lu.cpp:104-121), Gauss-Jordan
@@ -662,6 +795,63 @@ static void build_coarse(Gmg& g, const fsigpu_level_desc& d, cudaStream_t s) {
   }
 }
 
+// Pack the read-only arrays every V-cycle streams into one arena and set an
+// L2 access-policy window (hitProp persisting) on the hierarchy's stream, so
+// CUDA-graph kernel nodes captured from it keep them resident across cycles.
+static int g_l2_persist = 0;  // measured slower on config 0 (tools/ab_test.py)
+static void pin_hot_data(Gmg& g) {
+  std::vector<std::pair<void*, size_t>> items;  // (DevBuf*, bytes) via lambdas
+  std::vector<std::function<void(char*)>> movers;
+  size_t total = 0;
+  auto add = [&](auto& buf) {
+    using T = typename std::remove_reference<decltype(*buf.p)>::type;
+    if (!buf.n) return;
+    const size_t bytes = (buf.n * sizeof(T) + 255) & ~size_t(255);
+    const size_t off = total;
+    total += bytes;
+    movers.push_back([&buf, off, &g](char* base) { buf.rebase(reinterpret_cast<T*>(base + off), g.s); });
+  };
+  for (size_t l = 0; l < g.lv.size(); ++l) {
+    Level& L = g.lv[l];
+    add(L.A.val);
+    add(L.A.idx);
+    add(L.A.ptr);
+    if (l == 0) continue;
+    add(L.blocks.inv);
+    add(L.P.val);
+    add(L.P.idx);
+    add(L.P.ptr);
+    add(L.R.val);
+    add(L.R.idx);
+    add(L.R.ptr);
+  }
+  add(g.coarse_inv);
+  if (!total) return;
+  g.arena.alloc(total);
+  for (auto& mv : movers) mv(g.arena.p);
+  g.persist_bytes = 0;
+  if (!g_l2_persist) return;
+  int dev = 0, max_persist = 0, max_window = 0;
+  FSI_CUDA(cudaGetDevice(&dev));
+  FSI_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
+  FSI_CUDA(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+  if (max_persist <= 0 || max_window <= 0) return;
+  size_t cur = 0;
+  FSI_CUDA(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+  const size_t want = std::min<size_t>(total, (size_t)max_persist);
+  if (cur < want) FSI_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+  FSI_CUDA(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+  cudaStreamAttrValue attr = {};
+  const size_t win = std::min<size_t>(total, (size_t)max_window);
+  attr.accessPolicyWindow.base_ptr = g.arena.p;
+  attr.accessPolicyWindow.num_bytes = win;
+  attr.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)cur / (double)win);
+  attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  FSI_CUDA(cudaStreamSetAttribute(g.s, cudaStreamAttributeAccessPolicyWindow, &attr));
+  g.persist_bytes = cur;
+}
+
 // ------------------------------------------------------------ GMRES
 struct Gmres {
   Gmg* g = nullptr;
@@ -675,6 +865,12 @@ struct Gmres {
   int hist_cap = 0;
   cudaGraphExec_t cycle_exec = nullptr;
   cudaGraph_t cycle_graph = nullptr;
+  // persistent cooperative restart-cycle kernel (inverse-mode V-cycles)
+  bool mega = false;
+  bool force_mega = false;
+  int mega_grid = 0;
+  MegaArgs margs{};
+  DevBuf<GridBar> bar;
 
   ~Gmres() {
     if (cycle_exec) cudaGraphExecDestroy(cycle_exec);
@@ -775,6 +971,101 @@ struct Gmres {
     cudaGraphDestroy(post_g);
   }
 
+  void setup_mega() {
+    Gmg& G = *g;
+    mega = G.cyc == 'v' && (int)G.lv.size() <= kMegaMaxLevels && G.lv.size() >= 2;
+    for (size_t l = 1; l < G.lv.size(); ++l) mega = mega && G.lv[l].blocks.mode == kModeInverse;
+    // opt-in (measured slower than the graph path on config 0: its phases
+    // are latency-bound at 2 CTAs/SM)
+    const char* e = std::getenv("FSIGPU_MEGA");
+    mega = mega && (force_mega || (e && std::atoi(e) != 0));
+    if (!mega) return;
+    int dev = 0, sms = 0, occ = 0, coop = 0;
+    FSI_CUDA(cudaGetDevice(&dev));
+    FSI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    FSI_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+    FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fgmres_cycle_kernel, kMegaThreads, 0));
+    if (!coop || occ < 1) {
+      mega = false;
+      return;
+    }
+    mega_grid = sms * std::min(occ, 2);
+    if ((size_t)mega_grid * (kMaxRestart + 1) > partial.n) partial.alloc((size_t)mega_grid * (kMaxRestart + 1));
+    kb.partial = partial.p;
+    bar.alloc(1);
+    bar.zero(G.s);
+    MegaArgs& A = margs;
+    A.L = (int)G.lv.size();
+    for (int l = 0; l < A.L; ++l) {
+      Level& L = G.lv[l];
+      MLevel& M = A.lv[l];
+      M.n = L.n;
+      M.nc = L.nc;
+      M.a_ptr = L.A.ptr.p;
+      M.a_idx = L.A.idx.p;
+      M.a_val = L.A.val.p;
+      M.a_lpr = L.A.lpr;
+      M.rmask = L.rmask.p;
+      M.cmask = L.cmask.p;
+      M.b = L.bbuf.p;
+      M.x = L.xbuf.p;
+      M.r = L.rbuf.p;
+      if (l == 0) continue;
+      M.p_ptr = L.P.ptr.p;
+      M.p_idx = L.P.idx.p;
+      M.p_val = L.P.val.p;
+      M.p_lpr = L.P.lpr;
+      M.r_ptr = L.R.ptr.p;
+      M.r_idx = L.R.idx.p;
+      M.r_val = L.R.val.p;
+      M.r_lpr = L.R.lpr;
+      M.g1 = L.g1;
+      M.n_us = L.n_us;
+      M.lumped = L.lumped.p;
+      M.aus_ptr = L.aus_ptr.p;
+      M.aus_col = L.aus_col.p;
+      M.aus_val = L.aus_val.p;
+      M.bm = L.blocks.m.p;
+      M.row_off = L.blocks.row_off.p;
+      M.inv = L.blocks.inv.p;
+      M.inv_off = L.blocks.inv_off.p;
+      M.pos = L.blocks.pos.p;
+      M.tiles = L.blocks.inv_items.p;
+      M.n_tiles = L.blocks.n_inv_items;
+      M.inv_ptr = L.inv_ptr.p;
+      M.inv_idx = L.inv_idx.p;
+      M.delta = L.delta.p;
+    }
+    A.lv[A.L - 1].b = ubuf.p;
+    A.lv[A.L - 1].x = zbuf.p;
+    A.cinv = G.coarse_inv.p;
+    A.omega = G.omega;
+    A.pre = G.pre;
+    A.post = G.post;
+    A.kb = kb;
+    A.bar = bar.p;
+  }
+
+  void check_bar() {
+    GridBar hb;
+    FSI_CUDA(cudaMemcpyAsync(&hb, bar.p, sizeof(GridBar), cudaMemcpyDeviceToHost, g->s));
+    FSI_CUDA(cudaStreamSynchronize(g->s));
+    if (hb.error) {
+      bar.zero(g->s);
+      throw Error(FSIGPU_ERR_CUDA, "gmres: persistent kernel barrier watchdog tripped at phase " +
+                                       std::to_string(hb.phase) + " (count " + std::to_string(hb.count) + ")");
+    }
+  }
+
+  void launch_mega(int first) {
+    margs.kb = kb;
+    margs.first_cycle = first;
+    void* params[] = {&margs};
+    FSI_CUDA(cudaLaunchCooperativeKernel((const void*)fgmres_cycle_kernel, dim3(mega_grid), dim3(kMegaThreads),
+                                         params, 0, g->s));
+    counted();
+  }
+
   KState read_state() {
     KState h;
     FSI_CUDA(cudaMemcpyAsync(&h, st.p, sizeof(KState), cudaMemcpyDeviceToHost, g->s));
@@ -795,6 +1086,25 @@ struct Gmres {
     h0.rel_tol = rel_tol;
     h0.abs_tol = abs_tol;
     FSI_CUDA(cudaMemcpyAsync(st.p, &h0, sizeof(KState), cudaMemcpyHostToDevice, s));
+    if (mega && !g_prof.on) {
+      launch_mega(1);
+      KState h = read_state();
+      check_bar();
+      while (!h.converged && h.its < max_iters && !h.breakdown) {
+        const int before = h.its;
+        launch_mega(0);
+        h = read_state();
+        check_bar();
+        if (h.its == before) throw Error(FSIGPU_ERR_CUDA, "gmres: persistent cycle made no progress");
+      }
+      res->iterations = h.its;
+      res->converged = h.converged;
+      res->breakdown = h.breakdown;
+      res->n_history = h.its + 1;
+      res->m_applies = h.its;
+      res->true_residual = h.beta;
+      return;
+    }
     outer_resid();
     k_norm_r<<<grid, kKThreads, 0, s>>>(kb);
     FSI_CHECK_LAUNCH();
@@ -874,9 +1184,14 @@ const char* fsigpu_last_error(void) { return g_err.c_str(); }
 int fsigpu_last_singular_block(void) { return g_bad_block; }
 int fsigpu_version(void) { return 1; }
 long long fsigpu_launch_count(void) { return g_launches; }
+int fsigpu_set_l2_persist(int enable) {
+  return guarded([&] { g_l2_persist = enable != 0; });
+}
+long long fsigpu_gmg_persist_bytes(fsigpu_gmg g) { return g ? (long long)g->g.persist_bytes : 0; }
 int fsigpu_set_block_mode(int mode) {
   return guarded([&] {
-    require(mode == kModeLU || mode == kModeInverse, "block mode must be 0 (LU) or 1 (inverse)");
+    require(mode == kModeLU || mode == kModeInverse || mode == kModeAssembled,
+            "block mode must be 0 (LU), 1 (inverse) or 2 (assembled)");
     g_default_mode = mode;
   });
 }
@@ -1147,6 +1462,7 @@ int fsigpu_gmg_create(int n_levels, const fsigpu_level_desc* levels, double omeg
     g.lv.resize(n_levels);
     for (int l = 0; l < n_levels; ++l) build_level(g, l, levels[l], g.s);
     build_coarse(g, levels[0], g.s);
+    pin_hot_data(g);
     g.tmp_in.alloc(g.size());
     g.tmp_out.alloc(g.size());
     *out = h.release();
@@ -1187,11 +1503,15 @@ int fsigpu_fs_apply(fsigpu_gmg g, int level, const double* r, double* z) {
     dr.upload(r, (size_t)L.n, G.s);
     double* sx = L.x;
     L.x = dz.p;
-    // z = M r  ==  combine with omega = 1 from x = 0
+    // z = M r  ==  one sweep with omega = 1 from x = 0
     const double om = G.omega;
     G.omega = 1.0;
-    G.smooth_solve(level, dr.p);
-    G.combine(level, dr.p, 1);
+    if (L.assembled) {
+      G.fs_spmv(level, dr.p, 1);
+    } else {
+      G.smooth_solve(level, dr.p);
+      G.combine(level, dr.p, 1);
+    }
     G.omega = om;
     L.x = sx;
     FSI_CUDA(cudaMemcpyAsync(z, dz.p, sizeof(double) * L.n, cudaMemcpyDeviceToHost, G.s));
@@ -1277,6 +1597,7 @@ int fsigpu_gmres_create(fsigpu_gmg g, const double* frame_scale, int restart, fs
     kb.ticket = k.ticket.p;
     kb.st = k.st.p;
     k.ensure_history(2000);
+    k.setup_mega();
     FSI_CUDA(cudaStreamSynchronize(s));
     *out = h.release();
   });
@@ -1286,6 +1607,72 @@ int fsigpu_gmres_set_graphs(fsigpu_gmres s, int enable) {
   return guarded([&] {
     require(s != nullptr, "gmres: null");
     s->k.graphs = enable != 0;
+  });
+}
+
+int fsigpu_gmres_set_persistent(fsigpu_gmres s, int enable) {
+  return guarded([&] {
+    require(s != nullptr, "gmres: null");
+    if (enable) {
+      s->k.force_mega = true;
+      s->k.setup_mega();
+      require(s->k.mega, "gmres: persistent kernel needs inverse-mode FS smoothers, V-cycles and cooperative launch");
+    } else {
+      s->k.mega = false;
+    }
+  });
+}
+
+int fsigpu_gmres_is_persistent(fsigpu_gmres s) { return s && s->k.mega ? 1 : 0; }
+
+// debug: make every persistent-kernel thread exit after `limit` barriers
+int fsigpu_debug_phase_limit(fsigpu_gmres s, unsigned limit) {
+  return guarded([&] {
+    require(s != nullptr && s->k.mega, "debug: no persistent kernel");
+    FSI_CUDA(cudaMemcpyAsync(&s->k.bar.p->limit, &limit, sizeof(unsigned), cudaMemcpyHostToDevice, s->k.g->s));
+    FSI_CUDA(cudaStreamSynchronize(s->k.g->s));
+  });
+}
+
+// debug: phase timestamps (ns, globaltimer) of the persistent kernel since
+// the last reset; returns the count
+int fsigpu_debug_trace(fsigpu_gmres s, unsigned long long* out, int cap, int reset) {
+  int n = 0;
+  int rc = guarded([&] {
+    require(s != nullptr && s->k.mega, "debug: no persistent kernel");
+    GridBar h;
+    FSI_CUDA(cudaMemcpy(&h, s->k.bar.p, sizeof(GridBar), cudaMemcpyDeviceToHost));
+    n = std::min<int>(cap, (int)h.ntrace);
+    std::memcpy(out, h.trace, sizeof(unsigned long long) * n);
+    if (reset) {
+      const unsigned z = 0;
+      FSI_CUDA(cudaMemcpy(&s->k.bar.p->ntrace, &z, sizeof(unsigned), cudaMemcpyHostToDevice));
+    }
+  });
+  return rc == FSIGPU_OK ? n : -rc;
+}
+
+// debug: time `iters` software grid barriers on `grid` co-resident CTAs
+int fsigpu_debug_barrier(int grid, int iters, int kind, double* ms) {
+  return guarded([&] {
+    cudaStream_t st = new_stream();
+    DevBuf<GridBar> gb(1);
+    gb.zero(st);
+    void* params[] = {&gb.p, &iters, &kind};
+    cudaEvent_t e0, e1;
+    FSI_CUDA(cudaEventCreate(&e0));
+    FSI_CUDA(cudaEventCreate(&e1));
+    FSI_CUDA(cudaEventRecord(e0, st));
+    FSI_CUDA(cudaLaunchCooperativeKernel((const void*)barrier_test_kernel, dim3(grid), dim3(256), params, 0, st));
+    FSI_CUDA(cudaEventRecord(e1, st));
+    FSI_CUDA(cudaEventSynchronize(e1));
+    float t = 0;
+    FSI_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    *ms = t;
+    GridBar h;
+    FSI_CUDA(cudaMemcpy(&h, gb.p, sizeof(GridBar), cudaMemcpyDeviceToHost));
+    require(!h.error, "debug barrier watchdog tripped");
+    cudaStreamDestroy(st);
   });
 }
 

@@ -66,25 +66,26 @@ struct KBufs {
   KState* st;
 };
 
-// Block-level sum of NV register accumulators -> sp[v] (thread v < NV).
+// Block-level sums of NV per-thread accumulators -> out[v] (v < nv): the
+// accumulators are transposed through shared memory (sm: NV * kKThreads
+// doubles) and warp w sums vectors v = w, w + NW, ... (lanes stride the
+// threads, fixed xor tree): one shuffle tree per vector instead of one per
+// vector per warp.
 template <int NV>
 __device__ __forceinline__ void block_reduce_vec(double (&acc)[NV], int nv, double* sm, double* out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int NW = kKThreads / 32;
 #pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    if (v < nv) {
-      double s = acc[v];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-      if (lane == 0) sm[warp * NV + v] = s;
-    }
-  }
+  for (int v = 0; v < NV; ++v)
+    if (v < nv) sm[v * kKThreads + threadIdx.x] = acc[v];
   __syncthreads();
-  if (threadIdx.x < nv) {
+  for (int v = warp; v < nv; v += NW) {
     double s = 0.0;
-    for (int w = 0; w < NW; ++w) s += sm[w * NV + threadIdx.x];
-    out[threadIdx.x] = s;
+#pragma unroll
+    for (int q = 0; q < kKThreads / 32; ++q) s += sm[v * kKThreads + q * 32 + lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+    if (lane == 0) out[v] = s;
   }
 }
 
@@ -116,7 +117,7 @@ __device__ __forceinline__ void finish_sum(const KBufs& k, int nv, double* dst) 
 
 // h1 = V^T w  (+ Z[j] = zbuf)
 __global__ void __launch_bounds__(kKThreads) k_dots(KBufs k) {
-  __shared__ double sm[(kKThreads / 32) * kMaxRestart];
+  __shared__ double sm[kMaxRestart * kKThreads];
   const int j = k.st->j;
   const int nv = j + 1;
   double acc[kMaxRestart];
@@ -136,7 +137,7 @@ __global__ void __launch_bounds__(kKThreads) k_dots(KBufs k) {
 
 // w -= V h_in ; h_out = V^T w
 __global__ void __launch_bounds__(kKThreads) k_update_dots(KBufs k) {
-  __shared__ double sm[(kKThreads / 32) * kMaxRestart];
+  __shared__ double sm[kMaxRestart * kKThreads];
   __shared__ double hs[kMaxRestart];
   const int j = k.st->j;
   const int nv = j + 1;
@@ -171,14 +172,14 @@ __device__ void givens_step(const KBufs& k, double hn) {
   const int j = st->j;
   const int mr = k.mr;
   const int t = threadIdx.x;
-  if (t <= j) col[t] = st->h1[t] + st->h2[t];
+  if (t <= j) col[t] = __ldcg(st->h1 + t) + __ldcg(st->h2 + t);
   if (t < j) {
-    cs[t] = k.cs[t];
-    sn[t] = k.sn[t];
+    cs[t] = __ldcg(k.cs + t);
+    sn[t] = __ldcg(k.sn + t);
   }
   if (t == 0) {
     col[j + 1] = hn;
-    g2[0] = k.g[j];
+    g2[0] = __ldcg(k.g + j);
   }
   __syncthreads();
   if (t == 0) {
@@ -218,7 +219,7 @@ __device__ void givens_step(const KBufs& k, double hn) {
 
 // w -= V h2 ; ||w|| ; Givens
 __global__ void __launch_bounds__(kKThreads) k_update_norm(KBufs k) {
-  __shared__ double sm[(kKThreads / 32) * kMaxRestart];
+  __shared__ double sm[kKThreads];
   __shared__ double hs[kMaxRestart];
   const int j = k.st->j;
   const int nv = j + 1;
@@ -257,7 +258,7 @@ __global__ void k_normalize(KBufs k) {
 
 // ||r|| -> beta; on the first call also r0, history[0] and target.
 __global__ void __launch_bounds__(kKThreads) k_norm_r(KBufs k) {
-  __shared__ double sm[kKThreads / 32];
+  __shared__ double sm[kKThreads];
   double acc[1] = {0.0};
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x)
     acc[0] = fma(k.r[r], k.r[r], acc[0]);

@@ -51,6 +51,17 @@ struct EpiProlongAdd {  // x += P ec where !constrained_cols (gmg.cpp:233-236)
   }
 };
 
+struct EpiSetScaled {  // x = 0 + omega * (FS r)   (first Richardson sweep from x = 0)
+  double omega;
+  double* x;
+  __device__ void operator()(int i, double s) const { x[i] = add_rn(0.0, mul_rn(omega, s)); }
+};
+struct EpiAxpy {  // x += omega * (FS r)          (precond.cpp:315)
+  double omega;
+  double* x;
+  __device__ void operator()(int i, double s) const { x[i] = add_rn(x[i], mul_rn(omega, s)); }
+};
+
 // x gather, optionally masked (ec[constrained_cols below] = 0, gmg.cpp:230-231)
 struct GatherPlain {
   const double* x;
@@ -70,8 +81,10 @@ __global__ void __launch_bounds__(256) csr_kernel(int rows, const int* __restric
   const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int row = (int)(gt / LPR);
   const int lane = threadIdx.x & (LPR - 1);
-  if (row >= rows) return;  // whole row groups exit together (LPR divides 32)
-  const int k0 = __ldg(ptr + row), k1 = __ldg(ptr + row + 1);
+  // idle row groups still run the (empty) loop and the shuffle tree, so no
+  // full-mask shuffle waits on an exited lane
+  const bool ok = row < rows;
+  const int k0 = ok ? __ldg(ptr + row) : 0, k1 = ok ? __ldg(ptr + row + 1) : 0;
   double s = 0.0;
   // predicated batches of U entries per lane: all index/value loads of a
   // batch are in flight before the dependent x gathers (no early exits)
@@ -93,7 +106,7 @@ __global__ void __launch_bounds__(256) csr_kernel(int rows, const int* __restric
   }
 #pragma unroll
   for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, LPR);
-  if (lane == 0) epi(row, s);
+  if (ok && lane == 0) epi(row, s);
 }
 
 // FS combine on one level (precond.cpp:42-57 additive + 271-287 + 305-317):
@@ -127,7 +140,7 @@ __global__ void __launch_bounds__(256) gemv_kernel(int n, const double* __restri
                                                    double* __restrict__ x, int accumulate) {
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (row >= n) return;
+  if (row >= n) return;  // warp-uniform
   const double* Mr = M + (size_t)row * n;
   double s = 0.0;
   constexpr int U = 8;
@@ -231,4 +244,45 @@ __global__ void gj_init_kernel(int n, double* __restrict__ W) {
   W[(size_t)i * 2 * n + n + j] = (i == j) ? 1.0 : 0.0;
 }
 
+}  // namespace fsigpu
+
+namespace fsigpu {
+// ---- assembled FS operator (setup): COO entries of
+//   sum_b R_b^T inv(A_b) R_b / cover  (additive Schwarz, precond.cpp:44-57)
+// one CTA per block; key = (row << 32) | col
+__global__ void fs_coo_blocks_kernel(int nb, const int* __restrict__ msz, const long long* __restrict__ row_off,
+                                     const double* __restrict__ inv, const long long* __restrict__ inv_off,
+                                     const int* __restrict__ pos, const int* __restrict__ inv_ptr,
+                                     const long long* __restrict__ coo_off, unsigned long long* __restrict__ keys,
+                                     double* __restrict__ vals) {
+  const int b = blockIdx.x;
+  if (b >= nb) return;
+  const int m = msz[b];
+  const int ld = (m + 1) & ~1;
+  const long long ro = row_off[b];
+  const double* M = inv + inv_off[b];
+  const long long o = coo_off[b];
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    const int j = e / m, i = e % m;  // column-major walk
+    const int pi = pos[ro + i], pj = pos[ro + j];
+    const int cov = inv_ptr[pi + 1] - inv_ptr[pi];
+    double v = M[(size_t)j * ld + i];
+    if (cov > 1) v = v / (double)cov;
+    keys[o + e] = ((unsigned long long)(unsigned)pi << 32) | (unsigned)pj;
+    vals[o + e] = v;
+  }
+}
+
+__global__ void coo_row_count_kernel(long long nnz, const unsigned long long* __restrict__ keys,
+                                     int* __restrict__ cnt) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nnz) return;
+  atomicAdd(cnt + (int)(keys[e] >> 32) + 1, 1);
+}
+
+__global__ void coo_cols_kernel(long long nnz, const unsigned long long* __restrict__ keys, int* __restrict__ cols) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nnz) return;
+  cols[e] = (int)(keys[e] & 0xffffffffull);
+}
 }  // namespace fsigpu

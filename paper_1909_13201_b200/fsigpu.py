@@ -76,6 +76,8 @@ def lib():
             "fsigpu_version": ([], ip),
             "fsigpu_launch_count": ([], ll),
             "fsigpu_set_block_mode": ([ip], ip),
+            "fsigpu_set_l2_persist": ([ip], ip),
+            "fsigpu_gmg_persist_bytes": ([vp], ll),
             "fsigpu_gmg_stream": ([vp], vp),
             "fsigpu_csr_create": ([ip, ip, vp, vp, vp, C.POINTER(vp)], ip),
             "fsigpu_csr_multiply": ([vp, vp, vp], ip),
@@ -106,6 +108,8 @@ def lib():
             "fsigpu_gmres_solve": ([vp, vp, vp, vp, ip, d, d, vp, C.POINTER(GmresResultC)], ip),
             "fsigpu_gmres_solve_dev": ([vp, vp, vp, ip, d, d, vp, C.POINTER(GmresResultC)], ip),
             "fsigpu_gmres_set_graphs": ([vp, ip], ip),
+            "fsigpu_gmres_set_persistent": ([vp, ip], ip),
+            "fsigpu_gmres_is_persistent": ([vp], ip),
             "fsigpu_gmres_destroy": ([vp], None),
             "fsigpu_profile_enable": ([ip], ip),
             "fsigpu_profile_read": ([vp, vp, vp], ip),
@@ -293,6 +297,9 @@ class GmgPreconditioner:
     def size(self) -> int:
         return self.n
 
+    def persist_bytes(self) -> int:
+        return int(lib().fsigpu_gmg_persist_bytes(self.h))
+
     def stream(self) -> int:
         """cudaStream_t (as int) all kernels of this hierarchy run on."""
         return lib().fsigpu_gmg_stream(self.h) or 0
@@ -362,6 +369,14 @@ class GmresSolver:
     def set_graphs(self, on: bool):
         _check(lib().fsigpu_gmres_set_graphs(self.h, 1 if on else 0))
 
+    def set_persistent(self, on: bool):
+        """Persistent cooperative restart-cycle kernel (default when available)."""
+        _check(lib().fsigpu_gmres_set_persistent(self.h, 1 if on else 0))
+
+    @property
+    def persistent(self) -> bool:
+        return bool(lib().fsigpu_gmres_is_persistent(self.h))
+
     def solve(self, b, cfg: KrylovConfig, x0=None) -> GmresResult:
         n = self.gmg.n
         b = _f64(b)
@@ -394,13 +409,19 @@ class GmresSolver:
             self.h = None
 
 
-MODE_LU, MODE_INVERSE = 0, 1
+MODE_LU, MODE_INVERSE, MODE_ASSEMBLED = 0, 1, 2
 
 
 def set_block_mode(mode: int):
     """Block-solve mode for GMG hierarchies created afterwards (fsigpu_set_block_mode)."""
     init()
     _check(lib().fsigpu_set_block_mode(mode))
+
+
+def set_l2_persist(on: bool):
+    """L2 access-policy window over the hierarchy's read-only data (default on)."""
+    init()
+    _check(lib().fsigpu_set_l2_persist(1 if on else 0))
 
 
 def launch_count() -> int:
