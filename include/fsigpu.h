@@ -146,6 +146,13 @@ int fsigpu_gmg_apply_dev(fsigpu_gmg g, const double* d_r, double* d_z, void* str
 int fsigpu_fs_apply(fsigpu_gmg g, int level, const double* r, double* z);
 int fsigpu_coarse_solve(fsigpu_gmg g, const double* b, double* x);
 void fsigpu_gmg_destroy(fsigpu_gmg g);
+/* Device time (ms, CUDA events on the hierarchy stream) of one launch of a
+ * V-cycle kernel on `level` and its algorithmic bytes. which: 0 FS smoother
+ * SpMV, 1 level residual SpMV, 2 prolongation + fused residual, 3
+ * restriction, 4 coarse GEMV (level 0). cold: flush L2 (256 MB) before each
+ * launch; else back to back. */
+int fsigpu_gmg_time_kernel(fsigpu_gmg g, int which, int level, int reps, int cold, double* ms,
+                           double* bytes);
 
 /* ---- outer solver: gmres (krylov.cpp:20-126) on the row-equilibrated
  *      frame operator diag(frame_scale) A_top with M(r) = GMG(r/frame_scale)

@@ -429,6 +429,7 @@ struct Level {
   DevBuf<double> delta, bbuf, xbuf, rbuf;
   bool assembled = false;  // FS smoother as one sparse operator (kModeAssembled)
   Csr FS;
+  Csr AP;  // A * diag(!col_mask) * P : fused prolongation + post-smoothing residual
   double* b = nullptr;  // level rhs (top level: external)
   double* x = nullptr;  // level iterate (top level: external)
   double combine_bytes = 0;
@@ -483,16 +484,22 @@ struct Gmg {
     else
       L.FS.launch(GatherPlain{r}, EpiAxpy{omega, L.x}, s);
   }
-  // one FS-preconditioned Richardson sweep; x_zero: x == 0 on entry
-  void sweep(int l, int x_zero) {
+  // one FS-preconditioned Richardson sweep; x_zero: x == 0 on entry;
+  // r_ready: rbuf already holds b - A x (fused prolongation kernel)
+  void sweep(int l, int x_zero, bool r_ready = false) {
     Level& L = lv[l];
     if (L.assembled) {
       if (x_zero) {
         fs_spmv(l, L.b, 1);  // res = b - A*0 = b (precond.cpp:312-313)
       } else {
-        resid(l, L.rbuf.p);
+        if (!r_ready) resid(l, L.rbuf.p);
         fs_spmv(l, L.rbuf.p, 0);
       }
+      return;
+    }
+    if (r_ready && !x_zero) {
+      smooth_solve(l, L.rbuf.p);
+      combine(l, L.rbuf.p, 0);
       return;
     }
     if (x_zero) {
@@ -537,6 +544,29 @@ struct Gmg {
       case 'w': cycle(l - 1, 'w', 1); cycle(l - 1, 'w', 0); break;
       case 'f': cycle(l - 1, 'f', 1); cycle(l - 1, 'v', 0); break;
       default: throw Error(FSIGPU_ERR_INVALID, "gmg: unknown cycle type");
+    }
+    if (post > 0 && L.AP.rows) {
+      // x += P ec ; r = r_pre - AP ec  (one kernel; rbuf holds r_pre)
+      ProfScope ps(FSIGPU_K_TRANSFER, L.P.bytes(false) + L.AP.bytes(false) + 24.0 * L.n + L.n + L.nc, s);
+      const int grid = ceil_div((long long)L.n * L.AP.lpr, 256);
+      switch (L.AP.lpr) {
+#define FSI_PR(LP)                                                                                              \
+  case LP:                                                                                                      \
+    prolong_resid_kernel<LP><<<grid, 256, 0, s>>>(L.n, L.P.ptr.p, L.P.idx.p, L.P.val.p, L.AP.ptr.p, L.AP.idx.p, \
+                                                  L.AP.val.p, B.x, B.cmask.p, L.cmask.p, L.x, L.rbuf.p, L.rbuf.p); \
+    break;
+        FSI_PR(2)
+        FSI_PR(4)
+        FSI_PR(8)
+        FSI_PR(16)
+        default:
+          FSI_PR(32)
+#undef FSI_PR
+      }
+      FSI_CHECK_LAUNCH();
+      counted();
+      for (int k = 0; k < post; ++k) sweep(l, 0, k == 0);
+      return;
     }
     {
       ProfScope ps(FSIGPU_K_TRANSFER, L.P.bytes(false) + 8.0 * L.n + L.n + L.nc, s);
@@ -668,6 +698,40 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
   require(d.nc == g.lv[l - 1].n, "gmg: transfer size does not match the coarser level");
   L.P.create(d.n, d.nc, d.p_ptr, d.p_idx, d.p_val, s);
   L.R.create(d.nc, d.n, d.r_ptr, d.r_idx, d.r_val, s);
+  {
+    // AP_m = A * diag(!col_mask) * P (Gustavson, sorted rows)
+    std::vector<int> app(d.n + 1, 0), api;
+    std::vector<double> apv, acc(d.nc, 0.0);
+    std::vector<int> mark(d.nc, -1), touched;
+    for (int i = 0; i < d.n; ++i) {
+      touched.clear();
+      for (int k = d.a_ptr[i]; k < d.a_ptr[i + 1]; ++k) {
+        const int c = d.a_idx[k];
+        if (d.col_mask[c]) continue;
+        const double a = d.a_val[k];
+        for (int q = d.p_ptr[c]; q < d.p_ptr[c + 1]; ++q) {
+          const int cc = d.p_idx[q];
+          if (mark[cc] != i) {
+            mark[cc] = i;
+            acc[cc] = 0.0;
+            touched.push_back(cc);
+          }
+          acc[cc] += a * d.p_val[q];
+        }
+      }
+      std::sort(touched.begin(), touched.end());
+      for (int cc : touched) {
+        api.push_back(cc);
+        apv.push_back(acc[cc]);
+      }
+      app[i + 1] = (int)api.size();
+    }
+    if (api.empty()) {
+      api.push_back(0);
+      apv.push_back(0.0);
+    }
+    L.AP.create(d.n, d.nc, app.data(), api.data(), apv.data(), s);
+  }
   require(d.g1 >= 0 && d.n_us >= 0 && d.g1 + d.n_us <= d.n, "fs: bad group sizes");
   L.g1 = d.g1;
   L.n_us = d.n_us;
@@ -902,23 +966,28 @@ struct Gmres {
     ProfScope ps(FSIGPU_K_SPMV, T.A.bytes(true) + 8.0 * n, g->s);
     T.A.launch(GatherPlain{x.p}, EpiResidScaled{b.p, scale.p, r.p}, g->s);
   }
-  void arnoldi_tail() {
+  // outer SpMV + CGS2 Arnoldi + Givens + normalisation: 3 fused kernels
+  void arnoldi_fused(const KBufs& kk) {
     cudaStream_t s = g->s;
-    const double vb = 8.0 * n;
+    Level& T = g->lv.back();
+    const int gs = ceil_div(n, kFuseRows);
     {
-      ProfScope ps(FSIGPU_K_ARNOLDI, vb * 3, s);
-      k_dots<<<grid, kKThreads, 0, s>>>(kb);
-      k_update_dots<<<grid, kKThreads, 0, s>>>(kb);
-      k_update_norm<<<grid, kKThreads, 0, s>>>(kb);
-      k_normalize<<<grid, kKThreads, 0, s>>>(kb);
+      ProfScope ps(FSIGPU_K_SPMV, T.A.bytes(false) + 8.0 * n * 3, s);
+      // 128 rows per CTA in one pass: 8 lanes per row (1024 threads)
+      k_spmv_dots<8><<<gs, kFuseThreads, 0, s>>>(kk);
+    }
+    {
+      ProfScope ps(FSIGPU_K_ARNOLDI, 8.0 * n * 4, s);
+      const int ga = std::max(1, std::min(ceil_div(n, kArnThreads), 4 * 148));
+      k_update_dots_norm<<<ga, kArnThreads, 0, s>>>(kk);
+      k_update_normalize<<<ga, kArnThreads, 0, s>>>(kk);
     }
     FSI_CHECK_LAUNCH();
-    counted(4);
+    counted(3);
   }
-  void step_body() {
+  void step_body(const KBufs& kk) {
     g->apply(ubuf.p, zbuf.p);
-    outer_spmv(zbuf.p, w.p);
-    arnoldi_tail();
+    arnoldi_fused(kk);
   }
   void cycle_tail() {
     cudaStream_t s = g->s;
@@ -955,10 +1024,12 @@ struct Gmres {
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     FSI_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     const long long c1 = g_launches;
-    step_body();
-    k_set_continue<<<1, 1, 0, s>>>(st.p, h, mr);
+    KBufs kc = kb;  // the Givens step sets the WHILE condition
+    kc.cond = h;
+    kc.use_cond = 1;
+    step_body(kc);
     FSI_CUDA(cudaStreamEndCapture(s, &body));
-    body_launches = g_launches - c1 + 1;
+    body_launches = g_launches - c1;
     const long long c2 = g_launches;
     FSI_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     cycle_tail();
@@ -1122,8 +1193,7 @@ struct Gmres {
         FSI_CHECK_LAUNCH();
         counted();
         while (true) {
-          step_body();
-          counted();  // k_set_continue equivalent of the graph path
+          step_body(kb);
           KState t = read_state();
           if (t.stop || t.j >= mr || t.its >= max_iters) break;
         }
@@ -1538,6 +1608,106 @@ int fsigpu_coarse_solve(fsigpu_gmg g, const double* b, double* x) {
   });
 }
 
+// Average device time of one launch of a V-cycle kernel on `level`, each
+// launch timed alone with CUDA events on the hierarchy stream after an L2
+// flush (cold, HBM-bound) or back to back (warm). Algorithmic bytes of one
+// launch are returned alongside.
+//   which: 0 FS smoother SpMV (x += omega FS r), 1 level SpMV residual,
+//          2 prolongation (+ fused residual), 3 restriction, 4 coarse GEMV
+int fsigpu_gmg_time_kernel(fsigpu_gmg h, int which, int level, int reps, int cold, double* ms, double* bytes) {
+  return guarded([&] {
+    require(h != nullptr && reps > 0, "time: bad args");
+    Gmg& G = h->g;
+    require(level >= 0 && level < (int)G.lv.size(), "time: bad level");
+    Level& L = G.lv[level];
+    cudaStream_t s = G.s;
+    DevBuf<char> flush(cold ? (size_t)256 << 20 : 0);
+    DevBuf<double> v1(L.n), v2(L.n), v3(L.n);
+    v1.zero(s);
+    v2.zero(s);
+    v3.zero(s);
+    double* sb = L.b;
+    double* sx = L.x;
+    L.b = v1.p;
+    L.x = v2.p;
+    double by = 0.0;
+    auto launch = [&]() {
+      switch (which) {
+        case 0:
+          require(L.assembled, "time: level has no assembled FS operator");
+          L.FS.launch(GatherPlain{v3.p}, EpiAxpy{G.omega, L.x}, s);
+          by = L.FS.bytes(false) + 8.0 * L.n;
+          break;
+        case 1:
+          L.A.launch(GatherPlain{L.x}, EpiResid{L.b, v3.p}, s);
+          by = L.A.bytes(true);
+          break;
+        case 2: {
+          require(level > 0 && L.AP.rows, "time: no prolongation on this level");
+          Level& B = G.lv[level - 1];
+          const int grid = ceil_div((long long)L.n * L.AP.lpr, 256);
+          switch (L.AP.lpr) {
+            case 2: prolong_resid_kernel<2><<<grid, 256, 0, s>>>(L.n, L.P.ptr.p, L.P.idx.p, L.P.val.p, L.AP.ptr.p, L.AP.idx.p, L.AP.val.p, B.x, B.cmask.p, L.cmask.p, L.x, v3.p, v3.p); break;
+            case 4: prolong_resid_kernel<4><<<grid, 256, 0, s>>>(L.n, L.P.ptr.p, L.P.idx.p, L.P.val.p, L.AP.ptr.p, L.AP.idx.p, L.AP.val.p, B.x, B.cmask.p, L.cmask.p, L.x, v3.p, v3.p); break;
+            case 8: prolong_resid_kernel<8><<<grid, 256, 0, s>>>(L.n, L.P.ptr.p, L.P.idx.p, L.P.val.p, L.AP.ptr.p, L.AP.idx.p, L.AP.val.p, B.x, B.cmask.p, L.cmask.p, L.x, v3.p, v3.p); break;
+            case 16: prolong_resid_kernel<16><<<grid, 256, 0, s>>>(L.n, L.P.ptr.p, L.P.idx.p, L.P.val.p, L.AP.ptr.p, L.AP.idx.p, L.AP.val.p, B.x, B.cmask.p, L.cmask.p, L.x, v3.p, v3.p); break;
+            default: prolong_resid_kernel<32><<<grid, 256, 0, s>>>(L.n, L.P.ptr.p, L.P.idx.p, L.P.val.p, L.AP.ptr.p, L.AP.idx.p, L.AP.val.p, B.x, B.cmask.p, L.cmask.p, L.x, v3.p, v3.p); break;
+          }
+          by = L.P.bytes(false) + L.AP.bytes(false) + 24.0 * L.n + L.n + L.nc;
+          break;
+        }
+        case 3: {
+          require(level > 0, "time: no restriction on level 0");
+          Level& B = G.lv[level - 1];
+          DevBuf<double> rc;  // reuse v1 prefix as coarse output
+          L.R.launch(GatherPlain{L.x}, EpiRestrict{B.rmask.p, v1.p}, s);
+          by = L.R.bytes(false) + L.nc;
+          break;
+        }
+        case 4:
+          require(level == 0, "time: coarse GEMV lives on level 0");
+          gemv_kernel<<<ceil_div((long long)L.n * 32, 256), 256, 0, s>>>(L.n, G.coarse_inv.p, L.b, L.x, 0);
+          by = 8.0 * L.n * L.n + 16.0 * L.n;
+          break;
+        default:
+          throw Error(FSIGPU_ERR_INVALID, "time: unknown kernel");
+      }
+      FSI_CHECK_LAUNCH();
+    };
+    for (int i = 0; i < 3; ++i) launch();
+    cudaEvent_t e0, e1;
+    FSI_CUDA(cudaEventCreate(&e0));
+    FSI_CUDA(cudaEventCreate(&e1));
+    double tot = 0.0;
+    if (cold) {
+      for (int i = 0; i < reps; ++i) {
+        FSI_CUDA(cudaMemsetAsync(flush.p, i & 0xff, flush.n, s));
+        FSI_CUDA(cudaEventRecord(e0, s));
+        launch();
+        FSI_CUDA(cudaEventRecord(e1, s));
+        FSI_CUDA(cudaEventSynchronize(e1));
+        float t = 0;
+        FSI_CUDA(cudaEventElapsedTime(&t, e0, e1));
+        tot += t;
+      }
+    } else {
+      FSI_CUDA(cudaEventRecord(e0, s));
+      for (int i = 0; i < reps; ++i) launch();
+      FSI_CUDA(cudaEventRecord(e1, s));
+      FSI_CUDA(cudaEventSynchronize(e1));
+      float t = 0;
+      FSI_CUDA(cudaEventElapsedTime(&t, e0, e1));
+      tot = t;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    L.b = sb;
+    L.x = sx;
+    *ms = tot / reps;
+    *bytes = by;
+  });
+}
+
 void fsigpu_gmg_destroy(fsigpu_gmg g) {
   if (!g) return;
   cudaStreamSynchronize(g->g.s);
@@ -1573,7 +1743,7 @@ int fsigpu_gmres_create(fsigpu_gmg g, const double* frame_scale, int restart, fs
     k.sn.alloc(restart);
     k.gv.alloc(restart + 1);
     k.grid = std::max(1, std::min(ceil_div(n, kKThreads), 2 * 148));
-    k.partial.alloc((size_t)k.grid * (kMaxRestart + 1));
+    k.partial.alloc((size_t)std::max(std::max(k.grid, ceil_div(n, kFuseRows)), 4 * 148) * (kMaxRestart + 1));
     k.ticket.alloc(1);
     k.ticket.zero(s);
     k.st.alloc(1);
@@ -1596,6 +1766,14 @@ int fsigpu_gmres_create(fsigpu_gmg g, const double* frame_scale, int restart, fs
     kb.partial = k.partial.p;
     kb.ticket = k.ticket.p;
     kb.st = k.st.p;
+    {
+      Level& T = g->g.lv.back();
+      kb.a_ptr = T.A.ptr.p;
+      kb.a_idx = T.A.idx.p;
+      kb.a_val = T.A.val.p;
+      kb.a_lpr = T.A.lpr;
+      kb.use_cond = 0;
+    }
     k.ensure_history(2000);
     k.setup_mega();
     FSI_CUDA(cudaStreamSynchronize(s));

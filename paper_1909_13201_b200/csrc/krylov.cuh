@@ -64,6 +64,13 @@ struct KBufs {
   double* partial;      // grid x (kMaxRestart+1)
   unsigned int* ticket;
   KState* st;
+  // fused Arnoldi (3 kernels per step)
+  const int* a_ptr;            // top-level CSR (outer operator A_s = diag(scale) A)
+  const int* a_idx;
+  const double* a_val;
+  int a_lpr;
+  cudaGraphConditionalHandle cond;  // WHILE handle of the restart-cycle graph
+  int use_cond;
 };
 
 // Block-level sums of NV per-thread accumulators -> out[v] (v < nv): the
@@ -90,13 +97,19 @@ __device__ __forceinline__ void block_reduce_vec(double (&acc)[NV], int nv, doub
 }
 
 // Last-CTA detection; returns true in every thread of the last CTA.
+// bar.sync orders the CTA's partial writes before thread 0's gpu-scope
+// fence + arrival (cumulativity), so one fenced thread suffices (a fence in
+// every thread showed up as the top ERRBAR stall in ncu).
 __device__ __forceinline__ bool last_block(unsigned int* ticket) {
   __shared__ bool s_last;
-  __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) s_last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const bool last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+    if (last) __threadfence();
+    s_last = last;
+  }
   __syncthreads();
-  if (s_last) __threadfence();
   return s_last;
 }
 
@@ -107,7 +120,17 @@ __device__ __forceinline__ void finish_sum(const KBufs& k, int nv, double* dst) 
   constexpr int NW = kKThreads / 32;
   for (int v = warp; v < nv; v += NW) {
     double s = 0.0;
-    for (unsigned int b = lane; b < gridDim.x; b += 32) s += __ldcg(k.partial + (size_t)b * (kMaxRestart + 1) + v);
+    constexpr int U = 8;  // predicated load batches (no per-load exits)
+    for (unsigned int b0 = lane; b0 < gridDim.x; b0 += 32 * U) {
+      double pv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const unsigned int b = b0 + 32 * u;
+        pv[u] = b < gridDim.x ? __ldcg(k.partial + (size_t)b * (kMaxRestart + 1) + v) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) s += pv[u];
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
     if (lane == 0) dst[v] = s;
@@ -166,6 +189,7 @@ __global__ void __launch_bounds__(kKThreads) k_update_dots(KBufs k) {
 
 // Givens update of column j on device (krylov.cpp:79-100), staged in
 // shared memory by the whole (last) CTA; one thread runs the recurrence.
+// With use_cond, also sets the restart-cycle WHILE condition.
 __device__ void givens_step(const KBufs& k, double hn) {
   __shared__ double col[kMaxRestart + 2], cs[kMaxRestart + 1], sn[kMaxRestart + 1], g2[2];
   KState* st = k.st;
@@ -214,7 +238,13 @@ __device__ void givens_step(const KBufs& k, double hn) {
   __syncthreads();
   if (t <= j + 1) k.H[t * mr + j] = col[t];
   __syncthreads();
-  if (t == 0) st->j = j + 1;
+  if (t == 0) {
+    st->j = j + 1;
+    if (k.use_cond) {
+      const int go = (!st->stop && j + 1 < mr && st->its < st->max_iters) ? 1 : 0;
+      cudaGraphSetConditional(k.cond, go);
+    }
+  }
 }
 
 // w -= V h2 ; ||w|| ; Givens
@@ -338,4 +368,208 @@ __global__ void k_set_continue(const KState* st, cudaGraphConditionalHandle h, i
   cudaGraphSetConditional(h, go);
 }
 
+}  // namespace fsigpu
+
+namespace fsigpu {
+// ---- fused Arnoldi step (3 kernels): -----------------------------------
+// CTA-wide fixed-order sum of the per-CTA partials (vector v, CTA b):
+// thread t owns vector slot t % 32 and slice t / 32 of the CTAs; slices are
+// combined in order through shared memory. red: (T/32) x 32 doubles.
+template <int T>
+__device__ __forceinline__ void finish_wide(const KBufs& k, int nv, double* dst, double* red) {
+  constexpr int NS = T / 32;
+  const int v = threadIdx.x & 31, q = threadIdx.x >> 5;
+  double s = 0.0;
+  if (v < nv) {
+    constexpr int U = 8;
+    for (unsigned int b0 = q; b0 < gridDim.x; b0 += NS * U) {
+      double pv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const unsigned int b = b0 + NS * u;
+        pv[u] = b < gridDim.x ? __ldcg(k.partial + (size_t)b * (kMaxRestart + 1) + v) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) s += pv[u];
+    }
+  }
+  red[q * 32 + v] = s;
+  __syncthreads();
+  if (threadIdx.x < nv) {
+    double z = 0.0;
+    for (int i = 0; i < NS; ++i) z += red[i * 32 + threadIdx.x];
+    dst[threadIdx.x] = z;
+  }
+  if (threadIdx.x == 0) *k.ticket = 0;
+  __syncthreads();
+}
+
+// (A) w = diag(scale) A z_j and h1 = V^T w in one pass: a CTA owns 64 rows,
+//     computes them with LPR-lane CSR rows, keeps w in shared memory and
+//     forms its partial dots (Z[j] = zbuf copied on the way).
+constexpr int kFuseThreads = 1024;
+constexpr int kFuseRows = 128;  // rows per CTA of k_spmv_dots (one pass at LPR = 8)
+constexpr int kArnThreads = 128;  // CTA size of the fused update kernels
+template <int LPR>
+__device__ __forceinline__ double fused_row(const KBufs& k, int row, int lane) {
+  const int k0 = row >= 0 ? __ldg(k.a_ptr + row) : 0, k1 = row >= 0 ? __ldg(k.a_ptr + row + 1) : 0;
+  double s = 0.0;
+  constexpr int U = 4;
+  for (int kb = k0 + lane; kb < k1; kb += U * LPR) {
+    int c[U];
+    double v[U], xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int kk = kb + u * LPR;
+      const bool ok = kk < k1;
+      c[u] = ok ? __ldg(k.a_idx + kk) : -1;
+      v[u] = ok ? __ldg(k.a_val + kk) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = c[u] >= 0 ? k.zbuf[c[u]] : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) s = fma(v[u], xv[u], s);
+  }
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, LPR);
+  return s;
+}
+
+template <int LPR>
+__global__ void __launch_bounds__(kFuseThreads) k_spmv_dots(KBufs k) {
+  __shared__ double ws[kFuseRows];
+  __shared__ double red[kFuseThreads];
+  const int j = k.st->j;
+  const int nv = j + 1;
+  const int r0 = blockIdx.x * kFuseRows;
+  const int t = threadIdx.x;
+  constexpr int RPP = kFuseThreads / LPR;  // rows per pass
+  for (int p = 0; p < kFuseRows; p += RPP) {
+    const int rl = p + t / LPR;
+    const int row = r0 + rl;
+    const bool ok = rl < kFuseRows && row < k.n;
+    const double s = fused_row<LPR>(k, ok ? row : -1, t & (LPR - 1));
+    if (ok && (t & (LPR - 1)) == 0) {
+      const double w = k.scale[row] * s;
+      k.w[row] = w;
+      ws[rl] = w;
+    }
+  }
+  if (t < kFuseRows && r0 + t < k.n) k.Z[(size_t)j * k.n + r0 + t] = k.zbuf[r0 + t];
+  if (t < kFuseRows && r0 + t >= k.n) ws[t] = 0.0;
+  __syncthreads();
+  // partial dots: warp v (lanes over the CTA's 128 rows, 4 each)
+  const int v = t >> 5, lane = t & 31;
+  double s = 0.0;
+  if (v < nv) {
+    double vv[kFuseRows / 32];
+#pragma unroll
+    for (int q = 0; q < kFuseRows / 32; ++q) {
+      const int row = r0 + lane + 32 * q;
+      vv[q] = row < k.n ? k.V[(size_t)v * k.n + row] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < kFuseRows / 32; ++q) s = fma(vv[q], ws[lane + 32 * q], s);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  if (lane == 0 && v < nv) k.partial[(size_t)blockIdx.x * (kMaxRestart + 1) + v] = s;
+  if (last_block(k.ticket)) finish_wide<kFuseThreads>(k, nv, k.st->h1, red);
+}
+
+// (B) w -= V h1 ; h2 = V^T w ; ||w||^2 in one pass; the last CTA forms
+//     h_{j+1,j} = sqrt(||w||^2 - ||h2||^2) (the norm of w - V h2 for an
+//     orthonormal V; h2 is the small second CGS correction) and runs Givens.
+// per-CTA sums of NV per-thread values for CTAs of T threads: warp-level
+// trees, then warp totals combined in warp order (deterministic)
+template <int T, int NV>
+__device__ __forceinline__ void cta_reduce_wide(const double (&acc)[NV], int nv, double* sm, double* out) {
+  constexpr int NW = T / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    if (v < nv) {
+      double s = acc[v];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+      if (lane == 0) sm[v * NW + warp] = s;
+    }
+  }
+  __syncthreads();
+  // vector v summed by warp v mod NW (lanes over the NW warp totals)
+  for (int v = warp; v < nv; v += NW) {
+    double s = 0.0;
+    for (int i = lane; i < NW; i += 32) s += sm[v * NW + i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+    if (lane == 0) out[v] = s;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kArnThreads) k_update_dots_norm(KBufs k) {
+  __shared__ double sm[(kMaxRestart + 1) * (kArnThreads / 32)];
+  __shared__ double hs[kMaxRestart];
+  __shared__ double red[kArnThreads];
+  __shared__ double hsum[kMaxRestart + 1];
+  const int j = k.st->j;
+  const int nv = j + 1;
+  if (threadIdx.x < nv) hs[threadIdx.x] = k.st->h1[threadIdx.x];
+  __syncthreads();
+  double acc[kMaxRestart];
+#pragma unroll
+  for (int v = 0; v < kMaxRestart; ++v) acc[v] = 0.0;
+  double n2[1] = {0.0};
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x) {
+    double wr = k.w[r];
+#pragma unroll
+    for (int v = 0; v < kMaxRestart; ++v)
+      if (v < nv) wr = fma(-hs[v], k.V[(size_t)v * k.n + r], wr);
+    k.w[r] = wr;
+#pragma unroll
+    for (int v = 0; v < kMaxRestart; ++v)
+      if (v < nv) acc[v] = fma(k.V[(size_t)v * k.n + r], wr, acc[v]);  // L1 hits
+    n2[0] = fma(wr, wr, n2[0]);
+  }
+  // partial[cta][0..nv) = h2 dots, partial[cta][nv] = ||w||^2
+  double* part = k.partial + (size_t)blockIdx.x * (kMaxRestart + 1);
+  cta_reduce_wide<kArnThreads, kMaxRestart>(acc, nv, sm, part);
+  cta_reduce_wide<kArnThreads, 1>(n2, 1, sm, part + nv);
+  if (last_block(k.ticket)) {
+    finish_wide<kArnThreads>(k, nv + 1, hsum, red);
+    if (threadIdx.x < nv) k.st->h2[threadIdx.x] = hsum[threadIdx.x];
+    __shared__ double s_hn;
+    if (threadIdx.x == 0) {
+      double h2sq = 0.0;
+      for (int v = 0; v < nv; ++v) h2sq += hsum[v] * hsum[v];
+      s_hn = sqrt(fmax(hsum[nv] - h2sq, 0.0));
+    }
+    __syncthreads();
+    givens_step(k, s_hn);
+  }
+}
+
+// (C) w -= V h2 ; v_{j+1} = w / h_{j+1,j} ; u = v_{j+1} / scale
+__global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
+  __shared__ double hs[kMaxRestart];
+  const KState* st = k.st;
+  const int jn = st->j;  // already advanced by Givens
+  const int nv = jn;
+  if (threadIdx.x < nv) hs[threadIdx.x] = st->h2[threadIdx.x];
+  __syncthreads();
+  const double hn = st->hn;
+  const bool lucky = hn < 1e-14;
+  double* vj = k.V + (size_t)jn * k.n;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x) {
+    double wr = k.w[r];
+#pragma unroll
+    for (int v = 0; v < kMaxRestart; ++v)
+      if (v < nv) wr = fma(-hs[v], k.V[(size_t)v * k.n + r], wr);
+    if (!lucky) {
+      const double vv = wr / hn;
+      vj[r] = vv;
+      k.ubuf[r] = vv / k.scale[r];
+    }
+  }
+}
 }  // namespace fsigpu

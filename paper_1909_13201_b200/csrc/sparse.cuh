@@ -247,6 +247,58 @@ __global__ void gj_init_kernel(int n, double* __restrict__ W) {
 }  // namespace fsigpu
 
 namespace fsigpu {
+// ---- fused coarse-grid correction + post-smoothing residual -------------
+//   x[i]  += (P ec_m)[i]           if !cmask[i]      (gmg.cpp:233-236)
+//   r[i]   = r_pre[i] - (AP_m ec_m)[i]               (= b - A x_new)
+// with AP_m = A * diag(!cmask) * P precomputed at setup and ec_m the coarse
+// correction masked by the coarse col mask (gmg.cpp:230-231).
+template <int LPR>
+__device__ __forceinline__ double row_sum(const int* __restrict__ ptr, const int* __restrict__ idx,
+                                          const double* __restrict__ val, int row, int lane, const double* x,
+                                          const unsigned char* mask) {
+  const int k0 = row >= 0 ? __ldg(ptr + row) : 0, k1 = row >= 0 ? __ldg(ptr + row + 1) : 0;
+  double s = 0.0;
+  constexpr int U = 4;
+  for (int kb = k0 + lane; kb < k1; kb += U * LPR) {
+    int c[U];
+    double v[U], xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = kb + u * LPR;
+      const bool ok = k < k1;
+      c[u] = ok ? __ldg(idx + k) : -1;
+      v[u] = ok ? __ldg(val + k) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = (c[u] >= 0 && !__ldg(mask + c[u])) ? __ldg(x + c[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) s = fma(v[u], xv[u], s);
+  }
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, LPR);
+  return s;
+}
+
+template <int LPR>
+__global__ void __launch_bounds__(256) prolong_resid_kernel(int rows, const int* __restrict__ pp,
+                                                            const int* __restrict__ pi, const double* __restrict__ pv,
+                                                            const int* __restrict__ ap, const int* __restrict__ ai,
+                                                            const double* __restrict__ av, const double* ec,
+                                                            const unsigned char* __restrict__ cmask_coarse,
+                                                            const unsigned char* __restrict__ cmask, double* x,
+                                                            const double* r_pre, double* r) {
+  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = (int)(gt / LPR);
+  const int lane = threadIdx.x & (LPR - 1);
+  const bool ok = row < rows;
+  const double s1 = row_sum<LPR>(pp, pi, pv, ok ? row : -1, lane, ec, cmask_coarse);
+  const double s2 = row_sum<LPR>(ap, ai, av, ok ? row : -1, lane, ec, cmask_coarse);
+  if (ok && lane == 0) {
+    if (!cmask[row]) x[row] = x[row] + s1;
+    r[row] = r_pre[row] - s2;
+  }
+}
+
 // ---- assembled FS operator (setup): COO entries of
 //   sum_b R_b^T inv(A_b) R_b / cover  (additive Schwarz, precond.cpp:44-57)
 // one CTA per block; key = (row << 32) | col

@@ -104,6 +104,7 @@ def lib():
             "fsigpu_fs_apply": ([vp, ip, vp, vp], ip),
             "fsigpu_coarse_solve": ([vp, vp, vp], ip),
             "fsigpu_gmg_destroy": ([vp], None),
+            "fsigpu_gmg_time_kernel": ([vp, ip, ip, ip, ip, C.POINTER(d), C.POINTER(d)], ip),
             "fsigpu_gmres_create": ([vp, vp, ip, C.POINTER(vp)], ip),
             "fsigpu_gmres_solve": ([vp, vp, vp, vp, ip, d, d, vp, C.POINTER(GmresResultC)], ip),
             "fsigpu_gmres_solve_dev": ([vp, vp, vp, ip, d, d, vp, C.POINTER(GmresResultC)], ip),
@@ -296,6 +297,15 @@ class GmgPreconditioner:
 
     def size(self) -> int:
         return self.n
+
+    KERNELS = {"fs_smoother": 0, "residual": 1, "prolong_resid": 2, "restrict": 3, "coarse": 4}
+
+    def time_kernel(self, which: str, level: int, reps: int = 20, cold: bool = True):
+        """(ms per launch, algorithmic bytes per launch) of one V-cycle kernel."""
+        ms, by = C.c_double(), C.c_double()
+        _check(lib().fsigpu_gmg_time_kernel(self.h, self.KERNELS[which], level, reps, 1 if cold else 0,
+                                            C.byref(ms), C.byref(by)))
+        return ms.value, by.value
 
     def persist_bytes(self) -> int:
         return int(lib().fsigpu_gmg_persist_bytes(self.h))
