@@ -413,6 +413,33 @@ __global__ void __launch_bounds__(kSolveThreads) inv_gemv_kernel(SolveArgs a) {
 }
 
 // ---------------------------------------------------------------- LU
+// inv(L_pp) (unit lower, strict part) and inv(U_pp) (upper) of the kb x kb
+// diagonal tile at k0 of a column-major m x m factor A, written to S
+// (column c at S[c*33 ..], stride 33 keeps the 32 threads on distinct
+// banks). Thread c < kb inverts column c by column-oriented substitution:
+// within a step the updates are independent, so shared-memory accesses
+// pipeline instead of forming dependent chains.
+constexpr int kTileLd = 33;
+__device__ __forceinline__ void tile_inverses(const double* A, int m, int k0, int kb, double* S, int t) {
+  if (t >= kb) return;
+  const int c = t;
+  double* x = S + c * kTileLd;
+  for (int i = 0; i < kb; ++i) x[i] = (i == c) ? 1.0 : 0.0;
+  for (int k = c; k < kb; ++k) {  // lower: L x = e_c
+    const double xk = x[k];
+    const double* Lk = A + (size_t)(k0 + k) * m + k0;
+    for (int i = k + 1; i < kb; ++i) x[i] = fma(-Lk[i], xk, x[i]);
+  }
+  // the upper solve touches only x[0..c]: the strict-lower result at
+  // x[c+1..kb) stays in place
+  for (int i = 0; i <= c; ++i) x[i] = (i == c) ? 1.0 : 0.0;
+  for (int k = c; k >= 0; --k) {  // upper: U x = e_c
+    const double* Uk = A + (size_t)(k0 + k) * m + k0;
+    const double xk = x[k] / Uk[k];
+    x[k] = xk;
+    for (int i = 0; i < k; ++i) x[i] = fma(-Uk[i], xk, x[i]);
+  }
+}
 
 // Factor one block per CTA (DenseFactorization ctor, dense.cpp:31-67), then
 // write the solve format (tile inverses + packed panels, see PanelGeom).
@@ -549,24 +576,11 @@ __global__ void __launch_bounds__(NT)
   for (int p = 0; p < P; ++p) {
     const PanelGeom g(m, p);
     const int k0 = g.k0, kb = g.kb;
-    if (tid < kb) {
-      const int c = tid;
-      for (int i = c + 1; i < kb; ++i) {  // inv(L_pp)[i][c], unit lower
-        double s = A[(size_t)(k0 + c) * m + k0 + i];
-        for (int k = c + 1; k < i; ++k) s += A[(size_t)(k0 + k) * m + k0 + i] * S[c * 32 + k];
-        S[c * 32 + i] = -s;
-      }
-      S[c * 32 + c] = 1.0 / A[(size_t)(k0 + c) * m + k0 + c];  // inv(U_pp)[i][c], i <= c
-      for (int i = c - 1; i >= 0; --i) {
-        double s = 0.0;
-        for (int k = i + 1; k <= c; ++k) s += A[(size_t)(k0 + k) * m + k0 + i] * S[c * 32 + k];
-        S[c * 32 + i] = -s / A[(size_t)(k0 + i) * m + k0 + i];
-      }
-    }
+    tile_inverses(A, m, k0, kb, S, tid);
     __syncthreads();
     double* fw = dst + po;
     for (int kk = 0; kk < kb; ++kk)
-      for (int i = kk + 1 + tid; i < kb; i += NT) fw[ltri_col(kb, kk) + i - kk - 1] = S[kk * 32 + i];
+      for (int i = kk + 1 + tid; i < kb; i += NT) fw[ltri_col(kb, kk) + i - kk - 1] = S[kk * kTileLd + i];
     if (tid == 0 && g.lte > g.lt) fw[g.lt] = 0.0;
     double* lp = fw + g.lte;
     for (int e = tid; e < g.hLe * kb; e += NT) {
@@ -575,7 +589,7 @@ __global__ void __launch_bounds__(NT)
     }
     double* bw = fw + g.fwd_size();
     for (int jj = 0; jj < kb; ++jj)
-      for (int i = tid; i <= jj; i += NT) bw[utri_col(jj) + i] = S[jj * 32 + i];
+      for (int i = tid; i <= jj; i += NT) bw[utri_col(jj) + i] = S[jj * kTileLd + i];
     if (tid == 0 && g.ute > g.ut) bw[g.ut] = 0.0;
     double* up = bw + g.ute;
     for (int e = tid; e < k0 * kb; e += NT) {

@@ -258,60 +258,65 @@ struct Blocks {
     }
   }
 
-  // LU of every block from src (column-major, lu_off offsets).
-  void factor(const double* src, const int* src_pos, int pos_base, cudaStream_t s) {
-    DevBuf<int> fail(1);
-    const int big = INT_MAX;
-    FSI_CUDA(cudaMemcpyAsync(fail.p, &big, sizeof(int), cudaMemcpyHostToDevice, s));
-    std::vector<int> cls_s, cls_m, cls_g;
-    int mx_s = 0, mx_m = 0, mx_g = 0;
+  // LU of every block from src (column-major, lu_off offsets). The three
+  // size classes (register/smem small, smem large, global) and their block
+  // lists are fixed at layout time, so a refactor only launches kernels.
+  std::vector<int> h_cls[3];
+  DevBuf<int> d_cls[3];
+  int cls_max[3] = {0, 0, 0};
+  DevBuf<int> fail;
+  void build_classes(cudaStream_t s) {
+    for (int c = 0; c < 3; ++c) {
+      h_cls[c].clear();
+      cls_max[c] = 0;
+    }
     for (long long b = 0; b < nb; ++b) {
       const int mm = h_m[b];
-      if (mm <= 64) {
-        cls_s.push_back((int)b);
-        mx_s = std::max(mx_s, mm);
-      } else if (mm <= 164) {
-        cls_m.push_back((int)b);
-        mx_m = std::max(mx_m, mm);
-      } else {
-        cls_g.push_back((int)b);
-        mx_g = std::max(mx_g, mm);
-      }
+      const int c = mm <= 64 ? 0 : mm <= 164 ? 1 : 2;
+      h_cls[c].push_back((int)b);
+      cls_max[c] = std::max(cls_max[c], mm);
     }
+    for (int c = 0; c < 3; ++c)
+      if (!h_cls[c].empty()) d_cls[c].upload(h_cls[c], s);
+    fail.alloc(1);
+  }
+  void factor(const double* src, const int* src_pos, int pos_base, cudaStream_t s) {
+    if (!fail.n) build_classes(s);
+    const int big = INT_MAX;
+    FSI_CUDA(cudaMemcpyAsync(fail.p, &big, sizeof(int), cudaMemcpyHostToDevice, s));
     double* luo = keep_lu ? lu.p : nullptr;
     auto smem_bytes = [](int mx, bool staged) {
-      return (size_t)((staged ? (size_t)mx * mx : 0) + mx + (mx + 1) / 2 + 1024) * 8;
+      return (size_t)((staged ? (size_t)mx * mx : 0) + mx + (mx + 1) / 2 + 32 * 33 + 8) * 8;
     };
-    auto run = [&](std::vector<int>& cls, int mx, int which) {
-      if (cls.empty()) return;
-      DevBuf<int> bl;
-      bl.upload(cls, s);
-      const int grid = (int)cls.size();
+    auto run = [&](int which) {
+      if (h_cls[which].empty()) return;
+      const int grid = (int)h_cls[which].size();
+      const int mx = cls_max[which];
+      const int* bl = d_cls[which].p;
       if (which == 0) {
         const size_t sm = smem_bytes(mx, true);
         auto k = lu_factor_kernel<128, true>;
         FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        k<<<grid, 128, sm, s>>>(bl.p, m.p, lu_off.p, row_off.p, sf_off.p, src, nullptr, luo, sf.p, piv.p, gsrc.p,
+        k<<<grid, 128, sm, s>>>(bl, m.p, lu_off.p, row_off.p, sf_off.p, src, nullptr, luo, sf.p, piv.p, gsrc.p,
                                 lperm.p, src_pos, pos_base, fail.p);
       } else if (which == 1) {
         const size_t sm = smem_bytes(mx, true);
         auto k = lu_factor_kernel<256, true>;
         FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        k<<<grid, 256, sm, s>>>(bl.p, m.p, lu_off.p, row_off.p, sf_off.p, src, nullptr, luo, sf.p, piv.p, gsrc.p,
+        k<<<grid, 256, sm, s>>>(bl, m.p, lu_off.p, row_off.p, sf_off.p, src, nullptr, luo, sf.p, piv.p, gsrc.p,
                                 lperm.p, src_pos, pos_base, fail.p);
       } else {
         const size_t sm = smem_bytes(mx, false);
         auto k = lu_factor_kernel<256, false>;
         FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        k<<<grid, 256, sm, s>>>(bl.p, m.p, lu_off.p, row_off.p, sf_off.p, src, lu.p, lu.p, sf.p, piv.p, gsrc.p,
+        k<<<grid, 256, sm, s>>>(bl, m.p, lu_off.p, row_off.p, sf_off.p, src, lu.p, lu.p, sf.p, piv.p, gsrc.p,
                                 lperm.p, src_pos, pos_base, fail.p);
       }
       FSI_CHECK_LAUNCH();
-      FSI_CUDA(cudaStreamSynchronize(s));  // keep `bl` alive until done
     };
-    run(cls_s, mx_s, 0);
-    run(cls_m, mx_m, 1);
-    run(cls_g, mx_g, 2);
+    run(0);
+    run(1);
+    run(2);
     int bad = 0;
     FSI_CUDA(cudaMemcpyAsync(&bad, fail.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     FSI_CUDA(cudaStreamSynchronize(s));
