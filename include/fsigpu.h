@@ -151,6 +151,9 @@ void fsigpu_gmg_destroy(fsigpu_gmg g);
  * SpMV, 1 level residual SpMV, 2 prolongation + fused residual, 3
  * restriction, 4 coarse GEMV (level 0). cold: flush L2 (256 MB) before each
  * launch; else back to back. */
+/* tuning: lanes per row and batch depth of a level matrix's SpMV launches
+ * (which: 0 A, 1 FS, 2 A*P, 3 P, 4 R) */
+int fsigpu_gmg_set_launch(fsigpu_gmg g, int level, int which, int lpr, int unroll);
 int fsigpu_gmg_time_kernel(fsigpu_gmg g, int which, int level, int reps, int cold, double* ms,
                            double* bytes);
 

@@ -27,7 +27,8 @@
 //   fsi_ref_harness time-blocks <n54> <n59> <nsolve> [--threads T] [--seed S]
 // cases: cfg0 (unit square 8->16->32), sq4 (8->64, 4 levels), chan (reference
 // unit_solver channel nx=4 ny_fluid=2 ny_wall=1, 2 levels), changmg (unit_gmg
-// channel, ny_wall=2, 2 levels), cfg2 (bulge 16->256, 5 levels).
+// channel, ny_wall=2, 2 levels), cfg2 (bulge 16->256, 5 levels), cfg2l4 (bulge
+// 16->128, 4 levels).
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -180,7 +181,7 @@ CaseDef make_case(const std::string& name) {
     c.bcs = channel_pulse_bcs(name == "chan" ? 15.0 : 0.1);
     c.dt = 1.0 / 32.0;
     c.t_eval = 1.0 / 32.0;
-  } else if (name == "cfg2") {
+  } else if (name == "cfg2" || name == "cfg2l4") {
     // bulge, 1 coarse wall row -> 16 fine rows (D10)
     c.geo.name = "bulge";
     c.geo.length = 1.0;
@@ -192,7 +193,7 @@ CaseDef make_case(const std::string& name) {
     c.geo.bulge_height = 0.2;
     c.geo.bulge_width = 0.4;
     c.geo.bulge_center = 0.5;
-    c.levels = 5;
+    c.levels = (name == "cfg2") ? 5 : 4;  // cfg2l4: same case one level coarser (16 -> 128)
     c.mat = cfg_material();
     c.bcs = {bc("inlet", BcKind::DisplacementDirichlet), bc("inlet", BcKind::VelocityDirichlet),
              bc("clamp_in", BcKind::DisplacementDirichlet), bc("clamp_in", BcKind::VelocityDirichlet),
@@ -454,7 +455,7 @@ SolveOut run_gmres(const Problem& P, bool additive, const KrylovConfig& kc) {
 struct Args {
   std::vector<std::string> pos;
   unsigned long long seed = 20240901ull;
-  int reps = 1, max_iters = 2000, threads = 1;
+  int reps = 1, max_iters = 2000, threads = 1, block_stride = 1;
   double rtol = 1e-10;
   bool no_mult = false, no_gmres = false;
   std::string mode = "add";
@@ -473,6 +474,7 @@ Args parse(int argc, char** argv) {
     else if (s == "--max-iters") a.max_iters = std::stoi(next());
     else if (s == "--threads") a.threads = std::stoi(next());
     else if (s == "--rtol") a.rtol = std::stod(next());
+    else if (s == "--block-stride") a.block_stride = std::stoi(next());
     else if (s == "--mode") a.mode = next();
     else if (s == "--no-mult") a.no_mult = true;
     else if (s == "--no-gmres") a.no_gmres = true;
@@ -548,7 +550,10 @@ int cmd_export(const Args& a) {
     // per-block dense solves (AS1 then AS2 blocks of the fine level)
     const AdditiveFs& f = *P->fs_add[top];
     std::vector<double> rhs, xs;
-    for (int b = 0; b < f.as1->n_blocks(); ++b) {
+    std::vector<int> ids;  // sampled block ids (AS1 then AS2 numbering)
+    const int stride = std::max(1, a.block_stride);
+    for (int b = 0; b < f.as1->n_blocks(); b += stride) {
+      ids.push_back(b);
       const IndexSet& s = f.as1->block_dofs(b);
       auto lu = factor_principal_block(P->fs[top]->group1_matrix(), s);
       auto bb = seeded(s.size(), rng);
@@ -556,7 +561,8 @@ int cmd_export(const Args& a) {
       rhs.insert(rhs.end(), bb.begin(), bb.end());
       xs.insert(xs.end(), xx.begin(), xx.end());
     }
-    for (int b = 0; b < f.as2f->n_blocks(); ++b) {
+    for (int b = 0; b < f.as2f->n_blocks(); b += stride) {
+      ids.push_back(f.as1->n_blocks() + b);
       const IndexSet& s = f.as2f->block_dofs(b);
       auto lu = factor_principal_block(P->fs[top]->group2_matrix(), s);
       auto bb = seeded(s.size(), rng);
@@ -564,6 +570,7 @@ int cmd_export(const Args& a) {
       rhs.insert(rhs.end(), bb.begin(), bb.end());
       xs.insert(xs.end(), xx.begin(), xx.end());
     }
+    ar.put("golden/block_ids", ids);
     ar.put("golden/block_rhs", rhs);
     ar.put("golden/block_x", xs);
     // one V-cycle of the additive GMG

@@ -104,6 +104,19 @@ static long long g_launches = 0;
 static inline void counted(int k = 1) { g_launches += k; }
 
 // ------------------------------------------------------------ CSR
+// Lanes per row: the power of two nearest to avg_nnz / target, where target
+// entries per lane is 4 for small (latency-bound, L2-resident) matrices and
+// 8 for large (HBM-bound) ones; from the launch-shape sweeps of
+// tools/tune_spmv.py on configs 0 and 2.
+static int choose_lpr(long long rows, long long nnz) {
+  if (rows <= 0) return 2;
+  const double target = rows >= 65536 ? 8.0 : 4.0;
+  const double want = (double)nnz / rows / target;
+  int l = 2;
+  while (l < 32 && want > l * 1.41421356) l *= 2;
+  return l;
+}
+
 struct Csr {
   int rows = 0, cols = 0;
   long long nnz = 0;
@@ -126,9 +139,7 @@ struct Csr {
     ptr.upload(p, (size_t)r + 1, s);
     idx.upload(ix, (size_t)nnz, s);
     val.upload(v, (size_t)nnz, s);
-    const double avg = r ? (double)nnz / r : 0.0;
-    // ~4 entries per lane per row: one predicated batch (csr_kernel U = 4)
-    lpr = avg <= 6 ? 2 : avg <= 12 ? 4 : avg <= 24 ? 8 : avg <= 72 ? 16 : 32;
+    lpr = choose_lpr(r, nnz);
     if (keep_host) {
       h_ptr.assign(p, p + r + 1);
       h_idx.assign(ix, ix + nnz);
@@ -144,24 +155,36 @@ struct Csr {
     idx = std::move(ix);
     val = std::move(v);
     nnz = (long long)idx.n;
-    const double avg = r ? (double)nnz / r : 0.0;
-    lpr = avg <= 6 ? 2 : avg <= 12 ? 4 : avg <= 24 ? 8 : avg <= 72 ? 16 : 32;
+    lpr = choose_lpr(r, nnz);
   }
   double bytes(bool resid) const {
     return 12.0 * nnz + 4.0 * (rows + 1) + 8.0 * cols + 8.0 * rows + (resid ? 8.0 * rows : 0.0);
   }
+  int unroll = 4;  // entries per lane per predicated batch (4 or 8)
   template <class G, class E>
   void launch(G g, E e, cudaStream_t s) const {
     if (!rows) return;
     const long long threads = (long long)rows * lpr;
     const int grid = ceil_div(threads, 256);
-    switch (lpr) {
-      case 2: csr_kernel<2><<<grid, 256, 0, s>>>(rows, ptr.p, idx.p, val.p, g, e); break;
-      case 4: csr_kernel<4><<<grid, 256, 0, s>>>(rows, ptr.p, idx.p, val.p, g, e); break;
-      case 8: csr_kernel<8><<<grid, 256, 0, s>>>(rows, ptr.p, idx.p, val.p, g, e); break;
-      case 16: csr_kernel<16><<<grid, 256, 0, s>>>(rows, ptr.p, idx.p, val.p, g, e); break;
-      default: csr_kernel<32><<<grid, 256, 0, s>>>(rows, ptr.p, idx.p, val.p, g, e); break;
+#define FSI_CSR(LP, UU) csr_kernel<LP, G, E, UU><<<grid, 256, 0, s>>>(rows, ptr.p, idx.p, val.p, g, e)
+    if (unroll == 8) {
+      switch (lpr) {
+        case 2: FSI_CSR(2, 8); break;
+        case 4: FSI_CSR(4, 8); break;
+        case 8: FSI_CSR(8, 8); break;
+        case 16: FSI_CSR(16, 8); break;
+        default: FSI_CSR(32, 8); break;
+      }
+    } else {
+      switch (lpr) {
+        case 2: FSI_CSR(2, 4); break;
+        case 4: FSI_CSR(4, 4); break;
+        case 8: FSI_CSR(8, 4); break;
+        case 16: FSI_CSR(16, 4); break;
+        default: FSI_CSR(32, 4); break;
+      }
     }
+#undef FSI_CSR
     FSI_CHECK_LAUNCH();
     counted();
   }
@@ -1263,6 +1286,20 @@ int fsigpu_set_l2_persist(int enable) {
   return guarded([&] { g_l2_persist = enable != 0; });
 }
 long long fsigpu_gmg_persist_bytes(fsigpu_gmg g) { return g ? (long long)g->g.persist_bytes : 0; }
+
+// Tuning: launch shape (lanes per row, entries per lane per batch) of one
+// level matrix. which: 0 A, 1 FS, 2 AP, 3 P, 4 R.
+int fsigpu_gmg_set_launch(fsigpu_gmg h, int level, int which, int lpr, int unroll) {
+  return guarded([&] {
+    require(h != nullptr && level >= 0 && level < (int)h->g.lv.size(), "launch: bad level");
+    require(lpr == 2 || lpr == 4 || lpr == 8 || lpr == 16 || lpr == 32, "launch: lpr must be 2..32");
+    require(unroll == 4 || unroll == 8, "launch: unroll must be 4 or 8");
+    Level& L = h->g.lv[level];
+    Csr* c = which == 0 ? &L.A : which == 1 ? &L.FS : which == 2 ? &L.AP : which == 3 ? &L.P : &L.R;
+    c->lpr = lpr;
+    c->unroll = unroll;
+  });
+}
 int fsigpu_set_block_mode(int mode) {
   return guarded([&] {
     require(mode == kModeLU || mode == kModeInverse || mode == kModeAssembled,

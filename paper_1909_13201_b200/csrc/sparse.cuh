@@ -73,7 +73,7 @@ struct GatherMasked {
   __device__ double operator()(int c) const { return __ldg(mask + c) ? 0.0 : __ldg(x + c); }
 };
 
-template <int LPR, class Gather, class Epi>
+template <int LPR, class Gather, class Epi, int U = 4>
 __global__ void __launch_bounds__(256) csr_kernel(int rows, const int* __restrict__ ptr,
                                                   const int* __restrict__ idx,
                                                   const double* __restrict__ val, Gather gx,
@@ -88,7 +88,6 @@ __global__ void __launch_bounds__(256) csr_kernel(int rows, const int* __restric
   double s = 0.0;
   // predicated batches of U entries per lane: all index/value loads of a
   // batch are in flight before the dependent x gathers (no early exits)
-  constexpr int U = 4;
   for (int kb = k0 + lane; kb < k1; kb += U * LPR) {
     int c[U];
     double v[U], xv[U];

@@ -104,6 +104,7 @@ def lib():
             "fsigpu_fs_apply": ([vp, ip, vp, vp], ip),
             "fsigpu_coarse_solve": ([vp, vp, vp], ip),
             "fsigpu_gmg_destroy": ([vp], None),
+            "fsigpu_gmg_set_launch": ([vp, ip, ip, ip, ip], ip),
             "fsigpu_gmg_time_kernel": ([vp, ip, ip, ip, ip, C.POINTER(d), C.POINTER(d)], ip),
             "fsigpu_gmres_create": ([vp, vp, ip, C.POINTER(vp)], ip),
             "fsigpu_gmres_solve": ([vp, vp, vp, vp, ip, d, d, vp, C.POINTER(GmresResultC)], ip),
@@ -306,6 +307,10 @@ class GmgPreconditioner:
         _check(lib().fsigpu_gmg_time_kernel(self.h, self.KERNELS[which], level, reps, 1 if cold else 0,
                                             C.byref(ms), C.byref(by)))
         return ms.value, by.value
+
+    def set_launch(self, level: int, which: str, lpr: int, unroll: int = 4):
+        w = {"A": 0, "FS": 1, "AP": 2, "P": 3, "R": 4}[which]
+        _check(lib().fsigpu_gmg_set_launch(self.h, level, w, lpr, unroll))
 
     def persist_bytes(self) -> int:
         return int(lib().fsigpu_gmg_persist_bytes(self.h))
