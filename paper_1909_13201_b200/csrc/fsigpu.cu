@@ -503,25 +503,29 @@ struct Gmg {
     ProfScope ps(FSIGPU_K_SPMV, L.A.bytes(true), s);
     L.A.launch(GatherPlain{L.x}, EpiResid{L.b, r}, s);
   }
-  // x (+)= omega * FS r, fused into the FS SpMV epilogue
-  void fs_spmv(int l, const double* r, int x_zero) {
+  // x (+)= omega * FS r, fused into the FS SpMV epilogue; mask_out: the
+  // level's constrained columns are zeroed on the way out (last write of a
+  // coarse level in a V-cycle, see cycle())
+  void fs_spmv(int l, const double* r, int x_zero, bool mask_out = false) {
     Level& L = lv[l];
     ProfScope ps(FSIGPU_K_BLOCK_SOLVE, L.FS.bytes(false) + 8.0 * L.n, s);
     if (x_zero)
       L.FS.launch(GatherPlain{r}, EpiSetScaled{omega, L.x}, s);
+    else if (mask_out)
+      L.FS.launch(GatherPlain{r}, EpiAxpyMasked{omega, L.x, L.cmask.p}, s);
     else
       L.FS.launch(GatherPlain{r}, EpiAxpy{omega, L.x}, s);
   }
   // one FS-preconditioned Richardson sweep; x_zero: x == 0 on entry;
   // r_ready: rbuf already holds b - A x (fused prolongation kernel)
-  void sweep(int l, int x_zero, bool r_ready = false) {
+  void sweep(int l, int x_zero, bool r_ready = false, bool mask_out = false) {
     Level& L = lv[l];
     if (L.assembled) {
       if (x_zero) {
         fs_spmv(l, L.b, 1);  // res = b - A*0 = b (precond.cpp:312-313)
       } else {
         if (!r_ready) resid(l, L.rbuf.p);
-        fs_spmv(l, L.rbuf.p, 0);
+        fs_spmv(l, L.rbuf.p, 0, mask_out);
       }
       return;
     }
@@ -540,7 +544,7 @@ struct Gmg {
       combine(l, L.rbuf.p, 0);
     }
   }
-  void coarse(int x_zero) {
+  void coarse(int x_zero, bool mask_out = false) {
     Level& L = lv[0];
     const double* rhs = L.b;
     if (!x_zero) {
@@ -548,14 +552,17 @@ struct Gmg {
       rhs = L.rbuf.p;
     }
     ProfScope ps(FSIGPU_K_COARSE, 8.0 * L.n * L.n + 16.0 * L.n, s);
-    gemv_kernel<<<ceil_div((long long)L.n * 32, 256), 256, 0, s>>>(L.n, coarse_inv.p, rhs, L.x, x_zero ? 0 : 1);
+    gemv_kernel<<<ceil_div((long long)L.n * 32, 256), 256, 0, s>>>(L.n, coarse_inv.p, rhs, L.x, x_zero ? 0 : 1,
+                                                                    mask_out ? L.cmask.p : nullptr);
     FSI_CHECK_LAUNCH();
     counted();
   }
-  // GmgPreconditioner::cycle (gmg.cpp:188-239)
-  void cycle(int l, char mode, int x_zero) {
+  // GmgPreconditioner::cycle (gmg.cpp:188-239). mask_out: this is the last
+  // visit of a coarse level, so its final kernel may write the iterate with
+  // the constrained columns already zeroed (the caller's ec mask).
+  void cycle(int l, char mode, int x_zero, bool mask_out = false) {
     if (l == 0) {
-      coarse(x_zero);
+      coarse(x_zero, mask_out);
       return;
     }
     Level& L = lv[l];
@@ -567,10 +574,13 @@ struct Gmg {
       ProfScope ps(FSIGPU_K_TRANSFER, L.R.bytes(false) + L.nc, s);
       L.R.launch(GatherPlain{L.rbuf.p}, EpiRestrict{B.rmask.p, B.b}, s);
     }
+    // the last visit of level l-1 masks its output iff that level ends in a
+    // kernel that can (a post sweep of an assembled level, or the coarse GEMV)
+    const bool fused_mask = L.AP.rows && post > 0 && (l - 1 == 0 || (B.assembled && post > 0));
     switch (mode) {
-      case 'v': cycle(l - 1, 'v', 1); break;
-      case 'w': cycle(l - 1, 'w', 1); cycle(l - 1, 'w', 0); break;
-      case 'f': cycle(l - 1, 'f', 1); cycle(l - 1, 'v', 0); break;
+      case 'v': cycle(l - 1, 'v', 1, fused_mask); break;
+      case 'w': cycle(l - 1, 'w', 1); cycle(l - 1, 'w', 0, fused_mask); break;
+      case 'f': cycle(l - 1, 'f', 1); cycle(l - 1, 'v', 0, fused_mask); break;
       default: throw Error(FSIGPU_ERR_INVALID, "gmg: unknown cycle type");
     }
     if (post > 0 && L.AP.rows) {
@@ -581,7 +591,8 @@ struct Gmg {
 #define FSI_PR(LP)                                                                                              \
   case LP:                                                                                                      \
     prolong_resid_kernel<LP><<<grid, 256, 0, s>>>(L.n, L.P.ptr.p, L.P.idx.p, L.P.val.p, L.AP.ptr.p, L.AP.idx.p, \
-                                                  L.AP.val.p, B.x, B.cmask.p, L.cmask.p, L.x, L.rbuf.p, L.rbuf.p); \
+                                                  L.AP.val.p, B.x, fused_mask ? nullptr : B.cmask.p, L.cmask.p, \
+                                                  L.x, L.rbuf.p, L.rbuf.p);                                     \
     break;
         FSI_PR(2)
         FSI_PR(4)
@@ -593,7 +604,7 @@ struct Gmg {
       }
       FSI_CHECK_LAUNCH();
       counted();
-      for (int k = 0; k < post; ++k) sweep(l, 0, k == 0);
+      for (int k = 0; k < post; ++k) sweep(l, 0, k == 0, mask_out && k == post - 1);
       return;
     }
     {

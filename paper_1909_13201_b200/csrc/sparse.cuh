@@ -61,6 +61,15 @@ struct EpiAxpy {  // x += omega * (FS r)          (precond.cpp:315)
   double* x;
   __device__ void operator()(int i, double s) const { x[i] = add_rn(x[i], mul_rn(omega, s)); }
 };
+// last write of a coarse level's iterate in a V-cycle: the caller masks the
+// correction at constrained columns (gmg.cpp:230-231); doing it here lets
+// the prolongation gather plain values
+struct EpiAxpyMasked {
+  double omega;
+  double* x;
+  const unsigned char* mask;
+  __device__ void operator()(int i, double s) const { x[i] = mask[i] ? 0.0 : add_rn(x[i], mul_rn(omega, s)); }
+};
 
 // x gather, optionally masked (ec[constrained_cols below] = 0, gmg.cpp:230-231)
 struct GatherPlain {
@@ -136,7 +145,8 @@ __global__ void fs_combine_kernel(int n, int g1, int n_us, const int* __restrict
 // (row-major n0 x n0), one warp per row.
 __global__ void __launch_bounds__(256) gemv_kernel(int n, const double* __restrict__ M,
                                                    const double* __restrict__ b,
-                                                   double* __restrict__ x, int accumulate) {
+                                                   double* __restrict__ x, int accumulate,
+                                                   const unsigned char* __restrict__ mask_out = nullptr) {
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= n) return;  // warp-uniform
@@ -156,7 +166,7 @@ __global__ void __launch_bounds__(256) gemv_kernel(int n, const double* __restri
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-  if (lane == 0) x[row] = accumulate ? x[row] + s : s;
+  if (lane == 0) x[row] = (mask_out && mask_out[row]) ? 0.0 : (accumulate ? x[row] + s : s);
 }
 
 // ---- setup: Gauss-Jordan inverse with partial pivoting on W = [A | I] ----
@@ -254,7 +264,7 @@ namespace fsigpu {
 template <int LPR>
 __device__ __forceinline__ double row_sum(const int* __restrict__ ptr, const int* __restrict__ idx,
                                           const double* __restrict__ val, int row, int lane, const double* x,
-                                          const unsigned char* mask) {
+                                          const unsigned char* mask /* nullptr: x already masked */) {
   const int k0 = row >= 0 ? __ldg(ptr + row) : 0, k1 = row >= 0 ? __ldg(ptr + row + 1) : 0;
   double s = 0.0;
   constexpr int U = 4;
@@ -269,7 +279,8 @@ __device__ __forceinline__ double row_sum(const int* __restrict__ ptr, const int
       v[u] = ok ? __ldg(val + k) : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) xv[u] = (c[u] >= 0 && !__ldg(mask + c[u])) ? __ldg(x + c[u]) : 0.0;
+    for (int u = 0; u < U; ++u)
+      xv[u] = c[u] >= 0 ? ((mask && __ldg(mask + c[u])) ? 0.0 : __ldg(x + c[u])) : 0.0;
 #pragma unroll
     for (int u = 0; u < U; ++u) s = fma(v[u], xv[u], s);
   }
