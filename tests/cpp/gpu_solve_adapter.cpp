@@ -1,0 +1,114 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// The drop-in adapter of INTEGRATION.md, compiled against the reference's
+// own headers (proj/include/fsi) and the fsigpu C ABI. It is what a
+// maintainer adds to the reference tree to replace the solve block of
+// FsiSolver::newton_step (proj/src/driver.cpp:257-272). tests/test_abi.py
+// syntax-checks it here and, with a GPU, links it against libfsigpu.so.
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "fsi/driver.hpp"
+#include "fsi/errors.hpp"
+#include "fsi/gmg.hpp"
+#include "fsi/krylov.hpp"
+#include "fsi/precond.hpp"
+#include "fsigpu.h"
+
+namespace fsi {
+namespace {
+
+void check(int rc) {
+  if (rc == FSIGPU_OK) return;
+  if (rc == FSIGPU_ERR_SINGULAR) throw SingularBlockError(fsigpu_last_error());
+  if (rc == FSIGPU_ERR_INVALID) throw std::invalid_argument(fsigpu_last_error());
+  throw SolverError(fsigpu_last_error());
+}
+
+void flatten(const std::vector<const IndexSet*>& sets, std::vector<int>& ptr, std::vector<int>& idx) {
+  ptr.assign(1, 0);
+  idx.clear();
+  for (const IndexSet* s : sets) {
+    idx.insert(idx.end(), s->indices.begin(), s->indices.end());
+    ptr.push_back(static_cast<int>(idx.size()));
+  }
+}
+
+}  // namespace
+
+// GMG with FS smoothers on the GPU, presented as the reference's
+// LinearOperator (include/fsi/krylov.hpp:14-18).
+class GpuGmg final : public LinearOperator {
+ public:
+  GpuGmg(const std::vector<GmgLevel>& levels, const std::vector<const FsPreconditioner*>& fs,
+         const CycleConfig& cfg) {
+    std::vector<fsigpu_level_desc> d(levels.size());
+    for (size_t l = 0; l < levels.size(); ++l) {
+      const SparseMatrix& a = *levels[l].a;
+      fsigpu_level_desc& x = d[l];
+      x = fsigpu_level_desc{};
+      x.n = a.rows();
+      x.a_ptr = a.row_offsets().data();
+      x.a_idx = a.col_indices().data();
+      x.a_val = a.values().data();
+      x.row_mask = levels[l].constrained_rows.data();
+      x.col_mask = levels[l].constrained_cols.data();
+      if (l == 0) continue;
+      x.nc = levels[l].p.cols();
+      x.p_ptr = levels[l].p.row_offsets().data();
+      x.p_idx = levels[l].p.col_indices().data();
+      x.p_val = levels[l].p.values().data();
+      x.r_ptr = levels[l].r.row_offsets().data();
+      x.r_idx = levels[l].r.col_indices().data();
+      x.r_val = levels[l].r.values().data();
+      const FsPreconditioner& f = *fs[l];
+      x.g1 = f.group1_size();
+      x.n_us = f.solid_velocity_size();
+      x.lumped = f.lumped().data();
+      std::vector<const IndexSet*> s1, s2;
+      for (int b = 0; b < f.as1().n_blocks(); ++b) s1.push_back(&f.as1().block_dofs(b));
+      for (int b = 0; b < f.n_fluid_blocks(); ++b) s2.push_back(&f.fluid_block_dofs(b));
+      flatten(s1, as1_ptr_[l], as1_idx_[l]);
+      flatten(s2, as2_ptr_[l], as2_idx_[l]);
+      x.as1_n = static_cast<int>(as1_ptr_[l].size()) - 1;
+      x.as1_ptr = as1_ptr_[l].data();
+      x.as1_idx = as1_idx_[l].data();
+      x.as2_n = static_cast<int>(as2_ptr_[l].size()) - 1;
+      x.as2_ptr = as2_ptr_[l].data();
+      x.as2_idx = as2_idx_[l].data();
+    }
+    check(fsigpu_gmg_create(static_cast<int>(d.size()), d.data(), cfg.omega, cfg.pre, cfg.post, cfg.cycle, &h_));
+  }
+  ~GpuGmg() override { fsigpu_gmg_destroy(h_); }
+  int size() const override { return fsigpu_gmg_size(h_); }
+  void apply(const double* r, double* z) const override { check(fsigpu_gmg_apply(h_, r, z)); }
+  fsigpu_gmg handle() const { return h_; }
+
+ private:
+  fsigpu_gmg h_ = nullptr;
+  std::map<size_t, std::vector<int>> as1_ptr_, as1_idx_, as2_ptr_, as2_idx_;
+};
+
+// Drop-in for gmres(aop, mop, b, cfg) at driver.cpp:262-272.
+GmresResult gpu_gmres(const GpuGmg& g, const std::vector<double>& frame_scale, const std::vector<double>& b,
+                      const KrylovConfig& cfg) {
+  fsigpu_gmres s = nullptr;
+  check(fsigpu_gmres_create(g.handle(), frame_scale.data(), cfg.restart, &s));
+  GmresResult out;
+  out.x.resize(b.size());
+  out.history.resize(static_cast<size_t>(cfg.max_iters) + 2);
+  fsigpu_gmres_result r{};
+  const int rc = fsigpu_gmres_solve(s, b.data(), nullptr, out.x.data(), cfg.max_iters, cfg.rel_tol, cfg.abs_tol,
+                                    out.history.data(), &r);
+  fsigpu_gmres_destroy(s);
+  check(rc);
+  out.history.resize(r.n_history);
+  out.iterations = r.iterations;
+  out.converged = r.converged != 0;
+  out.breakdown = r.breakdown != 0;
+  return out;
+}
+
+}  // namespace fsi

@@ -57,3 +57,17 @@ def test_no_cpu_fallback():
     assert L.fsigpu_init(0) != fsigpu.FSIGPU_OK
     with pytest.raises(fsigpu.SolverError):
         fsigpu._check(L.fsigpu_init(0))
+
+
+def test_integration_adapter_compiles_against_reference_headers():
+    """INTEGRATION.md's drop-in adapter (tests/cpp/gpu_solve_adapter.cpp)
+    type-checks against the reference's headers and include/fsigpu.h."""
+    import shutil
+    import subprocess
+    inc = "/root/reference/proj/include"
+    if not os.path.isdir(inc) or not shutil.which("g++"):
+        pytest.skip("reference headers not available here")
+    src = os.path.join(ROOT, "tests", "cpp", "gpu_solve_adapter.cpp")
+    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-include", "cstdint", "-I", inc,
+                        "-I", os.path.join(ROOT, "include"), src], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]
