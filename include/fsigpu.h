@@ -131,6 +131,8 @@ int fsigpu_set_block_mode(int mode);
  * an access-policy window marks it persisting on the hierarchy's stream
  * (default off: measured slower on config 0). */
 int fsigpu_set_l2_persist(int enable);
+/* programmatic dependent launch of the solve-path kernels (default off: measured neutral) */
+int fsigpu_set_pdl(int enable);
 long long fsigpu_gmg_persist_bytes(fsigpu_gmg g);
 
 /* ---- GMG with additive FS smoothers: GmgPreconditioner (gmg.cpp:178-246),

@@ -109,4 +109,10 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// Programmatic dependent launch (sm_90+): a kernel lets its dependents be
+// scheduled immediately and waits for its producers only before touching
+// their data. Both are no-ops for kernels launched without the attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 }  // namespace fsigpu

@@ -307,7 +307,9 @@ __global__ void __launch_bounds__(kSolveThreads) block_solve_kernel(SolveArgs a)
   extern __shared__ __align__(16) double dsm[];
   __shared__ double xs[kLargeMax];
   __shared__ unsigned long long bars[2];
+  pdl_trigger();
   const SolveItem it = a.items[blockIdx.x];
+  pdl_wait();
   const int tid = threadIdx.x;
   if (it.type == 0 || it.type == 2) {
     const int w = tid >> 5;
@@ -368,7 +370,9 @@ __device__ __forceinline__ void inv_rowpair_dot(const double2* __restrict__ M, i
 __global__ void __launch_bounds__(kSolveThreads) inv_gemv_kernel(SolveArgs a) {
   __shared__ double xs[kLargeMax];
   __shared__ double red[8][kInvTileRows];
+  pdl_trigger();
   const SolveItem it = a.items[blockIdx.x];
+  pdl_wait();
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (it.type == 0) {  // small blocks: warp per block
     if (w >= it.count) return;

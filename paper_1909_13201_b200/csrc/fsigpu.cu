@@ -31,6 +31,28 @@
 
 namespace fsigpu {
 
+// ------------------------------------------------------------ launches
+// Solve-path kernels are launched with programmatic stream serialization
+// (PDL): inside the captured graphs consecutive kernels overlap launch and
+// prologue with the predecessor's tail (kernels call pdl_trigger/pdl_wait).
+static bool g_pdl = false;  // measured neutral on config 0 (tools/ab_test.py); opt-in
+template <typename... KArgs, typename... Args>
+static void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  if (e != cudaSuccess) throw Error(FSIGPU_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
+}
+
 // ------------------------------------------------------------ errors
 static thread_local std::string g_err;
 static thread_local int g_bad_block = -1;
@@ -166,7 +188,7 @@ struct Csr {
     if (!rows) return;
     const long long threads = (long long)rows * lpr;
     const int grid = ceil_div(threads, 256);
-#define FSI_CSR(LP, UU) csr_kernel<LP, G, E, UU><<<grid, 256, 0, s>>>(rows, ptr.p, idx.p, val.p, g, e)
+#define FSI_CSR(LP, UU) launch_k(csr_kernel<LP, G, E, UU>, dim3(grid), dim3(256), 0, s, rows, (const int*)ptr.p, (const int*)idx.p, (const double*)val.p, g, e)
     if (unroll == 8) {
       switch (lpr) {
         case 2: FSI_CSR(2, 8); break;
@@ -405,7 +427,7 @@ struct Blocks {
       a.inv_off = inv_off.p;
       a.pos = pos.n ? pos.p : nullptr;
       ProfScope ps(FSIGPU_K_BLOCK_SOLVE, solve_bytes, s);
-      inv_gemv_kernel<<<n_inv_items, kSolveThreads, 0, s>>>(a);
+      launch_k(inv_gemv_kernel, dim3(n_inv_items), dim3(kSolveThreads), 0, s, a);
       FSI_CHECK_LAUNCH();
       counted();
       return;
@@ -419,7 +441,7 @@ struct Blocks {
     a.items = items.p;
     a.smem_cap = smem_cap;
     ProfScope ps(FSIGPU_K_BLOCK_SOLVE, solve_bytes, s);
-    block_solve_kernel<<<n_items, kSolveThreads, (size_t)2 * smem_cap * 8, s>>>(a);
+    launch_k(block_solve_kernel, dim3(n_items), dim3(kSolveThreads), (size_t)2 * smem_cap * 8, s, a);
     FSI_CHECK_LAUNCH();
     counted();
   }
@@ -493,8 +515,9 @@ struct Gmg {
   void combine(int l, const double* r, int x_zero) {
     Level& L = lv[l];
     ProfScope ps(FSIGPU_K_COMBINE, L.combine_bytes, s);
-    fs_combine_kernel<<<ceil_div(L.n, 256), 256, 0, s>>>(L.n, L.g1, L.n_us, L.inv_ptr.p, L.inv_idx.p, L.delta.p, r,
-                                                         L.lumped.p, omega, L.x, x_zero);
+    launch_k(fs_combine_kernel, dim3(ceil_div(L.n, 256)), dim3(256), 0, s, L.n, L.g1, L.n_us,
+             (const int*)L.inv_ptr.p, (const int*)L.inv_idx.p, (const double*)L.delta.p, r,
+             (const double*)L.lumped.p, omega, L.x, x_zero);
     FSI_CHECK_LAUNCH();
     counted();
   }
@@ -552,8 +575,9 @@ struct Gmg {
       rhs = L.rbuf.p;
     }
     ProfScope ps(FSIGPU_K_COARSE, 8.0 * L.n * L.n + 16.0 * L.n, s);
-    gemv_kernel<<<ceil_div((long long)L.n * 32, 256), 256, 0, s>>>(L.n, coarse_inv.p, rhs, L.x, x_zero ? 0 : 1,
-                                                                    mask_out ? L.cmask.p : nullptr);
+    launch_k(gemv_kernel, dim3(ceil_div((long long)L.n * 32, 256)), dim3(256), 0, s, L.n,
+             (const double*)coarse_inv.p, rhs, L.x, x_zero ? 0 : 1,
+             (const unsigned char*)(mask_out ? L.cmask.p : nullptr));
     FSI_CHECK_LAUNCH();
     counted();
   }
@@ -590,9 +614,11 @@ struct Gmg {
       switch (L.AP.lpr) {
 #define FSI_PR(LP)                                                                                              \
   case LP:                                                                                                      \
-    prolong_resid_kernel<LP><<<grid, 256, 0, s>>>(L.n, L.P.ptr.p, L.P.idx.p, L.P.val.p, L.AP.ptr.p, L.AP.idx.p, \
-                                                  L.AP.val.p, B.x, fused_mask ? nullptr : B.cmask.p, L.cmask.p, \
-                                                  L.x, L.rbuf.p, L.rbuf.p);                                     \
+    launch_k(prolong_resid_kernel<LP>, dim3(grid), dim3(256), 0, s, L.n, (const int*)L.P.ptr.p,             \
+             (const int*)L.P.idx.p, (const double*)L.P.val.p, (const int*)L.AP.ptr.p, (const int*)L.AP.idx.p, \
+             (const double*)L.AP.val.p, (const double*)B.x,                                                 \
+             (const unsigned char*)(fused_mask ? nullptr : B.cmask.p), (const unsigned char*)L.cmask.p,     \
+             L.x, (const double*)L.rbuf.p, L.rbuf.p);                                                       \
     break;
         FSI_PR(2)
         FSI_PR(4)
@@ -1013,13 +1039,13 @@ struct Gmres {
     {
       ProfScope ps(FSIGPU_K_SPMV, T.A.bytes(false) + 8.0 * n * 3, s);
       // 128 rows per CTA in one pass: 8 lanes per row (1024 threads)
-      k_spmv_dots<8><<<gs, kFuseThreads, 0, s>>>(kk);
+      launch_k(k_spmv_dots<8>, dim3(gs), dim3(kFuseThreads), 0, s, kk);
     }
     {
       ProfScope ps(FSIGPU_K_ARNOLDI, 8.0 * n * 4, s);
       const int ga = std::max(1, std::min(ceil_div(n, kArnThreads), 4 * 148));
-      k_update_dots_norm<<<ga, kArnThreads, 0, s>>>(kk);
-      k_update_normalize<<<ga, kArnThreads, 0, s>>>(kk);
+      launch_k(k_update_dots_norm, dim3(ga), dim3(kArnThreads), 0, s, kk);
+      launch_k(k_update_normalize, dim3(ga), dim3(kArnThreads), 0, s, kk);
     }
     FSI_CHECK_LAUNCH();
     counted(3);
@@ -1030,10 +1056,10 @@ struct Gmres {
   }
   void cycle_tail() {
     cudaStream_t s = g->s;
-    k_solve_y<<<1, 256, 0, s>>>(kb);
-    k_update_x<<<grid, kKThreads, 0, s>>>(kb);
+    launch_k(k_solve_y, dim3(1), dim3(256), 0, s, kb);
+    launch_k(k_update_x, dim3(grid), dim3(kKThreads), 0, s, kb);
     outer_resid();
-    k_norm_r<<<grid, kKThreads, 0, s>>>(kb);
+    launch_k(k_norm_r, dim3(grid), dim3(kKThreads), 0, s, kb);
     FSI_CHECK_LAUNCH();
     counted(3);
   }
@@ -1293,6 +1319,9 @@ const char* fsigpu_last_error(void) { return g_err.c_str(); }
 int fsigpu_last_singular_block(void) { return g_bad_block; }
 int fsigpu_version(void) { return 1; }
 long long fsigpu_launch_count(void) { return g_launches; }
+int fsigpu_set_pdl(int enable) {
+  return guarded([&] { g_pdl = enable != 0; });
+}
 int fsigpu_set_l2_persist(int enable) {
   return guarded([&] { g_l2_persist = enable != 0; });
 }

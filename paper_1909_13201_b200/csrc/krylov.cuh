@@ -288,6 +288,8 @@ __global__ void k_normalize(KBufs k) {
 
 // ||r|| -> beta; on the first call also r0, history[0] and target.
 __global__ void __launch_bounds__(kKThreads) k_norm_r(KBufs k) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ double sm[kKThreads];
   double acc[1] = {0.0};
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x)
@@ -318,6 +320,8 @@ __global__ void __launch_bounds__(kKThreads) k_norm_r(KBufs k) {
 
 // v_0 = r / beta ; u = v_0 / scale
 __global__ void k_cycle_start(KBufs k) {
+  pdl_trigger();
+  pdl_wait();
   const double beta = k.st->beta;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x) {
     const double v = k.r[r] / beta;
@@ -329,6 +333,8 @@ __global__ void k_cycle_start(KBufs k) {
 // y = H^{-1} g (back substitution, krylov.cpp:103-109): H staged in
 // shared memory, one thread runs the recurrence.
 __global__ void k_solve_y(KBufs k) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ double Hs[kMaxRestart * kMaxRestart];
   __shared__ double gs[kMaxRestart + 1];
   KState* st = k.st;
@@ -350,6 +356,8 @@ __global__ void k_solve_y(KBufs k) {
 
 // x += Z y  (FGMRES: M(V y) = Z y for the fixed linear V-cycle)
 __global__ void k_update_x(KBufs k) {
+  pdl_trigger();
+  pdl_wait();
   const KState* st = k.st;
   const int j = st->j;
   __shared__ double ys[kMaxRestart];
@@ -437,6 +445,8 @@ __device__ __forceinline__ double fused_row(const KBufs& k, int row, int lane) {
 
 template <int LPR>
 __global__ void __launch_bounds__(kFuseThreads) k_spmv_dots(KBufs k) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ double ws[kFuseRows];
   __shared__ double red[kFuseThreads];
   const int j = k.st->j;
@@ -508,6 +518,8 @@ __device__ __forceinline__ void cta_reduce_wide(const double (&acc)[NV], int nv,
 }
 
 __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm(KBufs k) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ double sm[(kMaxRestart + 1) * (kArnThreads / 32)];
   __shared__ double hs[kMaxRestart];
   __shared__ double red[kArnThreads];
@@ -551,6 +563,8 @@ __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm(KBufs k) {
 
 // (C) w -= V h2 ; v_{j+1} = w / h_{j+1,j} ; u = v_{j+1} / scale
 __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ double hs[kMaxRestart];
   const KState* st = k.st;
   const int jn = st->j;  // already advanced by Givens

@@ -93,7 +93,9 @@ __global__ void __launch_bounds__(256) csr_kernel(int rows, const int* __restric
   // idle row groups still run the (empty) loop and the shuffle tree, so no
   // full-mask shuffle waits on an exited lane
   const bool ok = row < rows;
-  const int k0 = ok ? __ldg(ptr + row) : 0, k1 = ok ? __ldg(ptr + row + 1) : 0;
+  pdl_trigger();
+  const int k0 = ok ? __ldg(ptr + row) : 0, k1 = ok ? __ldg(ptr + row + 1) : 0;  // setup data
+  pdl_wait();
   double s = 0.0;
   // predicated batches of U entries per lane: all index/value loads of a
   // batch are in flight before the dependent x gathers (no early exits)
@@ -127,6 +129,8 @@ __global__ void fs_combine_kernel(int n, int g1, int n_us, const int* __restrict
                                   const double* __restrict__ r, const double* __restrict__ lumped,
                                   double omega, double* __restrict__ x, int x_zero) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  pdl_trigger();
+  pdl_wait();
   if (p >= n) return;
   double z;
   if (p >= g1 && p < g1 + n_us) {
@@ -149,6 +153,8 @@ __global__ void __launch_bounds__(256) gemv_kernel(int n, const double* __restri
                                                    const unsigned char* __restrict__ mask_out = nullptr) {
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
+  pdl_trigger();
+  pdl_wait();
   if (row >= n) return;  // warp-uniform
   const double* Mr = M + (size_t)row * n;
   double s = 0.0;
@@ -301,6 +307,8 @@ __global__ void __launch_bounds__(256) prolong_resid_kernel(int rows, const int*
   const int row = (int)(gt / LPR);
   const int lane = threadIdx.x & (LPR - 1);
   const bool ok = row < rows;
+  pdl_trigger();
+  pdl_wait();
   const double s1 = row_sum<LPR>(pp, pi, pv, ok ? row : -1, lane, ec, cmask_coarse);
   const double s2 = row_sum<LPR>(ap, ai, av, ok ? row : -1, lane, ec, cmask_coarse);
   if (ok && lane == 0) {

@@ -77,6 +77,7 @@ def lib():
             "fsigpu_launch_count": ([], ll),
             "fsigpu_set_block_mode": ([ip], ip),
             "fsigpu_set_l2_persist": ([ip], ip),
+            "fsigpu_set_pdl": ([ip], ip),
             "fsigpu_gmg_persist_bytes": ([vp], ll),
             "fsigpu_gmg_stream": ([vp], vp),
             "fsigpu_csr_create": ([ip, ip, vp, vp, vp, C.POINTER(vp)], ip),
@@ -437,6 +438,12 @@ def set_l2_persist(on: bool):
     """L2 access-policy window over the hierarchy's read-only data (default on)."""
     init()
     _check(lib().fsigpu_set_l2_persist(1 if on else 0))
+
+
+def set_pdl(on: bool):
+    """Programmatic dependent launch of the solve-path kernels (default off)."""
+    init()
+    _check(lib().fsigpu_set_pdl(1 if on else 0))
 
 
 def launch_count() -> int:

@@ -13,7 +13,8 @@ cfg = fsigpu.KrylovConfig(restart=30, max_iters=2000, rel_tol=1e-10, abs_tol=1e-
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
 
 
-def run(tag, persist=True, mode=fsigpu.MODE_INVERSE, mega=False, reps=5):
+def run(tag, persist=True, mode=fsigpu.MODE_INVERSE, mega=False, reps=5, pdl=True):
+    fsigpu.set_pdl(pdl)
     fsigpu.set_l2_persist(persist)
     fsigpu.set_block_mode(mode)
     G = fsigpu.GmgPreconditioner(P.levels)
@@ -41,6 +42,7 @@ def run(tag, persist=True, mode=fsigpu.MODE_INVERSE, mega=False, reps=5):
 
 
 if __name__ == "__main__":
+    run("assembled, no PDL", False, fsigpu.MODE_ASSEMBLED, pdl=False)
     run("assembled", False, fsigpu.MODE_ASSEMBLED)
     run("inverse", False, fsigpu.MODE_INVERSE)
     run("LU", False, fsigpu.MODE_LU)
