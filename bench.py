@@ -31,6 +31,12 @@ sys.path.insert(0, ROOT)
 METRIC = "FGMRES-GMG(FS-AS) solve time & V-cycles/s at 1 B200; AS/SpMV HBM GB/s vs roofline"
 DATA = os.path.join(ROOT, "data", "cfg0.fsix")
 DATA_CFG2 = os.path.join(ROOT, "data_cfg2", "cfg2l4.fsix")
+# full config 2 (1.59 GB) exceeds the gpurun snapshot: generate it on the box
+# first with the prebuilt reference exporter (a separate step, not bench.py):
+#   oracle/_ref/fsi_ref_harness export cfg2 data_cfg2/cfg2.fsix --no-mult --max-iters 30 --block-stride 997
+DATA_CFG2FULL = os.path.join(ROOT, "data_cfg2", "cfg2.fsix")
+WORKLOAD_CFG2FULL = ("config2: 2D aneurysm-like FSI (bulge case, 1 coarse wall row), Q2/P1disc 16->256 (5 GMG levels), "
+                     "1,249,284 dofs, 81.9M nnz, FGMRES(30), AS1 epb=4 / AS2 epb=16, V(1,1) additive FS omega=0.7")
 WORKLOAD_CFG2 = ("config2 at 4 levels (fits the 512 MiB gpurun snapshot): bulge case, 1 coarse wall row, Q2/P1disc 16->128, "
                  "313,348 dofs, 20.5M nnz, FGMRES(30), AS1 epb=4 / AS2 epb=16, V(1,1) additive FS omega=0.7")
 HARNESS = os.path.join(ROOT, "oracle", "_ref", "fsi_ref_harness")
@@ -261,7 +267,9 @@ def run_ours(args, ws, rank, local):
     torch.cuda.set_device(local)
     fsigpu.init(local)
     hbm_peak, peak_kind = peaks()
-    data = DATA_CFG2 if args.config == "cfg2" else DATA
+    data = {"cfg2": DATA_CFG2, "cfg2full": DATA_CFG2FULL}.get(args.config, DATA)
+    if args.smoother == "as":  # AS (Vanka, J1) smoother: the paper's pure-DD comparison
+        data = data.replace(".fsix", "_as.fsix")
     if not os.path.exists(data):
         raise SystemExit(f"{data} missing: run __graft_entry__.build() in the container with /root/reference")
     P = load_case(data, args.config)
@@ -366,8 +374,9 @@ def run_ours(args, ws, rank, local):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference-assembled rest-state FSI Jacobian, seeded uniform RHS; fixtures from oracle/_ref)",
-        "config": {"workload": WORKLOAD if args.config == "cfg0" else WORKLOAD_CFG2, "n_dofs": n,
-                   "max_iters": max_iters, "nnz_fine": P.levels[-1].A.nnz,
+        "config": {"workload": {"cfg0": WORKLOAD, "cfg2": WORKLOAD_CFG2}.get(args.config, WORKLOAD_CFG2FULL),
+                   "n_dofs": n,
+                   "max_iters": max_iters, "smoother": args.smoother, "nnz_fine": P.levels[-1].A.nnz,
                    "parallelism": "replicas" if ws > 1 else "single", "l2": "flushed (256 MB write) between timed solves",
                    "restart": 30, "rel_tol": 1e-10, "cuda_graphs": "conditional WHILE per restart cycle"},
         "solve_ms": ms, "iterations": int(statistics.median(its)), "v_cycles_per_solve": vcyc_per_step,
@@ -409,7 +418,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-microbench", action="store_true")
-    ap.add_argument("--config", choices=["cfg0", "cfg2"], default="cfg0")
+    ap.add_argument("--config", choices=["cfg0", "cfg2", "cfg2full"], default="cfg0")
+    ap.add_argument("--smoother", choices=["fs", "as"], default="fs")
     ap.add_argument("--max-iters", type=int, default=0)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

@@ -21,7 +21,7 @@
 //
 // Usage:
 //   fsi_ref_harness export <case> <out.fsix> [--seed S] [--reps R] [--no-mult]
-//                          [--max-iters N] [--no-gmres]
+//                          [--max-iters N] [--no-gmres] [--smoother fs|as]
 //   fsi_ref_harness solve  <case> [--mode add|mult] [--reps R] [--max-iters N]
 //   fsi_ref_harness blocks <out.fsix> [--seed S]     (golden dense LU blocks)
 //   fsi_ref_harness time-blocks <n54> <n59> <nsolve> [--threads T] [--seed S]
@@ -231,11 +231,18 @@ LevelStack make_stack(const CaseDef& c) {
     st.assemblers.push_back(std::make_unique<Assembler>(st.problems[l]));
     st.orderings.push_back(build_orderings(st.spaces[l].layout));
   }
-  for (int l = 1; l < levels; ++l)
+  for (int l = 1; l < levels; ++l) {
     st.transfers_j2.push_back(build_transfer(st.hier, l, st.spaces[l - 1], st.spaces[l],
                                              st.orderings[l - 1].j2, st.orderings[l].j2));
+    st.transfers_j1.push_back(build_transfer(st.hier, l, st.spaces[l - 1], st.spaces[l],
+                                             st.orderings[l - 1].j1, st.orderings[l].j1));
+  }
+  for (int l = 0; l < levels; ++l) st.vanka_blocks.push_back(build_vanka_blocks(st.spaces[l], c.epb1));
   return st;
 }
+
+// --smoother as: the AS (Vanka, J1) smoother (precond.cpp:99-117) instead of FS
+static bool g_as = false;
 
 // Additive FS smoother from the reference's own classes (SURVEY §8c recipe).
 struct AdditiveFs final : LinearOperator {
@@ -255,6 +262,20 @@ struct AdditiveFs final : LinearOperator {
     as2f = std::make_unique<SchwarzSweep>(fs.group2_matrix(), std::move(s2), SchwarzMode::Additive);
     lumped = fs.lumped();
     csc_g2 = SparseCsc::from_csr(fs.group2_matrix());
+  }
+  // AS smoother: one additive sweep over the Vanka blocks of the J1 frame
+  // (the reference's AsPreconditioner sets, precond.cpp:99-117), no split
+  AdditiveFs(const AsPreconditioner& as, const SparseMatrix& frame) {
+    n = frame.rows();
+    g1 = n;
+    g2 = 0;
+    n_us = 0;
+    std::vector<IndexSet> s1;
+    for (int b = 0; b < as.sweep().n_blocks(); ++b) s1.push_back(as.sweep().block_dofs(b));
+    as1 = std::make_unique<SchwarzSweep>(frame, std::move(s1), SchwarzMode::Additive);
+    SparseMatrix empty(0, 0);
+    as2f = std::make_unique<SchwarzSweep>(empty, std::vector<IndexSet>{}, SchwarzMode::Additive);
+    csc_g2 = SparseCsc::from_csr(empty);
   }
   int size() const override { return n; }
   void apply(const double* r, double* z) const override {
@@ -283,6 +304,7 @@ struct Problem {
   std::vector<std::vector<Constraint>> cs;
   std::vector<ConstraintMasks> cmask;
   std::vector<std::unique_ptr<FsPreconditioner>> fs, fs_as2;  // as2 sets from epb2 instance
+  std::vector<std::unique_ptr<AsPreconditioner>> as_mult;    // --smoother as
   std::vector<std::unique_ptr<AdditiveFs>> fs_add;
   std::vector<GmgLevel> levels_mult, levels_add;
   std::unique_ptr<GmgPreconditioner> gmg_mult, gmg_add;
@@ -333,7 +355,7 @@ std::unique_ptr<Problem> build_problem(const std::string& name, unsigned long lo
     SparseMatrix jl = st.assemblers[l]->jacobian();
     std::vector<double> rl = st.assemblers[l]->residual();
     apply_dirichlet(jl, rl, P->cs[l], xl[l]);
-    P->frame[l] = st.orderings[l].j2.apply(jl);
+    P->frame[l] = (g_as ? st.orderings[l].j1 : st.orderings[l].j2).apply(jl);
     if (l == top) jac_top = std::move(jl);
   }
   P->setup_assembly_s = now_s() - t0;
@@ -342,7 +364,13 @@ std::unique_ptr<Problem> build_problem(const std::string& name, unsigned long lo
   P->fs.resize(L);
   P->fs_as2.resize(L);
   P->fs_add.resize(L);
-  for (int l = 1; l <= top; ++l) {
+  P->as_mult.resize(L);
+  for (int l = 1; l <= top && g_as; ++l) {
+    P->as_mult[l] = std::make_unique<AsPreconditioner>(P->frame[l], st.orderings[l].j1, st.vanka_blocks[l],
+                                                       &P->cmask[l]);
+    P->fs_add[l] = std::make_unique<AdditiveFs>(*P->as_mult[l], P->frame[l]);
+  }
+  for (int l = 1; l <= top && !g_as; ++l) {
     FieldSplitPlan p1{P->def.epb1, P->def.overlap};
     P->fs[l] = std::make_unique<FsPreconditioner>(P->frame[l], st.orderings[l].j2, st.spaces[l], p1,
                                                   &P->cmask[l]);
@@ -364,12 +392,13 @@ std::unique_ptr<Problem> build_problem(const std::string& name, unsigned long lo
       g.a = &P->frame[l];
       g.smoother = (l == 0) ? nullptr
                    : additive ? static_cast<const LinearOperator*>(P->fs_add[l].get())
+                   : g_as     ? static_cast<const LinearOperator*>(P->as_mult[l].get())
                               : static_cast<const LinearOperator*>(P->fs[l].get());
       if (l > 0) {
-        g.p = st.transfers_j2[l - 1].p;
-        g.r = st.transfers_j2[l - 1].r;
+        g.p = (g_as ? st.transfers_j1 : st.transfers_j2)[l - 1].p;
+        g.r = (g_as ? st.transfers_j1 : st.transfers_j2)[l - 1].r;
       }
-      const OrderingPlan& plan = st.orderings[l].j2;
+      const OrderingPlan& plan = g_as ? st.orderings[l].j1 : st.orderings[l].j2;
       g.constrained_rows.assign(st.spaces[l].layout.n_dofs, 0);
       g.constrained_cols.assign(st.spaces[l].layout.n_dofs, 0);
       for (const auto& c : P->cs[l]) {
@@ -408,7 +437,7 @@ std::unique_ptr<Problem> build_problem(const std::string& name, unsigned long lo
     for (int i = 0; i < n; ++i)
       for (int k = off[i]; k < off[i + 1]; ++k) vals[k] *= row_scale[i];
   }
-  const OrderingPlan& plan_top = st.orderings[top].j2;
+  const OrderingPlan& plan_top = g_as ? st.orderings[top].j1 : st.orderings[top].j2;
   P->a_scaled = plan_top.apply(jac_scaled);
   P->frame_scale.resize(n);
   for (int i = 0; i < n; ++i) P->frame_scale[i] = row_scale[plan_top.row_from[i]];
@@ -475,6 +504,7 @@ Args parse(int argc, char** argv) {
     else if (s == "--threads") a.threads = std::stoi(next());
     else if (s == "--rtol") a.rtol = std::stod(next());
     else if (s == "--block-stride") a.block_stride = std::stoi(next());
+    else if (s == "--smoother") g_as = (next() == "as");
     else if (s == "--mode") a.mode = next();
     else if (s == "--no-mult") a.no_mult = true;
     else if (s == "--no-gmres") a.no_gmres = true;
@@ -546,6 +576,9 @@ int cmd_export(const Args& a) {
     if (P->fs[top]) {
       P->fs[top]->apply(r.data(), z.data());
       ar.put("golden/fs_z_mult", z);
+    } else if (P->as_mult[top]) {
+      P->as_mult[top]->apply(r.data(), z.data());
+      ar.put("golden/fs_z_mult", z);
     }
     // per-block dense solves (AS1 then AS2 blocks of the fine level)
     const AdditiveFs& f = *P->fs_add[top];
@@ -555,7 +588,7 @@ int cmd_export(const Args& a) {
     for (int b = 0; b < f.as1->n_blocks(); b += stride) {
       ids.push_back(b);
       const IndexSet& s = f.as1->block_dofs(b);
-      auto lu = factor_principal_block(P->fs[top]->group1_matrix(), s);
+      auto lu = factor_principal_block(g_as ? P->frame[top] : P->fs[top]->group1_matrix(), s);
       auto bb = seeded(s.size(), rng);
       auto xx = lu.solve(bb);
       rhs.insert(rhs.end(), bb.begin(), bb.end());
@@ -564,7 +597,7 @@ int cmd_export(const Args& a) {
     for (int b = 0; b < f.as2f->n_blocks(); b += stride) {
       ids.push_back(f.as1->n_blocks() + b);
       const IndexSet& s = f.as2f->block_dofs(b);
-      auto lu = factor_principal_block(P->fs[top]->group2_matrix(), s);
+      auto lu = factor_principal_block(P->fs[top]->group2_matrix(), s);  // FS only (AS has no AS2)
       auto bb = seeded(s.size(), rng);
       auto xx = lu.solve(bb);
       rhs.insert(rhs.end(), bb.begin(), bb.end());
@@ -599,13 +632,13 @@ int cmd_export(const Args& a) {
     ar.put_d("gmres/rel_tol", a.rtol);
     auto sa = run_gmres(*P, true, kc);
     put_solve(ar, "gmres_add", sa);
-    std::printf("%s additive FS: its=%d conv=%d M=%lld %.3fs relres=%.3e\n", name.c_str(),
+    std::printf("%s additive %s: its=%d conv=%d M=%lld %.3fs relres=%.3e\n", name.c_str(), g_as ? "AS" : "FS",
                 sa.res.iterations, (int)sa.res.converged, sa.m_applies, sa.seconds,
                 sa.true_res / sa.res.history.front());
     if (!a.no_mult) {
       auto sm = run_gmres(*P, false, kc);
       put_solve(ar, "gmres_mult", sm);
-      std::printf("%s multiplicative FS: its=%d conv=%d M=%lld %.3fs relres=%.3e\n", name.c_str(),
+      std::printf("%s multiplicative %s: its=%d conv=%d M=%lld %.3fs relres=%.3e\n", name.c_str(), g_as ? "AS" : "FS",
                   sm.res.iterations, (int)sm.res.converged, sm.m_applies, sm.seconds,
                   sm.true_res / sm.res.history.front());
     }

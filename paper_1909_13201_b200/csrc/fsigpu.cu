@@ -1729,11 +1729,11 @@ int fsigpu_gmg_time_kernel(fsigpu_gmg h, int which, int level, int reps, int col
           Level& B = G.lv[level - 1];
           const int grid = ceil_div((long long)L.n * L.AP.lpr, 256);
           switch (L.AP.lpr) {
-            case 2: prolong_resid_kernel<2><<<grid, 256, 0, s>>>(L.n, L.P.ptr.p, L.P.idx.p, L.P.val.p, L.AP.ptr.p, L.AP.idx.p, L.AP.val.p, B.x, B.cmask.p, L.cmask.p, L.x, v3.p, v3.p); break;
-            case 4: prolong_resid_kernel<4><<<grid, 256, 0, s>>>(L.n, L.P.ptr.p, L.P.idx.p, L.P.val.p, L.AP.ptr.p, L.AP.idx.p, L.AP.val.p, B.x, B.cmask.p, L.cmask.p, L.x, v3.p, v3.p); break;
-            case 8: prolong_resid_kernel<8><<<grid, 256, 0, s>>>(L.n, L.P.ptr.p, L.P.idx.p, L.P.val.p, L.AP.ptr.p, L.AP.idx.p, L.AP.val.p, B.x, B.cmask.p, L.cmask.p, L.x, v3.p, v3.p); break;
-            case 16: prolong_resid_kernel<16><<<grid, 256, 0, s>>>(L.n, L.P.ptr.p, L.P.idx.p, L.P.val.p, L.AP.ptr.p, L.AP.idx.p, L.AP.val.p, B.x, B.cmask.p, L.cmask.p, L.x, v3.p, v3.p); break;
-            default: prolong_resid_kernel<32><<<grid, 256, 0, s>>>(L.n, L.P.ptr.p, L.P.idx.p, L.P.val.p, L.AP.ptr.p, L.AP.idx.p, L.AP.val.p, B.x, B.cmask.p, L.cmask.p, L.x, v3.p, v3.p); break;
+            case 2: prolong_resid_kernel<2><<<grid, 256, 0, s>>>(L.n, L.P.ptr.p, L.P.idx.p, L.P.val.p, L.AP.ptr.p, L.AP.idx.p, L.AP.val.p, B.x, (const unsigned char*)nullptr, L.cmask.p, L.x, v3.p, v3.p); break;
+            case 4: prolong_resid_kernel<4><<<grid, 256, 0, s>>>(L.n, L.P.ptr.p, L.P.idx.p, L.P.val.p, L.AP.ptr.p, L.AP.idx.p, L.AP.val.p, B.x, (const unsigned char*)nullptr, L.cmask.p, L.x, v3.p, v3.p); break;
+            case 8: prolong_resid_kernel<8><<<grid, 256, 0, s>>>(L.n, L.P.ptr.p, L.P.idx.p, L.P.val.p, L.AP.ptr.p, L.AP.idx.p, L.AP.val.p, B.x, (const unsigned char*)nullptr, L.cmask.p, L.x, v3.p, v3.p); break;
+            case 16: prolong_resid_kernel<16><<<grid, 256, 0, s>>>(L.n, L.P.ptr.p, L.P.idx.p, L.P.val.p, L.AP.ptr.p, L.AP.idx.p, L.AP.val.p, B.x, (const unsigned char*)nullptr, L.cmask.p, L.x, v3.p, v3.p); break;
+            default: prolong_resid_kernel<32><<<grid, 256, 0, s>>>(L.n, L.P.ptr.p, L.P.idx.p, L.P.val.p, L.AP.ptr.p, L.AP.idx.p, L.AP.val.p, B.x, (const unsigned char*)nullptr, L.cmask.p, L.x, v3.p, v3.p); break;
           }
           by = L.P.bytes(false) + L.AP.bytes(false) + 24.0 * L.n + L.n + L.nc;
           break;

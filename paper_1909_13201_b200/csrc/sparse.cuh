@@ -267,13 +267,12 @@ namespace fsigpu {
 //   r[i]   = r_pre[i] - (AP_m ec_m)[i]               (= b - A x_new)
 // with AP_m = A * diag(!cmask) * P precomputed at setup and ec_m the coarse
 // correction masked by the coarse col mask (gmg.cpp:230-231).
-template <int LPR>
+template <int LPR, int U = 8>
 __device__ __forceinline__ double row_sum(const int* __restrict__ ptr, const int* __restrict__ idx,
                                           const double* __restrict__ val, int row, int lane, const double* x,
                                           const unsigned char* mask /* nullptr: x already masked */) {
   const int k0 = row >= 0 ? __ldg(ptr + row) : 0, k1 = row >= 0 ? __ldg(ptr + row + 1) : 0;
   double s = 0.0;
-  constexpr int U = 4;
   for (int kb = k0 + lane; kb < k1; kb += U * LPR) {
     int c[U];
     double v[U], xv[U];
@@ -309,8 +308,8 @@ __global__ void __launch_bounds__(256) prolong_resid_kernel(int rows, const int*
   const bool ok = row < rows;
   pdl_trigger();
   pdl_wait();
-  const double s1 = row_sum<LPR>(pp, pi, pv, ok ? row : -1, lane, ec, cmask_coarse);
-  const double s2 = row_sum<LPR>(ap, ai, av, ok ? row : -1, lane, ec, cmask_coarse);
+  const double s1 = row_sum<LPR, 2>(pp, pi, pv, ok ? row : -1, lane, ec, cmask_coarse);  // P: ~4 nnz/row
+  const double s2 = row_sum<LPR, 8>(ap, ai, av, ok ? row : -1, lane, ec, cmask_coarse);
   if (ok && lane == 0) {
     if (!cmask[row]) x[row] = x[row] + s1;
     r[row] = r_pre[row] - s2;

@@ -23,6 +23,21 @@ def chan():
 
 
 @pytest.fixture(scope="session")
+def chan_as():
+    from paper_1909_13201_b200.problem import load_case
+    return load_case(os.path.join(GOLDEN, "chan_as.fsix"), "chan_as")
+
+
+@pytest.fixture(scope="session")
+def cfg0_as():
+    from paper_1909_13201_b200.problem import load_case
+    path = os.path.join(DATA, "cfg0_as.fsix")
+    if not os.path.exists(path):
+        pytest.skip("data/cfg0_as.fsix not generated")
+    return load_case(path, "cfg0_as")
+
+
+@pytest.fixture(scope="session")
 def cfg0():
     from paper_1909_13201_b200.problem import load_case
     path = os.path.join(DATA, "cfg0.fsix")

@@ -292,14 +292,15 @@ def test_gmres_restart_and_x0(cfg0):
 
 
 # ---------------------------------------------------------------- config 2
-@pytest.fixture(scope="module")
-def cfg2():
+@pytest.fixture(scope="module", params=["cfg2l4", "cfg2"])
+def cfg2(request):
     import os
     from paper_1909_13201_b200.problem import load_case
-    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "data_cfg2", "cfg2l4.fsix")
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "data_cfg2",
+                        request.param + ".fsix")
     if not os.path.exists(path):
-        pytest.skip("data_cfg2/cfg2l4.fsix not present (400 MB; exported by oracle/_ref, travels on demand)")
-    return load_case(path, "cfg2")
+        pytest.skip(f"data_cfg2/{request.param}.fsix not present (exported by oracle/_ref on demand)")
+    return load_case(path, request.param)
 
 
 @pytest.mark.slow
@@ -318,3 +319,21 @@ def test_cfg2_fs_apply_vcycle_and_gmres(cfg2):
     n = min(len(h), len(hr))
     assert n >= 30
     assert np.all(np.abs(h[:n] - hr[:n]) <= 1e-6 * hr[:n] + 1e-12 * hr[0])
+
+
+# ---------------------------------------------------------------- AS smoother
+def test_as_smoother_cfg0(cfg0_as):
+    """AS (Vanka, J1 ordering) smoother: additive Schwarz over the reference's
+    AsPreconditioner blocks (precond.cpp:99-117) through the same C ABI
+    (one group, no lumped part): sweep, V-cycle and GMRES against the
+    reference's golden outputs (additive AS: 76 iterations)."""
+    g = cfg0_as.golden
+    for mode in [fsigpu.MODE_ASSEMBLED, fsigpu.MODE_INVERSE, fsigpu.MODE_LU]:
+        G = gmg(cfg0_as.levels, mode)
+        assert rel(G.fs_apply(len(cfg0_as.levels) - 1, g["golden/fs_r"]), g["golden/fs_z_add"]) <= 1e-12
+        assert rel(G.apply(g["golden/vcycle_r"]), g["golden/vcycle_z_add"]) <= 1e-9
+    cfg = fsigpu.KrylovConfig(restart=30, max_iters=2000, rel_tol=1e-10, abs_tol=1e-300)
+    res = fsigpu.gmres(G, cfg0_as.frame_scale, cfg0_as.b, cfg)
+    assert res.converged
+    assert abs(res.iterations - int(g["gmres_add/iterations"][0])) <= 1
+    assert rel(res.x, g["gmres_add/x"]) <= 1e-6

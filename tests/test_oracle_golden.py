@@ -164,3 +164,18 @@ def test_oracle_cfg0_matches_reference(cfg0):
     assert np.array_equal(z, g["golden/fs_z_add"])
     r = G.gmres(cfg0.frame_scale, cfg0.b, restart=30, max_iters=2000, rel_tol=1e-10, abs_tol=1e-300)
     assert r["iterations"] == int(g["gmres_add/iterations"][0])
+
+
+# ---- AS (Vanka, J1) smoother: additive sweep over the reference's
+# AsPreconditioner blocks (precond.cpp:99-117; build_vanka_blocks,
+# ordering.cpp:77-115) -- the "pure DD" smoother of BASELINE configs 0/4
+def test_as_smoother_chan_matches_reference(chan_as):
+    g = chan_as.golden
+    top = chan_as.levels[-1]
+    assert top.g1 == top.n and top.n_us == 0 and top.as2.n == 0
+    G = O.OracleGmg(chan_as.levels)
+    assert np.array_equal(G.fs_apply(1, g["golden/fs_r"]), g["golden/fs_z_add"])
+    assert rel(G.apply(g["golden/vcycle_r"]), g["golden/vcycle_z_add"]) <= 1e-10
+    r = G.gmres(chan_as.frame_scale, chan_as.b, restart=30, max_iters=300, rel_tol=1e-8)
+    assert r["iterations"] == int(g["gmres_add/iterations"][0])
+    assert rel(r["x"], g["gmres_add/x"]) <= 1e-9
