@@ -126,18 +126,22 @@ static long long g_launches = 0;
 static inline void counted(int k = 1) { g_launches += k; }
 
 // ------------------------------------------------------------ CSR
-// Lanes per row: the power of two nearest to avg_nnz / target, where target
-// entries per lane is 4 for small (latency-bound, L2-resident) matrices and
-// 8 for large (HBM-bound) ones; from the launch-shape sweeps of
-// tools/tune_spmv.py on configs 0 and 2.
+// Lanes per row: the power of two nearest to avg_nnz / target. The entries
+// per lane that hide latency best grow with the level size: ~2 on tiny
+// (L2-resident, launch-bound) levels, 4 below 64k rows, 8 up to 128k, 16 on HBM-bound
+// levels, where fewer lanes per row keep more rows -- hence more independent
+// loads -- in flight per warp. Batch depth 8 only pays on tiny levels. From
+// the per-level sweeps of tools/tune_spmv.py on configs 0 and 2
+// (profiles/r01_tune_spmv_*.txt).
 static int choose_lpr(long long rows, long long nnz) {
   if (rows <= 0) return 2;
-  const double target = rows >= 65536 ? 8.0 : 4.0;
+  const double target = rows < 16384 ? 2.0 : rows < 65536 ? 4.0 : rows < 131072 ? 8.0 : 16.0;
   const double want = (double)nnz / rows / target;
   int l = 2;
   while (l < 32 && want > l * 1.41421356) l *= 2;
   return l;
 }
+static int choose_unroll(long long rows) { return rows < 16384 ? 8 : 4; }
 
 struct Csr {
   int rows = 0, cols = 0;
@@ -162,6 +166,7 @@ struct Csr {
     idx.upload(ix, (size_t)nnz, s);
     val.upload(v, (size_t)nnz, s);
     lpr = choose_lpr(r, nnz);
+    unroll = choose_unroll(r);
     if (keep_host) {
       h_ptr.assign(p, p + r + 1);
       h_idx.assign(ix, ix + nnz);
@@ -178,6 +183,7 @@ struct Csr {
     val = std::move(v);
     nnz = (long long)idx.n;
     lpr = choose_lpr(r, nnz);
+    unroll = choose_unroll(r);
   }
   double bytes(bool resid) const {
     return 12.0 * nnz + 4.0 * (rows + 1) + 8.0 * cols + 8.0 * rows + (resid ? 8.0 * rows : 0.0);
@@ -485,6 +491,33 @@ struct Level {
   double combine_bytes = 0;
 };
 
+// x += P ec ; r = r_pre - AP ec on level L (ec: the next-coarser iterate;
+// cmask_coarse: nullptr when ec is already masked). Lanes per row follow AP.
+static void launch_prolong_resid(const Level& L, const double* ec, const unsigned char* cmask_coarse,
+                                 const double* r_pre, double* r, cudaStream_t s) {
+  const int grid = ceil_div((long long)L.n * L.AP.lpr, 256);
+#define FSI_PR(LP, UA)                                                                                           \
+  launch_k(prolong_resid_kernel<LP, UA>, dim3(grid), dim3(256), 0, s, L.n, (const int*)L.P.ptr.p,             \
+           (const int*)L.P.idx.p, (const double*)L.P.val.p, (const int*)L.AP.ptr.p, (const int*)L.AP.idx.p, \
+           (const double*)L.AP.val.p, ec, cmask_coarse, (const unsigned char*)L.cmask.p, L.x, r_pre, r)
+#define FSI_PR_L(UA)                 \
+  switch (L.AP.lpr) {                \
+    case 2: FSI_PR(2, UA); break;    \
+    case 4: FSI_PR(4, UA); break;    \
+    case 8: FSI_PR(8, UA); break;    \
+    case 16: FSI_PR(16, UA); break;  \
+    default: FSI_PR(32, UA); break;  \
+  }
+  if (L.AP.unroll == 4) {
+    FSI_PR_L(4)
+  } else {
+    FSI_PR_L(8)
+  }
+#undef FSI_PR_L
+#undef FSI_PR
+  FSI_CHECK_LAUNCH();
+}
+
 struct Gmg {
   std::vector<Level> lv;
   // read-only hot data (level matrices, transfers, block inverses, coarse
@@ -610,25 +643,7 @@ struct Gmg {
     if (post > 0 && L.AP.rows) {
       // x += P ec ; r = r_pre - AP ec  (one kernel; rbuf holds r_pre)
       ProfScope ps(FSIGPU_K_TRANSFER, L.P.bytes(false) + L.AP.bytes(false) + 24.0 * L.n + L.n + L.nc, s);
-      const int grid = ceil_div((long long)L.n * L.AP.lpr, 256);
-      switch (L.AP.lpr) {
-#define FSI_PR(LP)                                                                                              \
-  case LP:                                                                                                      \
-    launch_k(prolong_resid_kernel<LP>, dim3(grid), dim3(256), 0, s, L.n, (const int*)L.P.ptr.p,             \
-             (const int*)L.P.idx.p, (const double*)L.P.val.p, (const int*)L.AP.ptr.p, (const int*)L.AP.idx.p, \
-             (const double*)L.AP.val.p, (const double*)B.x,                                                 \
-             (const unsigned char*)(fused_mask ? nullptr : B.cmask.p), (const unsigned char*)L.cmask.p,     \
-             L.x, (const double*)L.rbuf.p, L.rbuf.p);                                                       \
-    break;
-        FSI_PR(2)
-        FSI_PR(4)
-        FSI_PR(8)
-        FSI_PR(16)
-        default:
-          FSI_PR(32)
-#undef FSI_PR
-      }
-      FSI_CHECK_LAUNCH();
+      launch_prolong_resid(L, B.x, fused_mask ? nullptr : B.cmask.p, L.rbuf.p, L.rbuf.p, s);
       counted();
       for (int k = 0; k < post; ++k) sweep(l, 0, k == 0, mask_out && k == post - 1);
       return;
@@ -796,6 +811,7 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
       apv.push_back(0.0);
     }
     L.AP.create(d.n, d.nc, app.data(), api.data(), apv.data(), s);
+    L.AP.unroll = 4;  // its P half already adds 2 loads per lane to the batch
   }
   require(d.g1 >= 0 && d.n_us >= 0 && d.g1 + d.n_us <= d.n, "fs: bad group sizes");
   L.g1 = d.g1;
@@ -1727,14 +1743,7 @@ int fsigpu_gmg_time_kernel(fsigpu_gmg h, int which, int level, int reps, int col
         case 2: {
           require(level > 0 && L.AP.rows, "time: no prolongation on this level");
           Level& B = G.lv[level - 1];
-          const int grid = ceil_div((long long)L.n * L.AP.lpr, 256);
-          switch (L.AP.lpr) {
-            case 2: prolong_resid_kernel<2><<<grid, 256, 0, s>>>(L.n, L.P.ptr.p, L.P.idx.p, L.P.val.p, L.AP.ptr.p, L.AP.idx.p, L.AP.val.p, B.x, (const unsigned char*)nullptr, L.cmask.p, L.x, v3.p, v3.p); break;
-            case 4: prolong_resid_kernel<4><<<grid, 256, 0, s>>>(L.n, L.P.ptr.p, L.P.idx.p, L.P.val.p, L.AP.ptr.p, L.AP.idx.p, L.AP.val.p, B.x, (const unsigned char*)nullptr, L.cmask.p, L.x, v3.p, v3.p); break;
-            case 8: prolong_resid_kernel<8><<<grid, 256, 0, s>>>(L.n, L.P.ptr.p, L.P.idx.p, L.P.val.p, L.AP.ptr.p, L.AP.idx.p, L.AP.val.p, B.x, (const unsigned char*)nullptr, L.cmask.p, L.x, v3.p, v3.p); break;
-            case 16: prolong_resid_kernel<16><<<grid, 256, 0, s>>>(L.n, L.P.ptr.p, L.P.idx.p, L.P.val.p, L.AP.ptr.p, L.AP.idx.p, L.AP.val.p, B.x, (const unsigned char*)nullptr, L.cmask.p, L.x, v3.p, v3.p); break;
-            default: prolong_resid_kernel<32><<<grid, 256, 0, s>>>(L.n, L.P.ptr.p, L.P.idx.p, L.P.val.p, L.AP.ptr.p, L.AP.idx.p, L.AP.val.p, B.x, (const unsigned char*)nullptr, L.cmask.p, L.x, v3.p, v3.p); break;
-          }
+          launch_prolong_resid(L, B.x, nullptr, v3.p, v3.p, s);
           by = L.P.bytes(false) + L.AP.bytes(false) + 24.0 * L.n + L.n + L.nc;
           break;
         }

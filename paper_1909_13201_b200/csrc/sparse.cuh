@@ -294,7 +294,11 @@ __device__ __forceinline__ double row_sum(const int* __restrict__ ptr, const int
   return s;
 }
 
-template <int LPR>
+// x += P ec ; r = r_pre - (A P) ec for one fine row per LPR lanes. The P
+// row (<= 9 entries for Q2 / 3 for P1disc) and the first UA*LPR entries of
+// the AP row are fetched in ONE predicated batch, so the two independent
+// pointer -> index -> gather chains overlap instead of running back to back.
+template <int LPR, int UA>
 __global__ void __launch_bounds__(256) prolong_resid_kernel(int rows, const int* __restrict__ pp,
                                                             const int* __restrict__ pi, const double* __restrict__ pv,
                                                             const int* __restrict__ ap, const int* __restrict__ ai,
@@ -302,14 +306,69 @@ __global__ void __launch_bounds__(256) prolong_resid_kernel(int rows, const int*
                                                             const unsigned char* __restrict__ cmask_coarse,
                                                             const unsigned char* __restrict__ cmask, double* x,
                                                             const double* r_pre, double* r) {
+  constexpr int UP = 2;
   const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int row = (int)(gt / LPR);
   const int lane = threadIdx.x & (LPR - 1);
   const bool ok = row < rows;
   pdl_trigger();
   pdl_wait();
-  const double s1 = row_sum<LPR, 2>(pp, pi, pv, ok ? row : -1, lane, ec, cmask_coarse);  // P: ~4 nnz/row
-  const double s2 = row_sum<LPR, 8>(ap, ai, av, ok ? row : -1, lane, ec, cmask_coarse);
+  int p0 = 0, p1 = 0, a0 = 0, a1 = 0;
+  if (ok) {
+    p0 = __ldg(pp + row);
+    p1 = __ldg(pp + row + 1);
+    a0 = __ldg(ap + row);
+    a1 = __ldg(ap + row + 1);
+  }
+  auto gather = [&](int c) -> double {
+    return c >= 0 ? ((cmask_coarse && __ldg(cmask_coarse + c)) ? 0.0 : __ldg(ec + c)) : 0.0;
+  };
+  double s1 = 0.0, s2 = 0.0;
+  int kp = p0 + lane, ka = a0 + lane;
+  {
+    int c[UP + UA];
+    double v[UP + UA], xv[UP + UA];
+#pragma unroll
+    for (int u = 0; u < UP; ++u) {
+      const int k = kp + u * LPR;
+      const bool in = k < p1;
+      c[u] = in ? __ldg(pi + k) : -1;
+      v[u] = in ? __ldg(pv + k) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < UA; ++u) {
+      const int k = ka + u * LPR;
+      const bool in = k < a1;
+      c[UP + u] = in ? __ldg(ai + k) : -1;
+      v[UP + u] = in ? __ldg(av + k) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < UP + UA; ++u) xv[u] = gather(c[u]);
+#pragma unroll
+    for (int u = 0; u < UP; ++u) s1 = fma(v[u], xv[u], s1);
+#pragma unroll
+    for (int u = 0; u < UA; ++u) s2 = fma(v[UP + u], xv[UP + u], s2);
+  }
+  // tails (rows longer than one batch)
+  for (kp += UP * LPR; kp < p1; kp += LPR) s1 = fma(__ldg(pv + kp), gather(__ldg(pi + kp)), s1);
+  for (ka += UA * LPR; ka < a1; ka += UA * LPR) {
+    int c[UA];
+    double v[UA];
+#pragma unroll
+    for (int u = 0; u < UA; ++u) {
+      const int k = ka + u * LPR;
+      const bool in = k < a1;
+      c[u] = in ? __ldg(ai + k) : -1;
+      v[u] = in ? __ldg(av + k) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < UA; ++u) s2 = fma(v[u], gather(c[u]), s2);
+  }
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) {
+    s1 += __shfl_xor_sync(kFull, s1, o, LPR);
+    s2 += __shfl_xor_sync(kFull, s2, o, LPR);
+  }
   if (ok && lane == 0) {
     if (!cmask[row]) x[row] = x[row] + s1;
     r[row] = r_pre[row] - s2;

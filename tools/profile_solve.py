@@ -1,5 +1,7 @@
-"""One warm config-0 solve for ncu (graphs off so every launch is a plain
-kernel launch); `--blocks` instead times the config-1 block solve."""
+"""One warm solve for ncu (graphs off so every launch is a plain kernel
+launch). Modes: solve | graph | vcycle-lu | vcycle-inv | blocks (config-1
+block solve) | kernel:<name>:<level> (one launch of a single V-cycle kernel,
+e.g. kernel:fs_smoother:4). FSI_DATA picks the .fsix (default data/cfg0)."""
 import os
 import sys
 
@@ -25,7 +27,8 @@ def main():
             B.solve_dev(rhs.data_ptr(), x.data_ptr(), s.cuda_stream)
         torch.cuda.synchronize()
         return
-    P = load_case(os.path.join(ROOT, "data", "cfg0.fsix"), "cfg0")
+    data = os.environ.get("FSI_DATA", os.path.join(ROOT, "data", "cfg0.fsix"))
+    P = load_case(data, "case")
     if mode in ("vcycle-lu", "vcycle-inv"):
         fsigpu.set_block_mode(fsigpu.MODE_LU if mode == "vcycle-lu" else fsigpu.MODE_INVERSE)
         G = fsigpu.GmgPreconditioner(P.levels)
@@ -34,8 +37,14 @@ def main():
         print("vcycle ok", float(np.linalg.norm(z)))
         return
     G = fsigpu.GmgPreconditioner(P.levels)
+    if mode.startswith("kernel:"):
+        _, name, level = mode.split(":")
+        ms, by = G.time_kernel(name, int(level), reps=1, cold=True)
+        print(f"{name}@L{level} {ms * 1000:.1f} us {by / ms / 1e6:.0f} GB/s")
+        return
     S = fsigpu.GmresSolver(G, P.frame_scale, restart=30, graphs=(mode == "graph"))
-    cfg = fsigpu.KrylovConfig(restart=30, max_iters=2000, rel_tol=1e-10, abs_tol=1e-300)
+    cfg = fsigpu.KrylovConfig(restart=30, max_iters=int(os.environ.get("FSI_MAXIT", "2000")), rel_tol=1e-10,
+                              abs_tol=1e-300)
     for _ in range(2):
         r = S.solve(P.b, cfg)
     print("its", r.iterations, "relres", r.true_residual / np.linalg.norm(P.b))

@@ -1,4 +1,7 @@
-"""Sweep SpMV launch shapes (lanes per row x batch depth) on one hierarchy."""
+"""Sweep SpMV launch shapes (lanes per row x batch depth) on one hierarchy.
+
+usage: tune_spmv.py [data.fsix] [level ...]   (default: every level >= 1)
+"""
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -8,15 +11,18 @@ fsigpu.init(0)
 path = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "data", "cfg0.fsix")
 P = load_case(path)
 G = fsigpu.GmgPreconditioner(P.levels)
-top = len(P.levels) - 1
-for which, kname in [("A", "residual"), ("FS", "fs_smoother"), ("AP", "prolong_resid")]:
-    best = None
-    for lpr in [4, 8, 16, 32]:
-        for u in [4, 8]:
-            G.set_launch(top, which, lpr, u)
-            ms, by = G.time_kernel(kname, top, reps=10, cold=True)
-            gb = by / ms / 1e6
-            print(f"{which:3s} lpr={lpr:2d} u={u} cold {ms*1000:8.2f} us {gb:8.1f} GB/s", flush=True)
-            if best is None or ms < best[0]:
-                best = (ms, lpr, u)
-    print(f"{which} best lpr={best[1]} u={best[2]} {best[0]*1000:.2f} us", flush=True)
+levels = [int(a) for a in sys.argv[2:]] or list(range(1, len(P.levels)))
+for lev in levels:
+    L = P.levels[lev]
+    for which, kname in [("A", "residual"), ("FS", "fs_smoother"), ("AP", "prolong_resid")]:
+        best, default = None, None
+        default = G.time_kernel(kname, lev, reps=10, cold=True)[0]
+        for lpr in [2, 4, 8, 16, 32]:
+            for u in [4, 8]:
+                G.set_launch(lev, which, lpr, u)
+                ms, by = G.time_kernel(kname, lev, reps=10, cold=True)
+                if best is None or ms < best[0]:
+                    best = (ms, lpr, u, by)
+        print(f"L{lev} n={L.n:8d} nnz/row={L.A.nnz / L.n:5.1f} {which:3s} default {default*1000:8.2f} us  best lpr={best[1]:2d} u={best[2]} "
+              f"{best[0]*1000:8.2f} us {best[3]/best[0]/1e6:7.0f} GB/s", flush=True)
+        G.set_launch(lev, which, best[1], best[2])
