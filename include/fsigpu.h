@@ -133,6 +133,9 @@ int fsigpu_set_block_mode(int mode);
 int fsigpu_set_l2_persist(int enable);
 /* programmatic dependent launch of the solve-path kernels (default off: measured neutral) */
 int fsigpu_set_pdl(int enable);
+/* default staged-SpMV capacity for level matrices created afterwards
+ * (-1: the built-in per-size rule, 0: off, >0: entries per CTA) */
+int fsigpu_set_stage_cap(int cap);
 long long fsigpu_gmg_persist_bytes(fsigpu_gmg g);
 
 /* ---- GMG with additive FS smoothers: GmgPreconditioner (gmg.cpp:178-246),
@@ -156,6 +159,10 @@ void fsigpu_gmg_destroy(fsigpu_gmg g);
 /* tuning: lanes per row and batch depth of a level matrix's SpMV launches
  * (which: 0 A, 1 FS, 2 A*P, 3 P, 4 R) */
 int fsigpu_gmg_set_launch(fsigpu_gmg g, int level, int which, int lpr, int unroll);
+/* tuning: shared-memory staged SpMV (one bulk copy of a CTA's CSR slice,
+ * then a CSR-stream product/row-sum) with at most `cap` entries per CTA;
+ * cap 0 selects the per-row vector kernel. Same `which` as set_launch. */
+int fsigpu_gmg_set_staging(fsigpu_gmg g, int level, int which, int cap);
 int fsigpu_gmg_time_kernel(fsigpu_gmg g, int which, int level, int reps, int cold, double* ms,
                            double* bytes);
 

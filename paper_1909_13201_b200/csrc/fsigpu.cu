@@ -142,6 +142,13 @@ static int choose_lpr(long long rows, long long nnz) {
   return l;
 }
 static int choose_unroll(long long rows) { return rows < 16384 ? 8 : 4; }
+// Staged-kernel capacity (entries per CTA); 0 keeps csr_kernel.
+static int g_stage_cap = 0;
+static int choose_stage_cap(long long rows, long long nnz) {
+  (void)rows;
+  (void)nnz;
+  return g_stage_cap > 0 ? g_stage_cap : 0;
+}
 
 struct Csr {
   int rows = 0, cols = 0;
@@ -163,15 +170,22 @@ struct Csr {
     for (int i = 0; i < r; ++i) require(p[i] <= p[i + 1], "csr: offsets not nondecreasing");
     for (long long k = 0; k < nnz; ++k) require(ix[k] >= 0 && ix[k] < c, "csr: column range");
     ptr.upload(p, (size_t)r + 1, s);
-    idx.upload(ix, (size_t)nnz, s);
-    val.upload(v, (size_t)nnz, s);
+    // padded by 4 entries: the staged kernel's bulk copies round their
+    // ranges out to 16-byte boundaries
+    idx.alloc((size_t)nnz + 4);
+    val.alloc((size_t)nnz + 4);
+    if (nnz) {
+      FSI_CUDA(cudaMemcpyAsync(idx.p, ix, sizeof(int) * nnz, cudaMemcpyHostToDevice, s));
+      FSI_CUDA(cudaMemcpyAsync(val.p, v, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+    }
     lpr = choose_lpr(r, nnz);
     unroll = choose_unroll(r);
+    h_ptr.assign(p, p + r + 1);
     if (keep_host) {
-      h_ptr.assign(p, p + r + 1);
       h_idx.assign(ix, ix + nnz);
       h_val.assign(v, v + nnz);
     }
+    stage(choose_stage_cap(r, nnz), s);
     FSI_CUDA(cudaStreamSynchronize(s));
   }
   // take ownership of device CSR arrays built on the GPU
@@ -179,12 +193,47 @@ struct Csr {
     rows = r;
     cols = c;
     ptr = std::move(p);
-    idx = std::move(ix);
-    val = std::move(v);
-    nnz = (long long)idx.n;
+    nnz = (long long)ix.n;
+    idx.alloc((size_t)nnz + 4);
+    val.alloc((size_t)nnz + 4);
+    if (nnz) {
+      FSI_CUDA(cudaMemcpy(idx.p, ix.p, sizeof(int) * nnz, cudaMemcpyDeviceToDevice));
+      FSI_CUDA(cudaMemcpy(val.p, v.p, sizeof(double) * nnz, cudaMemcpyDeviceToDevice));
+    }
+    ix.release();
+    v.release();
     lpr = choose_lpr(r, nnz);
     unroll = choose_unroll(r);
+    h_ptr = ptr.download();
+    stage(choose_stage_cap(r, nnz), 0);
   }
+  // Staged (shared-memory CSR-stream) launch: CTA row ranges holding at most
+  // `cap` entries each. cap 0, or a row longer than cap, selects csr_kernel.
+  DevBuf<int> rb;
+  int nstage = 0, cap = 0, slpr = 4;
+  void stage(int cap_, cudaStream_t s) {
+    nstage = 0;
+    cap = 0;
+    if (cap_ <= 0 || rows == 0) return;
+    std::vector<int> b{0};
+    int r = 0;
+    while (r < rows) {
+      const int begin = r;
+      long long e = 0;
+      while (r < rows && e + (h_ptr[r + 1] - h_ptr[r]) <= cap_) e += h_ptr[r + 1] - h_ptr[r], ++r;
+      if (r == begin) return;  // a row longer than cap
+      b.push_back(r);
+    }
+    rb.upload(b, s);
+    FSI_CUDA(cudaStreamSynchronize(s));
+    nstage = (int)b.size() - 1;
+    cap = cap_;
+    // phase-2 lanes per row: ~4 products per lane
+    const double want = (double)nnz / rows / 4.0;
+    slpr = 1;
+    while (slpr < 32 && want > slpr * 1.41421356) slpr *= 2;
+  }
+  size_t stage_smem() const { return 8 * (size_t)((cap + 3) & ~1) + 4 * (size_t)(cap + 8); }
   double bytes(bool resid) const {
     return 12.0 * nnz + 4.0 * (rows + 1) + 8.0 * cols + 8.0 * rows + (resid ? 8.0 * rows : 0.0);
   }
@@ -192,6 +241,10 @@ struct Csr {
   template <class G, class E>
   void launch(G g, E e, cudaStream_t s) const {
     if (!rows) return;
+    if (nstage) {
+      launch_staged(g, e, s);
+      return;
+    }
     const long long threads = (long long)rows * lpr;
     const int grid = ceil_div(threads, 256);
 #define FSI_CSR(LP, UU) launch_k(csr_kernel<LP, G, E, UU>, dim3(grid), dim3(256), 0, s, rows, (const int*)ptr.p, (const int*)idx.p, (const double*)val.p, g, e)
@@ -213,6 +266,31 @@ struct Csr {
       }
     }
 #undef FSI_CSR
+    FSI_CHECK_LAUNCH();
+    counted();
+  }
+  template <int LP, class G, class E>
+  void launch_staged_lp(G g, E e, cudaStream_t s) const {
+    static size_t attr = 48 * 1024;
+    const size_t sm = stage_smem();
+    if (sm > attr) {
+      FSI_CUDA(cudaFuncSetAttribute(csr_staged_kernel<LP, G, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)sm));
+      attr = sm;
+    }
+    launch_k(csr_staged_kernel<LP, G, E>, dim3(nstage), dim3(256), sm, s, (const int*)rb.p, (const int*)ptr.p,
+             (const int*)idx.p, (const double*)val.p, cap, g, e);
+  }
+  template <class G, class E>
+  void launch_staged(G g, E e, cudaStream_t s) const {
+    switch (slpr) {
+      case 1: launch_staged_lp<1>(g, e, s); break;
+      case 2: launch_staged_lp<2>(g, e, s); break;
+      case 4: launch_staged_lp<4>(g, e, s); break;
+      case 8: launch_staged_lp<8>(g, e, s); break;
+      case 16: launch_staged_lp<16>(g, e, s); break;
+      default: launch_staged_lp<32>(g, e, s); break;
+    }
     FSI_CHECK_LAUNCH();
     counted();
   }
@@ -1354,6 +1432,21 @@ int fsigpu_gmg_set_launch(fsigpu_gmg h, int level, int which, int lpr, int unrol
     Csr* c = which == 0 ? &L.A : which == 1 ? &L.FS : which == 2 ? &L.AP : which == 3 ? &L.P : &L.R;
     c->lpr = lpr;
     c->unroll = unroll;
+  });
+}
+int fsigpu_gmg_set_staging(fsigpu_gmg h, int level, int which, int cap) {
+  return guarded([&] {
+    require(h != nullptr && level >= 0 && level < (int)h->g.lv.size(), "staging: bad level");
+    require(cap >= 0 && cap <= 16384, "staging: cap must be 0..16384");
+    Level& L = h->g.lv[level];
+    Csr* c = which == 0 ? &L.A : which == 1 ? &L.FS : which == 2 ? &L.AP : which == 3 ? &L.P : &L.R;
+    c->stage(cap, h->g.s);
+  });
+}
+int fsigpu_set_stage_cap(int cap) {
+  return guarded([&] {
+    require(cap >= -1 && cap <= 16384, "stage cap must be -1..16384");
+    g_stage_cap = cap;
   });
 }
 int fsigpu_set_block_mode(int mode) {

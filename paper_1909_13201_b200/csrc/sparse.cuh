@@ -119,6 +119,81 @@ __global__ void __launch_bounds__(256) csr_kernel(int rows, const int* __restric
   if (ok && lane == 0) epi(row, s);
 }
 
+// Shared-memory staged CSR ("CSR-stream"). CTA b owns rows [rb[b], rb[b+1])
+// whose entries [ptr[rb[b]], ptr[rb[b+1]]) are contiguous in idx / val, at
+// most `cap` of them. One thread brings both slices into shared memory with
+// two bulk copies (cp.async.bulk + mbarrier complete_tx), issued BEFORE the
+// PDL wait: the matrix is setup data, so its fetch overlaps the producer
+// kernel's tail. Then
+//   phase 1: every thread forms val[k] * x[idx[k]] for k = t, t + 256, ...
+//            (U independent gathers in flight per thread, whatever the row
+//            lengths) and writes the product over val in place;
+//   phase 2: LPR lanes per row add the row's products out of shared memory
+//            (fixed strided order + xor tree: deterministic).
+// Compared with csr_kernel the per-warp dependent chain drops from
+// ptr -> (idx, val) -> x per batch to one bulk copy + one gather round.
+template <int LPR, class Gather, class Epi, int U = 8>
+__global__ void __launch_bounds__(256) csr_staged_kernel(const int* __restrict__ rb, const int* __restrict__ ptr,
+                                                         const int* __restrict__ idx,
+                                                         const double* __restrict__ val, int cap, Gather gx,
+                                                         Epi epi) {
+  extern __shared__ __align__(128) unsigned char stage[];
+  __shared__ __align__(8) unsigned long long bar;
+  double* s_val = reinterpret_cast<double*>(stage);  // cap + 2 doubles
+  int* s_idx = reinterpret_cast<int*>(stage + 8 * (size_t)((cap + 2 + 1) & ~1));  // cap + 8 ints
+  const int t = threadIdx.x;
+  const int r0 = __ldg(rb + blockIdx.x), r1 = __ldg(rb + blockIdx.x + 1);
+  const int k0 = __ldg(ptr + r0), k1 = __ldg(ptr + r1);
+  const int kv0 = k0 & ~1, ki0 = k0 & ~3;  // 16-byte aligned sources
+  const unsigned bv = 8u * (unsigned)(((k1 + 1) & ~1) - kv0);
+  const unsigned bi = 4u * (unsigned)(((k1 + 3) & ~3) - ki0);
+  if (t == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (t == 0) {
+    mbar_arrive_expect_tx(&bar, k1 > k0 ? bv + bi : 0u);
+    if (k1 > k0) {
+      tma_bulk_g2s(s_val, val + kv0, bv, &bar);
+      tma_bulk_g2s(s_idx, idx + ki0, bi, &bar);
+    }
+  }
+  pdl_trigger();
+  pdl_wait();
+  mbar_wait(&bar, 0);
+  // phase 1: products
+  for (int kb = k0 + t; kb < k1; kb += 256 * U) {
+    int c[U];
+    double xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = kb + 256 * u;
+      c[u] = k < k1 ? s_idx[k - ki0] : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = c[u] >= 0 ? gx(c[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = kb + 256 * u;
+      if (k < k1) s_val[k - kv0] *= xv[u];
+    }
+  }
+  __syncthreads();
+  // phase 2: row sums
+  const int lane = t & (LPR - 1);
+  for (int base = r0; base < r1; base += 256 / LPR) {
+    const int row = base + t / LPR;
+    const bool ok = row < r1;
+    const int a = ok ? __ldg(ptr + row) : 0, b = ok ? __ldg(ptr + row + 1) : 0;
+    double s = 0.0;
+    for (int k = a + lane; k < b; k += LPR) s += s_val[k - kv0];
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, LPR);
+    if (ok && lane == 0) epi(row, s);
+  }
+}
+
 // FS combine on one level (precond.cpp:42-57 additive + 271-287 + 305-317):
 //   p <  g1, p >= g1+n_us : z = sum_{(b,i) covering p, block order} delta / cover
 //   g1 <= p < g1+n_us     : z = r[p] / lumped[p-g1]

@@ -106,6 +106,8 @@ def lib():
             "fsigpu_coarse_solve": ([vp, vp, vp], ip),
             "fsigpu_gmg_destroy": ([vp], None),
             "fsigpu_gmg_set_launch": ([vp, ip, ip, ip, ip], ip),
+            "fsigpu_gmg_set_staging": ([vp, ip, ip, ip], ip),
+            "fsigpu_set_stage_cap": ([ip], ip),
             "fsigpu_gmg_time_kernel": ([vp, ip, ip, ip, ip, C.POINTER(d), C.POINTER(d)], ip),
             "fsigpu_gmres_create": ([vp, vp, ip, C.POINTER(vp)], ip),
             "fsigpu_gmres_solve": ([vp, vp, vp, vp, ip, d, d, vp, C.POINTER(GmresResultC)], ip),
@@ -313,6 +315,11 @@ class GmgPreconditioner:
         w = {"A": 0, "FS": 1, "AP": 2, "P": 3, "R": 4}[which]
         _check(lib().fsigpu_gmg_set_launch(self.h, level, w, lpr, unroll))
 
+    def set_staging(self, level: int, which: str, cap: int):
+        """Staged (shared-memory CSR-stream) SpMV with <= cap entries per CTA; 0 = off."""
+        w = {"A": 0, "FS": 1, "AP": 2, "P": 3, "R": 4}[which]
+        _check(lib().fsigpu_gmg_set_staging(self.h, level, w, cap))
+
     def persist_bytes(self) -> int:
         return int(lib().fsigpu_gmg_persist_bytes(self.h))
 
@@ -435,9 +442,15 @@ def set_block_mode(mode: int):
 
 
 def set_l2_persist(on: bool):
-    """L2 access-policy window over the hierarchy's read-only data (default on)."""
+    """L2 access-policy window over the hierarchy's read-only data (default off)."""
     init()
     _check(lib().fsigpu_set_l2_persist(1 if on else 0))
+
+
+def set_stage_cap(cap: int):
+    """Staged-SpMV capacity for hierarchies created afterwards (-1 rule, 0 off)."""
+    init()
+    _check(lib().fsigpu_set_stage_cap(cap))
 
 
 def set_pdl(on: bool):

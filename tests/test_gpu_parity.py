@@ -337,3 +337,24 @@ def test_as_smoother_cfg0(cfg0_as):
     assert res.converged
     assert abs(res.iterations - int(g["gmres_add/iterations"][0])) <= 1
     assert rel(res.x, g["gmres_add/x"]) <= 1e-6
+
+
+def test_staged_spmv_opt_in(cfg0):
+    """The shared-memory staged SpMV (opt-in, csr_staged_kernel) gives the
+    same V-cycle and GMRES result as the default vector kernel."""
+    g = cfg0.golden
+    fsigpu.set_stage_cap(2048)
+    try:
+        G = fsigpu.GmgPreconditioner(cfg0.levels)
+    finally:
+        fsigpu.set_stage_cap(0)
+    z = G.apply(g["golden/vcycle_r"])
+    assert rel(z, g["golden/vcycle_z_add"]) <= 1e-9
+    zd = fsigpu.GmgPreconditioner(cfg0.levels).apply(g["golden/vcycle_r"])
+    assert rel(z, zd) <= 1e-13
+    cfg = fsigpu.KrylovConfig(restart=30, max_iters=2000, rel_tol=1e-10, abs_tol=1e-300)
+    res = fsigpu.gmres(G, cfg0.frame_scale, cfg0.b, cfg)
+    assert res.converged
+    assert abs(res.iterations - int(g["gmres_add/iterations"][0])) <= 1
+    with pytest.raises(ValueError):
+        G.set_staging(1, "FS", -5)
