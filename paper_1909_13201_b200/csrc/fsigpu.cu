@@ -1081,7 +1081,7 @@ struct Gmres {
   int n = 0, mr = 30;
   int grid = 0;
   bool graphs = true;
-  DevBuf<double> scale, V, Z, w, zbuf, ubuf, r, x, b, H, cs, sn, gv, hist, partial;
+  DevBuf<double> scale, V, Z, w, zbuf, ubuf, r, x, b, H, cs, sn, gv, hist, partial, partial2;
   DevBuf<unsigned int> ticket;
   DevBuf<KState> st;
   KBufs kb{};
@@ -1136,10 +1136,10 @@ struct Gmres {
       launch_k(k_spmv_dots<8>, dim3(gs), dim3(kFuseThreads), 0, s, kk);
     }
     {
+      // (B) on parts_b CTAs; (C) on parts_b row CTAs + 1 Givens CTA
       ProfScope ps(FSIGPU_K_ARNOLDI, 8.0 * n * 4, s);
-      const int ga = std::max(1, std::min(ceil_div(n, kArnThreads), 4 * 148));
-      launch_k(k_update_dots_norm, dim3(ga), dim3(kArnThreads), 0, s, kk);
-      launch_k(k_update_normalize, dim3(ga), dim3(kArnThreads), 0, s, kk);
+      launch_k(k_update_dots_norm, dim3(kk.parts_b), dim3(kArnThreads), 0, s, kk);
+      launch_k(k_update_normalize, dim3(kk.parts_b + 1), dim3(kArnThreads), 0, s, kk);
     }
     FSI_CHECK_LAUNCH();
     counted(3);
@@ -1928,6 +1928,7 @@ int fsigpu_gmres_create(fsigpu_gmg g, const double* frame_scale, int restart, fs
     k.gv.alloc(restart + 1);
     k.grid = std::max(1, std::min(ceil_div(n, kKThreads), 2 * 148));
     k.partial.alloc((size_t)std::max(std::max(k.grid, ceil_div(n, kFuseRows)), 4 * 148) * (kMaxRestart + 1));
+    k.partial2.alloc((size_t)4 * 148 * (kMaxRestart + 1));
     k.ticket.alloc(1);
     k.ticket.zero(s);
     k.st.alloc(1);
@@ -1948,6 +1949,9 @@ int fsigpu_gmres_create(fsigpu_gmg g, const double* frame_scale, int restart, fs
     kb.sn = k.sn.p;
     kb.g = k.gv.p;
     kb.partial = k.partial.p;
+    kb.partial2 = k.partial2.p;
+    kb.parts_a = ceil_div(n, kFuseRows);
+    kb.parts_b = std::max(1, std::min(ceil_div(n, kArnThreads), 4 * 148));
     kb.ticket = k.ticket.p;
     kb.st = k.st.p;
     {

@@ -33,7 +33,7 @@ struct KState {
   int first;      // next norm is ||r0||
   int converged;
   int keep_going; // cycle-level continue flag (host side)
-  int pad;
+  int jc;         // Krylov column k_update_normalize writes (set by k_update_dots_norm)
   double target;
   double beta;
   double rho;
@@ -62,6 +62,9 @@ struct KBufs {
   double* g;
   double* history;      // max_iters + 2
   double* partial;      // grid x (kMaxRestart+1)
+  double* partial2;     // second partial buffer of the fused Arnoldi step
+  int parts_a;          // CTAs of k_spmv_dots (rows of partial it writes)
+  int parts_b;          // CTAs of k_update_dots_norm (rows of partial2)
   unsigned int* ticket;
   KState* st;
   // fused Arnoldi (3 kernels per step)
@@ -380,38 +383,6 @@ __global__ void k_set_continue(const KState* st, cudaGraphConditionalHandle h, i
 
 namespace fsigpu {
 // ---- fused Arnoldi step (3 kernels): -----------------------------------
-// CTA-wide fixed-order sum of the per-CTA partials (vector v, CTA b):
-// thread t owns vector slot t % 32 and slice t / 32 of the CTAs; slices are
-// combined in order through shared memory. red: (T/32) x 32 doubles.
-template <int T>
-__device__ __forceinline__ void finish_wide(const KBufs& k, int nv, double* dst, double* red) {
-  constexpr int NS = T / 32;
-  const int v = threadIdx.x & 31, q = threadIdx.x >> 5;
-  double s = 0.0;
-  if (v < nv) {
-    constexpr int U = 8;
-    for (unsigned int b0 = q; b0 < gridDim.x; b0 += NS * U) {
-      double pv[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const unsigned int b = b0 + NS * u;
-        pv[u] = b < gridDim.x ? __ldcg(k.partial + (size_t)b * (kMaxRestart + 1) + v) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) s += pv[u];
-    }
-  }
-  red[q * 32 + v] = s;
-  __syncthreads();
-  if (threadIdx.x < nv) {
-    double z = 0.0;
-    for (int i = 0; i < NS; ++i) z += red[i * 32 + threadIdx.x];
-    dst[threadIdx.x] = z;
-  }
-  if (threadIdx.x == 0) *k.ticket = 0;
-  __syncthreads();
-}
-
 // (A) w = diag(scale) A z_j and h1 = V^T w in one pass: a CTA owns 64 rows,
 //     computes them with LPR-lane CSR rows, keeps w in shared memory and
 //     forms its partial dots (Z[j] = zbuf copied on the way).
@@ -448,7 +419,6 @@ __global__ void __launch_bounds__(kFuseThreads) k_spmv_dots(KBufs k) {
   pdl_trigger();
   pdl_wait();
   __shared__ double ws[kFuseRows];
-  __shared__ double red[kFuseThreads];
   const int j = k.st->j;
   const int nv = j + 1;
   const int r0 = blockIdx.x * kFuseRows;
@@ -484,54 +454,96 @@ __global__ void __launch_bounds__(kFuseThreads) k_spmv_dots(KBufs k) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
   if (lane == 0 && v < nv) k.partial[(size_t)blockIdx.x * (kMaxRestart + 1) + v] = s;
-  if (last_block(k.ticket)) finish_wide<kFuseThreads>(k, nv, k.st->h1, red);
 }
 
-// (B) w -= V h1 ; h2 = V^T w ; ||w||^2 in one pass; the last CTA forms
-//     h_{j+1,j} = sqrt(||w||^2 - ||h2||^2) (the norm of w - V h2 for an
-//     orthonormal V; h2 is the small second CGS correction) and runs Givens.
-// per-CTA sums of NV per-thread values for CTAs of T threads: warp-level
-// trees, then warp totals combined in warp order (deterministic)
-template <int T, int NV>
-__device__ __forceinline__ void cta_reduce_wide(const double (&acc)[NV], int nv, double* sm, double* out) {
+// Per-CTA sums of 32 per-thread values plus one extra: a butterfly
+// transpose-reduction gives lane L of every warp its warp's total of value
+// L in 31 shuffles (16+8+4+2+1) instead of 32 separate 5-level trees; warp
+// totals are then added in warp order. out[0..nv) = sums, out[nv] = extra.
+template <int T>
+__device__ __forceinline__ void cta_reduce_t32(double (&a)[32], double extra, int nv, double* sm, double* out) {
   constexpr int NW = T / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    if (v < nv) {
-      double s = acc[v];
+  for (int w = 16; w > 0; w >>= 1) {
+    const bool up = lane & w;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-      if (lane == 0) sm[v * NW + warp] = s;
+    for (int i = 0; i < w; ++i) {
+      const double send = up ? a[i] : a[i + w];
+      const double keep = up ? a[i + w] : a[i];
+      a[i] = keep + __shfl_xor_sync(kFull, send, w);
     }
   }
-  __syncthreads();
-  // vector v summed by warp v mod NW (lanes over the NW warp totals)
-  for (int v = warp; v < nv; v += NW) {
-    double s = 0.0;
-    for (int i = lane; i < NW; i += 32) s += sm[v * NW + i];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-    if (lane == 0) out[v] = s;
+  for (int o = 16; o > 0; o >>= 1) extra += __shfl_xor_sync(kFull, extra, o);
+  sm[warp * 33 + lane] = a[0];
+  if (lane == 0) sm[warp * 33 + 32] = extra;
+  __syncthreads();
+  if (threadIdx.x <= nv) {
+    const int v = threadIdx.x < nv ? threadIdx.x : 32;
+    double s = 0.0;
+    for (int i = 0; i < NW; ++i) s += sm[i * 33 + v];
+    out[threadIdx.x] = s;
   }
   __syncthreads();
 }
 
+// Fixed-order sum of `nparts` per-CTA partial rows (row stride
+// kMaxRestart+1) for values 0..nv-1 (nv <= kMaxRestart+1) into dst[]:
+// lanes own values, warps own CTA slices, slices added in order. Every CTA
+// of the consumer kernel runs it on the producer's partials, so no CTA of
+// the producer has to finish the reduction (no last-CTA tail).
+template <int T>
+__device__ __forceinline__ void sum_partials(const double* __restrict__ part, int nparts, int nv, double* dst,
+                                             double* red /* (T/32) x (kMaxRestart+1) */) {
+  constexpr int NS = T / 32;
+  constexpr int LD = kMaxRestart + 1;
+  const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+  for (int v = lane; v < LD; v += 32) {
+    double s = 0.0;
+    if (v < nv) {
+      constexpr int U = 10;
+      for (int b0 = q; b0 < nparts; b0 += NS * U) {
+        double pv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int b = b0 + NS * u;
+          pv[u] = b < nparts ? __ldcg(part + (size_t)b * LD + v) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) s += pv[u];
+      }
+    }
+    red[q * LD + v] = s;
+  }
+  __syncthreads();
+  for (int v = threadIdx.x; v < nv; v += T) {
+    double z = 0.0;
+    for (int i = 0; i < NS; ++i) z += red[i * LD + v];
+    dst[v] = z;
+  }
+  __syncthreads();
+}
+
+// (B) h1 = sum of (A)'s partials (every CTA); w -= V h1 ; partial2 <- V^T w
+//     and ||w||^2 (h2 and the norm are finished by the CTAs of (C)).
 __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm(KBufs k) {
   pdl_trigger();
   pdl_wait();
   __shared__ double sm[(kMaxRestart + 1) * (kArnThreads / 32)];
-  __shared__ double hs[kMaxRestart];
-  __shared__ double red[kArnThreads];
-  __shared__ double hsum[kMaxRestart + 1];
+  __shared__ double hs[kMaxRestart + 1];
+  __shared__ double red[(kMaxRestart + 1) * (kArnThreads / 32)];
   const int j = k.st->j;
   const int nv = j + 1;
-  if (threadIdx.x < nv) hs[threadIdx.x] = k.st->h1[threadIdx.x];
-  __syncthreads();
+  sum_partials<kArnThreads>(k.partial, k.parts_a, nv, hs, red);
+  if (blockIdx.x == 0) {
+    if (threadIdx.x < nv) k.st->h1[threadIdx.x] = hs[threadIdx.x];
+    if (threadIdx.x == 0) k.st->jc = j + 1;
+  }
   double acc[kMaxRestart];
 #pragma unroll
   for (int v = 0; v < kMaxRestart; ++v) acc[v] = 0.0;
-  double n2[1] = {0.0};
+  double n2 = 0.0;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x) {
     double wr = k.w[r];
 #pragma unroll
@@ -541,40 +553,46 @@ __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm(KBufs k) {
 #pragma unroll
     for (int v = 0; v < kMaxRestart; ++v)
       if (v < nv) acc[v] = fma(k.V[(size_t)v * k.n + r], wr, acc[v]);  // L1 hits
-    n2[0] = fma(wr, wr, n2[0]);
+    n2 = fma(wr, wr, n2);
   }
-  // partial[cta][0..nv) = h2 dots, partial[cta][nv] = ||w||^2
-  double* part = k.partial + (size_t)blockIdx.x * (kMaxRestart + 1);
-  cta_reduce_wide<kArnThreads, kMaxRestart>(acc, nv, sm, part);
-  cta_reduce_wide<kArnThreads, 1>(n2, 1, sm, part + nv);
-  if (last_block(k.ticket)) {
-    finish_wide<kArnThreads>(k, nv + 1, hsum, red);
-    if (threadIdx.x < nv) k.st->h2[threadIdx.x] = hsum[threadIdx.x];
-    __shared__ double s_hn;
-    if (threadIdx.x == 0) {
-      double h2sq = 0.0;
-      for (int v = 0; v < nv; ++v) h2sq += hsum[v] * hsum[v];
-      s_hn = sqrt(fmax(hsum[nv] - h2sq, 0.0));
-    }
-    __syncthreads();
-    givens_step(k, s_hn);
-  }
+  // partial2[cta][0..nv) = h2 dots, partial2[cta][nv] = ||w||^2
+  static_assert(kMaxRestart == 32, "cta_reduce_t32 holds one slot per Krylov vector");
+  cta_reduce_t32<kArnThreads>(acc, n2, nv, sm, k.partial2 + (size_t)blockIdx.x * (kMaxRestart + 1));
 }
 
-// (C) w -= V h2 ; v_{j+1} = w / h_{j+1,j} ; u = v_{j+1} / scale
+// (C) every CTA sums (B)'s partials into h2 and ||w||^2 and forms
+//     h_{j+1,j} = sqrt(||w||^2 - ||h2||^2) (the norm of w - V h2 for an
+//     orthonormal V; h2 is the small second CGS correction). The LAST CTA
+//     only runs the Givens step (and sets the CUDA-graph WHILE condition),
+//     overlapping the others, which do w -= V h2 ; v_{j+1} = w / h_{j+1,j} ;
+//     u = v_{j+1} / scale over the rows. Launched with one extra CTA.
 __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
   pdl_trigger();
   pdl_wait();
-  __shared__ double hs[kMaxRestart];
-  const KState* st = k.st;
-  const int jn = st->j;  // already advanced by Givens
+  __shared__ double hs[kMaxRestart + 1];
+  __shared__ double red[(kMaxRestart + 1) * (kArnThreads / 32)];
+  __shared__ double s_hn;
+  const int jn = k.st->jc;  // = j + 1; st->j itself is advanced by the Givens CTA
   const int nv = jn;
-  if (threadIdx.x < nv) hs[threadIdx.x] = st->h2[threadIdx.x];
+  sum_partials<kArnThreads>(k.partial2, k.parts_b, nv + 1, hs, red);
+  if (threadIdx.x == 0) {
+    double h2sq = 0.0;
+    for (int v = 0; v < nv; ++v) h2sq += hs[v] * hs[v];
+    s_hn = sqrt(fmax(hs[nv] - h2sq, 0.0));
+  }
   __syncthreads();
-  const double hn = st->hn;
+  const double hn = s_hn;
+  if (blockIdx.x == gridDim.x - 1) {
+    if (threadIdx.x < nv) k.st->h2[threadIdx.x] = hs[threadIdx.x];
+    __threadfence_block();
+    __syncthreads();
+    givens_step(k, hn);
+    return;
+  }
   const bool lucky = hn < 1e-14;
   double* vj = k.V + (size_t)jn * k.n;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x) {
+  const int nb = gridDim.x - 1;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += nb * blockDim.x) {
     double wr = k.w[r];
 #pragma unroll
     for (int v = 0; v < kMaxRestart; ++v)
