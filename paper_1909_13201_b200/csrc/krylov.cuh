@@ -393,7 +393,7 @@ template <int LPR>
 __device__ __forceinline__ double fused_row(const KBufs& k, int row, int lane) {
   const int k0 = row >= 0 ? __ldg(k.a_ptr + row) : 0, k1 = row >= 0 ? __ldg(k.a_ptr + row + 1) : 0;
   double s = 0.0;
-  constexpr int U = 4;
+  constexpr int U = 8;
   for (int kb = k0 + lane; kb < k1; kb += U * LPR) {
     int c[U];
     double v[U], xv[U];
@@ -493,34 +493,35 @@ __device__ __forceinline__ void cta_reduce_t32(double (&a)[32], double extra, in
 // lanes own values, warps own CTA slices, slices added in order. Every CTA
 // of the consumer kernel runs it on the producer's partials, so no CTA of
 // the producer has to finish the reduction (no last-CTA tail).
+constexpr int kSumSlices = 16;
 template <int T>
 __device__ __forceinline__ void sum_partials(const double* __restrict__ part, int nparts, int nv, double* dst,
-                                             double* red /* (T/32) x (kMaxRestart+1) */) {
-  constexpr int NS = T / 32;
+                                             double* red /* kSumSlices x (kMaxRestart+1) */) {
   constexpr int LD = kMaxRestart + 1;
-  const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
-  for (int v = lane; v < LD; v += 32) {
+  // thread t -> value t % nv of CTA slice t / nv (ns slices, fixed for a
+  // given nv, so the summation order is deterministic)
+  const int ns = min(kSumSlices, T / nv);
+  const int v = threadIdx.x % nv, q = threadIdx.x / nv;
+  if (q < ns) {
     double s = 0.0;
-    if (v < nv) {
-      constexpr int U = 10;
-      for (int b0 = q; b0 < nparts; b0 += NS * U) {
-        double pv[U];
+    constexpr int U = 10;
+    for (int b0 = q; b0 < nparts; b0 += ns * U) {
+      double pv[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int b = b0 + NS * u;
-          pv[u] = b < nparts ? __ldcg(part + (size_t)b * LD + v) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) s += pv[u];
+      for (int u = 0; u < U; ++u) {
+        const int b = b0 + ns * u;
+        pv[u] = b < nparts ? __ldcg(part + (size_t)b * LD + v) : 0.0;
       }
+#pragma unroll
+      for (int u = 0; u < U; ++u) s += pv[u];
     }
     red[q * LD + v] = s;
   }
   __syncthreads();
-  for (int v = threadIdx.x; v < nv; v += T) {
+  for (int w = threadIdx.x; w < nv; w += T) {
     double z = 0.0;
-    for (int i = 0; i < NS; ++i) z += red[i * LD + v];
-    dst[v] = z;
+    for (int i = 0; i < ns; ++i) z += red[i * LD + w];
+    dst[w] = z;
   }
   __syncthreads();
 }
@@ -532,9 +533,16 @@ __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm(KBufs k) {
   pdl_wait();
   __shared__ double sm[(kMaxRestart + 1) * (kArnThreads / 32)];
   __shared__ double hs[kMaxRestart + 1];
-  __shared__ double red[(kMaxRestart + 1) * (kArnThreads / 32)];
+  __shared__ double red[(kMaxRestart + 1) * kSumSlices];
   const int j = k.st->j;
   const int nv = j + 1;
+  // this thread's first row is loaded before the h1 reduction (independent
+  // of it), so the two latencies overlap
+  const int r0 = blockIdx.x * blockDim.x + threadIdx.x;
+  double w0 = 0.0, v0[kMaxRestart];
+#pragma unroll
+  for (int v = 0; v < kMaxRestart; ++v) v0[v] = (r0 < k.n && v < nv) ? k.V[(size_t)v * k.n + r0] : 0.0;
+  if (r0 < k.n) w0 = k.w[r0];
   sum_partials<kArnThreads>(k.partial, k.parts_a, nv, hs, red);
   if (blockIdx.x == 0) {
     if (threadIdx.x < nv) k.st->h1[threadIdx.x] = hs[threadIdx.x];
@@ -544,7 +552,18 @@ __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm(KBufs k) {
 #pragma unroll
   for (int v = 0; v < kMaxRestart; ++v) acc[v] = 0.0;
   double n2 = 0.0;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x) {
+  if (r0 < k.n) {
+    double wr = w0;
+#pragma unroll
+    for (int v = 0; v < kMaxRestart; ++v)
+      if (v < nv) wr = fma(-hs[v], v0[v], wr);
+    k.w[r0] = wr;
+#pragma unroll
+    for (int v = 0; v < kMaxRestart; ++v)
+      if (v < nv) acc[v] = fma(v0[v], wr, acc[v]);
+    n2 = fma(wr, wr, n2);
+  }
+  for (int r = r0 + gridDim.x * blockDim.x; r < k.n; r += gridDim.x * blockDim.x) {
     double wr = k.w[r];
 #pragma unroll
     for (int v = 0; v < kMaxRestart; ++v)
@@ -570,10 +589,19 @@ __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
   pdl_trigger();
   pdl_wait();
   __shared__ double hs[kMaxRestart + 1];
-  __shared__ double red[(kMaxRestart + 1) * (kArnThreads / 32)];
+  __shared__ double red[(kMaxRestart + 1) * kSumSlices];
   __shared__ double s_hn;
   const int jn = k.st->jc;  // = j + 1; st->j itself is advanced by the Givens CTA
   const int nv = jn;
+  const int nb = gridDim.x - 1;
+  const bool rows_cta = blockIdx.x < nb;
+  // first row prefetched before the reduction (see k_update_dots_norm)
+  const int r0 = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool has0 = rows_cta && r0 < k.n;
+  double w0 = 0.0, v0[kMaxRestart];
+#pragma unroll
+  for (int v = 0; v < kMaxRestart; ++v) v0[v] = (has0 && v < nv) ? k.V[(size_t)v * k.n + r0] : 0.0;
+  if (has0) w0 = k.w[r0];
   sum_partials<kArnThreads>(k.partial2, k.parts_b, nv + 1, hs, red);
   if (threadIdx.x == 0) {
     double h2sq = 0.0;
@@ -591,8 +619,18 @@ __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
   }
   const bool lucky = hn < 1e-14;
   double* vj = k.V + (size_t)jn * k.n;
-  const int nb = gridDim.x - 1;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += nb * blockDim.x) {
+  if (has0) {
+    double wr = w0;
+#pragma unroll
+    for (int v = 0; v < kMaxRestart; ++v)
+      if (v < nv) wr = fma(-hs[v], v0[v], wr);
+    if (!lucky) {
+      const double vv = wr / hn;
+      vj[r0] = vv;
+      k.ubuf[r0] = vv / k.scale[r0];
+    }
+  }
+  for (int r = r0 + nb * blockDim.x; r < k.n; r += nb * blockDim.x) {
     double wr = k.w[r];
 #pragma unroll
     for (int v = 0; v < kMaxRestart; ++v)

@@ -17,49 +17,64 @@
 
 namespace fsigpu {
 
-// Epilogues: out-of-line functors applied by lane 0 of each row.
+// Epilogues: functors applied by lane 0 of each row. pre(i) loads the
+// row's own operands (b[i], x[i], mask[i]); kernels call it right after the
+// PDL wait, BEFORE the row's dot product, so those loads overlap the
+// gathers instead of adding one dependent round trip at the end.
+struct EpiPre {
+  double a;
+  unsigned char m;
+};
 struct EpiPlain {  // y = A x                       (sparse.cpp:70-76)
   double* y;
-  __device__ void operator()(int i, double s) const { y[i] = s; }
+  __device__ EpiPre pre(int) const { return {0.0, 0}; }
+  __device__ void operator()(int i, double s, EpiPre) const { y[i] = s; }
 };
 struct EpiResid {  // r = b - A x                   (gmg.cpp:205-206, precond.cpp:312-313)
   const double* b;
   double* r;
-  __device__ void operator()(int i, double s) const { r[i] = b[i] - s; }
+  __device__ EpiPre pre(int i) const { return {b[i], 0}; }
+  __device__ void operator()(int i, double s, EpiPre p) const { r[i] = p.a - s; }
 };
 struct EpiScaled {  // w = diag(s) A z              (driver.cpp:177-183,261-262)
   const double* scale;
   double* y;
-  __device__ void operator()(int i, double s) const { y[i] = scale[i] * s; }
+  __device__ EpiPre pre(int i) const { return {scale[i], 0}; }
+  __device__ void operator()(int i, double s, EpiPre p) const { y[i] = p.a * s; }
 };
 struct EpiResidScaled {  // r = b - diag(s) A x     (krylov.cpp:31-32,116-117)
   const double* b;
   const double* scale;
   double* r;
-  __device__ void operator()(int i, double s) const { r[i] = b[i] - scale[i] * s; }
+  __device__ EpiPre pre(int i) const { return {b[i], 0}; }
+  __device__ void operator()(int i, double s, EpiPre p) const { r[i] = p.a - scale[i] * s; }
 };
 struct EpiRestrict {  // rc = R r, rc[constrained_rows below] = 0 (gmg.cpp:208-212)
   const unsigned char* mask;
   double* y;
-  __device__ void operator()(int i, double s) const { y[i] = mask[i] ? 0.0 : s; }
+  __device__ EpiPre pre(int i) const { return {0.0, mask[i]}; }
+  __device__ void operator()(int i, double s, EpiPre p) const { y[i] = p.m ? 0.0 : s; }
 };
 struct EpiProlongAdd {  // x += P ec where !constrained_cols (gmg.cpp:233-236)
   const unsigned char* mask;
   double* x;
-  __device__ void operator()(int i, double s) const {
-    if (!mask[i]) x[i] = x[i] + s;
+  __device__ EpiPre pre(int i) const { return {x[i], mask[i]}; }
+  __device__ void operator()(int i, double s, EpiPre p) const {
+    if (!p.m) x[i] = p.a + s;
   }
 };
 
 struct EpiSetScaled {  // x = 0 + omega * (FS r)   (first Richardson sweep from x = 0)
   double omega;
   double* x;
-  __device__ void operator()(int i, double s) const { x[i] = add_rn(0.0, mul_rn(omega, s)); }
+  __device__ EpiPre pre(int) const { return {0.0, 0}; }
+  __device__ void operator()(int i, double s, EpiPre) const { x[i] = add_rn(0.0, mul_rn(omega, s)); }
 };
 struct EpiAxpy {  // x += omega * (FS r)          (precond.cpp:315)
   double omega;
   double* x;
-  __device__ void operator()(int i, double s) const { x[i] = add_rn(x[i], mul_rn(omega, s)); }
+  __device__ EpiPre pre(int i) const { return {x[i], 0}; }
+  __device__ void operator()(int i, double s, EpiPre p) const { x[i] = add_rn(p.a, mul_rn(omega, s)); }
 };
 // last write of a coarse level's iterate in a V-cycle: the caller masks the
 // correction at constrained columns (gmg.cpp:230-231); doing it here lets
@@ -68,7 +83,8 @@ struct EpiAxpyMasked {
   double omega;
   double* x;
   const unsigned char* mask;
-  __device__ void operator()(int i, double s) const { x[i] = mask[i] ? 0.0 : add_rn(x[i], mul_rn(omega, s)); }
+  __device__ EpiPre pre(int i) const { return {x[i], mask[i]}; }
+  __device__ void operator()(int i, double s, EpiPre p) const { x[i] = p.m ? 0.0 : add_rn(p.a, mul_rn(omega, s)); }
 };
 
 // x gather, optionally masked (ec[constrained_cols below] = 0, gmg.cpp:230-231)
@@ -96,6 +112,8 @@ __global__ void __launch_bounds__(256) csr_kernel(int rows, const int* __restric
   pdl_trigger();
   const int k0 = ok ? __ldg(ptr + row) : 0, k1 = ok ? __ldg(ptr + row + 1) : 0;  // setup data
   pdl_wait();
+  EpiPre pe{0.0, 0};
+  if (ok && lane == 0) pe = epi.pre(row);
   double s = 0.0;
   // predicated batches of U entries per lane: all index/value loads of a
   // batch are in flight before the dependent x gathers (no early exits)
@@ -116,7 +134,7 @@ __global__ void __launch_bounds__(256) csr_kernel(int rows, const int* __restric
   }
 #pragma unroll
   for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, LPR);
-  if (ok && lane == 0) epi(row, s);
+  if (ok && lane == 0) epi(row, s, pe);
 }
 
 // Shared-memory staged CSR ("CSR-stream"). CTA b owns rows [rb[b], rb[b+1])
@@ -190,7 +208,7 @@ __global__ void __launch_bounds__(256) csr_staged_kernel(const int* __restrict__
     for (int k = a + lane; k < b; k += LPR) s += s_val[k - kv0];
 #pragma unroll
     for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, LPR);
-    if (ok && lane == 0) epi(row, s);
+    if (ok && lane == 0) epi(row, s, epi.pre(row));
   }
 }
 
@@ -395,6 +413,14 @@ __global__ void __launch_bounds__(256) prolong_resid_kernel(int rows, const int*
     a0 = __ldg(ap + row);
     a1 = __ldg(ap + row + 1);
   }
+  // the row's own operands, loaded before the dot products (see EpiPre)
+  unsigned char cm = 1;
+  double xo = 0.0, rp = 0.0;
+  if (ok && lane == 0) {
+    cm = cmask[row];
+    xo = x[row];
+    rp = r_pre[row];
+  }
   auto gather = [&](int c) -> double {
     return c >= 0 ? ((cmask_coarse && __ldg(cmask_coarse + c)) ? 0.0 : __ldg(ec + c)) : 0.0;
   };
@@ -445,8 +471,8 @@ __global__ void __launch_bounds__(256) prolong_resid_kernel(int rows, const int*
     s2 += __shfl_xor_sync(kFull, s2, o, LPR);
   }
   if (ok && lane == 0) {
-    if (!cmask[row]) x[row] = x[row] + s1;
-    r[row] = r_pre[row] - s2;
+    if (!cm) x[row] = xo + s1;
+    r[row] = rp - s2;
   }
 }
 
