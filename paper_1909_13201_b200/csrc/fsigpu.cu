@@ -686,7 +686,7 @@ struct Gmg {
       rhs = L.rbuf.p;
     }
     ProfScope ps(FSIGPU_K_COARSE, 8.0 * L.n * L.n + 16.0 * L.n, s);
-    launch_k(gemv_kernel, dim3(ceil_div((long long)L.n * 32, 256)), dim3(256), 0, s, L.n,
+    launch_k(gemv_kernel, dim3(L.n), dim3(kGemvThreads), 0, s, L.n,
              (const double*)coarse_inv.p, rhs, L.x, x_zero ? 0 : 1,
              (const unsigned char*)(mask_out ? L.cmask.p : nullptr));
     FSI_CHECK_LAUNCH();
@@ -1850,7 +1850,7 @@ int fsigpu_gmg_time_kernel(fsigpu_gmg h, int which, int level, int reps, int col
         }
         case 4:
           require(level == 0, "time: coarse GEMV lives on level 0");
-          gemv_kernel<<<ceil_div((long long)L.n * 32, 256), 256, 0, s>>>(L.n, G.coarse_inv.p, L.b, L.x, 0);
+          gemv_kernel<<<L.n, kGemvThreads, 0, s>>>(L.n, G.coarse_inv.p, L.b, L.x, 0);
           by = 8.0 * L.n * L.n + 16.0 * L.n;
           break;
         default:

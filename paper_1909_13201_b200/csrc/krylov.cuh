@@ -423,31 +423,37 @@ __global__ void __launch_bounds__(kFuseThreads) k_spmv_dots(KBufs k) {
   const int nv = j + 1;
   const int r0 = blockIdx.x * kFuseRows;
   const int t = threadIdx.x;
+  // operands that do not depend on w are loaded before the SpMV so their
+  // latency overlaps it: the V entries of the partial dots (warp v, lanes
+  // over the CTA's 128 rows, 4 each) and z_j for the copy into Z[j]
+  const int v = t >> 5, lane = t & 31;
+  double vv[kFuseRows / 32];
+#pragma unroll
+  for (int q = 0; q < kFuseRows / 32; ++q) {
+    const int row = r0 + lane + 32 * q;
+    vv[q] = (v < nv && row < k.n) ? k.V[(size_t)v * k.n + row] : 0.0;
+  }
+  const bool zc = t < kFuseRows && r0 + t < k.n;
+  const double zj = zc ? k.zbuf[r0 + t] : 0.0;
   constexpr int RPP = kFuseThreads / LPR;  // rows per pass
   for (int p = 0; p < kFuseRows; p += RPP) {
     const int rl = p + t / LPR;
     const int row = r0 + rl;
     const bool ok = rl < kFuseRows && row < k.n;
+    const bool head = ok && (t & (LPR - 1)) == 0;
+    const double sc = head ? k.scale[row] : 0.0;
     const double s = fused_row<LPR>(k, ok ? row : -1, t & (LPR - 1));
-    if (ok && (t & (LPR - 1)) == 0) {
-      const double w = k.scale[row] * s;
+    if (head) {
+      const double w = sc * s;
       k.w[row] = w;
       ws[rl] = w;
     }
   }
-  if (t < kFuseRows && r0 + t < k.n) k.Z[(size_t)j * k.n + r0 + t] = k.zbuf[r0 + t];
+  if (zc) k.Z[(size_t)j * k.n + r0 + t] = zj;
   if (t < kFuseRows && r0 + t >= k.n) ws[t] = 0.0;
   __syncthreads();
-  // partial dots: warp v (lanes over the CTA's 128 rows, 4 each)
-  const int v = t >> 5, lane = t & 31;
   double s = 0.0;
   if (v < nv) {
-    double vv[kFuseRows / 32];
-#pragma unroll
-    for (int q = 0; q < kFuseRows / 32; ++q) {
-      const int row = r0 + lane + 32 * q;
-      vv[q] = row < k.n ? k.V[(size_t)v * k.n + row] : 0.0;
-    }
 #pragma unroll
     for (int q = 0; q < kFuseRows / 32; ++q) s = fma(vv[q], ws[lane + 32 * q], s);
   }

@@ -239,24 +239,33 @@ __global__ void fs_combine_kernel(int n, int g1, int n_us, const int* __restrict
 }
 
 // Coarse solve x0 (+)= Ainv' b0 with the explicit equilibrated inverse
-// (row-major n0 x n0), one warp per row.
-__global__ void __launch_bounds__(256) gemv_kernel(int n, const double* __restrict__ M,
-                                                   const double* __restrict__ b,
-                                                   double* __restrict__ x, int accumulate,
-                                                   const unsigned char* __restrict__ mask_out = nullptr) {
-  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+// (row-major n0 x n0): one 256-thread CTA per row, so a row of <= 2048
+// columns is ONE predicated batch of loads per thread (latency-bound at
+// these sizes); xor tree per warp, warp sums added in warp order.
+constexpr int kGemvThreads = 256;
+__global__ void __launch_bounds__(kGemvThreads) gemv_kernel(int n, const double* __restrict__ M,
+                                                            const double* __restrict__ b,
+                                                            double* __restrict__ x, int accumulate,
+                                                            const unsigned char* __restrict__ mask_out = nullptr) {
+  __shared__ double red[kGemvThreads / 32];
+  const int row = blockIdx.x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   pdl_trigger();
   pdl_wait();
-  if (row >= n) return;  // warp-uniform
   const double* Mr = M + (size_t)row * n;
+  double xo = 0.0;
+  unsigned char mo = 0;
+  if (t == 0) {
+    if (accumulate) xo = x[row];
+    if (mask_out) mo = mask_out[row];
+  }
   double s = 0.0;
   constexpr int U = 8;
-  for (int jb = lane; jb < n; jb += 32 * U) {
+  for (int jb = t; jb < n; jb += kGemvThreads * U) {
     double mv[U], bv[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int j = jb + 32 * u;
+      const int j = jb + kGemvThreads * u;
       mv[u] = j < n ? __ldg(Mr + j) : 0.0;
       bv[u] = j < n ? __ldg(b + j) : 0.0;
     }
@@ -265,7 +274,14 @@ __global__ void __launch_bounds__(256) gemv_kernel(int n, const double* __restri
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-  if (lane == 0) x[row] = (mask_out && mask_out[row]) ? 0.0 : (accumulate ? x[row] + s : s);
+  if (lane == 0) red[warp] = s;
+  __syncthreads();
+  if (t == 0) {
+    double z = 0.0;
+#pragma unroll
+    for (int w = 0; w < kGemvThreads / 32; ++w) z += red[w];
+    x[row] = mo ? 0.0 : (accumulate ? xo + z : z);
+  }
 }
 
 // ---- setup: Gauss-Jordan inverse with partial pivoting on W = [A | I] ----
