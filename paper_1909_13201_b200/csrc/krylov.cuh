@@ -191,25 +191,16 @@ __global__ void __launch_bounds__(kKThreads) k_update_dots(KBufs k) {
 }
 
 // Givens update of column j on device (krylov.cpp:79-100), staged in
-// shared memory by the whole (last) CTA; one thread runs the recurrence.
-// With use_cond, also sets the restart-cycle WHILE condition.
-__device__ void givens_step(const KBufs& k, double hn) {
-  __shared__ double col[kMaxRestart + 2], cs[kMaxRestart + 1], sn[kMaxRestart + 1], g2[2];
+// shared memory by the whole CTA; one thread runs the recurrence. With
+// use_cond, also sets the restart-cycle WHILE condition. Core: col[0..j]
+// already holds H(:,j) = h1 + h2, cs/sn[0..j) the previous rotations and
+// gj = g[j]; all in shared memory / registers (loaded by the caller).
+__device__ void givens_core(const KBufs& k, int j, double hn, double* col, double* cs, double* sn, double gj) {
   KState* st = k.st;
-  const int j = st->j;
   const int mr = k.mr;
   const int t = threadIdx.x;
-  if (t <= j) col[t] = __ldcg(st->h1 + t) + __ldcg(st->h2 + t);
-  if (t < j) {
-    cs[t] = __ldcg(k.cs + t);
-    sn[t] = __ldcg(k.sn + t);
-  }
   if (t == 0) {
     col[j + 1] = hn;
-    g2[0] = __ldcg(k.g + j);
-  }
-  __syncthreads();
-  if (t == 0) {
     int lucky = 0;
     if (hn < 1e-14) {
       st->breakdown = 1;
@@ -222,11 +213,8 @@ __device__ void givens_step(const KBufs& k, double hn) {
     }
     const double denom = hypot(col[j], col[j + 1]);
     const double c = col[j] / denom, sj = col[j + 1] / denom;
-    cs[j] = c;
-    sn[j] = sj;
     col[j] = denom;
     col[j + 1] = 0.0;
-    const double gj = g2[0];
     k.g[j + 1] = -sj * gj;
     k.g[j] = c * gj;
     const double rho = fabs(-sj * gj);
@@ -240,7 +228,6 @@ __device__ void givens_step(const KBufs& k, double hn) {
   }
   __syncthreads();
   if (t <= j + 1) k.H[t * mr + j] = col[t];
-  __syncthreads();
   if (t == 0) {
     st->j = j + 1;
     if (k.use_cond) {
@@ -248,6 +235,22 @@ __device__ void givens_step(const KBufs& k, double hn) {
       cudaGraphSetConditional(k.cond, go);
     }
   }
+}
+
+__device__ void givens_step(const KBufs& k, double hn) {
+  __shared__ double col[kMaxRestart + 2], cs[kMaxRestart + 1], sn[kMaxRestart + 1];
+  __shared__ double s_gj;
+  const KState* st = k.st;
+  const int j = st->j;
+  const int t = threadIdx.x;
+  if (t <= j) col[t] = __ldcg(st->h1 + t) + __ldcg(st->h2 + t);
+  if (t < j) {
+    cs[t] = __ldcg(k.cs + t);
+    sn[t] = __ldcg(k.sn + t);
+  }
+  if (t == 0) s_gj = __ldcg(k.g + j);
+  __syncthreads();
+  givens_core(k, j, hn, col, cs, sn, s_gj);
 }
 
 // w -= V h2 ; ||w|| ; Givens
@@ -601,6 +604,18 @@ __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
   const int nv = jn;
   const int nb = gridDim.x - 1;
   const bool rows_cta = blockIdx.x < nb;
+  // Givens CTA: its inputs other than h2 are loaded before the reduction
+  __shared__ double g_col[kMaxRestart + 2], g_cs[kMaxRestart + 1], g_sn[kMaxRestart + 1];
+  double h1t = 0.0, gj = 0.0;
+  if (!rows_cta) {
+    const int t = threadIdx.x;
+    if (t < nv) h1t = __ldcg(k.st->h1 + t);
+    if (t < nv - 1) {
+      g_cs[t] = __ldcg(k.cs + t);
+      g_sn[t] = __ldcg(k.sn + t);
+    }
+    if (t == 0) gj = __ldcg(k.g + nv - 1);
+  }
   // first row prefetched before the reduction (see k_update_dots_norm)
   const int r0 = blockIdx.x * blockDim.x + threadIdx.x;
   const bool has0 = rows_cta && r0 < k.n;
@@ -616,11 +631,13 @@ __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
   }
   __syncthreads();
   const double hn = s_hn;
-  if (blockIdx.x == gridDim.x - 1) {
-    if (threadIdx.x < nv) k.st->h2[threadIdx.x] = hs[threadIdx.x];
-    __threadfence_block();
+  if (!rows_cta) {
+    if (threadIdx.x < nv) {
+      k.st->h2[threadIdx.x] = hs[threadIdx.x];
+      g_col[threadIdx.x] = h1t + hs[threadIdx.x];
+    }
     __syncthreads();
-    givens_step(k, hn);
+    givens_core(k, nv - 1, hn, g_col, g_cs, g_sn, gj);
     return;
   }
   const bool lucky = hn < 1e-14;
