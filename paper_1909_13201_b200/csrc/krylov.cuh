@@ -206,13 +206,17 @@ __device__ void givens_core(const KBufs& k, int j, double hn, double* col, doubl
       st->breakdown = 1;
       lucky = 1;
     }
+    // the running element stays in a register: the dependent chain is two
+    // flops per rotation, the shared-memory traffic is off it
+    double carry = col[0];
+#pragma unroll 4
     for (int i = 0; i < j; ++i) {
-      const double tt = cs[i] * col[i] + sn[i] * col[i + 1];
-      col[i + 1] = -sn[i] * col[i] + cs[i] * col[i + 1];
-      col[i] = tt;
+      const double nxt = col[i + 1], c = cs[i], sg = sn[i];
+      col[i] = c * carry + sg * nxt;
+      carry = -sg * carry + c * nxt;
     }
-    const double denom = hypot(col[j], col[j + 1]);
-    const double c = col[j] / denom, sj = col[j + 1] / denom;
+    const double denom = hypot(carry, hn);
+    const double c = carry / denom, sj = hn / denom;
     col[j] = denom;
     col[j + 1] = 0.0;
     k.g[j + 1] = -sj * gj;
@@ -624,10 +628,12 @@ __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
   for (int v = 0; v < kMaxRestart; ++v) v0[v] = (has0 && v < nv) ? k.V[(size_t)v * k.n + r0] : 0.0;
   if (has0) w0 = k.w[r0];
   sum_partials<kArnThreads>(k.partial2, k.parts_b, nv + 1, hs, red);
-  if (threadIdx.x == 0) {
-    double h2sq = 0.0;
-    for (int v = 0; v < nv; ++v) h2sq += hs[v] * hs[v];
-    s_hn = sqrt(fmax(hs[nv] - h2sq, 0.0));
+  if (threadIdx.x < 32) {
+    double q = 0.0;
+    for (int v = threadIdx.x; v < nv; v += 32) q = fma(hs[v], hs[v], q);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(kFull, q, o);
+    if (threadIdx.x == 0) s_hn = sqrt(fmax(hs[nv] - q, 0.0));
   }
   __syncthreads();
   const double hn = s_hn;
