@@ -889,7 +889,15 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
       apv.push_back(0.0);
     }
     L.AP.create(d.n, d.nc, app.data(), api.data(), apv.data(), s);
-    L.AP.unroll = 4;  // its P half already adds 2 loads per lane to the batch
+    // its P half already adds 2 loads per lane to each batch: on large
+    // (HBM-bound) levels batches of 4 AP entries; on small (L2-resident)
+    // ones half the lanes with batches of 8 (warm sweeps, tools/tune_spmv.py)
+    if (d.n < 65536) {
+      L.AP.lpr = std::max(2, L.AP.lpr / 2);
+      L.AP.unroll = 8;
+    } else {
+      L.AP.unroll = 4;
+    }
   }
   require(d.g1 >= 0 && d.n_us >= 0 && d.g1 + d.n_us <= d.n, "fs: bad group sizes");
   L.g1 = d.g1;

@@ -1,6 +1,8 @@
 """Sweep SpMV launch shapes (lanes per row x batch depth) on one hierarchy.
 
 usage: tune_spmv.py [data.fsix] [level ...]   (default: every level >= 1)
+FSI_WARM=1 times back-to-back launches (L2-resident, the in-solve regime of
+small hierarchies) instead of launches after an L2 flush.
 """
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -12,15 +14,16 @@ path = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "data", "cfg0.fs
 P = load_case(path)
 G = fsigpu.GmgPreconditioner(P.levels)
 levels = [int(a) for a in sys.argv[2:]] or list(range(1, len(P.levels)))
+cold = os.environ.get("FSI_WARM", "0") != "1"
 for lev in levels:
     L = P.levels[lev]
     for which, kname in [("A", "residual"), ("FS", "fs_smoother"), ("AP", "prolong_resid")]:
         best, default = None, None
-        default = G.time_kernel(kname, lev, reps=10, cold=True)[0]
+        default = G.time_kernel(kname, lev, reps=10, cold=cold)[0]
         for lpr in [2, 4, 8, 16, 32]:
             for u in [4, 8]:
                 G.set_launch(lev, which, lpr, u)
-                ms, by = G.time_kernel(kname, lev, reps=10, cold=True)
+                ms, by = G.time_kernel(kname, lev, reps=10, cold=cold)
                 if best is None or ms < best[0]:
                     best = (ms, lpr, u, by)
         print(f"L{lev} n={L.n:8d} nnz/row={L.A.nnz / L.n:5.1f} {which:3s} default {default*1000:8.2f} us  best lpr={best[1]:2d} u={best[2]} "
