@@ -414,6 +414,133 @@ __device__ __forceinline__ void tile_inverses(const double* A, int m, int k0, in
   }
 }
 
+// Register version of tile_inverses for one warp, lane c = column c:
+// which == 0 writes the strict lower part of inv(L_pp), which == 1 the upper
+// part of inv(U_pp) (incl. the diagonal), into the same S layout. The loops
+// run over all 32 steps (x[k] = 0 for the steps before column c, so those
+// updates leave x unchanged) and index x at compile time; the diagonal
+// reciprocals are formed once per lane and broadcast by shuffle, which
+// takes the divisions off the back-substitution chain.
+__device__ __forceinline__ void tile_inverse_warp(const double* A, int m, int k0, int kb, double* S, int c,
+                                                  int which) {
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) x[i] = (i == c) ? 1.0 : 0.0;
+  if (which == 0) {
+#pragma unroll
+    for (int k = 0; k < 31; ++k) {
+      if (k < kb - 1) {
+        const double xk = x[k];
+        const double* Lk = A + (size_t)(k0 + k) * m + k0;
+        // rows i >= kb read past the tile (still inside the staged block
+        // and its scratch); they never feed back into x[k < kb]
+#pragma unroll
+        for (int i = k + 1; i < 32; ++i) x[i] = fma(-Lk[i], xk, x[i]);
+      }
+    }
+    if (c < kb) {
+#pragma unroll
+      for (int i = 1; i < 32; ++i)
+        if (i > c && i < kb) S[c * kTileLd + i] = x[i];
+    }
+  } else {
+    const double rinv = (c < kb) ? 1.0 / A[(size_t)(k0 + c) * m + k0 + c] : 0.0;
+#pragma unroll
+    for (int k = 31; k >= 0; --k) {
+      if (k < kb) {
+        const double xk = x[k] * __shfl_sync(kFull, rinv, k);
+        x[k] = xk;
+        const double* Uk = A + (size_t)(k0 + k) * m + k0;
+#pragma unroll
+        for (int i = 0; i < k; ++i) x[i] = fma(-Uk[i], xk, x[i]);
+      }
+    }
+    if (c < kb) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i <= c) S[c * kTileLd + i] = x[i];
+    }
+  }
+}
+
+// Outputs of a finished factorization held column-major in A (shared or
+// global): pivots, the composed gather map, the optional bit-exact LU and
+// the solve format (tile inverses + packed panels, see PanelGeom).
+// perm[k] = pivot row of step k; scratch: m doubles; S: 32 x kTileLd doubles.
+template <int NT, bool REG_TILE>
+__device__ __forceinline__ void lu_write_outputs(const double* A, int m, int b, const int* perm, double* scratch,
+                                                 double* S, const long long* __restrict__ row_off,
+                                                 const long long* __restrict__ lu_off,
+                                                 const long long* __restrict__ sf_off, double* __restrict__ lu_out,
+                                                 bool write_lu, double* __restrict__ sf_out, int* __restrict__ piv_out,
+                                                 int* __restrict__ gsrc_out, int* __restrict__ lperm_out,
+                                                 const int* __restrict__ src_pos, int pos_base) {
+  const int tid = threadIdx.x;
+  const long long ro = row_off[b];
+  const long long off = lu_off[b];
+  if (tid == 0) {
+    for (int k = 0; k < m; ++k) piv_out[ro + k] = perm[k];
+    // compose the sequential swaps (dense.cpp:74-75) into one gather map
+    for (int k = 0; k < m; ++k) scratch[k] = (double)k;
+    for (int k = 0; k < m; ++k) {
+      const int p = perm[k];
+      const double t2 = scratch[k];
+      scratch[k] = scratch[p];
+      scratch[p] = t2;
+    }
+  }
+  __syncthreads();
+  for (int s2 = tid; s2 < m; s2 += NT) {
+    const int loc = (int)scratch[s2];
+    gsrc_out[ro + s2] = src_pos ? src_pos[ro + loc] + pos_base : (int)(ro + loc);
+    lperm_out[ro + s2] = loc;
+  }
+  if (lu_out && write_lu)
+    for (long long e = tid; e < (long long)m * m; e += NT) lu_out[off + e] = A[e];
+
+  // ---- solve format: tile inverses + packed panels
+  double* dst = sf_out + sf_off[b];
+  const int P = (m + 31) / 32;
+  long long po = 0;
+  for (int p = 0; p < P; ++p) {
+    const PanelGeom g(m, p);
+    const int k0 = g.k0, kb = g.kb;
+    if (!REG_TILE) {
+      tile_inverses(A, m, k0, kb, S, tid);
+    } else if (NT >= 64) {
+      if (tid < 64) tile_inverse_warp(A, m, k0, kb, S, tid & 31, tid >> 5);
+    } else {
+      tile_inverse_warp(A, m, k0, kb, S, tid, 0);
+      tile_inverse_warp(A, m, k0, kb, S, tid, 1);
+    }
+    __syncthreads();
+    double* fw = dst + po;
+    for (int e = tid; e < 32 * 32; e += NT) {
+      const int kk = e >> 5, i = e & 31;
+      if (kk < kb && i < kb && i > kk) fw[ltri_col(kb, kk) + i - kk - 1] = S[kk * kTileLd + i];
+    }
+    if (tid == 0 && g.lte > g.lt) fw[g.lt] = 0.0;
+    double* lp = fw + g.lte;
+    for (int e = tid; e < g.hLe * kb; e += NT) {
+      const int kk = e / g.hLe, r = e % g.hLe;
+      lp[e] = r < g.hL ? A[(size_t)(k0 + kk) * m + k0 + kb + r] : 0.0;
+    }
+    double* bw = fw + g.fwd_size();
+    for (int e = tid; e < 32 * 32; e += NT) {
+      const int jj = e >> 5, i = e & 31;
+      if (jj < kb && i <= jj) bw[utri_col(jj) + i] = S[jj * kTileLd + i];
+    }
+    if (tid == 0 && g.ute > g.ut) bw[g.ut] = 0.0;
+    double* up = bw + g.ute;
+    for (int e = tid; e < k0 * kb; e += NT) {
+      const int jj = e / k0, r = e % k0;
+      up[e] = A[(size_t)(k0 + jj) * m + r];
+    }
+    po += g.size();
+    __syncthreads();
+  }
+}
+
 // Factor one block per CTA (DenseFactorization ctor, dense.cpp:31-67), then
 // write the solve format (tile inverses + packed panels, see PanelGeom).
 // src: column-major input (same offsets as lu_off). SMEM: the block is
@@ -521,57 +648,152 @@ __global__ void __launch_bounds__(NT)
     return;
   }
   __syncthreads();
-  const long long ro = row_off[b];
-  if (tid == 0) {
-    for (int k = 0; k < m; ++k) piv_out[ro + k] = perm[k];
-    // compose the sequential swaps (dense.cpp:74-75) into one gather map
-    for (int k = 0; k < m; ++k) rowmax[k] = (double)k;
-    for (int k = 0; k < m; ++k) {
-      const int p = perm[k];
-      const double t2 = rowmax[k];
-      rowmax[k] = rowmax[p];
-      rowmax[p] = t2;
+  lu_write_outputs<NT, false>(A, m, b, perm, rowmax, S, row_off, lu_off, sf_off, lu_out, SMEM || lu_out != work, sf_out,
+                       piv_out, gsrc_out, lperm_out, src_pos, pos_base);
+}
+
+// One elimination step k = K of lu_reg_kernel, recursing to K + 1: the
+// step index is a template parameter so every register index is a
+// compile-time constant (a rolled loop would put the row array in local
+// memory). m is uniform per CTA. One CTA barrier per step: each warp's
+// best candidate row publishes itself in a per-warp slot (double-buffered
+// by step parity) before the barrier; after it every thread picks the
+// winning slot. Slot layout (16-B aligned doubles): [0] |pivot| bits + 1
+// (0 = no candidate), [1] logical row | singular flag << 30, then the row
+// with the pivot's reciprocal at index K. Returns true on a singular pivot.
+template <int MM>
+struct LuSlot {
+  static constexpr int kStride = MM + 2;  // even: keeps every slot 16-B aligned
+};
+__device__ __forceinline__ unsigned long long lu_vkey(double v) {
+  return (unsigned long long)__double_as_longlong(v) + (1ull << 32);
+}
+template <int K, int MM, int NW>
+struct LuRegStep {
+  static __device__ __forceinline__ bool run(double (&a)[MM], double rmax, int& pos, int m, int t, double* slots,
+                                             int* perm) {
+    constexpr int kNone = 1 << 20;
+    constexpr int kStride = LuSlot<MM>::kStride;
+    if (K >= m) return false;
+    const int lane = t & 31, warp = t >> 5;
+    constexpr int buf = K & 1;
+    // candidate of this row; its reciprocal is formed off the critical path
+    const bool cand = pos >= K && pos < m;
+    const double my_inv = 1.0 / a[K];
+    // warp argmax of (|a_k|, -row): |a| >= 0 orders like its bit pattern,
+    // so three redux steps (high word, low word, lowest row) replace the
+    // shuffle tree
+    const unsigned long long vb = cand ? lu_vkey(fabs(a[K])) : 0ull;
+    const unsigned hi = (unsigned)(vb >> 32), lo = (unsigned)vb;
+    const unsigned mh = __reduce_max_sync(kFull, hi);
+    const unsigned ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
+    const unsigned key = __reduce_min_sync(kFull, (cand && hi == mh && lo == ml) ? (unsigned)pos : (unsigned)kNone);
+    double* slot = slots + (size_t)(buf * NW + warp) * kStride;
+    if (mh == 0) {  // no candidate row in this warp: an empty slot
+      if (lane == 0) slot[0] = __longlong_as_double(0);
+    } else if ((unsigned)pos == key) {  // this warp's best row publishes itself
+      const int bad = fabs(a[K]) <= 1e-14 * fmax(rmax, 1e-300);
+      reinterpret_cast<double2*>(slot)[0] =
+          make_double2(__longlong_as_double((long long)vb), __longlong_as_double((long long)(key | (bad << 30))));
+      double* r = slot + 2;
+      r[K] = my_inv;
+#pragma unroll
+      for (int j = K + 1; j < MM; ++j) r[j] = a[j];
     }
+    if (NW > 1) __syncthreads();
+    else __syncwarp();
+    // the reference scan starts from |a_kk| and keeps the first strictly
+    // larger value: the maximum at the lowest logical row
+    int ws = buf * NW;
+    unsigned long long bv = (unsigned long long)__double_as_longlong(slots[(size_t)ws * kStride]);
+    int bk = (int)__double_as_longlong(slots[(size_t)ws * kStride + 1]);
+#pragma unroll
+    for (int w = 1; w < NW; ++w) {
+      const double2 o = reinterpret_cast<const double2*>(slots + (size_t)(buf * NW + w) * kStride)[0];
+      const unsigned long long ov = (unsigned long long)__double_as_longlong(o.x);
+      const int ok = (int)__double_as_longlong(o.y);
+      if (ov > bv || (ov == bv && (ok & 0x3fffffff) < (bk & 0x3fffffff))) {
+        bv = ov;
+        bk = ok;
+        ws = buf * NW + w;
+      }
+    }
+    if (NW == 1) bk = (int)__double_as_longlong(slots[(size_t)ws * kStride + 1]);
+    const int p = bk & 0x3fffffff;
+    if (t == 0) perm[K] = p;
+    pos = (pos == p) ? K : (pos == K ? p : pos);
+    if (bk >> 30) return true;
+    if (pos > K && pos < m) {
+      const double* r = slots + (size_t)ws * kStride + 2;
+      const double l = mul_rn(a[K], r[K]);
+      a[K] = l;
+#pragma unroll
+      for (int j = K + 1; j < MM; ++j) a[j] = sub_rn(a[j], mul_rn(l, r[j]));
+    }
+    if constexpr (K + 1 < MM) return LuRegStep<K + 1, MM, NW>::run(a, rmax, pos, m, t, slots, perm);
+    return false;
+  }
+};
+
+// Register-resident LU for small blocks (m <= MM <= 64): one thread per
+// block row, the row held in registers (a[MM], compile-time indexed: the
+// elimination loop is fully unrolled). Row interchanges are not data moves:
+// each thread tracks the logical position `pos` of its physical row, and a
+// swap (k, p) only exchanges two positions. This is the same sequence of
+// rounded operations per entry as DenseFactorization (dense.cpp:31-67):
+//   * pivot = largest |a_ik| over logical rows i >= k, ties to the lowest
+//     logical row (the reference's first-strictly-larger scan),
+//   * row_max travels with its row (it is per thread), singular test
+//     |pivot| <= 1e-14 * max(row_max, 1e-300),
+//   * l = a_ik * (1/pivot), then a_ij = a_ij - l * a_kj, non-fused, k ascending.
+// Per step: a shuffle argmax per warp + one cross-warp combine, the pivot
+// thread publishes its row in shared memory, every active row updates its
+// registers. Two CTA barriers per step and no shared-memory traffic for the
+// trailing matrix. The finished rows are placed at their logical positions
+// in shared memory and the common writer produces the solve format.
+// dynamic smem (doubles): [A: m*m][scratch: m][perm: m ints][S: 32*kTileLd]
+template <int MM>
+__global__ void __launch_bounds__(MM <= 32 ? 32 : 64)
+    lu_reg_kernel(const int* __restrict__ blist, const int* __restrict__ msz, const long long* __restrict__ lu_off,
+                  const long long* __restrict__ row_off, const long long* __restrict__ sf_off,
+                  const double* __restrict__ src, double* __restrict__ lu_out, double* __restrict__ sf_out,
+                  int* __restrict__ piv_out, int* __restrict__ gsrc_out, int* __restrict__ lperm_out,
+                  const int* __restrict__ src_pos, int pos_base, int* __restrict__ fail) {
+  constexpr int NT = MM <= 32 ? 32 : 64;
+  constexpr int NW = NT / 32;
+  constexpr int kNone = 1 << 20;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ __align__(16) double s_slots[2 * NW * LuSlot<MM>::kStride];
+  const int b = blist[blockIdx.x];
+  const int m = msz[b];
+  const long long off = lu_off[b];
+  const int t = threadIdx.x;
+  double* A = smem;
+  double* scratch = smem + (size_t)m * m;
+  int* perm = reinterpret_cast<int*>(scratch + m);
+  double* S = scratch + m + (m + 1) / 2;
+
+  double a[MM];
+  const bool valid = t < m;
+#pragma unroll
+  for (int j = 0; j < MM; ++j) a[j] = (valid && j < m) ? __ldg(src + off + (size_t)j * m + t) : 0.0;
+  double rmax = 0.0;
+#pragma unroll
+  for (int j = 0; j < MM; ++j) rmax = fmax(rmax, fabs(a[j]));
+  int pos = valid ? t : kNone;
+  if (LuRegStep<0, MM, NW>::run(a, rmax, pos, m, t, s_slots, perm)) {
+    if (t == 0) atomicMin(fail, b);
+    return;
+  }
+  // rows to their logical positions, column-major
+  if (valid) {
+#pragma unroll
+    for (int j = 0; j < MM; ++j)
+      if (j < m) A[(size_t)j * m + pos] = a[j];
   }
   __syncthreads();
-  for (int s2 = tid; s2 < m; s2 += NT) {
-    const int loc = (int)rowmax[s2];
-    gsrc_out[ro + s2] = src_pos ? src_pos[ro + loc] + pos_base : (int)(ro + loc);
-    lperm_out[ro + s2] = loc;
-  }
-  if (lu_out && (SMEM || lu_out != work))
-    for (long long e = tid; e < (long long)m * m; e += NT) lu_out[off + e] = A[e];
-
-  // ---- solve format: tile inverses + packed panels
-  double* dst = sf_out + sf_off[b];
-  const int P = (m + 31) / 32;
-  long long po = 0;
-  for (int p = 0; p < P; ++p) {
-    const PanelGeom g(m, p);
-    const int k0 = g.k0, kb = g.kb;
-    tile_inverses(A, m, k0, kb, S, tid);
-    __syncthreads();
-    double* fw = dst + po;
-    for (int kk = 0; kk < kb; ++kk)
-      for (int i = kk + 1 + tid; i < kb; i += NT) fw[ltri_col(kb, kk) + i - kk - 1] = S[kk * kTileLd + i];
-    if (tid == 0 && g.lte > g.lt) fw[g.lt] = 0.0;
-    double* lp = fw + g.lte;
-    for (int e = tid; e < g.hLe * kb; e += NT) {
-      const int kk = e / g.hLe, r = e % g.hLe;
-      lp[e] = r < g.hL ? A[(size_t)(k0 + kk) * m + k0 + kb + r] : 0.0;
-    }
-    double* bw = fw + g.fwd_size();
-    for (int jj = 0; jj < kb; ++jj)
-      for (int i = tid; i <= jj; i += NT) bw[utri_col(jj) + i] = S[jj * kTileLd + i];
-    if (tid == 0 && g.ute > g.ut) bw[g.ut] = 0.0;
-    double* up = bw + g.ute;
-    for (int e = tid; e < k0 * kb; e += NT) {
-      const int jj = e / k0, r = e % k0;
-      up[e] = A[(size_t)(k0 + jj) * m + r];
-    }
-    po += g.size();
-    __syncthreads();
-  }
+  lu_write_outputs<NT, true>(A, m, b, perm, scratch, S, row_off, lu_off, sf_off, lu_out, true, sf_out, piv_out,
+                       gsrc_out, lperm_out, src_pos, pos_base);
 }
 
 // Principal block A[dofs, dofs] of a CSR matrix into column-major dense

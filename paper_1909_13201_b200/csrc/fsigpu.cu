@@ -303,6 +303,13 @@ struct Csr {
 enum BlockMode { kModeLU = 0, kModeInverse = 1, kModeAssembled = 2 };
 static int g_default_mode = kModeAssembled;
 
+// Small-block LU variant: register-resident rows (default) or the
+// shared-memory CTA kernel (FSIGPU_LU_SMEM=1, kept for A/B measurement).
+static bool lu_register_path() {
+  const char* e = std::getenv("FSIGPU_LU_SMEM");
+  return !(e && e[0] == '1');
+}
+
 struct Blocks {
   int mode = kModeLU;
   long long nb = 0;
@@ -390,24 +397,43 @@ struct Blocks {
   // LU of every block from src (column-major, lu_off offsets). The three
   // size classes (register/smem small, smem large, global) and their block
   // lists are fixed at layout time, so a refactor only launches kernels.
-  std::vector<int> h_cls[3];
-  DevBuf<int> d_cls[3];
-  int cls_max[3] = {0, 0, 0};
+  // classes 0..4: register LU, rows of MM = 16/32/48/56/64 (one thread per
+  // row); 5: shared-memory staged (m <= 164); 6: in place in global memory.
+  static constexpr int kNumCls = 7;
+  static constexpr int kRegMM[5] = {16, 32, 48, 56, 64};
+  std::vector<int> h_cls[kNumCls];
+  DevBuf<int> d_cls[kNumCls];
+  int cls_max[kNumCls] = {};
   DevBuf<int> fail;
   void build_classes(cudaStream_t s) {
-    for (int c = 0; c < 3; ++c) {
+    for (int c = 0; c < kNumCls; ++c) {
       h_cls[c].clear();
       cls_max[c] = 0;
     }
+    const bool reg = lu_register_path();
     for (long long b = 0; b < nb; ++b) {
       const int mm = h_m[b];
-      const int c = mm <= 64 ? 0 : mm <= 164 ? 1 : 2;
+      int c = mm <= 164 ? 5 : 6;
+      if (reg && mm <= 64) {
+        c = 0;
+        while (mm > kRegMM[c]) ++c;
+      }
       h_cls[c].push_back((int)b);
       cls_max[c] = std::max(cls_max[c], mm);
     }
-    for (int c = 0; c < 3; ++c)
+    for (int c = 0; c < kNumCls; ++c)
       if (!h_cls[c].empty()) d_cls[c].upload(h_cls[c], s);
     fail.alloc(1);
+  }
+  template <int MM>
+  void launch_reg(int which, const double* src, double* luo, const int* src_pos, int pos_base, cudaStream_t s) {
+    const int mx = cls_max[which];
+    const size_t sm = (size_t)((size_t)mx * mx + mx + (mx + 1) / 2 + 32 * kTileLd + 8) * 8;
+    auto k = lu_reg_kernel<MM>;
+    FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k<<<(int)h_cls[which].size(), MM <= 32 ? 32 : 64, sm, s>>>(d_cls[which].p, m.p, lu_off.p, row_off.p,
+                                                             sf_off.p, src, luo, sf.p, piv.p, gsrc.p, lperm.p,
+                                                             src_pos, pos_base, fail.p);
   }
   void factor(const double* src, const int* src_pos, int pos_base, cudaStream_t s) {
     if (!fail.n) build_classes(s);
@@ -422,30 +448,38 @@ struct Blocks {
       const int grid = (int)h_cls[which].size();
       const int mx = cls_max[which];
       const int* bl = d_cls[which].p;
-      if (which == 0) {
-        const size_t sm = smem_bytes(mx, true);
-        auto k = lu_factor_kernel<128, true>;
-        FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        k<<<grid, 128, sm, s>>>(bl, m.p, lu_off.p, row_off.p, sf_off.p, src, nullptr, luo, sf.p, piv.p, gsrc.p,
-                                lperm.p, src_pos, pos_base, fail.p);
-      } else if (which == 1) {
-        const size_t sm = smem_bytes(mx, true);
-        auto k = lu_factor_kernel<256, true>;
-        FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        k<<<grid, 256, sm, s>>>(bl, m.p, lu_off.p, row_off.p, sf_off.p, src, nullptr, luo, sf.p, piv.p, gsrc.p,
-                                lperm.p, src_pos, pos_base, fail.p);
-      } else {
-        const size_t sm = smem_bytes(mx, false);
-        auto k = lu_factor_kernel<256, false>;
-        FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        k<<<grid, 256, sm, s>>>(bl, m.p, lu_off.p, row_off.p, sf_off.p, src, lu.p, lu.p, sf.p, piv.p, gsrc.p,
-                                lperm.p, src_pos, pos_base, fail.p);
+      switch (which) {
+        case 0: launch_reg<16>(which, src, luo, src_pos, pos_base, s); break;
+        case 1: launch_reg<32>(which, src, luo, src_pos, pos_base, s); break;
+        case 2: launch_reg<48>(which, src, luo, src_pos, pos_base, s); break;
+        case 3: launch_reg<56>(which, src, luo, src_pos, pos_base, s); break;
+        case 4: launch_reg<64>(which, src, luo, src_pos, pos_base, s); break;
+        case 5: {
+          const size_t sm = smem_bytes(mx, true);
+          if (mx <= 64) {
+            auto k = lu_factor_kernel<128, true>;
+            FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            k<<<grid, 128, sm, s>>>(bl, m.p, lu_off.p, row_off.p, sf_off.p, src, nullptr, luo, sf.p, piv.p, gsrc.p,
+                                    lperm.p, src_pos, pos_base, fail.p);
+          } else {
+            auto k = lu_factor_kernel<256, true>;
+            FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            k<<<grid, 256, sm, s>>>(bl, m.p, lu_off.p, row_off.p, sf_off.p, src, nullptr, luo, sf.p, piv.p, gsrc.p,
+                                    lperm.p, src_pos, pos_base, fail.p);
+          }
+          break;
+        }
+        default: {
+          const size_t sm = smem_bytes(mx, false);
+          auto k = lu_factor_kernel<256, false>;
+          FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+          k<<<grid, 256, sm, s>>>(bl, m.p, lu_off.p, row_off.p, sf_off.p, src, lu.p, lu.p, sf.p, piv.p, gsrc.p,
+                                  lperm.p, src_pos, pos_base, fail.p);
+        }
       }
       FSI_CHECK_LAUNCH();
     };
-    run(0);
-    run(1);
-    run(2);
+    for (int c = 0; c < kNumCls; ++c) run(c);
     int bad = 0;
     FSI_CUDA(cudaMemcpyAsync(&bad, fail.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     FSI_CUDA(cudaStreamSynchronize(s));

@@ -228,6 +228,43 @@ def test_block_edge_cases():
     assert E.solve(np.zeros(0)).shape == (0,)
 
 
+@pytest.mark.parametrize("variant", ["register", "smem"])
+def test_small_lu_variants_ties_bitexact(variant, monkeypatch):
+    """Both small-block LU kernels (register rows, the default; shared-memory
+    CTA, FSIGPU_LU_SMEM=1) against DenseFactorization, on sign matrices where
+    every pivot search sees ties (the reference keeps the lowest row,
+    dense.cpp:42-49) and on random blocks of every register class size."""
+    monkeypatch.setenv("FSIGPU_LU_SMEM", "1" if variant == "smem" else "0")
+    rng = np.random.default_rng(11)
+    mats = []
+    for m in [3, 8, 16, 17, 31, 32, 40, 48, 49, 54, 56, 59, 62, 64]:
+        mats.append(rng.uniform(-1, 1, (m, m)))
+        s = rng.choice([-1.0, 1.0], (m, m))
+        try:
+            O.dense_factor(s)
+            mats.append(s)
+        except ZeroDivisionError:
+            pass
+    B = fsigpu.DenseBlocks.from_dense(mats)
+    sizes = [a.shape[0] for a in mats]
+    for a, (lu, piv) in zip(mats, B.lu(sizes)):
+        lo, po = O.dense_factor(a)
+        assert np.array_equal(piv, po), f"pivots differ (m={a.shape[0]})"
+        assert np.array_equal(lu, lo), f"LU not bit-identical (m={a.shape[0]})"
+    rhs = [rng.uniform(-1, 1, m) for m in sizes]
+    x = B.solve(np.concatenate(rhs))
+    o = 0
+    for a, b in zip(mats, rhs):
+        m = a.shape[0]
+        lo, po = O.dense_factor(a)
+        assert rel(x[o:o + m], O.dense_solve(lo, po, b)) <= 1e-12
+        o += m
+    # a singular block in a register class still reports its label
+    with pytest.raises(fsigpu.SingularBlockError) as e:
+        fsigpu.DenseBlocks.from_dense([np.eye(40), np.ones((50, 50))], labels=["ok", "fs-solid-dp-7"])
+    assert e.value.label == "fs-solid-dp-7"
+
+
 def test_singular_block_label():
     mats = [np.eye(3), np.array([[1.0, 2.0], [2.0, 4.0]]), np.eye(2)]
     with pytest.raises(fsigpu.SingularBlockError) as e:
