@@ -306,6 +306,187 @@ __global__ void __launch_bounds__(kSolveThreads) block_solve_kernel(SolveArgs a)
   }
 }
 
+// ---------------------------------------------------------------- pipelined small-block solve
+// Batched LU solve of blocks with m <= 64 and a plain gathered right-hand
+// side (config 1: no lumped-Jacobi rows). Each warp streams its own blocks
+// (block = gw, gw + G, ...) through two shared-memory buffers: one
+// cp.async.bulk moves a block's whole solve format (contiguous, 16-B
+// aligned, ~8 m^2 bytes) while the warp solves the previous block out of
+// shared memory, so the HBM stream never waits on the dependent phases of
+// a solve. The gathered right-hand side runs two blocks ahead in
+// registers (index loads for block i+2, value loads for block i+1).
+// dynamic smem: [NW][2][cap] doubles, then xs[NW][64]; static: mbarriers.
+struct SmallPipeArgs {
+  const int* m;
+  const long long* sf_off;
+  const long long* row_off;
+  const double* sf;
+  const int* gsrc;
+  const double* r;
+  double* out;
+  long long nb;
+  int cap;  // doubles per buffer
+};
+
+// solve one block (m <= 64) whose solve format is at blk (shared memory);
+// xs holds the pivoted right-hand side on entry and the solution on exit
+__device__ __forceinline__ void small_solve_smem(const double* blk, int m, double* xs, int lane) {
+  const int P = (m + 31) / 32;
+  const long long po1 = PanelGeom(m, 0).size();
+  for (int q = 0; q < 2 * P; ++q) {
+    const bool fwd = q < P;
+    const int p = fwd ? q : 2 * P - 1 - q;
+    const PanelGeom g(m, p);
+    const double* src = blk + (p ? po1 : 0) + (fwd ? 0 : g.fwd_size());
+    const int k0 = g.k0, kb = g.kb;
+    const int i = lane;
+    // diagonal tile: two interleaved partial sums halve the FMA chain
+    double s0 = 0.0, s1 = 0.0;
+    if (fwd) {
+#pragma unroll
+      for (int kk = 0; kk < 32; kk += 2) {
+        const double v0 = (kk < i && i < kb) ? src[ltri_col(kb, kk) + i - kk - 1] : 0.0;
+        const double v1 = (kk + 1 < i && i < kb) ? src[ltri_col(kb, kk + 1) + i - kk - 2] : 0.0;
+        s0 = fma(v0, xs[k0 + kk], s0);
+        s1 = fma(v1, xs[k0 + kk + 1], s1);
+      }
+    } else {
+#pragma unroll
+      for (int jj = 0; jj < 32; jj += 2) {
+        const double v0 = (jj < kb && jj >= i) ? src[utri_col(jj) + i] : 0.0;
+        const double v1 = (jj + 1 < kb && jj + 1 >= i) ? src[utri_col(jj + 1) + i] : 0.0;
+        s0 = fma(v0, jj < kb ? xs[k0 + jj] : 0.0, s0);
+        s1 = fma(v1, jj + 1 < kb ? xs[k0 + jj + 1] : 0.0, s1);
+      }
+    }
+    const double y = fwd ? xs[k0 + i] + (s0 + s1) : s0 + s1;
+    __syncwarp();
+    if (i < kb) xs[k0 + i] = y;
+    __syncwarp();
+    // off-diagonal panel: rows below (fwd, h = hL <= 32) or above (bwd, h = k0 <= 32)
+    const int h = fwd ? g.hL : k0;
+    if (h > 0) {
+      const int ld = fwd ? g.hLe : k0;
+      const double* pan = fwd ? src + g.lte : src + g.ute;
+      const int rbase = fwd ? k0 + kb : 0;
+      double t0 = 0.0, t1 = 0.0;
+      if (lane < h) {
+#pragma unroll
+        for (int kk = 0; kk < 32; kk += 2) {
+          if (kk < kb) t0 = fma(pan[(size_t)kk * ld + lane], xs[k0 + kk], t0);
+          if (kk + 1 < kb) t1 = fma(pan[(size_t)(kk + 1) * ld + lane], xs[k0 + kk + 1], t1);
+        }
+        xs[rbase + lane] -= t0 + t1;
+      }
+      __syncwarp();
+    }
+  }
+}
+
+constexpr int kPipeMaxWarps = 8;
+__global__ void __launch_bounds__(kPipeMaxWarps * 32) small_pipe_solve_kernel(SmallPipeArgs a) {
+  extern __shared__ __align__(16) double dsm[];
+  __shared__ unsigned long long bars[kPipeMaxWarps][2];
+  const int NW = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long G = (long long)gridDim.x * NW;
+  const long long b0 = (long long)blockIdx.x * NW + warp;  // iteration j handles block b0 + j*G
+  double* buf = dsm + (size_t)warp * 2 * a.cap;
+  double* xs = dsm + (size_t)NW * 2 * a.cap + warp * 64;
+  unsigned long long* bar = bars[warp];
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  if (b0 >= a.nb) return;
+  // block metadata for 32 iterations at a time: lane l holds iteration
+  // 32*batch + l; two batches in registers so lookups up to 2 ahead never
+  // wait on a dependent global load
+  long long c_ro = 0, c_o0 = 0, n_ro = 0, n_o0 = 0;
+  int c_m = -1, c_sz = 0, n_m = -1, n_sz = 0;
+  auto load_batch = [&](int j0, long long& ro, long long& o0, int& m, int& sz) {
+    const long long bb = b0 + (long long)(j0 + lane) * G;
+    m = -1;
+    if (bb < a.nb) {
+      ro = a.row_off[bb];
+      m = (int)(a.row_off[bb + 1] - ro);
+      o0 = a.sf_off[bb];
+      sz = (int)(a.sf_off[bb + 1] - o0);
+    }
+  };
+  load_batch(0, c_ro, c_o0, c_m, c_sz);
+  load_batch(32, n_ro, n_o0, n_m, n_sz);
+  int it = 0;
+  auto meta = [&](int j, long long& ro, long long& o0, int& m, int& sz) {
+    const bool cur = (j >> 5) == (it >> 5);
+    const int l = j & 31;
+    ro = __shfl_sync(kFull, cur ? c_ro : n_ro, l);
+    o0 = __shfl_sync(kFull, cur ? c_o0 : n_o0, l);
+    m = __shfl_sync(kFull, cur ? c_m : n_m, l);
+    sz = __shfl_sync(kFull, cur ? c_sz : n_sz, l);
+  };
+  auto issue = [&](long long o0, int sz, int slot) {
+    mbar_arrive_expect_tx(&bar[slot], (unsigned)(8 * sz));
+    tma_bulk_g2s(buf + (size_t)slot * a.cap, a.sf + o0, (unsigned)(8 * sz), &bar[slot]);
+  };
+  auto load_idx = [&](long long ro, int mm, int& i0, int& i1) {
+    i0 = (lane < mm) ? __ldg(a.gsrc + ro + lane) : -1;
+    i1 = (lane + 32 < mm) ? __ldg(a.gsrc + ro + lane + 32) : -1;
+  };
+  long long ro, o0;
+  int m, sz;
+  meta(0, ro, o0, m, sz);
+  if (lane == 0) issue(o0, sz, 0);
+  // right-hand side two blocks ahead: values of iteration it + 1, indices of it + 2
+  int c0, c1, n0, n1;
+  load_idx(ro, m, c0, c1);
+  double v0 = c0 >= 0 ? __ldg(a.r + c0) : 0.0, v1 = c1 >= 0 ? __ldg(a.r + c1) : 0.0;
+  {
+    long long r1, q1;
+    int m1, s1;
+    meta(1, r1, q1, m1, s1);
+    load_idx(r1, m1, n0, n1);
+  }
+  for (;; ++it) {
+    if ((it & 31) == 0 && it > 0) {
+      c_ro = n_ro, c_o0 = n_o0, c_m = n_m, c_sz = n_sz;
+      load_batch(it + 32, n_ro, n_o0, n_m, n_sz);
+    }
+    meta(it, ro, o0, m, sz);
+    if (m < 0) break;
+    {
+      long long r1, q1;
+      int m1, s1;
+      meta(it + 1, r1, q1, m1, s1);
+      if (m1 >= 0 && lane == 0) {
+        fence_proxy_async();  // the buffer's last generic reads precede the async write
+        issue(q1, s1, (it + 1) & 1);
+      }
+    }
+    // next block's values (its indices arrived during the last solve) and
+    // the indices of the block after it
+    const double w0 = n0 >= 0 ? __ldg(a.r + n0) : 0.0, w1 = n1 >= 0 ? __ldg(a.r + n1) : 0.0;
+    {
+      long long r2, q2;
+      int m2, s2;
+      meta(it + 2, r2, q2, m2, s2);
+      load_idx(r2, m2, n0, n1);
+    }
+    xs[lane] = v0;
+    xs[lane + 32] = v1;
+    mbar_wait(&bar[it & 1], (it >> 1) & 1);
+    __syncwarp();
+    small_solve_smem(buf + (size_t)(it & 1) * a.cap, m, xs, lane);
+    if (lane < m) a.out[ro + lane] = xs[lane];
+    if (lane + 32 < m) a.out[ro + lane + 32] = xs[lane + 32];
+    __syncwarp();
+    v0 = w0;
+    v1 = w1;
+  }
+}
+
 // ---------------------------------------------------------------- inverse mode
 // delta_b = inv(A_b) * rhs_b  (rhs gathered in block-local order). inv(A_b)
 // is column-major with even leading dimension ld. Small blocks (m <= 64):

@@ -272,9 +272,12 @@ def test_singular_block_label():
     assert e.value.label == "fs-fluid-up-4"
 
 
-def test_config1_sample_parity():
-    """Config-1 generator (2,048 + 1,024 blocks) against the oracle."""
+@pytest.mark.parametrize("pipe", ["0", "1"])
+def test_config1_sample_parity(pipe, monkeypatch):
+    """Config-1 generator (2,048 + 1,024 blocks) against the oracle, through
+    block_solve_kernel and the opt-in pipelined small-block solve."""
     import torch
+    monkeypatch.setenv("FSIGPU_SOLVE_PIPE", pipe)
     B = fsigpu.DenseBlocks.generate_dominant(2048, 1024, 99)
     rhs = torch.empty(B.total_rows, dtype=torch.float64, device="cuda")
     x = torch.empty_like(rhs)

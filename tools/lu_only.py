@@ -13,3 +13,12 @@ n59 = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 B = fsigpu.DenseBlocks.generate_dominant(n54, n59, 20240901)
 torch.cuda.synchronize()
 print("factored", B.total_rows, "rows")
+if len(sys.argv) > 3 and sys.argv[3] == "solve":
+    rhs = torch.empty(B.total_rows, dtype=torch.float64, device="cuda")
+    x = torch.empty_like(rhs)
+    B.generate_rhs(7, rhs.data_ptr())
+    s = torch.cuda.Stream()
+    for _ in range(3):
+        B.solve_dev(rhs.data_ptr(), x.data_ptr(), s.cuda_stream)
+    torch.cuda.synchronize()
+    print("solved")
