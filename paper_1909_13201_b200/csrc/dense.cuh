@@ -655,11 +655,12 @@ __device__ __forceinline__ void lu_write_outputs(const double* A, int m, int b, 
                                                  const long long* __restrict__ sf_off, double* __restrict__ lu_out,
                                                  bool write_lu, double* __restrict__ sf_out, int* __restrict__ piv_out,
                                                  int* __restrict__ gsrc_out, int* __restrict__ lperm_out,
-                                                 const int* __restrict__ src_pos, int pos_base) {
+                                                 const int* __restrict__ src_pos, int pos_base,
+                                                 bool maps_done = false) {
   const int tid = threadIdx.x;
   const long long ro = row_off[b];
   const long long off = lu_off[b];
-  if (tid == 0) {
+  if (!maps_done && tid == 0) {
     for (int k = 0; k < m; ++k) piv_out[ro + k] = perm[k];
     // compose the sequential swaps (dense.cpp:74-75) into one gather map
     for (int k = 0; k < m; ++k) scratch[k] = (double)k;
@@ -671,7 +672,7 @@ __device__ __forceinline__ void lu_write_outputs(const double* A, int m, int b, 
     }
   }
   __syncthreads();
-  for (int s2 = tid; s2 < m; s2 += NT) {
+  for (int s2 = tid; s2 < m && !maps_done; s2 += NT) {
     const int loc = (int)scratch[s2];
     gsrc_out[ro + s2] = src_pos ? src_pos[ro + loc] + pos_base : (int)(ro + loc);
     lperm_out[ro + s2] = loc;
@@ -876,10 +877,11 @@ struct LuRegStep {
       const int bad = fabs(a[K]) <= 1e-14 * fmax(rmax, 1e-300);
       reinterpret_cast<double2*>(slot)[0] =
           make_double2(__longlong_as_double((long long)vb), __longlong_as_double((long long)(key | (bad << 30))));
-      double* r = slot + 2;
-      r[K] = my_inv;
+      // the row (reciprocal at K) in 16-B pairs; slot + 2 is 16-B aligned
+      double2* r2 = reinterpret_cast<double2*>(slot + 2);
 #pragma unroll
-      for (int j = K + 1; j < MM; ++j) r[j] = a[j];
+      for (int j = K & ~1; j < MM; j += 2)
+        r2[j >> 1] = make_double2(j == K ? my_inv : a[j], j + 1 == K ? my_inv : a[j + 1]);
     }
     if (NW > 1) __syncthreads();
     else __syncwarp();
@@ -905,11 +907,17 @@ struct LuRegStep {
     pos = (pos == p) ? K : (pos == K ? p : pos);
     if (bk >> 30) return true;
     if (pos > K && pos < m) {
-      const double* r = slots + (size_t)ws * kStride + 2;
-      const double l = mul_rn(a[K], r[K]);
+      const double2* r2 = reinterpret_cast<const double2*>(slots + (size_t)ws * kStride + 2);
+      const double2 first = r2[K >> 1];
+      const double l = mul_rn(a[K], (K & 1) ? first.y : first.x);
       a[K] = l;
+      if (!(K & 1) && K + 1 < MM) a[K + 1] = sub_rn(a[K + 1], mul_rn(l, first.y));
 #pragma unroll
-      for (int j = K + 1; j < MM; ++j) a[j] = sub_rn(a[j], mul_rn(l, r[j]));
+      for (int j = (K + 2) & ~1; j < MM; j += 2) {
+        const double2 u = r2[j >> 1];
+        a[j] = sub_rn(a[j], mul_rn(l, u.x));
+        a[j + 1] = sub_rn(a[j + 1], mul_rn(l, u.y));
+      }
     }
     if constexpr (K + 1 < MM) return LuRegStep<K + 1, MM, NW>::run(a, rmax, pos, m, t, slots, perm);
     return false;
@@ -966,15 +974,21 @@ __global__ void __launch_bounds__(MM <= 32 ? 32 : 64)
     if (t == 0) atomicMin(fail, b);
     return;
   }
-  // rows to their logical positions, column-major
+  // rows to their logical positions, column-major. The swaps applied to the
+  // right-hand side (dense.cpp:74-75) move entry t to the final position of
+  // row t, so each thread writes its own gather-map entry.
+  const long long ro = row_off[b];
   if (valid) {
 #pragma unroll
     for (int j = 0; j < MM; ++j)
       if (j < m) A[(size_t)j * m + pos] = a[j];
+    gsrc_out[ro + pos] = src_pos ? src_pos[ro + t] + pos_base : (int)(ro + t);
+    lperm_out[ro + pos] = t;
+    piv_out[ro + t] = perm[t];
   }
   __syncthreads();
   lu_write_outputs<NT, true>(A, m, b, perm, scratch, S, row_off, lu_off, sf_off, lu_out, true, sf_out, piv_out,
-                       gsrc_out, lperm_out, src_pos, pos_base);
+                             gsrc_out, lperm_out, src_pos, pos_base, /*maps_done=*/true);
 }
 
 // Principal block A[dofs, dofs] of a CSR matrix into column-major dense

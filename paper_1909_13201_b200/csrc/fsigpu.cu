@@ -141,7 +141,14 @@ static int choose_lpr(long long rows, long long nnz) {
   while (l < 32 && want > l * 1.41421356) l *= 2;
   return l;
 }
-static int choose_unroll(long long rows) { return rows < 16384 ? 8 : 4; }
+static int choose_unroll(long long rows) {
+  static const int pair = [] {
+    const char* e = std::getenv("FSIGPU_SPMV_PAIR");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (pair && rows >= 16384) return pair;  // 22 or 24 (A/B of the paired kernel)
+  return rows < 16384 ? 8 : 4;
+}
 // Staged-kernel capacity (entries per CTA); 0 keeps csr_kernel.
 static int g_stage_cap = 0;
 static int choose_stage_cap(long long rows, long long nnz) {
@@ -237,7 +244,7 @@ struct Csr {
   double bytes(bool resid) const {
     return 12.0 * nnz + 4.0 * (rows + 1) + 8.0 * cols + 8.0 * rows + (resid ? 8.0 * rows : 0.0);
   }
-  int unroll = 4;  // entries per lane per predicated batch (4 or 8)
+  int unroll = 4;  // entries per lane per predicated batch (4 or 8); 22/24: paired loads, 2/4 pairs
   template <class G, class E>
   void launch(G g, E e, cudaStream_t s) const {
     if (!rows) return;
@@ -248,7 +255,26 @@ struct Csr {
     const long long threads = (long long)rows * lpr;
     const int grid = ceil_div(threads, 256);
 #define FSI_CSR(LP, UU) launch_k(csr_kernel<LP, G, E, UU>, dim3(grid), dim3(256), 0, s, rows, (const int*)ptr.p, (const int*)idx.p, (const double*)val.p, g, e)
-    if (unroll == 8) {
+#define FSI_CSRP(LP, UU) launch_k(csr_pair_kernel<LP, G, E, UU>, dim3(grid), dim3(256), 0, s, rows, (const int*)ptr.p, (const int*)idx.p, (const double*)val.p, g, e)
+    if (unroll == 22 || unroll == 24) {  // paired loads, 2 or 4 pairs per lane per batch
+      if (unroll == 22) {
+        switch (lpr) {
+          case 2: FSI_CSRP(2, 2); break;
+          case 4: FSI_CSRP(4, 2); break;
+          case 8: FSI_CSRP(8, 2); break;
+          case 16: FSI_CSRP(16, 2); break;
+          default: FSI_CSRP(32, 2); break;
+        }
+      } else {
+        switch (lpr) {
+          case 2: FSI_CSRP(2, 4); break;
+          case 4: FSI_CSRP(4, 4); break;
+          case 8: FSI_CSRP(8, 4); break;
+          case 16: FSI_CSRP(16, 4); break;
+          default: FSI_CSRP(32, 4); break;
+        }
+      }
+    } else if (unroll == 8) {
       switch (lpr) {
         case 2: FSI_CSR(2, 8); break;
         case 4: FSI_CSR(4, 8); break;
@@ -266,6 +292,7 @@ struct Csr {
       }
     }
 #undef FSI_CSR
+#undef FSI_CSRP
     FSI_CHECK_LAUNCH();
     counted();
   }
@@ -910,6 +937,15 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
   L.n = d.n;
   require(d.a_ptr && d.a_idx && d.a_val && d.row_mask && d.col_mask, "gmg: null level arrays");
   L.A.create(d.n, d.n, d.a_ptr, d.a_idx, d.a_val, s);
+  // level operators (~65 entries per row) on HBM-bound levels: paired
+  // 16-byte index/value loads, 4 pairs per lane (csr_pair_kernel). Cold
+  // sweeps on config 2 (profiles/r01_tune_cfg2full_pair.txt): L4 5.0 -> 5.3,
+  // L3 3.9 -> 4.2, L2 2.6 -> 2.8 TB/s. The FS operator (long rows) stays on
+  // the scalar kernel, which is faster there.
+  if (d.n >= 65536 && !std::getenv("FSIGPU_SPMV_PAIR")) {
+    L.A.lpr = d.n >= 131072 ? 4 : 8;
+    L.A.unroll = 24;
+  }
   L.rmask.upload(d.row_mask, (size_t)d.n, s);
   L.cmask.upload(d.col_mask, (size_t)d.n, s);
   L.rbuf.alloc(d.n);
@@ -1208,10 +1244,10 @@ struct Gmres {
   void arnoldi_fused(const KBufs& kk) {
     cudaStream_t s = g->s;
     Level& T = g->lv.back();
-    const int gs = ceil_div(n, kFuseRows);
+    const int gs = kk.parts_a;
     {
       ProfScope ps(FSIGPU_K_SPMV, T.A.bytes(false) + 8.0 * n * 3, s);
-      // 128 rows per CTA in one pass: 8 lanes per row (1024 threads)
+      // 128-row tiles, 8 lanes per row (1024 threads), grid-stride over tiles
       launch_k(k_spmv_dots<8>, dim3(gs), dim3(kFuseThreads), 0, s, kk);
     }
     {
@@ -1506,7 +1542,8 @@ int fsigpu_gmg_set_launch(fsigpu_gmg h, int level, int which, int lpr, int unrol
   return guarded([&] {
     require(h != nullptr && level >= 0 && level < (int)h->g.lv.size(), "launch: bad level");
     require(lpr == 2 || lpr == 4 || lpr == 8 || lpr == 16 || lpr == 32, "launch: lpr must be 2..32");
-    require(unroll == 4 || unroll == 8, "launch: unroll must be 4 or 8");
+    require(unroll == 4 || unroll == 8 || ((unroll == 22 || unroll == 24) && which != 2),
+            "launch: unroll must be 4 or 8 (22/24: paired loads, not for AP)");
     Level& L = h->g.lv[level];
     Csr* c = which == 0 ? &L.A : which == 1 ? &L.FS : which == 2 ? &L.AP : which == 3 ? &L.P : &L.R;
     c->lpr = lpr;
@@ -2029,8 +2066,22 @@ int fsigpu_gmres_create(fsigpu_gmg g, const double* frame_scale, int restart, fs
     kb.g = k.gv.p;
     kb.partial = k.partial.p;
     kb.partial2 = k.partial2.p;
-    kb.parts_a = ceil_div(n, kFuseRows);
-    kb.parts_b = std::max(1, std::min(ceil_div(n, kArnThreads), 4 * 148));
+    {
+      // resident CTAs of k_spmv_dots (1024 threads): the tile loop's grid
+      int dev = 0, sms = 0, occ = 0;
+      FSI_CUDA(cudaGetDevice(&dev));
+      FSI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_dots<8>, kFuseThreads, 0));
+      kb.parts_a = std::max(1, std::min(ceil_div(n, kFuseRows), sms * std::max(occ, 1)));
+    }
+    {
+      // (B)/(C) grid: one wave of resident CTAs of (B), at most 4 per SM
+      int dev = 0, sms = 0, occ = 0;
+      FSI_CUDA(cudaGetDevice(&dev));
+      FSI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_dots_norm, kArnThreads, 0));
+      kb.parts_b = std::max(1, std::min(ceil_div(n, kArnThreads), sms * std::min(std::max(occ, 1), 4)));
+    }
     kb.ticket = k.ticket.p;
     kb.st = k.st.p;
     {

@@ -421,6 +421,10 @@ __device__ __forceinline__ double fused_row(const KBufs& k, int row, int lane) {
   return s;
 }
 
+// Grid-stride over 128-row tiles with the grid capped at the resident CTA
+// count (k.parts_a): the partial-dot rows the consumers sum stay <= 2 per
+// SM however large n is (on the 1.25M-dof config-2 fine level a CTA per
+// tile left 9,761 partials that every CTA of (B) summed, ~1 MB each).
 template <int LPR>
 __global__ void __launch_bounds__(kFuseThreads) k_spmv_dots(KBufs k) {
   pdl_trigger();
@@ -428,41 +432,45 @@ __global__ void __launch_bounds__(kFuseThreads) k_spmv_dots(KBufs k) {
   __shared__ double ws[kFuseRows];
   const int j = k.st->j;
   const int nv = j + 1;
-  const int r0 = blockIdx.x * kFuseRows;
   const int t = threadIdx.x;
-  // operands that do not depend on w are loaded before the SpMV so their
-  // latency overlaps it: the V entries of the partial dots (warp v, lanes
-  // over the CTA's 128 rows, 4 each) and z_j for the copy into Z[j]
   const int v = t >> 5, lane = t & 31;
-  double vv[kFuseRows / 32];
-#pragma unroll
-  for (int q = 0; q < kFuseRows / 32; ++q) {
-    const int row = r0 + lane + 32 * q;
-    vv[q] = (v < nv && row < k.n) ? k.V[(size_t)v * k.n + row] : 0.0;
-  }
-  const bool zc = t < kFuseRows && r0 + t < k.n;
-  const double zj = zc ? k.zbuf[r0 + t] : 0.0;
-  constexpr int RPP = kFuseThreads / LPR;  // rows per pass
-  for (int p = 0; p < kFuseRows; p += RPP) {
-    const int rl = p + t / LPR;
-    const int row = r0 + rl;
-    const bool ok = rl < kFuseRows && row < k.n;
-    const bool head = ok && (t & (LPR - 1)) == 0;
-    const double sc = head ? k.scale[row] : 0.0;
-    const double s = fused_row<LPR>(k, ok ? row : -1, t & (LPR - 1));
-    if (head) {
-      const double w = sc * s;
-      k.w[row] = w;
-      ws[rl] = w;
-    }
-  }
-  if (zc) k.Z[(size_t)j * k.n + r0 + t] = zj;
-  if (t < kFuseRows && r0 + t >= k.n) ws[t] = 0.0;
-  __syncthreads();
+  const int ntiles = (k.n + kFuseRows - 1) / kFuseRows;
   double s = 0.0;
-  if (v < nv) {
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int r0 = tile * kFuseRows;
+    // operands that do not depend on w are loaded before the SpMV so their
+    // latency overlaps it: the V entries of the partial dots (warp v, lanes
+    // over the tile's 128 rows, 4 each) and z_j for the copy into Z[j]
+    double vv[kFuseRows / 32];
 #pragma unroll
-    for (int q = 0; q < kFuseRows / 32; ++q) s = fma(vv[q], ws[lane + 32 * q], s);
+    for (int q = 0; q < kFuseRows / 32; ++q) {
+      const int row = r0 + lane + 32 * q;
+      vv[q] = (v < nv && row < k.n) ? k.V[(size_t)v * k.n + row] : 0.0;
+    }
+    const bool zc = t < kFuseRows && r0 + t < k.n;
+    const double zj = zc ? k.zbuf[r0 + t] : 0.0;
+    constexpr int RPP = kFuseThreads / LPR;  // rows per pass
+    for (int p = 0; p < kFuseRows; p += RPP) {
+      const int rl = p + t / LPR;
+      const int row = r0 + rl;
+      const bool ok = rl < kFuseRows && row < k.n;
+      const bool head = ok && (t & (LPR - 1)) == 0;
+      const double sc = head ? k.scale[row] : 0.0;
+      const double sr = fused_row<LPR>(k, ok ? row : -1, t & (LPR - 1));
+      if (head) {
+        const double w = sc * sr;
+        k.w[row] = w;
+        ws[rl] = w;
+      }
+    }
+    if (zc) k.Z[(size_t)j * k.n + r0 + t] = zj;
+    if (t < kFuseRows && r0 + t >= k.n) ws[t] = 0.0;
+    __syncthreads();
+    if (v < nv) {
+#pragma unroll
+      for (int q = 0; q < kFuseRows / 32; ++q) s = fma(vv[q], ws[lane + 32 * q], s);
+    }
+    __syncthreads();  // ws is rewritten by the next tile
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
@@ -576,16 +584,26 @@ __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm(KBufs k) {
       if (v < nv) acc[v] = fma(v0[v], wr, acc[v]);
     n2 = fma(wr, wr, n2);
   }
-  for (int r = r0 + gridDim.x * blockDim.x; r < k.n; r += gridDim.x * blockDim.x) {
-    double wr = k.w[r];
+  {
+    // restrict-qualified views: w's store does not alias V, so the next
+    // row's loads may be issued before this row's store
+    const double* __restrict__ V = k.V;
+    double* __restrict__ W = k.w;
+    const size_t n = (size_t)k.n;
+    for (int r = r0 + gridDim.x * blockDim.x; r < k.n; r += gridDim.x * blockDim.x) {
+      double vr[kMaxRestart];
 #pragma unroll
-    for (int v = 0; v < kMaxRestart; ++v)
-      if (v < nv) wr = fma(-hs[v], k.V[(size_t)v * k.n + r], wr);
-    k.w[r] = wr;
+      for (int v = 0; v < kMaxRestart; ++v) vr[v] = v < nv ? __ldg(V + (size_t)v * n + r) : 0.0;
+      double wr = W[r];
 #pragma unroll
-    for (int v = 0; v < kMaxRestart; ++v)
-      if (v < nv) acc[v] = fma(k.V[(size_t)v * k.n + r], wr, acc[v]);  // L1 hits
-    n2 = fma(wr, wr, n2);
+      for (int v = 0; v < kMaxRestart; ++v)
+        if (v < nv) wr = fma(-hs[v], vr[v], wr);
+      W[r] = wr;
+#pragma unroll
+      for (int v = 0; v < kMaxRestart; ++v)
+        if (v < nv) acc[v] = fma(vr[v], wr, acc[v]);
+      n2 = fma(wr, wr, n2);
+    }
   }
   // partial2[cta][0..nv) = h2 dots, partial2[cta][nv] = ||w||^2
   static_assert(kMaxRestart == 32, "cta_reduce_t32 holds one slot per Krylov vector");

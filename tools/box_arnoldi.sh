@@ -1,0 +1,11 @@
+set -x
+mkdir -p gpurun_out data_cfg2
+timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest.log 2>&1
+timeout 600 python bench.py --no-cpu-baseline --no-microbench > gpurun_out/bench_cfg0.json 2>&1
+oracle/_ref/fsi_ref_harness export cfg2 data_cfg2/cfg2.fsix --no-mult --max-iters 30 --block-stride 997 > gpurun_out/export.log 2>&1
+timeout 600 python -m pytest tests -m gpu -x -q -k cfg2 > gpurun_out/pytest_cfg2.log 2>&1
+timeout 600 python bench.py --config cfg2full --no-cpu-baseline --no-microbench --steps 5 --warmup 3 > gpurun_out/bench_cfg2full.json 2>gpurun_out/bench_cfg2full.err
+export FSI_DATA=data_cfg2/cfg2.fsix
+FSI_MAXIT=30 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file /tmp/launches.csv python tools/profile_solve.py solve > gpurun_out/ncu_list.log 2>&1
+python tools/launch_table.py /tmp/launches.csv > gpurun_out/launch_table_cfg2full.txt 2>&1
+du -sh gpurun_out

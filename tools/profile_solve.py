@@ -40,8 +40,16 @@ def main():
         return
     G = fsigpu.GmgPreconditioner(P.levels)
     if mode.startswith("kernel:"):
+        # only this launch (and its L2 flush) inside the profiler range:
+        # ncu --profile-from-start off -c 2
+        import torch
         _, name, level = mode.split(":")
+        G.time_kernel(name, int(level), reps=1, cold=True)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
         ms, by = G.time_kernel(name, int(level), reps=1, cold=True)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
         print(f"{name}@L{level} {ms * 1000:.1f} us {by / ms / 1e6:.0f} GB/s")
         return
     S = fsigpu.GmresSolver(G, P.frame_scale, restart=30, graphs=(mode == "graph"))
