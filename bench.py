@@ -274,6 +274,9 @@ def run_ours(args, ws, rank, local):
         raise SystemExit(f"{data} missing: run __graft_entry__.build() in the container with /root/reference")
     P = load_case(data, args.config)
     n = P.n
+    # FSI_PAD_MB: device allocation made before the hierarchy (placement
+    # sensitivity studies only; 0 by default)
+    _pad = torch.empty(int(os.environ.get("FSI_PAD_MB", "0")) * (1 << 20), dtype=torch.uint8, device="cuda")
     t0 = time.time()
     G = fsigpu.GmgPreconditioner(P.levels)
     S = fsigpu.GmresSolver(G, P.frame_scale, restart=30)

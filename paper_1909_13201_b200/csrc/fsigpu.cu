@@ -2072,7 +2072,10 @@ int fsigpu_gmres_create(fsigpu_gmg g, const double* frame_scale, int restart, fs
       FSI_CUDA(cudaGetDevice(&dev));
       FSI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
       FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_dots<8>, kFuseThreads, 0));
-      kb.parts_a = std::max(1, std::min(ceil_div(n, kFuseRows), sms * std::max(occ, 1)));
+      // small systems keep one tile per CTA (config 0: 157 tiles); only
+      // grids beyond 8 tiles per SM fold onto the resident CTAs
+      const int tiles = ceil_div(n, kFuseRows);
+      kb.parts_a = tiles <= 8 * sms ? tiles : sms * std::max(occ, 1);
     }
     {
       // (B)/(C) grid: one wave of resident CTAs of (B), at most 4 per SM

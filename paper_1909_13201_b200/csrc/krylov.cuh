@@ -677,15 +677,29 @@ __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
       k.ubuf[r0] = vv / k.scale[r0];
     }
   }
-  for (int r = r0 + nb * blockDim.x; r < k.n; r += nb * blockDim.x) {
-    double wr = k.w[r];
+  {
+    // restrict-qualified views (see k_update_dots_norm): the stores of v_{j+1}
+    // and u do not alias V, w or scale, so row loads run ahead of them
+    const double* __restrict__ V = k.V;
+    const double* __restrict__ W = k.w;
+    const double* __restrict__ S = k.scale;
+    double* __restrict__ VJ = vj;
+    double* __restrict__ UB = k.ubuf;
+    const size_t n = (size_t)k.n;
+    for (int r = r0 + nb * blockDim.x; r < k.n; r += nb * blockDim.x) {
+      double vr[kMaxRestart];
 #pragma unroll
-    for (int v = 0; v < kMaxRestart; ++v)
-      if (v < nv) wr = fma(-hs[v], k.V[(size_t)v * k.n + r], wr);
-    if (!lucky) {
-      const double vv = wr / hn;
-      vj[r] = vv;
-      k.ubuf[r] = vv / k.scale[r];
+      for (int v = 0; v < kMaxRestart; ++v) vr[v] = v < nv ? __ldg(V + (size_t)v * n + r) : 0.0;
+      double wr = W[r];
+      const double sc = S[r];
+#pragma unroll
+      for (int v = 0; v < kMaxRestart; ++v)
+        if (v < nv) wr = fma(-hs[v], vr[v], wr);
+      if (!lucky) {
+        const double vv = wr / hn;
+        VJ[r] = vv;
+        UB[r] = vv / sc;
+      }
     }
   }
 }

@@ -34,7 +34,9 @@ import numpy as np
 from .problem import Csr, Level, level_descs
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfsigpu.so")
+# FSIGPU_LIB: an alternative in-tree build of the same library (A/B timing
+# of two builds, tools/ab_build.sh); default the package's own libfsigpu.so
+LIB_PATH = os.environ.get("FSIGPU_LIB") or os.path.join(_HERE, "libfsigpu.so")
 
 FSIGPU_OK, FSIGPU_ERR_INVALID, FSIGPU_ERR_SINGULAR, FSIGPU_ERR_CUDA = 0, 1, 2, 3
 KERNEL_CLASSES = ["block_solve", "spmv", "transfer", "combine", "coarse", "arnoldi"]
