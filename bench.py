@@ -361,16 +361,34 @@ def run_ours(args, ws, rank, local):
         ms_w, _ = G.time_kernel(name, lvl, reps=50, cold=False)
         kt[f"{name}@L{lvl}"] = {"ms_cold": ms_c, "ms_warm": ms_w, "bytes": by, "per_vcycle": per_cycle,
                                 "GBps_cold": by / ms_c / 1e6, "GBps_warm": by / ms_w / 1e6}
-    dom = max(kt, key=lambda k: kt[k]["ms_cold"] * kt[k]["per_vcycle"])
-    per_launch_bytes = kt[dom]["bytes"]
-    per_launch_ms = kt[dom]["ms_cold"]
+    # ---- in-solve view: one instrumented solve right after the timed
+    # region (same inputs, same L2 flush before it), graphs off, CUDA events
+    # around every launch on the library stream; per kernel class the
+    # algorithmic bytes of its launches / their summed device time
+    flush.fill_(1.0)
+    x.zero_()
+    torch.cuda.synchronize()
+    fsigpu.Profile.reset()
+    fsigpu.Profile.enable(True)
+    S_prof = fsigpu.GmresSolver(G, P.frame_scale, restart=30, graphs=False)
+    S_prof.solve_dev(b.data_ptr(), x.data_ptr(), cfg)
+    torch.cuda.synchronize()
+    fsigpu.Profile.enable(False)
+    cls = {k: v for k, v in fsigpu.Profile.read().items() if v["launches"]}
+    insolve = {k: {"ms_total": v["ms"], "launches": v["launches"], "avg_launch_us": 1000.0 * v["ms"] / v["launches"],
+                   "bytes_per_launch": v["bytes"] / v["launches"], "GBps": v["bytes"] / v["ms"] / 1e6}
+               for k, v in cls.items()}
+    tot_cls = sum(v["ms"] for v in cls.values())
+    dom = max(cls, key=lambda k: cls[k]["ms"])
+    per_launch_bytes = insolve[dom]["bytes_per_launch"]
+    per_launch_ms = insolve[dom]["avg_launch_us"] / 1000.0
     achieved = per_launch_bytes / per_launch_ms / 1e6  # GB/s
-    share = kt[dom]["ms_cold"] * kt[dom]["per_vcycle"] / sum(v["ms_cold"] * v["per_vcycle"] for v in kt.values())
+    share = cls[dom]["ms"] / tot_cls
     traffic = None
     ncu_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(ncu_path):
         with open(ncu_path) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch", {}).get(dom)
+            traffic = json.load(f).get("dram_bytes_per_launch", {}).get(f"{dom}@{args.config}")
 
     out = {
         "metric": METRIC, "value": value, "unit": "V-cycles/s", "n_gpus": ws,
@@ -390,9 +408,14 @@ def run_ours(args, ws, rank, local):
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak,
                      "traffic": traffic, "algorithmic_bytes_per_launch": per_launch_bytes,
-                     "avg_launch_us": per_launch_ms * 1000.0, "share_of_vcycle_kernel_time": share,
-                     "timing": "CUDA events per launch on the library stream, 256 MB L2 flush before each"},
+                     "avg_launch_us": per_launch_ms * 1000.0, "share_of_solve_kernel_time": share,
+                     "timing": "kernel class with the largest device time in an instrumented solve after the timed "
+                               "region (CUDA events around every launch on the library stream, graphs off, L2 "
+                               "flushed before the solve); bytes = algorithmic bytes of its launches (DESIGN 3.6)"},
+        "insolve_kernel_classes": insolve,
         "kernel_roofline": kt,
+        "kernel_roofline_timing": "each V-cycle kernel alone, CUDA events per launch, 256 MB L2 flush before each "
+                                  "(cold) or back to back (warm)",
     }
     # whole V-cycle against the HBM floor: algorithmic bytes of every V-cycle
     # kernel (all levels) / measured peak, against the measured time per

@@ -672,22 +672,23 @@ struct Level {
 static void launch_prolong_resid(const Level& L, const double* ec, const unsigned char* cmask_coarse,
                                  const double* r_pre, double* r, cudaStream_t s) {
   const int grid = ceil_div((long long)L.n * L.AP.lpr, 256);
-#define FSI_PR(LP, UA)                                                                                           \
-  launch_k(prolong_resid_kernel<LP, UA>, dim3(grid), dim3(256), 0, s, L.n, (const int*)L.P.ptr.p,             \
-           (const int*)L.P.idx.p, (const double*)L.P.val.p, (const int*)L.AP.ptr.p, (const int*)L.AP.idx.p, \
-           (const double*)L.AP.val.p, ec, cmask_coarse, (const unsigned char*)L.cmask.p, L.x, r_pre, r)
-#define FSI_PR_L(UA)                 \
-  switch (L.AP.lpr) {                \
-    case 2: FSI_PR(2, UA); break;    \
-    case 4: FSI_PR(4, UA); break;    \
-    case 8: FSI_PR(8, UA); break;    \
-    case 16: FSI_PR(16, UA); break;  \
-    default: FSI_PR(32, UA); break;  \
+#define FSI_PR(K, LP, UA)                                                                                        \
+  launch_k(K<LP, UA>, dim3(grid), dim3(256), 0, s, L.n, (const int*)L.P.ptr.p, (const int*)L.P.idx.p,         \
+           (const double*)L.P.val.p, (const int*)L.AP.ptr.p, (const int*)L.AP.idx.p, (const double*)L.AP.val.p, \
+           ec, cmask_coarse, (const unsigned char*)L.cmask.p, L.x, r_pre, r)
+#define FSI_PR_L(K, UA)                 \
+  switch (L.AP.lpr) {                   \
+    case 2: FSI_PR(K, 2, UA); break;    \
+    case 4: FSI_PR(K, 4, UA); break;    \
+    case 8: FSI_PR(K, 8, UA); break;    \
+    case 16: FSI_PR(K, 16, UA); break;  \
+    default: FSI_PR(K, 32, UA); break;  \
   }
-  if (L.AP.unroll == 4) {
-    FSI_PR_L(4)
-  } else {
-    FSI_PR_L(8)
+  switch (L.AP.unroll) {
+    case 22: FSI_PR_L(prolong_resid_pair_kernel, 2) break;  // paired A*P loads, 2 / 4 pairs
+    case 24: FSI_PR_L(prolong_resid_pair_kernel, 4) break;
+    case 4: FSI_PR_L(prolong_resid_kernel, 4) break;
+    default: FSI_PR_L(prolong_resid_kernel, 8) break;
   }
 #undef FSI_PR_L
 #undef FSI_PR
@@ -1002,6 +1003,12 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
     if (d.n < 65536) {
       L.AP.lpr = std::max(2, L.AP.lpr / 2);
       L.AP.unroll = 8;
+    } else if (d.n >= 131072 && !std::getenv("FSIGPU_SPMV_PAIR")) {
+      // HBM-bound levels: the A*P half as 16-byte pairs (cold sweeps on the
+      // config-2 hierarchy, profiles/r01_tune_cfg2full_ap.txt: L4 227 -> 190
+      // us at 2 lanes x 4 pairs, L3 67 -> 60 us at 4 lanes x 2 pairs)
+      L.AP.lpr = d.n >= 1048576 ? 2 : 4;
+      L.AP.unroll = d.n >= 1048576 ? 24 : 22;
     } else {
       L.AP.unroll = 4;
     }
@@ -1247,8 +1254,12 @@ struct Gmres {
     const int gs = kk.parts_a;
     {
       ProfScope ps(FSIGPU_K_SPMV, T.A.bytes(false) + 8.0 * n * 3, s);
-      // 128-row tiles, 8 lanes per row (1024 threads), grid-stride over tiles
-      launch_k(k_spmv_dots<8>, dim3(gs), dim3(kFuseThreads), 0, s, kk);
+      // 128-row tiles, 8 lanes per row (1024 threads), grid-stride over
+      // tiles; large systems: 32-row tiles on 256-thread CTAs
+      if (kk.fuse_small)
+        launch_k(k_spmv_dots_s, dim3(gs), dim3(kFuseThreadsS), 0, s, kk);
+      else
+        launch_k(k_spmv_dots<8>, dim3(gs), dim3(kFuseThreads), 0, s, kk);
     }
     {
       // (B) on parts_b CTAs; (C) on parts_b row CTAs + 1 Givens CTA
@@ -1542,8 +1553,8 @@ int fsigpu_gmg_set_launch(fsigpu_gmg h, int level, int which, int lpr, int unrol
   return guarded([&] {
     require(h != nullptr && level >= 0 && level < (int)h->g.lv.size(), "launch: bad level");
     require(lpr == 2 || lpr == 4 || lpr == 8 || lpr == 16 || lpr == 32, "launch: lpr must be 2..32");
-    require(unroll == 4 || unroll == 8 || ((unroll == 22 || unroll == 24) && which != 2),
-            "launch: unroll must be 4 or 8 (22/24: paired loads, not for AP)");
+    require(unroll == 4 || unroll == 8 || unroll == 22 || unroll == 24,
+            "launch: unroll must be 4 or 8 (22/24: paired loads, 2/4 pairs)");
     Level& L = h->g.lv[level];
     Csr* c = which == 0 ? &L.A : which == 1 ? &L.FS : which == 2 ? &L.AP : which == 3 ? &L.P : &L.R;
     c->lpr = lpr;
@@ -2072,10 +2083,16 @@ int fsigpu_gmres_create(fsigpu_gmg g, const double* frame_scale, int restart, fs
       FSI_CUDA(cudaGetDevice(&dev));
       FSI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
       FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_dots<8>, kFuseThreads, 0));
-      // small systems keep one tile per CTA (config 0: 157 tiles); only
-      // grids beyond 8 tiles per SM fold onto the resident CTAs
+      // small systems keep one 128-row tile per CTA (config 0: 157 tiles);
+      // large ones run k_spmv_dots_s on up to 4 resident CTAs per SM
       const int tiles = ceil_div(n, kFuseRows);
-      kb.parts_a = tiles <= 8 * sms ? tiles : sms * std::max(occ, 1);
+      kb.fuse_small = tiles > 8 * sms && !std::getenv("FSIGPU_FUSE_BIG");
+      if (kb.fuse_small) {
+        FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_dots_s, kFuseThreadsS, 0));
+        kb.parts_a = sms * std::min(std::max(occ, 1), 4);
+      } else {
+        kb.parts_a = tiles <= 8 * sms ? tiles : sms * std::max(occ, 1);
+      }
     }
     {
       // (B)/(C) grid: one wave of resident CTAs of (B), at most 4 per SM

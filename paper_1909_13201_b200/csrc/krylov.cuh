@@ -64,6 +64,7 @@ struct KBufs {
   double* partial;      // grid x (kMaxRestart+1)
   double* partial2;     // second partial buffer of the fused Arnoldi step
   int parts_a;          // CTAs of k_spmv_dots (rows of partial it writes)
+  int fuse_small;       // (A) runs as k_spmv_dots_s (large n)
   int parts_b;          // CTAs of k_update_dots_norm (rows of partial2)
   unsigned int* ticket;
   KState* st;
@@ -545,6 +546,68 @@ __device__ __forceinline__ void sum_partials(const double* __restrict__ part, in
     dst[w] = z;
   }
   __syncthreads();
+}
+
+// Large-n variant of (A): 256-thread CTAs on 32-row tiles (8 lanes per
+// row, one pass), several CTAs per SM, grid-stride over tiles with the grid
+// at the resident CTA count. With one 1024-thread CTA per SM (k_spmv_dots)
+// every SM worked on a single tile at a time, so each tile's dependent
+// pointer -> index -> gather rounds were exposed (config-2 fine level: 272
+// us for 1.23 GB). Warp w owns the dots of vectors w, w+8, w+16, w+24.
+constexpr int kFuseThreadsS = 256;
+constexpr int kFuseRowsS = 32;
+__global__ void __launch_bounds__(kFuseThreadsS) k_spmv_dots_s(KBufs k) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ double ws[kFuseRowsS];
+  const int j = k.st->j;
+  const int nv = j + 1;
+  const int t = threadIdx.x;
+  const int warp = t >> 5, lane = t & 31;
+  constexpr int LPR = 8;
+  constexpr int NQ = kMaxRestart / (kFuseThreadsS / 32);  // vectors per warp
+  const int ntiles = (k.n + kFuseRowsS - 1) / kFuseRowsS;
+  double s[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) s[q] = 0.0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int r0 = tile * kFuseRowsS;
+    const int rowv = r0 + lane;
+    double vv[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int v = warp + 8 * q;
+      vv[q] = (v < nv && rowv < k.n) ? k.V[(size_t)v * k.n + rowv] : 0.0;
+    }
+    const bool zc = t < kFuseRowsS && r0 + t < k.n;
+    const double zj = zc ? k.zbuf[r0 + t] : 0.0;
+    const int rl = t / LPR;
+    const int row = r0 + rl;
+    const bool ok = row < k.n;
+    const bool head = ok && (t & (LPR - 1)) == 0;
+    const double sc = head ? k.scale[row] : 0.0;
+    const double sr = fused_row<LPR>(k, ok ? row : -1, t & (LPR - 1));
+    if (head) {
+      const double w = sc * sr;
+      k.w[row] = w;
+      ws[rl] = w;
+    }
+    if (zc) k.Z[(size_t)j * k.n + r0 + t] = zj;
+    if (t < kFuseRowsS && r0 + t >= k.n) ws[t] = 0.0;
+    __syncthreads();
+    const double wl = ws[lane];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) s[q] = fma(vv[q], wl, s[q]);
+    __syncthreads();  // ws is rewritten by the next tile
+  }
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    double x = s[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+    const int v = warp + 8 * q;
+    if (lane == 0 && v < nv) k.partial[(size_t)blockIdx.x * (kMaxRestart + 1) + v] = x;
+  }
 }
 
 // (B) h1 = sum of (A)'s partials (every CTA); w -= V h1 ; partial2 <- V^T w

@@ -549,6 +549,113 @@ __global__ void __launch_bounds__(256) prolong_resid_kernel(int rows, const int*
   }
 }
 
+// prolong_resid_kernel with the A*P half streamed as 16-byte pairs (int2
+// columns, double2 values; see csr_pair_kernel), UA pairs per lane per
+// batch. The P half and the first A*P batch are still fetched together.
+template <int LPR, int UA>
+__global__ void __launch_bounds__(256) prolong_resid_pair_kernel(
+    int rows, const int* __restrict__ pp, const int* __restrict__ pi, const double* __restrict__ pv,
+    const int* __restrict__ ap, const int* __restrict__ ai, const double* __restrict__ av, const double* ec,
+    const unsigned char* __restrict__ cmask_coarse, const unsigned char* __restrict__ cmask, double* x,
+    const double* r_pre, double* r) {
+  constexpr int UP = (9 + LPR - 1) / LPR;
+  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = (int)(gt / LPR);
+  const int lane = threadIdx.x & (LPR - 1);
+  const bool ok = row < rows;
+  pdl_trigger();
+  pdl_wait();
+  int p0 = 0, p1 = 0, a0 = 0, a1 = 0;
+  if (ok) {
+    p0 = __ldg(pp + row);
+    p1 = __ldg(pp + row + 1);
+    a0 = __ldg(ap + row);
+    a1 = __ldg(ap + row + 1);
+  }
+  unsigned char cm = 1;
+  double xo = 0.0, rp = 0.0;
+  if (ok && lane == 0) {
+    cm = cmask[row];
+    xo = x[row];
+    rp = r_pre[row];
+  }
+  auto gather = [&](int c) -> double {
+    return c >= 0 ? ((cmask_coarse && __ldg(cmask_coarse + c)) ? 0.0 : __ldg(ec + c)) : 0.0;
+  };
+  auto load_pairs = [&](int kb, int2 (&c)[UA], double2 (&v)[UA]) {
+#pragma unroll
+    for (int u = 0; u < UA; ++u) {
+      const int k = kb + 2 * u * LPR;
+      if (k < a1) {
+        c[u] = __ldg(reinterpret_cast<const int2*>(ai + k));
+        v[u] = __ldg(reinterpret_cast<const double2*>(av + k));
+        if (k < a0) c[u].x = -1;
+        if (k + 1 >= a1) c[u].y = -1;
+      } else {
+        c[u] = make_int2(-1, -1);
+        v[u] = make_double2(0.0, 0.0);
+      }
+    }
+  };
+  double s1 = 0.0, s2 = 0.0;
+  int kp = p0 + lane, ka = (a0 & ~1) + 2 * lane;
+  {
+    int cp[UP];
+    double vp[UP];
+#pragma unroll
+    for (int u = 0; u < UP; ++u) {
+      const int k = kp + u * LPR;
+      const bool in = k < p1;
+      cp[u] = in ? __ldg(pi + k) : -1;
+      vp[u] = in ? __ldg(pv + k) : 0.0;
+    }
+    int2 c[UA];
+    double2 v[UA];
+    load_pairs(ka, c, v);
+    double xp[UP], x0[UA], x1[UA];
+#pragma unroll
+    for (int u = 0; u < UP; ++u) xp[u] = gather(cp[u]);
+#pragma unroll
+    for (int u = 0; u < UA; ++u) {
+      x0[u] = gather(c[u].x);
+      x1[u] = gather(c[u].y);
+    }
+#pragma unroll
+    for (int u = 0; u < UP; ++u) s1 = fma(vp[u], xp[u], s1);
+#pragma unroll
+    for (int u = 0; u < UA; ++u) {
+      s2 = fma(v[u].x, x0[u], s2);
+      s2 = fma(v[u].y, x1[u], s2);
+    }
+  }
+  for (kp += UP * LPR; kp < p1; kp += LPR) s1 = fma(__ldg(pv + kp), gather(__ldg(pi + kp)), s1);
+  for (ka += 2 * UA * LPR; ka < a1; ka += 2 * UA * LPR) {
+    int2 c[UA];
+    double2 v[UA];
+    load_pairs(ka, c, v);
+    double x0[UA], x1[UA];
+#pragma unroll
+    for (int u = 0; u < UA; ++u) {
+      x0[u] = gather(c[u].x);
+      x1[u] = gather(c[u].y);
+    }
+#pragma unroll
+    for (int u = 0; u < UA; ++u) {
+      s2 = fma(v[u].x, x0[u], s2);
+      s2 = fma(v[u].y, x1[u], s2);
+    }
+  }
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) {
+    s1 += __shfl_xor_sync(kFull, s1, o, LPR);
+    s2 += __shfl_xor_sync(kFull, s2, o, LPR);
+  }
+  if (ok && lane == 0) {
+    if (!cm) x[row] = xo + s1;
+    r[row] = rp - s2;
+  }
+}
+
 // ---- assembled FS operator (setup): COO entries of
 //   sum_b R_b^T inv(A_b) R_b / cover  (additive Schwarz, precond.cpp:44-57)
 // one CTA per block; key = (row << 32) | col

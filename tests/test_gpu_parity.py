@@ -320,6 +320,26 @@ def test_execution_paths_agree(cfg0):
     assert rel(a.x, p1.x) <= 1e-8
 
 
+@pytest.mark.parametrize("unroll", [22, 24])
+def test_paired_load_kernels(cfg0, unroll):
+    """The paired-load SpMV and prolongation kernels (16-byte index/value
+    pairs, any row alignment) on every level operator and transfer: V-cycle
+    and FS apply against the oracle, GMRES iterations against the reference."""
+    G = fsigpu.GmgPreconditioner(cfg0.levels)
+    OG = O.OracleGmg(cfg0.levels)
+    for lev in range(1, len(cfg0.levels)):
+        for which in ["A", "FS", "AP", "R"]:
+            for lpr in [2, 8]:
+                G.set_launch(lev, which, lpr, unroll)
+                r = np.random.default_rng(lev).uniform(-1, 1, cfg0.levels[lev].n)
+                assert rel(G.fs_apply(lev, r), OG.fs_apply(lev, r)) <= 1e-12
+    g = cfg0.golden
+    assert rel(G.apply(g["golden/vcycle_r"]), g["golden/vcycle_z_add"]) <= 1e-9
+    cfg = fsigpu.KrylovConfig(restart=30, max_iters=2000, rel_tol=1e-10, abs_tol=1e-300)
+    res = fsigpu.gmres(G, cfg0.frame_scale, cfg0.b, cfg)
+    assert res.converged and abs(res.iterations - int(g["gmres_add/iterations"][0])) <= 1
+
+
 def test_gmres_restart_and_x0(cfg0):
     """Restart length 10 and a nonzero initial guess still converge to the
     same solution (krylov.cpp:29-34,116-122)."""

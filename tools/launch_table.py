@@ -29,7 +29,7 @@ def main(path):
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
             d["bytes"] = d.get("bytes", 0.0) + v * scale
     seq = list(launches.values())
-    first = next((i for i, d in enumerate(seq) if "k_spmv_dots" in d["name"]), 0)
+    first = next((i for i, d in enumerate(seq) if "k_spmv_dots" in d["name"] or "k_cycle_start" in d["name"]), 0)
     agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
     for d in seq[first:]:
         base = re.sub(r"\(.*", "", d["name"])
