@@ -272,7 +272,10 @@ __device__ void solve_block(const SolveArgs& a, int b, double* xs, double* buf, 
 // block; type 2 = (block first, columns pad..pad+count-1) of a small block,
 // one column per warp; type 3 = (block first, column pad) of a large block.
 // Types 2/3 compute inverse columns (setup of the explicit-inverse mode).
-__global__ void __launch_bounds__(kSolveThreads) block_solve_kernel(SolveArgs a) {
+// Three CTAs per SM (<= 80 registers): 24 warps keep more blocks' phases in
+// flight; config-1 solve 2.51 -> 2.33 ms (4.07 -> 4.37 TB/s). Four CTAs
+// (64 registers) spill and lose it again.
+__global__ void __launch_bounds__(kSolveThreads, 3) block_solve_kernel(SolveArgs a) {
   extern __shared__ __align__(16) double dsm[];
   __shared__ double xs[kLargeMax];
   __shared__ unsigned long long bars[2];
