@@ -337,6 +337,21 @@ static bool lu_register_path() {
   return !(e && e[0] == '1');
 }
 
+// FSIGPU_FORCE_BIG=1: take the large-system kernel variants at any size
+// (k_spmv_dots_s, the cp.async Arnoldi stages, paired SpMV / A*P loads), so
+// the parity tests cover them on the small committed fixtures.
+static bool force_big() {
+  const char* e = std::getenv("FSIGPU_FORCE_BIG");
+  return e && e[0] == '1';
+}
+
+// Large-system Arnoldi (B)/(C) through cp.async row stages (default);
+// FSIGPU_ARNOLDI_CP=0 selects the register-row variants for A/B.
+static bool arnoldi_cp() {
+  const char* e = std::getenv("FSIGPU_ARNOLDI_CP");
+  return !(e && e[0] == '0');
+}
+
 struct Blocks {
   int mode = kModeLU;
   long long nb = 0;
@@ -943,7 +958,7 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
   // sweeps on config 2 (profiles/r01_tune_cfg2full_pair.txt): L4 5.0 -> 5.3,
   // L3 3.9 -> 4.2, L2 2.6 -> 2.8 TB/s. The FS operator (long rows) stays on
   // the scalar kernel, which is faster there.
-  if (d.n >= 65536 && !std::getenv("FSIGPU_SPMV_PAIR")) {
+  if ((d.n >= 65536 || force_big()) && !std::getenv("FSIGPU_SPMV_PAIR")) {
     L.A.lpr = d.n >= 131072 ? 4 : 8;
     L.A.unroll = 24;
   }
@@ -1000,10 +1015,11 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
     // its P half already adds 2 loads per lane to each batch: on large
     // (HBM-bound) levels batches of 4 AP entries; on small (L2-resident)
     // ones half the lanes with batches of 8 (warm sweeps, tools/tune_spmv.py)
-    if (d.n < 65536) {
+    const bool pair_ap = (d.n >= 131072 || (force_big() && d.n >= 4096)) && !std::getenv("FSIGPU_SPMV_PAIR");
+    if (d.n < 65536 && !pair_ap) {
       L.AP.lpr = std::max(2, L.AP.lpr / 2);
       L.AP.unroll = 8;
-    } else if (d.n >= 131072 && !std::getenv("FSIGPU_SPMV_PAIR")) {
+    } else if (pair_ap) {
       // HBM-bound levels: the A*P half as 16-byte pairs (cold sweeps on the
       // config-2 hierarchy, profiles/r01_tune_cfg2full_ap.txt: L4 227 -> 190
       // us at 2 lanes x 4 pairs, L3 67 -> 60 us at 4 lanes x 2 pairs)
@@ -1258,14 +1274,24 @@ struct Gmres {
       // tiles; large systems: 32-row tiles on 256-thread CTAs
       if (kk.fuse_small)
         launch_k(k_spmv_dots_s, dim3(gs), dim3(kFuseThreadsS), 0, s, kk);
+      else if (gs == ceil_div(n, kFuseRows))
+        launch_k(k_spmv_dots_1<8>, dim3(gs), dim3(kFuseThreads), 0, s, kk);
       else
         launch_k(k_spmv_dots<8>, dim3(gs), dim3(kFuseThreads), 0, s, kk);
     }
     {
       // (B) on parts_b CTAs; (C) on parts_b row CTAs + 1 Givens CTA
       ProfScope ps(FSIGPU_K_ARNOLDI, 8.0 * n * 4, s);
-      launch_k(k_update_dots_norm, dim3(kk.parts_b), dim3(kArnThreads), 0, s, kk);
-      launch_k(k_update_normalize, dim3(kk.parts_b + 1), dim3(kArnThreads), 0, s, kk);
+      if (kk.fuse_small && arnoldi_cp()) {  // large systems: rows streamed through cp.async stages
+        launch_k(k_update_dots_norm_cp, dim3(kk.parts_b), dim3(kArnThreads), kStageSmem, s, kk);
+        launch_k(k_update_normalize<false>, dim3(kk.parts_c + 1), dim3(kArnThreads), 0, s, kk);
+      } else if (kk.fuse_small) {  // large systems: no first-row prefetch, (C) on its own grid
+        launch_k(k_update_dots_norm<false>, dim3(kk.parts_b), dim3(kArnThreads), 0, s, kk);
+        launch_k(k_update_normalize<false>, dim3(kk.parts_c + 1), dim3(kArnThreads), 0, s, kk);
+      } else {
+        launch_k(k_update_dots_norm<true>, dim3(kk.parts_b), dim3(kArnThreads), 0, s, kk);
+        launch_k(k_update_normalize<true>, dim3(kk.parts_b + 1), dim3(kArnThreads), 0, s, kk);
+      }
     }
     FSI_CHECK_LAUNCH();
     counted(3);
@@ -2055,7 +2081,7 @@ int fsigpu_gmres_create(fsigpu_gmg g, const double* frame_scale, int restart, fs
     k.gv.alloc(restart + 1);
     k.grid = std::max(1, std::min(ceil_div(n, kKThreads), 2 * 148));
     k.partial.alloc((size_t)std::max(std::max(k.grid, ceil_div(n, kFuseRows)), 4 * 148) * (kMaxRestart + 1));
-    k.partial2.alloc((size_t)4 * 148 * (kMaxRestart + 1));
+    k.partial2.alloc((size_t)16 * 148 * (kMaxRestart + 1));  // (B) grid <= 16 CTAs per SM
     k.ticket.alloc(1);
     k.ticket.zero(s);
     k.st.alloc(1);
@@ -2086,7 +2112,7 @@ int fsigpu_gmres_create(fsigpu_gmg g, const double* frame_scale, int restart, fs
       // small systems keep one 128-row tile per CTA (config 0: 157 tiles);
       // large ones run k_spmv_dots_s on up to 4 resident CTAs per SM
       const int tiles = ceil_div(n, kFuseRows);
-      kb.fuse_small = tiles > 8 * sms && !std::getenv("FSIGPU_FUSE_BIG");
+      kb.fuse_small = (tiles > 8 * sms || force_big()) && !std::getenv("FSIGPU_FUSE_BIG");
       if (kb.fuse_small) {
         FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_dots_s, kFuseThreadsS, 0));
         kb.parts_a = sms * std::min(std::max(occ, 1), 4);
@@ -2099,8 +2125,31 @@ int fsigpu_gmres_create(fsigpu_gmg g, const double* frame_scale, int restart, fs
       int dev = 0, sms = 0, occ = 0;
       FSI_CUDA(cudaGetDevice(&dev));
       FSI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_dots_norm, kArnThreads, 0));
-      kb.parts_b = std::max(1, std::min(ceil_div(n, kArnThreads), sms * std::min(std::max(occ, 1), 4)));
+      const bool big = (ceil_div(n, kFuseRows) > 8 * sms || force_big()) && !std::getenv("FSIGPU_FUSE_BIG");
+      if (big && arnoldi_cp()) {
+        FSI_CUDA(cudaFuncSetAttribute(k_update_dots_norm_cp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kStageSmem));
+        FSI_CUDA(cudaFuncSetAttribute(k_update_normalize_cp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kStageSmem));
+        FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_dots_norm_cp, kArnThreads, kStageSmem));
+        kb.parts_b = std::max(1, std::min(ceil_div(n, kArnThreads), sms * std::min(std::max(occ, 1), 16)));
+        // (C) stays on registers: at 80 registers it runs 6 CTAs per SM
+        // (50.6 us on the config-2 fine level) against 3 for the 70 KB
+        // staged variant (61.5 us); k_update_normalize_cp is kept for A/B
+        int occ_c = 0;
+        FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, k_update_normalize<false>, kArnThreads, 0));
+        kb.parts_c = std::max(1, std::min(ceil_div(n, kArnThreads), sms * std::max(occ_c, 1) - 1));
+      } else if (big) {
+        FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_dots_norm<false>, kArnThreads, 0));
+        kb.parts_b = std::max(1, std::min(ceil_div(n, kArnThreads), sms * std::min(std::max(occ, 1), 16)));
+        int occ_c = 0;
+        FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, k_update_normalize<false>, kArnThreads, 0));
+        kb.parts_c = std::max(1, std::min(ceil_div(n, kArnThreads), sms * std::max(occ_c, 1) - 1));
+      } else {
+        FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_dots_norm<true>, kArnThreads, 0));
+        kb.parts_b = std::max(1, std::min(ceil_div(n, kArnThreads), sms * std::min(std::max(occ, 1), 4)));
+        kb.parts_c = kb.parts_b;
+      }
     }
     kb.ticket = k.ticket.p;
     kb.st = k.st.p;

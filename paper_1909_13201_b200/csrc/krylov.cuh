@@ -66,6 +66,7 @@ struct KBufs {
   int parts_a;          // CTAs of k_spmv_dots (rows of partial it writes)
   int fuse_small;       // (A) runs as k_spmv_dots_s (large n)
   int parts_b;          // CTAs of k_update_dots_norm (rows of partial2)
+  int parts_c;          // row CTAs of k_update_normalize (+1 Givens CTA)
   unsigned int* ticket;
   KState* st;
   // fused Arnoldi (3 kernels per step)
@@ -422,6 +423,56 @@ __device__ __forceinline__ double fused_row(const KBufs& k, int row, int lane) {
   return s;
 }
 
+// Small systems: one 128-row tile per CTA (no tile loop), as first tuned
+// on config 0.
+template <int LPR>
+__global__ void __launch_bounds__(kFuseThreads) k_spmv_dots_1(KBufs k) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ double ws[kFuseRows];
+  const int j = k.st->j;
+  const int nv = j + 1;
+  const int r0 = blockIdx.x * kFuseRows;
+  const int t = threadIdx.x;
+  // operands that do not depend on w are loaded before the SpMV so their
+  // latency overlaps it: the V entries of the partial dots (warp v, lanes
+  // over the CTA's 128 rows, 4 each) and z_j for the copy into Z[j]
+  const int v = t >> 5, lane = t & 31;
+  double vv[kFuseRows / 32];
+#pragma unroll
+  for (int q = 0; q < kFuseRows / 32; ++q) {
+    const int row = r0 + lane + 32 * q;
+    vv[q] = (v < nv && row < k.n) ? k.V[(size_t)v * k.n + row] : 0.0;
+  }
+  const bool zc = t < kFuseRows && r0 + t < k.n;
+  const double zj = zc ? k.zbuf[r0 + t] : 0.0;
+  constexpr int RPP = kFuseThreads / LPR;  // rows per pass
+  for (int p = 0; p < kFuseRows; p += RPP) {
+    const int rl = p + t / LPR;
+    const int row = r0 + rl;
+    const bool ok = rl < kFuseRows && row < k.n;
+    const bool head = ok && (t & (LPR - 1)) == 0;
+    const double sc = head ? k.scale[row] : 0.0;
+    const double s = fused_row<LPR>(k, ok ? row : -1, t & (LPR - 1));
+    if (head) {
+      const double w = sc * s;
+      k.w[row] = w;
+      ws[rl] = w;
+    }
+  }
+  if (zc) k.Z[(size_t)j * k.n + r0 + t] = zj;
+  if (t < kFuseRows && r0 + t >= k.n) ws[t] = 0.0;
+  __syncthreads();
+  double s = 0.0;
+  if (v < nv) {
+#pragma unroll
+    for (int q = 0; q < kFuseRows / 32; ++q) s = fma(vv[q], ws[lane + 32 * q], s);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  if (lane == 0 && v < nv) k.partial[(size_t)blockIdx.x * (kMaxRestart + 1) + v] = s;
+}
+
 // Grid-stride over 128-row tiles with the grid capped at the resident CTA
 // count (k.parts_a): the partial-dot rows the consumers sum stay <= 2 per
 // SM however large n is (on the 1.25M-dof config-2 fine level a CTA per
@@ -612,6 +663,10 @@ __global__ void __launch_bounds__(kFuseThreadsS) k_spmv_dots_s(KBufs k) {
 
 // (B) h1 = sum of (A)'s partials (every CTA); w -= V h1 ; partial2 <- V^T w
 //     and ||w||^2 (h2 and the norm are finished by the CTAs of (C)).
+// PF: the first row's operands are loaded before the h1 reduction (small
+// systems, one row per thread); large systems skip it: the row loop alone
+// streams every row, and the 64 freed registers double the resident warps.
+template <bool PF>
 __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm(KBufs k) {
   pdl_trigger();
   pdl_wait();
@@ -623,10 +678,12 @@ __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm(KBufs k) {
   // this thread's first row is loaded before the h1 reduction (independent
   // of it), so the two latencies overlap
   const int r0 = blockIdx.x * blockDim.x + threadIdx.x;
-  double w0 = 0.0, v0[kMaxRestart];
+  double w0 = 0.0, v0[PF ? kMaxRestart : 1];
+  if constexpr (PF) {
 #pragma unroll
-  for (int v = 0; v < kMaxRestart; ++v) v0[v] = (r0 < k.n && v < nv) ? k.V[(size_t)v * k.n + r0] : 0.0;
-  if (r0 < k.n) w0 = k.w[r0];
+    for (int v = 0; v < kMaxRestart; ++v) v0[v] = (r0 < k.n && v < nv) ? k.V[(size_t)v * k.n + r0] : 0.0;
+    if (r0 < k.n) w0 = k.w[r0];
+  }
   sum_partials<kArnThreads>(k.partial, k.parts_a, nv, hs, red);
   if (blockIdx.x == 0) {
     if (threadIdx.x < nv) k.st->h1[threadIdx.x] = hs[threadIdx.x];
@@ -636,24 +693,36 @@ __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm(KBufs k) {
 #pragma unroll
   for (int v = 0; v < kMaxRestart; ++v) acc[v] = 0.0;
   double n2 = 0.0;
-  if (r0 < k.n) {
+  if (PF && r0 < k.n) {
     double wr = w0;
 #pragma unroll
     for (int v = 0; v < kMaxRestart; ++v)
-      if (v < nv) wr = fma(-hs[v], v0[v], wr);
+      if (v < nv) wr = fma(-hs[v], v0[PF ? v : 0], wr);
     k.w[r0] = wr;
 #pragma unroll
     for (int v = 0; v < kMaxRestart; ++v)
-      if (v < nv) acc[v] = fma(v0[v], wr, acc[v]);
+      if (v < nv) acc[v] = fma(v0[PF ? v : 0], wr, acc[v]);
     n2 = fma(wr, wr, n2);
   }
-  {
+  if constexpr (PF) {
+    for (int r = r0 + gridDim.x * blockDim.x; r < k.n; r += gridDim.x * blockDim.x) {
+      double wr = k.w[r];
+  #pragma unroll
+      for (int v = 0; v < kMaxRestart; ++v)
+        if (v < nv) wr = fma(-hs[v], k.V[(size_t)v * k.n + r], wr);
+      k.w[r] = wr;
+  #pragma unroll
+      for (int v = 0; v < kMaxRestart; ++v)
+        if (v < nv) acc[v] = fma(k.V[(size_t)v * k.n + r], wr, acc[v]);  // L1 hits
+      n2 = fma(wr, wr, n2);
+    }
+  } else {
     // restrict-qualified views: w's store does not alias V, so the next
     // row's loads may be issued before this row's store
     const double* __restrict__ V = k.V;
     double* __restrict__ W = k.w;
     const size_t n = (size_t)k.n;
-    for (int r = r0 + gridDim.x * blockDim.x; r < k.n; r += gridDim.x * blockDim.x) {
+    for (int r = PF ? r0 + gridDim.x * blockDim.x : r0; r < k.n; r += gridDim.x * blockDim.x) {
       double vr[kMaxRestart];
 #pragma unroll
       for (int v = 0; v < kMaxRestart; ++v) vr[v] = v < nv ? __ldg(V + (size_t)v * n + r) : 0.0;
@@ -673,12 +742,75 @@ __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm(KBufs k) {
   cta_reduce_t32<kArnThreads>(acc, n2, nv, sm, k.partial2 + (size_t)blockIdx.x * (kMaxRestart + 1));
 }
 
+// Large-n variants of (B) and (C): each thread streams its rows' operands
+// (the nv basis entries, w, and for (C) the frame scale) into its own
+// shared-memory slots with 8-byte cp.async, one row ahead (two stages), so
+// the next row's loads are in flight while the current row's dependent FMA
+// chain runs, without holding them in registers. A thread reads back only
+// what it copied itself, so cp.async.wait_group alone orders the stages.
+// Slots: stage s, value q, thread t at stg[(s * kStageVals + q) * kArnThreads + t].
+constexpr int kStageVals = kMaxRestart + 2;
+constexpr size_t kStageSmem = 2 * kStageVals * kArnThreads * sizeof(double);
+
+__device__ __forceinline__ void stage_row(const KBufs& k, double* stg, int st, int r, int nv, bool with_scale) {
+  const int t = threadIdx.x;
+  if (r < k.n) {
+    double* base = stg + (size_t)st * kStageVals * kArnThreads + t;
+    for (int v = 0; v < nv; ++v) cp_async8(base + (size_t)v * kArnThreads, k.V + (size_t)v * k.n + r);
+    cp_async8(base + (size_t)kMaxRestart * kArnThreads, k.w + r);
+    if (with_scale) cp_async8(base + (size_t)(kMaxRestart + 1) * kArnThreads, k.scale + r);
+  }
+  cp_async_commit();
+}
+
+__global__ void __launch_bounds__(kArnThreads) k_update_dots_norm_cp(KBufs k) {
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ __align__(16) double stg[];
+  __shared__ double sm[(kMaxRestart + 1) * (kArnThreads / 32)];
+  __shared__ double hs[kMaxRestart + 1];
+  __shared__ double red[(kMaxRestart + 1) * kSumSlices];
+  const int j = k.st->j;
+  const int nv = j + 1;
+  const int t = threadIdx.x;
+  const int stride = gridDim.x * blockDim.x;
+  int r = blockIdx.x * blockDim.x + t;
+  stage_row(k, stg, 0, r, nv, false);  // overlaps the h1 reduction
+  sum_partials<kArnThreads>(k.partial, k.parts_a, nv, hs, red);
+  if (blockIdx.x == 0) {
+    if (t < nv) k.st->h1[t] = hs[t];
+    if (t == 0) k.st->jc = j + 1;
+  }
+  double acc[kMaxRestart];
+#pragma unroll
+  for (int v = 0; v < kMaxRestart; ++v) acc[v] = 0.0;
+  double n2 = 0.0;
+  double* __restrict__ W = k.w;
+  for (int it = 0; r < k.n; ++it, r += stride) {
+    stage_row(k, stg, (it + 1) & 1, r + stride, nv, false);
+    cp_async_wait<1>();
+    const double* row = stg + (size_t)(it & 1) * kStageVals * kArnThreads + t;
+    double wr = row[(size_t)kMaxRestart * kArnThreads];
+#pragma unroll
+    for (int v = 0; v < kMaxRestart; ++v)
+      if (v < nv) wr = fma(-hs[v], row[(size_t)v * kArnThreads], wr);
+    W[r] = wr;
+#pragma unroll
+    for (int v = 0; v < kMaxRestart; ++v)
+      if (v < nv) acc[v] = fma(row[(size_t)v * kArnThreads], wr, acc[v]);
+    n2 = fma(wr, wr, n2);
+  }
+  cp_async_wait<0>();
+  cta_reduce_t32<kArnThreads>(acc, n2, nv, sm, k.partial2 + (size_t)blockIdx.x * (kMaxRestart + 1));
+}
+
 // (C) every CTA sums (B)'s partials into h2 and ||w||^2 and forms
 //     h_{j+1,j} = sqrt(||w||^2 - ||h2||^2) (the norm of w - V h2 for an
 //     orthonormal V; h2 is the small second CGS correction). The LAST CTA
 //     only runs the Givens step (and sets the CUDA-graph WHILE condition),
 //     overlapping the others, which do w -= V h2 ; v_{j+1} = w / h_{j+1,j} ;
 //     u = v_{j+1} / scale over the rows. Launched with one extra CTA.
+template <bool PF>
 __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
   pdl_trigger();
   pdl_wait();
@@ -704,10 +836,12 @@ __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
   // first row prefetched before the reduction (see k_update_dots_norm)
   const int r0 = blockIdx.x * blockDim.x + threadIdx.x;
   const bool has0 = rows_cta && r0 < k.n;
-  double w0 = 0.0, v0[kMaxRestart];
+  double w0 = 0.0, v0[PF ? kMaxRestart : 1];
+  if constexpr (PF) {
 #pragma unroll
-  for (int v = 0; v < kMaxRestart; ++v) v0[v] = (has0 && v < nv) ? k.V[(size_t)v * k.n + r0] : 0.0;
-  if (has0) w0 = k.w[r0];
+    for (int v = 0; v < kMaxRestart; ++v) v0[v] = (has0 && v < nv) ? k.V[(size_t)v * k.n + r0] : 0.0;
+    if (has0) w0 = k.w[r0];
+  }
   sum_partials<kArnThreads>(k.partial2, k.parts_b, nv + 1, hs, red);
   if (threadIdx.x < 32) {
     double q = 0.0;
@@ -729,18 +863,30 @@ __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
   }
   const bool lucky = hn < 1e-14;
   double* vj = k.V + (size_t)jn * k.n;
-  if (has0) {
+  if (PF && has0) {
     double wr = w0;
 #pragma unroll
     for (int v = 0; v < kMaxRestart; ++v)
-      if (v < nv) wr = fma(-hs[v], v0[v], wr);
+      if (v < nv) wr = fma(-hs[v], v0[PF ? v : 0], wr);
     if (!lucky) {
       const double vv = wr / hn;
       vj[r0] = vv;
       k.ubuf[r0] = vv / k.scale[r0];
     }
   }
-  {
+  if constexpr (PF) {
+    for (int r = r0 + nb * blockDim.x; r < k.n; r += nb * blockDim.x) {
+      double wr = k.w[r];
+  #pragma unroll
+      for (int v = 0; v < kMaxRestart; ++v)
+        if (v < nv) wr = fma(-hs[v], k.V[(size_t)v * k.n + r], wr);
+      if (!lucky) {
+        const double vv = wr / hn;
+        vj[r] = vv;
+        k.ubuf[r] = vv / k.scale[r];
+      }
+    }
+  } else {
     // restrict-qualified views (see k_update_dots_norm): the stores of v_{j+1}
     // and u do not alias V, w or scale, so row loads run ahead of them
     const double* __restrict__ V = k.V;
@@ -749,7 +895,7 @@ __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
     double* __restrict__ VJ = vj;
     double* __restrict__ UB = k.ubuf;
     const size_t n = (size_t)k.n;
-    for (int r = r0 + nb * blockDim.x; r < k.n; r += nb * blockDim.x) {
+    for (int r = PF ? r0 + nb * blockDim.x : (rows_cta ? r0 : k.n); r < k.n; r += nb * blockDim.x) {
       double vr[kMaxRestart];
 #pragma unroll
       for (int v = 0; v < kMaxRestart; ++v) vr[v] = v < nv ? __ldg(V + (size_t)v * n + r) : 0.0;
@@ -765,5 +911,71 @@ __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
       }
     }
   }
+}
+
+// (C) for large n: the rows stream through cp.async stages as in
+// k_update_dots_norm_cp; the Givens CTA is unchanged.
+__global__ void __launch_bounds__(kArnThreads) k_update_normalize_cp(KBufs k) {
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ __align__(16) double stg[];
+  __shared__ double hs[kMaxRestart + 1];
+  __shared__ double red[(kMaxRestart + 1) * kSumSlices];
+  __shared__ double s_hn;
+  const int jn = k.st->jc;
+  const int nv = jn;
+  const int nb = gridDim.x - 1;
+  const bool rows_cta = blockIdx.x < nb;
+  __shared__ double g_col[kMaxRestart + 2], g_cs[kMaxRestart + 1], g_sn[kMaxRestart + 1];
+  double h1t = 0.0, gj = 0.0;
+  const int t = threadIdx.x;
+  if (!rows_cta) {
+    if (t < nv) h1t = __ldcg(k.st->h1 + t);
+    if (t < nv - 1) {
+      g_cs[t] = __ldcg(k.cs + t);
+      g_sn[t] = __ldcg(k.sn + t);
+    }
+    if (t == 0) gj = __ldcg(k.g + nv - 1);
+  }
+  const int stride = nb * blockDim.x;
+  int r = rows_cta ? blockIdx.x * blockDim.x + t : k.n;
+  if (rows_cta) stage_row(k, stg, 0, r, nv, true);  // overlaps the reduction
+  sum_partials<kArnThreads>(k.partial2, k.parts_b, nv + 1, hs, red);
+  if (t < 32) {
+    double q = 0.0;
+    for (int v = t; v < nv; v += 32) q = fma(hs[v], hs[v], q);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(kFull, q, o);
+    if (t == 0) s_hn = sqrt(fmax(hs[nv] - q, 0.0));
+  }
+  __syncthreads();
+  const double hn = s_hn;
+  if (!rows_cta) {
+    if (t < nv) {
+      k.st->h2[t] = hs[t];
+      g_col[t] = h1t + hs[t];
+    }
+    __syncthreads();
+    givens_core(k, nv - 1, hn, g_col, g_cs, g_sn, gj);
+    return;
+  }
+  const bool lucky = hn < 1e-14;
+  double* __restrict__ VJ = k.V + (size_t)jn * k.n;
+  double* __restrict__ UB = k.ubuf;
+  for (int it = 0; r < k.n; ++it, r += stride) {
+    stage_row(k, stg, (it + 1) & 1, r + stride, nv, true);
+    cp_async_wait<1>();
+    const double* row = stg + (size_t)(it & 1) * kStageVals * kArnThreads + t;
+    double wr = row[(size_t)kMaxRestart * kArnThreads];
+#pragma unroll
+    for (int v = 0; v < kMaxRestart; ++v)
+      if (v < nv) wr = fma(-hs[v], row[(size_t)v * kArnThreads], wr);
+    if (!lucky) {
+      const double vv = wr / hn;
+      VJ[r] = vv;
+      UB[r] = vv / row[(size_t)(kMaxRestart + 1) * kArnThreads];
+    }
+  }
+  cp_async_wait<0>();
 }
 }  // namespace fsigpu

@@ -470,9 +470,10 @@ __global__ void __launch_bounds__(256) prolong_resid_kernel(int rows, const int*
                                                             const unsigned char* __restrict__ cmask, double* x,
                                                             const double* r_pre, double* r) {
   // P rows hold <= 9 entries (Q2 natural injection, 3 for the P1disc
-  // pressure): size the P batch so one batch covers them at any LPR; the
-  // tail loop below then only runs for unusual transfer operators
-  constexpr int UP = (9 + LPR - 1) / LPR;
+  // pressure): size the P batch so one batch covers them at any LPR (at
+  // least 2 per lane, the config-0 tuning); the tail loop below then only
+  // runs for unusual transfer operators
+  constexpr int UP = (9 + LPR - 1) / LPR > 2 ? (9 + LPR - 1) / LPR : 2;
   const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int row = (int)(gt / LPR);
   const int lane = threadIdx.x & (LPR - 1);

@@ -340,6 +340,25 @@ def test_paired_load_kernels(cfg0, unroll):
     assert res.converged and abs(res.iterations - int(g["gmres_add/iterations"][0])) <= 1
 
 
+def test_large_system_kernel_variants(cfg0, monkeypatch):
+    """FSIGPU_FORCE_BIG=1 takes the kernels config 2 runs on (k_spmv_dots_s,
+    the cp.async Arnoldi stages, paired SpMV and A*P loads) on config 0:
+    V-cycle against the reference's golden output, GMRES iterations within
+    +-1 and the final relative residual within 1e-8 of the reference's."""
+    monkeypatch.setenv("FSIGPU_FORCE_BIG", "1")
+    G = fsigpu.GmgPreconditioner(cfg0.levels)
+    g = cfg0.golden
+    assert rel(G.apply(g["golden/vcycle_r"]), g["golden/vcycle_z_add"]) <= 1e-9
+    cfg = fsigpu.KrylovConfig(restart=30, max_iters=2000, rel_tol=1e-10, abs_tol=1e-300)
+    for graphs in (True, False):
+        res = fsigpu.GmresSolver(G, cfg0.frame_scale, 30, graphs=graphs).solve(cfg0.b, cfg)
+        assert res.converged
+        assert abs(res.iterations - int(g["gmres_add/iterations"][0])) <= 1
+        ref_rel = g["gmres_add/true_residual"][0] / g["gmres_add/history"][0]
+        assert abs(res.true_residual / res.history[0] - ref_rel) <= 1e-8
+        assert rel(res.x, g["gmres_add/x"]) <= 1e-6
+
+
 def test_gmres_restart_and_x0(cfg0):
     """Restart length 10 and a nonzero initial guess still converge to the
     same solution (krylov.cpp:29-34,116-122)."""
