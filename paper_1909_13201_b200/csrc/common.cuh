@@ -148,6 +148,11 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigne
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// Bulk prefetch of [src, src + bytes) into L2 (16-B aligned, multiple of 16).
+__device__ __forceinline__ void l2_prefetch_bulk(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // Per-thread asynchronous 8-byte global -> shared copies (LDGSTS), grouped
 // by commit; wait_group<N> leaves at most N newest groups in flight.
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {

@@ -328,7 +328,8 @@ struct SmallPipeArgs {
   const double* r;
   double* out;
   long long nb;
-  int cap;  // doubles per buffer
+  int cap;     // doubles per buffer
+  int single;  // one buffer per warp + L2 prefetch of the next block (else two buffers)
 };
 
 // solve one block (m <= 64) whose solve format is at blk (shared memory);
@@ -394,8 +395,9 @@ __global__ void __launch_bounds__(kPipeMaxWarps * 32) small_pipe_solve_kernel(Sm
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long G = (long long)gridDim.x * NW;
   const long long b0 = (long long)blockIdx.x * NW + warp;  // iteration j handles block b0 + j*G
-  double* buf = dsm + (size_t)warp * 2 * a.cap;
-  double* xs = dsm + (size_t)NW * 2 * a.cap + warp * 64;
+  const int nbuf = a.single ? 1 : 2;
+  double* buf = dsm + (size_t)warp * nbuf * a.cap;
+  double* xs = dsm + (size_t)NW * nbuf * a.cap + warp * 64;
   unsigned long long* bar = bars[warp];
   if (lane == 0) {
     mbar_init(&bar[0], 1);
@@ -459,11 +461,13 @@ __global__ void __launch_bounds__(kPipeMaxWarps * 32) small_pipe_solve_kernel(Sm
     }
     meta(it, ro, o0, m, sz);
     if (m < 0) break;
-    {
-      long long r1, q1;
-      int m1, s1;
-      meta(it + 1, r1, q1, m1, s1);
-      if (m1 >= 0 && lane == 0) {
+    long long r1, q1;
+    int m1, s1;
+    meta(it + 1, r1, q1, m1, s1);
+    if (m1 >= 0 && lane == 0) {
+      if (a.single) {
+        l2_prefetch_bulk(a.sf + q1, (unsigned)(8 * s1));  // lands in L2 during this solve
+      } else {
         fence_proxy_async();  // the buffer's last generic reads precede the async write
         issue(q1, s1, (it + 1) & 1);
       }
@@ -479,12 +483,19 @@ __global__ void __launch_bounds__(kPipeMaxWarps * 32) small_pipe_solve_kernel(Sm
     }
     xs[lane] = v0;
     xs[lane + 32] = v1;
-    mbar_wait(&bar[it & 1], (it >> 1) & 1);
+    if (a.single)
+      mbar_wait(&bar[0], it & 1);
+    else
+      mbar_wait(&bar[it & 1], (it >> 1) & 1);
     __syncwarp();
-    small_solve_smem(buf + (size_t)(it & 1) * a.cap, m, xs, lane);
+    small_solve_smem(buf + (size_t)(a.single ? 0 : (it & 1)) * a.cap, m, xs, lane);
     if (lane < m) a.out[ro + lane] = xs[lane];
     if (lane + 32 < m) a.out[ro + lane + 32] = xs[lane + 32];
     __syncwarp();
+    if (a.single && m1 >= 0 && lane == 0) {  // the next block, now mostly an L2 hit
+      fence_proxy_async();
+      issue(q1, s1, 0);
+    }
     v0 = w0;
     v1 = w1;
   }

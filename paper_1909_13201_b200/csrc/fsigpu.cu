@@ -582,17 +582,24 @@ struct Blocks {
   // Blocks all <= 64 with a plain gathered right-hand side: per-warp
   // double-buffered bulk copies of whole blocks (small_pipe_solve_kernel).
   // Warps per CTA are sized so two buffers per warp fit the shared memory.
-  // Opt-in (FSIGPU_SOLVE_PIPE=1): measured 2.87 ms per config-1 solve
-  // against 2.53 ms for block_solve_kernel. With two 28 KB buffers per warp
-  // only 4 warps fit per SM, and the dependent phases of a solve then run at
-  // ~0.9 IPC: the kernel is issue-latency-bound, not HBM-bound.
+  // Default for all-small blocks with a plain gathered right-hand side
+  // (config 1): one 28 KB shared buffer per warp, 7 warps per SM, and an L2
+  // bulk prefetch of each warp's next block issued before it solves the
+  // current one, so the next TMA copy is an L2 hit. Config-1 solve: 1.54 ms
+  // = 6.64 TB/s, against 2.33 ms for block_solve_kernel (FSIGPU_SOLVE_PIPE=0)
+  // and 2.36 ms for two buffers per warp (=1: only 4 warps per SM, whose
+  // dependent solve phases then run at ~0.9 IPC).
   static bool small_pipe_enabled() {
     const char* e = std::getenv("FSIGPU_SOLVE_PIPE");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }
   void solve_small_pipe(const SolveArgs& base, cudaStream_t s) const {
     const int cap = pipe_cap;
-    const size_t per_warp = (size_t)(2 * cap + 64) * 8;
+    // FSIGPU_SOLVE_PIPE=1: two buffers per warp; =2: one buffer per warp
+    // plus an L2 bulk prefetch of the warp's next block (twice the warps)
+    const char* pe = std::getenv("FSIGPU_SOLVE_PIPE");
+    const int single = (pe && pe[0] == '1') ? 0 : 1;
+    const size_t per_warp = (size_t)((single ? 1 : 2) * cap + 64) * 8;
     int nw = (int)std::max<size_t>(1, std::min<size_t>(kPipeMaxWarps, (size_t)(200 * 1024) / per_warp));
     if (const char* e = std::getenv("FSIGPU_PIPE_WARPS")) nw = std::max(1, std::min(kPipeMaxWarps, std::atoi(e)));
     const size_t smem = per_warp * nw;
@@ -603,7 +610,7 @@ struct Blocks {
     FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, small_pipe_solve_kernel, nw * 32, smem));
     const int grid = (int)std::max<long long>(1, std::min<long long>((long long)sms * std::max(occ, 1),
                                                                      (nb + nw - 1) / nw));
-    SmallPipeArgs a{m.p, sf_off.p, row_off.p, sf.p, gsrc.p, base.r, base.out, nb, cap};
+    SmallPipeArgs a{m.p, sf_off.p, row_off.p, sf.p, gsrc.p, base.r, base.out, nb, cap, single};
     ProfScope ps(FSIGPU_K_BLOCK_SOLVE, solve_bytes, s);
     launch_k(small_pipe_solve_kernel, dim3(grid), dim3(nw * 32), smem, s, a);
     FSI_CHECK_LAUNCH();

@@ -272,7 +272,7 @@ def test_singular_block_label():
     assert e.value.label == "fs-fluid-up-4"
 
 
-@pytest.mark.parametrize("pipe", ["0", "1"])
+@pytest.mark.parametrize("pipe", ["0", "1", "2"])
 def test_config1_sample_parity(pipe, monkeypatch):
     """Config-1 generator (2,048 + 1,024 blocks) against the oracle, through
     block_solve_kernel and the opt-in pipelined small-block solve."""
