@@ -1310,7 +1310,9 @@ struct Gmres {
   void cycle_tail() {
     cudaStream_t s = g->s;
     launch_k(k_solve_y, dim3(1), dim3(256), 0, s, kb);
-    launch_k(k_update_x, dim3(grid), dim3(kKThreads), 0, s, kb);
+    // x += Z y: one row per thread (a grid-stride loop over ~16 rows per
+    // thread left the config-2 update at 1.1 TB/s)
+    launch_k(k_update_x, dim3(std::max(grid, (int)ceil_div(n, kKThreads))), dim3(kKThreads), 0, s, kb);
     outer_resid();
     launch_k(k_norm_r, dim3(grid), dim3(kKThreads), 0, s, kb);
     FSI_CHECK_LAUNCH();

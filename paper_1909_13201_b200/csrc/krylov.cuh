@@ -375,10 +375,20 @@ __global__ void k_update_x(KBufs k) {
   __shared__ double ys[kMaxRestart];
   if (threadIdx.x < j) ys[threadIdx.x] = st->y[threadIdx.x];
   __syncthreads();
+  // all j loads of a row issued before its FMA chain (predicated batch of
+  // kMaxRestart; a runtime-bound loop left one DRAM latency per term)
+  const double* __restrict__ Z = k.Z;
+  double* __restrict__ X = k.x;
+  const size_t n = (size_t)k.n;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x) {
+    double z[kMaxRestart];
+#pragma unroll
+    for (int i = 0; i < kMaxRestart; ++i) z[i] = i < j ? __ldg(Z + (size_t)i * n + r) : 0.0;
     double s = 0.0;
-    for (int i = 0; i < j; ++i) s = fma(ys[i], k.Z[(size_t)i * k.n + r], s);
-    k.x[r] += s;
+#pragma unroll
+    for (int i = 0; i < kMaxRestart; ++i)
+      if (i < j) s = fma(ys[i], z[i], s);
+    X[r] += s;
   }
 }
 
@@ -597,6 +607,46 @@ __device__ __forceinline__ void sum_partials(const double* __restrict__ part, in
     dst[w] = z;
   }
   __syncthreads();
+}
+
+// fused_row with 16-byte index/value pairs (see csr_pair_kernel), UP pairs
+// per lane per batch. Not used by default: in k_spmv_dots_s (LPR 8, UP 5)
+// its 80 registers cost a CTA per SM and the config-2 step went 243 -> 265 us.
+template <int LPR, int UP>
+__device__ __forceinline__ double fused_row_pair(const KBufs& k, int row, int lane) {
+  const int k0 = row >= 0 ? __ldg(k.a_ptr + row) : 0, k1 = row >= 0 ? __ldg(k.a_ptr + row + 1) : 0;
+  double s = 0.0;
+  for (int kb = (k0 & ~1) + 2 * lane; kb < k1; kb += 2 * UP * LPR) {
+    int2 c[UP];
+    double2 v[UP];
+#pragma unroll
+    for (int u = 0; u < UP; ++u) {
+      const int kk = kb + 2 * u * LPR;
+      if (kk < k1) {
+        c[u] = __ldg(reinterpret_cast<const int2*>(k.a_idx + kk));
+        v[u] = __ldg(reinterpret_cast<const double2*>(k.a_val + kk));
+        if (kk < k0) c[u].x = -1;
+        if (kk + 1 >= k1) c[u].y = -1;
+      } else {
+        c[u] = make_int2(-1, -1);
+        v[u] = make_double2(0.0, 0.0);
+      }
+    }
+    double x0[UP], x1[UP];
+#pragma unroll
+    for (int u = 0; u < UP; ++u) {
+      x0[u] = c[u].x >= 0 ? k.zbuf[c[u].x] : 0.0;
+      x1[u] = c[u].y >= 0 ? k.zbuf[c[u].y] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < UP; ++u) {
+      s = fma(v[u].x, x0[u], s);
+      s = fma(v[u].y, x1[u], s);
+    }
+  }
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, LPR);
+  return s;
 }
 
 // Large-n variant of (A): 256-thread CTAs on 32-row tiles (8 lanes per
