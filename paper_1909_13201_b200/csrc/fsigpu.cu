@@ -447,7 +447,8 @@ struct Blocks {
   static constexpr int kNumCls = 7;
   static constexpr int kRegMM[5] = {16, 32, 48, 56, 64};
   std::vector<int> h_cls[kNumCls];
-  DevBuf<int> d_cls[kNumCls];
+  DevBuf<int> d_cls_all;  // the class lists back to back (one allocation)
+  const int* d_cls[kNumCls] = {};
   int cls_max[kNumCls] = {};
   DevBuf<int> fail;
   void build_classes(cudaStream_t s) {
@@ -466,8 +467,14 @@ struct Blocks {
       h_cls[c].push_back((int)b);
       cls_max[c] = std::max(cls_max[c], mm);
     }
-    for (int c = 0; c < kNumCls; ++c)
-      if (!h_cls[c].empty()) d_cls[c].upload(h_cls[c], s);
+    std::vector<int> all;
+    std::vector<size_t> off(kNumCls, 0);
+    for (int c = 0; c < kNumCls; ++c) {
+      off[c] = all.size();
+      all.insert(all.end(), h_cls[c].begin(), h_cls[c].end());
+    }
+    if (!all.empty()) d_cls_all.upload(all, s);
+    for (int c = 0; c < kNumCls; ++c) d_cls[c] = h_cls[c].empty() ? nullptr : d_cls_all.p + off[c];
     fail.alloc(1);
   }
   template <int MM>
@@ -476,7 +483,7 @@ struct Blocks {
     const size_t sm = (size_t)((size_t)mx * mx + mx + (mx + 1) / 2 + 32 * kTileLd + 8) * 8;
     auto k = lu_reg_kernel<MM>;
     FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    k<<<(int)h_cls[which].size(), MM <= 32 ? 32 : 64, sm, s>>>(d_cls[which].p, m.p, lu_off.p, row_off.p,
+    k<<<(int)h_cls[which].size(), MM <= 32 ? 32 : 64, sm, s>>>(d_cls[which], m.p, lu_off.p, row_off.p,
                                                              sf_off.p, src, luo, sf.p, piv.p, gsrc.p, lperm.p,
                                                              src_pos, pos_base, fail.p);
   }
@@ -492,7 +499,7 @@ struct Blocks {
       if (h_cls[which].empty()) return;
       const int grid = (int)h_cls[which].size();
       const int mx = cls_max[which];
-      const int* bl = d_cls[which].p;
+      const int* bl = d_cls[which];
       switch (which) {
         case 0: launch_reg<16>(which, src, luo, src_pos, pos_base, s); break;
         case 1: launch_reg<32>(which, src, luo, src_pos, pos_base, s); break;
@@ -2090,7 +2097,7 @@ int fsigpu_gmres_create(fsigpu_gmg g, const double* frame_scale, int restart, fs
     k.gv.alloc(restart + 1);
     k.grid = std::max(1, std::min(ceil_div(n, kKThreads), 2 * 148));
     k.partial.alloc((size_t)std::max(std::max(k.grid, ceil_div(n, kFuseRows)), 4 * 148) * (kMaxRestart + 1));
-    k.partial2.alloc((size_t)16 * 148 * (kMaxRestart + 1));  // (B) grid <= 16 CTAs per SM
+    k.partial2.alloc((size_t)(n > 8 * 148 * kFuseRows ? 16 : 4) * 148 * (kMaxRestart + 1));  // (B) grid <= 16 (big) / 4 CTAs per SM
     k.ticket.alloc(1);
     k.ticket.zero(s);
     k.st.alloc(1);
