@@ -1005,6 +1005,144 @@ __global__ void __launch_bounds__(MM <= 32 ? 32 : 64)
                              gsrc_out, lperm_out, src_pos, pos_base, /*maps_done=*/true);
 }
 
+// Two threads per block row (lu_reg2_kernel): thread (row i, half h) keeps
+// the columns j = 2q + h of row i in registers (a[MM/2]); the pair sits in
+// adjacent lanes. Same rounded operations per entry as LuRegStep (and the
+// reference): the owner of column K (h = K & 1) offers the pivot candidate
+// and forms l = a_iK * (1/pivot), which its partner takes by shuffle; both
+// halves update their own columns. Half the per-thread update work and
+// twice the warps per SM of the one-thread-per-row kernel.
+template <int K, int MM, int NW>
+struct LuReg2Step {
+  static __device__ __forceinline__ bool run(double (&a)[MM / 2], double rmax, int& pos, int m, int t,
+                                             double* slots, int* perm) {
+    constexpr int kNone = 1 << 20;
+    constexpr int kStride = LuSlot<MM>::kStride;
+    constexpr int HO = K & 1, QO = K >> 1;  // owner half and its register index
+    if (K >= m) return false;
+    const int lane = t & 31, warp = t >> 5, h = t & 1;
+    constexpr int buf = K & 1;
+    const bool owner = h == HO;
+    const bool cand = owner && pos >= K && pos < m;
+    const double my_inv = 1.0 / a[QO];
+    const unsigned long long vb = cand ? lu_vkey(fabs(a[QO])) : 0ull;
+    const unsigned hi = (unsigned)(vb >> 32), lo = (unsigned)vb;
+    const unsigned mh = __reduce_max_sync(kFull, hi);
+    const unsigned ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
+    const unsigned key = __reduce_min_sync(kFull, (cand && hi == mh && lo == ml) ? (unsigned)pos : (unsigned)kNone);
+    double* slot = slots + (size_t)(buf * NW + warp) * kStride;
+    if (mh == 0) {
+      if (lane == 0) slot[0] = __longlong_as_double(0);
+    } else if ((unsigned)pos == key) {  // both halves of this warp's best row publish
+      double* r = slot + 2;
+      if (owner) {
+        const int bad = fabs(a[QO]) <= 1e-14 * fmax(rmax, 1e-300);
+        reinterpret_cast<double2*>(slot)[0] =
+            make_double2(__longlong_as_double((long long)vb), __longlong_as_double((long long)(key | (bad << 30))));
+        r[K] = my_inv;
+      }
+#pragma unroll
+      for (int q = 0; q < MM / 2; ++q)
+        if (2 * q + 1 > K) {  // columns 2q + h > K (h = 0 needs 2q > K)
+          if (2 * q > K || h == 1) r[2 * q + h] = a[q];
+        }
+    }
+    __syncthreads();
+    int ws = buf * NW;
+    unsigned long long bv = (unsigned long long)__double_as_longlong(slots[(size_t)ws * kStride]);
+    int bk = (int)__double_as_longlong(slots[(size_t)ws * kStride + 1]);
+#pragma unroll
+    for (int w = 1; w < NW; ++w) {
+      const double2 o = reinterpret_cast<const double2*>(slots + (size_t)(buf * NW + w) * kStride)[0];
+      const unsigned long long ov = (unsigned long long)__double_as_longlong(o.x);
+      const int ok = (int)__double_as_longlong(o.y);
+      if (ov > bv || (ov == bv && (ok & 0x3fffffff) < (bk & 0x3fffffff))) {
+        bv = ov;
+        bk = ok;
+        ws = buf * NW + w;
+      }
+    }
+    const int p = bk & 0x3fffffff;
+    if (t == 0) perm[K] = p;
+    pos = (pos == p) ? K : (pos == K ? p : pos);
+    if (bk >> 30) return true;
+    const double* r = slots + (size_t)ws * kStride + 2;
+    const bool active = pos > K && pos < m;
+    // multiplier formed by the owner half, shared with its partner
+    const double lo_own = (owner && active) ? mul_rn(a[QO], r[K]) : 0.0;
+    const double lo_partner = __shfl_xor_sync(kFull, lo_own, 1);  // every lane takes part
+    const double l = owner ? lo_own : lo_partner;
+    if (active) {
+      if (owner) a[QO] = l;
+#pragma unroll
+      for (int q = 0; q < MM / 2; ++q)
+        if (2 * q + 1 > K) {
+          if (2 * q > K || h == 1) a[q] = sub_rn(a[q], mul_rn(l, r[2 * q + h]));
+        }
+    }
+    if constexpr (K + 1 < MM) return LuReg2Step<K + 1, MM, NW>::run(a, rmax, pos, m, t, slots, perm);
+    return false;
+  }
+};
+
+// dynamic smem as lu_reg_kernel: [A: m*m][scratch: m][perm: m ints][S: 32*kTileLd]
+template <int MM>
+__global__ void __launch_bounds__(128, 4)
+    lu_reg2_kernel(const int* __restrict__ blist, const int* __restrict__ msz, const long long* __restrict__ lu_off,
+                   const long long* __restrict__ row_off, const long long* __restrict__ sf_off,
+                   const double* __restrict__ src, double* __restrict__ lu_out, double* __restrict__ sf_out,
+                   int* __restrict__ piv_out, int* __restrict__ gsrc_out, int* __restrict__ lperm_out,
+                   const int* __restrict__ src_pos, int pos_base, int* __restrict__ fail) {
+  static_assert(MM % 2 == 0 && MM <= 64 && MM > 32, "two threads per row: 33..64 rows");
+  constexpr int NT = 128;
+  constexpr int NW = NT / 32;
+  constexpr int kNone = 1 << 20;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ __align__(16) double s_slots[2 * NW * LuSlot<MM>::kStride];
+  const int b = blist[blockIdx.x];
+  const int m = msz[b];
+  const long long off = lu_off[b];
+  const int t = threadIdx.x;
+  const int i = t >> 1, h = t & 1;
+  double* A = smem;
+  double* scratch = smem + (size_t)m * m;
+  int* perm = reinterpret_cast<int*>(scratch + m);
+  double* S = scratch + m + (m + 1) / 2;
+
+  double a[MM / 2];
+  const bool valid = i < m;
+#pragma unroll
+  for (int q = 0; q < MM / 2; ++q) {
+    const int j = 2 * q + h;
+    a[q] = (valid && j < m) ? __ldg(src + off + (size_t)j * m + i) : 0.0;
+  }
+  double rmax = 0.0;
+#pragma unroll
+  for (int q = 0; q < MM / 2; ++q) rmax = fmax(rmax, fabs(a[q]));
+  rmax = fmax(rmax, __shfl_xor_sync(kFull, rmax, 1));
+  int pos = valid ? i : kNone;
+  if (LuReg2Step<0, MM, NW>::run(a, rmax, pos, m, t, s_slots, perm)) {
+    if (t == 0) atomicMin(fail, b);
+    return;
+  }
+  const long long ro = row_off[b];
+  if (valid) {
+#pragma unroll
+    for (int q = 0; q < MM / 2; ++q) {
+      const int j = 2 * q + h;
+      if (j < m) A[(size_t)j * m + pos] = a[q];
+    }
+    if (h == 0) {
+      gsrc_out[ro + pos] = src_pos ? src_pos[ro + i] + pos_base : (int)(ro + i);
+      lperm_out[ro + pos] = i;
+      piv_out[ro + i] = perm[i];
+    }
+  }
+  __syncthreads();
+  lu_write_outputs<NT, true>(A, m, b, perm, scratch, S, row_off, lu_off, sf_off, lu_out, true, sf_out, piv_out,
+                             gsrc_out, lperm_out, src_pos, pos_base, /*maps_done=*/true);
+}
+
 // Principal block A[dofs, dofs] of a CSR matrix into column-major dense
 // storage (dst pre-zeroed). One warp per block row; columns located by
 // binary search in the sorted block index list (extract_submatrix,

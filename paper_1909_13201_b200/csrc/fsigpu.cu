@@ -330,6 +330,16 @@ struct Csr {
 enum BlockMode { kModeLU = 0, kModeInverse = 1, kModeAssembled = 2 };
 static int g_default_mode = kModeAssembled;
 
+// Register LU with two threads per row for blocks of 33..64 rows: opt-in
+// (FSIGPU_LU_TWO=1). Bit-identical, but the config-1 LU takes 39.2 ms
+// against 30.1 ms with one thread per row: four warps per block make the
+// per-step barrier and the 4-slot pivot combine longer, and at 128
+// registers only 4 CTAs (16 warps) fit per SM.
+static bool lu_two_per_row() {
+  const char* e = std::getenv("FSIGPU_LU_TWO");
+  return e && e[0] == '1';
+}
+
 // Small-block LU variant: register-resident rows (default) or the
 // shared-memory CTA kernel (FSIGPU_LU_SMEM=1, kept for A/B measurement).
 static bool lu_register_path() {
@@ -481,6 +491,15 @@ struct Blocks {
   void launch_reg(int which, const double* src, double* luo, const int* src_pos, int pos_base, cudaStream_t s) {
     const int mx = cls_max[which];
     const size_t sm = (size_t)((size_t)mx * mx + mx + (mx + 1) / 2 + 32 * kTileLd + 8) * 8;
+    if constexpr (MM > 32) {
+      if (lu_two_per_row()) {
+        auto k2 = lu_reg2_kernel<MM>;
+        FSI_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k2<<<(int)h_cls[which].size(), 128, sm, s>>>(d_cls[which], m.p, lu_off.p, row_off.p, sf_off.p, src, luo,
+                                                   sf.p, piv.p, gsrc.p, lperm.p, src_pos, pos_base, fail.p);
+        return;
+      }
+    }
     auto k = lu_reg_kernel<MM>;
     FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     k<<<(int)h_cls[which].size(), MM <= 32 ? 32 : 64, sm, s>>>(d_cls[which], m.p, lu_off.p, row_off.p,

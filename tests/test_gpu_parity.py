@@ -228,13 +228,14 @@ def test_block_edge_cases():
     assert E.solve(np.zeros(0)).shape == (0,)
 
 
-@pytest.mark.parametrize("variant", ["register", "smem"])
+@pytest.mark.parametrize("variant", ["register", "register2", "smem"])
 def test_small_lu_variants_ties_bitexact(variant, monkeypatch):
     """Both small-block LU kernels (register rows, the default; shared-memory
     CTA, FSIGPU_LU_SMEM=1) against DenseFactorization, on sign matrices where
     every pivot search sees ties (the reference keeps the lowest row,
     dense.cpp:42-49) and on random blocks of every register class size."""
     monkeypatch.setenv("FSIGPU_LU_SMEM", "1" if variant == "smem" else "0")
+    monkeypatch.setenv("FSIGPU_LU_TWO", "1" if variant == "register2" else "0")
     rng = np.random.default_rng(11)
     mats = []
     for m in [3, 8, 16, 17, 31, 32, 40, 48, 49, 54, 56, 59, 62, 64]:
