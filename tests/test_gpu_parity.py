@@ -360,6 +360,37 @@ def test_large_system_kernel_variants(cfg0, monkeypatch):
         assert rel(res.x, g["gmres_add/x"]) <= 1e-6
 
 
+def test_gmres_edge_cases(chan):
+    """krylov.cpp:20-42 edge behaviour on the reference's channel case: a zero
+    right-hand side converges with zero iterations and x = 0 (r0 <= target);
+    max_iters = 0 returns x0 unconverged; GMRES(1) follows the oracle's
+    iteration count; bad configs raise like std::invalid_argument."""
+    G = fsigpu.GmgPreconditioner(chan.levels)
+    OG = O.OracleGmg(chan.levels)
+    n = chan.levels[-1].n
+    cfg = fsigpu.KrylovConfig(restart=30, max_iters=100, rel_tol=1e-8, abs_tol=1e-300)
+    z = fsigpu.gmres(G, chan.frame_scale, np.zeros(n), cfg)
+    assert z.converged and z.iterations == 0 and not np.any(z.x) and z.history[0] == 0.0
+    x0 = np.random.default_rng(4).uniform(-1, 1, n)
+    c0 = fsigpu.KrylovConfig(restart=30, max_iters=0, rel_tol=1e-8, abs_tol=1e-300)
+    r = fsigpu.GmresSolver(G, chan.frame_scale, 30).solve(chan.b, c0, x0)
+    assert not r.converged and r.iterations == 0 and np.array_equal(r.x, x0)
+    c1 = fsigpu.KrylovConfig(restart=1, max_iters=60, rel_tol=1e-6, abs_tol=1e-300)
+    g1 = fsigpu.gmres(G, chan.frame_scale, chan.b, c1)
+    o1 = OG.gmres(chan.frame_scale, chan.b, restart=1, max_iters=60, rel_tol=1e-6, abs_tol=1e-300)
+    assert g1.converged == o1["converged"]
+    assert abs(g1.iterations - o1["iterations"]) <= 1
+    assert np.all(np.diff(g1.history) <= 1e-12 * g1.history[0])  # GMRES(1): monotone per cycle
+    for bad in [fsigpu.KrylovConfig(restart=30, max_iters=10, rel_tol=0.0),
+                fsigpu.KrylovConfig(restart=30, max_iters=10, rel_tol=1e-8, abs_tol=0.0)]:
+        with pytest.raises(ValueError):
+            fsigpu.gmres(G, chan.frame_scale, chan.b, bad)
+    with pytest.raises(ValueError):
+        fsigpu.GmresSolver(G, chan.frame_scale, 0)
+    with pytest.raises(ValueError):
+        fsigpu.gmres(G, chan.frame_scale, chan.b[:-1], cfg)
+
+
 def test_gmres_restart_and_x0(cfg0):
     """Restart length 10 and a nonzero initial guess still converge to the
     same solution (krylov.cpp:29-34,116-122)."""
