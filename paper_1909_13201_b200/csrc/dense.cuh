@@ -1143,6 +1143,242 @@ __global__ void __launch_bounds__(128, 4)
                              gsrc_out, lperm_out, src_pos, pos_base, /*maps_done=*/true);
 }
 
+// ---------------------------------------------------------------- blocked LU (m > 164)
+// Right-looking LU in panels of kBigNB columns for the large blocks (the
+// pure-DD Vanka patches of config 4, m ~ 500-780), factored in place in
+// global memory (column-major), one launch pair per panel for the whole
+// batch:
+//   lu_big_panel_kernel  (one CTA per block): for each panel column k the
+//     pivot search (largest |a_ik|, lowest row on ties), the swap of the
+//     whole rows k and p (and of their original row maxima), the singular
+//     test, l = a_ik * (1/pivot), the rank-1 update of the remaining panel
+//     columns; then the panel rows of the trailing columns (U12): per
+//     column, a_ij -= l_ik * a_kj for k = k0..i-1 in order;
+//   lu_big_update_kernel (a CTA per 64x64 tile of A22): a_ij -= l_ik * u_kj
+//     for the panel's k in order, non-fused, from shared-memory tiles of
+//     L21 and U12.
+// Every entry therefore receives the reference's rounded updates in the
+// reference's k order (DenseFactorization, dense.cpp:31-67): the factors
+// are bit-identical. Row swaps move whole rows immediately, as the
+// reference does.
+constexpr int kBigNB = 32;
+constexpr int kBigTile = 64;
+
+__global__ void __launch_bounds__(256) lu_big_init_kernel(const int* __restrict__ blist, const int* __restrict__ msz,
+                                                          const long long* __restrict__ lu_off,
+                                                          const long long* __restrict__ row_off,
+                                                          const double* __restrict__ src, double* __restrict__ work,
+                                                          double* __restrict__ rowmax, int* __restrict__ bad) {
+  const int bi = blockIdx.x;
+  const int b = blist[bi];
+  const int m = msz[b];
+  const long long off = lu_off[b], ro = row_off[b];
+  if (src != work)
+    for (long long e = threadIdx.x; e < (long long)m * m; e += blockDim.x) work[off + e] = src[off + e];
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    double mx = 0.0;
+    for (int j = 0; j < m; ++j) mx = fmax(mx, fabs(src[off + (size_t)j * m + i]));
+    rowmax[ro + i] = mx;
+  }
+  if (threadIdx.x == 0) bad[bi] = 0;
+}
+
+__global__ void __launch_bounds__(256, 2) lu_big_panel_kernel(const int* __restrict__ blist, const int* __restrict__ msz,
+                                                           const long long* __restrict__ lu_off,
+                                                           const long long* __restrict__ row_off, double* work,
+                                                           double* rowmax, int* __restrict__ piv, int* bad,
+                                                           int* __restrict__ fail, int k0) {
+  const int bi = blockIdx.x;
+  const int b = blist[bi];
+  const int m = msz[b];
+  if (k0 >= m || bad[bi]) return;
+  const long long off = lu_off[b], ro = row_off[b];
+  double* A = work + off;
+  double* rm = rowmax + ro;
+  const int kb = min(kBigNB, m - k0);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  __shared__ double s_v[8];
+  __shared__ int s_i[8];
+  __shared__ int s_p, s_bad;
+  for (int k = k0; k < k0 + kb; ++k) {
+    // pivot: max |a_ik| over i >= k, lowest i among equals (the reference's
+    // first-strictly-larger scan from i = k)
+    double best = -1.0;
+    int bidx = m;
+    for (int i = k + t; i < m; i += blockDim.x) {
+      const double v = fabs(A[(size_t)k * m + i]);
+      if (v > best) {
+        best = v;
+        bidx = i;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(kFull, best, o);
+      const int oi = __shfl_xor_sync(kFull, bidx, o);
+      if (ob > best || (ob == best && oi < bidx)) {
+        best = ob;
+        bidx = oi;
+      }
+    }
+    if (lane == 0) {
+      s_v[warp] = best;
+      s_i[warp] = bidx;
+    }
+    __syncthreads();
+    if (t == 0) {
+      double bv = s_v[0];
+      int bx = s_i[0];
+      for (int w = 1; w < 8; ++w)
+        if (s_v[w] > bv || (s_v[w] == bv && s_i[w] < bx)) {
+          bv = s_v[w];
+          bx = s_i[w];
+        }
+      int p = bx < m ? bx : k;
+      if (!(fabs(A[(size_t)k * m + k]) < bv)) p = k;
+      s_p = p;
+      // singular test on the pivot row's own original maximum (dense.cpp:57)
+      const double pivot = A[(size_t)k * m + p];
+      s_bad = fabs(pivot) <= 1e-14 * fmax(rm[p], 1e-300);
+      piv[ro + k] = p;
+    }
+    __syncthreads();
+    if (s_bad) {
+      if (t == 0) {
+        bad[bi] = 1;
+        atomicMin(fail, b);
+      }
+      return;
+    }
+    const int p = s_p;
+    if (p != k) {
+      for (int j = t; j < m; j += blockDim.x) {
+        const double a0 = A[(size_t)j * m + k];
+        A[(size_t)j * m + k] = A[(size_t)j * m + p];
+        A[(size_t)j * m + p] = a0;
+      }
+      if (t == 0) {
+        const double r0 = rm[k];
+        rm[k] = rm[p];
+        rm[p] = r0;
+      }
+    }
+    __syncthreads();
+    const double inv = 1.0 / A[(size_t)k * m + k];
+    for (int i = k + 1 + t; i < m; i += blockDim.x) A[(size_t)k * m + i] = mul_rn(A[(size_t)k * m + i], inv);
+    __syncthreads();
+    // rank-1 update of the panel columns right of k
+    const int nc = k0 + kb - (k + 1);
+    const int nr = m - (k + 1);
+    for (int e = t; e < nc * nr; e += blockDim.x) {
+      const int jj = k + 1 + e / nr, i = k + 1 + e % nr;
+      A[(size_t)jj * m + i] = sub_rn(A[(size_t)jj * m + i], mul_rn(A[(size_t)k * m + i], A[(size_t)jj * m + k]));
+    }
+    __syncthreads();
+  }
+  // U12: panel rows of the trailing columns, one column per thread
+  for (int j = k0 + kb + t; j < m; j += blockDim.x) {
+    double u[kBigNB];
+#pragma unroll
+    for (int q = 0; q < kBigNB; ++q) u[q] = q < kb ? A[(size_t)j * m + k0 + q] : 0.0;
+#pragma unroll
+    for (int i = 1; i < kBigNB; ++i)
+#pragma unroll
+      for (int q = 0; q < i; ++q)
+        if (i < kb) u[i] = sub_rn(u[i], mul_rn(A[(size_t)(k0 + q) * m + k0 + i], u[q]));
+#pragma unroll
+    for (int q = 1; q < kBigNB; ++q)
+      if (q < kb) A[(size_t)j * m + k0 + q] = u[q];
+  }
+}
+
+// A22 -= L21 * U12 for panel k0 (full panels only: the last, partial panel
+// has no trailing block). grid = (tiles_r * tiles_c, blocks).
+__global__ void __launch_bounds__(256) lu_big_update_kernel(const int* __restrict__ blist,
+                                                            const int* __restrict__ msz,
+                                                            const long long* __restrict__ lu_off, double* work,
+                                                            const int* __restrict__ bad, int k0, int tiles_c) {
+  const int bi = blockIdx.y;
+  const int b = blist[bi];
+  const int m = msz[b];
+  const int r0 = k0 + kBigNB + (blockIdx.x / tiles_c) * kBigTile;
+  const int c0 = k0 + kBigNB + (blockIdx.x % tiles_c) * kBigTile;
+  if (r0 >= m || c0 >= m || bad[bi]) return;
+  double* A = work + lu_off[b];
+  __shared__ __align__(16) double Ls[kBigNB][kBigTile];
+  __shared__ __align__(16) double Us[kBigNB][kBigTile];
+  const int t = threadIdx.x;
+  for (int e = t; e < kBigNB * kBigTile; e += 256) {
+    const int k = e / kBigTile, i = e % kBigTile;  // L21: column k0+k, row r0+i (coalesced over i)
+    Ls[k][i] = r0 + i < m ? A[(size_t)(k0 + k) * m + r0 + i] : 0.0;
+  }
+  for (int e = t; e < kBigNB * kBigTile; e += 256) {
+    const int j = e / kBigNB, k = e % kBigNB;  // U12: row k0+k, column c0+j (coalesced over k)
+    Us[k][j] = c0 + j < m ? A[(size_t)(c0 + j) * m + k0 + k] : 0.0;
+  }
+  __syncthreads();
+  const int tx = t & 15, ty = t >> 4;  // 4x4 entries per thread: rows ty*4.., cols tx*4..
+  double acc[4][4];
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) {
+    const int c = c0 + tx * 4 + jj;
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) {
+      const int r = r0 + ty * 4 + ii;
+      acc[ii][jj] = (r < m && c < m) ? A[(size_t)c * m + r] : 0.0;
+    }
+  }
+#pragma unroll 4
+  for (int k = 0; k < kBigNB; ++k) {
+    const double2 l01 = *reinterpret_cast<const double2*>(&Ls[k][ty * 4]);
+    const double2 l23 = *reinterpret_cast<const double2*>(&Ls[k][ty * 4 + 2]);
+    const double2 u01 = *reinterpret_cast<const double2*>(&Us[k][tx * 4]);
+    const double2 u23 = *reinterpret_cast<const double2*>(&Us[k][tx * 4 + 2]);
+    const double l[4] = {l01.x, l01.y, l23.x, l23.y};
+    const double u[4] = {u01.x, u01.y, u23.x, u23.y};
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = sub_rn(acc[ii][jj], mul_rn(l[ii], u[jj]));
+  }
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) {
+    const int c = c0 + tx * 4 + jj;
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) {
+      const int r = r0 + ty * 4 + ii;
+      if (r < m && c < m) A[(size_t)c * m + r] = acc[ii][jj];
+    }
+  }
+}
+
+// Outputs of the blocked LU: gather map from the pivots, optional LU copy,
+// solve format (lu_write_outputs on the factor in global memory).
+// dynamic smem (doubles): [scratch: m][perm: m ints][S: 32*kTileLd]
+__global__ void __launch_bounds__(256) lu_big_finish_kernel(const int* __restrict__ blist, const int* __restrict__ msz,
+                                                            const long long* __restrict__ lu_off,
+                                                            const long long* __restrict__ row_off,
+                                                            const long long* __restrict__ sf_off,
+                                                            const double* __restrict__ work,
+                                                            double* __restrict__ sf_out, int* __restrict__ piv,
+                                                            int* __restrict__ gsrc_out, int* __restrict__ lperm_out,
+                                                            const int* __restrict__ src_pos, int pos_base,
+                                                            const int* __restrict__ bad) {
+  extern __shared__ __align__(16) double smem[];
+  const int bi = blockIdx.x;
+  if (bad[bi]) return;
+  const int b = blist[bi];
+  const int m = msz[b];
+  const long long ro = row_off[b];
+  double* scratch = smem;
+  int* perm = reinterpret_cast<int*>(scratch + m);
+  double* S = scratch + m + (m + 1) / 2;
+  for (int k = threadIdx.x; k < m; k += blockDim.x) perm[k] = piv[ro + k];
+  __syncthreads();
+  lu_write_outputs<256, false>(work + lu_off[b], m, b, perm, scratch, S, row_off, lu_off, sf_off, nullptr, false,
+                               sf_out, piv, gsrc_out, lperm_out, src_pos, pos_base);
+}
+
 // Principal block A[dofs, dofs] of a CSR matrix into column-major dense
 // storage (dst pre-zeroed). One warp per block row; columns located by
 // binary search in the sorted block index list (extract_submatrix,

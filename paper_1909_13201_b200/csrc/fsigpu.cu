@@ -330,6 +330,13 @@ struct Csr {
 enum BlockMode { kModeLU = 0, kModeInverse = 1, kModeAssembled = 2 };
 static int g_default_mode = kModeAssembled;
 
+// Blocks above 164 rows: blocked LU (default) or the single-CTA in-place
+// kernel (FSIGPU_LU_BIG_OLD=1, A/B).
+static bool lu_big_old() {
+  const char* e = std::getenv("FSIGPU_LU_BIG_OLD");
+  return e && e[0] == '1';
+}
+
 // Register LU with two threads per row for blocks of 33..64 rows: opt-in
 // (FSIGPU_LU_TWO=1). Bit-identical, but the config-1 LU takes 39.2 ms
 // against 30.1 ms with one thread per row: four warps per block make the
@@ -461,6 +468,8 @@ struct Blocks {
   const int* d_cls[kNumCls] = {};
   int cls_max[kNumCls] = {};
   DevBuf<int> fail;
+  DevBuf<double> big_rowmax;  // blocked LU: original row maxima, swapped with their rows
+  DevBuf<int> big_bad;        // blocked LU: per-block singular flag
   void build_classes(cudaStream_t s) {
     for (int c = 0; c < kNumCls; ++c) {
       h_cls[c].clear();
@@ -541,11 +550,33 @@ struct Blocks {
           break;
         }
         default: {
-          const size_t sm = smem_bytes(mx, false);
-          auto k = lu_factor_kernel<256, false>;
-          FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-          k<<<grid, 256, sm, s>>>(bl, m.p, lu_off.p, row_off.p, sf_off.p, src, lu.p, lu.p, sf.p, piv.p, gsrc.p,
-                                  lperm.p, src_pos, pos_base, fail.p);
+          if (lu_big_old()) {
+            const size_t sm = smem_bytes(mx, false);
+            auto k = lu_factor_kernel<256, false>;
+            FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            k<<<grid, 256, sm, s>>>(bl, m.p, lu_off.p, row_off.p, sf_off.p, src, lu.p, lu.p, sf.p, piv.p, gsrc.p,
+                                    lperm.p, src_pos, pos_base, fail.p);
+            break;
+          }
+          // blocked LU in global memory: init, (panel, trailing update) per
+          // 32-column panel for the whole class, then the outputs
+          if (big_rowmax.n < (size_t)total_rows) big_rowmax.alloc((size_t)total_rows);
+          if (big_bad.n < (size_t)grid) big_bad.alloc((size_t)grid);
+          lu_big_init_kernel<<<grid, 256, 0, s>>>(bl, m.p, lu_off.p, row_off.p, src, lu.p, big_rowmax.p, big_bad.p);
+          for (int k0 = 0; k0 < mx; k0 += kBigNB) {
+            lu_big_panel_kernel<<<grid, 256, 0, s>>>(bl, m.p, lu_off.p, row_off.p, lu.p, big_rowmax.p, piv.p,
+                                                     big_bad.p, fail.p, k0);
+            if (k0 + kBigNB < mx) {
+              const int tiles = ceil_div(mx - k0 - kBigNB, kBigTile);
+              lu_big_update_kernel<<<dim3(tiles * tiles, grid), 256, 0, s>>>(bl, m.p, lu_off.p, lu.p, big_bad.p,
+                                                                             k0, tiles);
+            }
+          }
+          const size_t smf = (size_t)(mx + (mx + 1) / 2 + 32 * kTileLd + 8) * 8;
+          FSI_CUDA(cudaFuncSetAttribute(lu_big_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smf));
+          lu_big_finish_kernel<<<grid, 256, smf, s>>>(bl, m.p, lu_off.p, row_off.p, sf_off.p, lu.p, sf.p, piv.p,
+                                                      gsrc.p, lperm.p, src_pos, pos_base, big_bad.p);
         }
       }
       FSI_CHECK_LAUNCH();

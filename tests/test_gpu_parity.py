@@ -211,7 +211,7 @@ def test_bad_cycle_config_rejected(chan):
 def test_block_edge_cases():
     # m = 1, 2, 33 (panel boundary), 64/65 (warp/CTA boundary), 165 (global LU)
     rng = np.random.default_rng(5)
-    sizes = [1, 2, 31, 32, 33, 63, 64, 65, 96, 129, 165, 200]
+    sizes = [1, 2, 31, 32, 33, 63, 64, 65, 96, 129, 165, 200, 300, 513]
     mats = [rng.uniform(-1, 1, (m, m)) for m in sizes]  # non-dominant: pivots
     B = fsigpu.DenseBlocks.from_dense(mats)
     rhs = [rng.uniform(-1, 1, m) for m in sizes]
@@ -264,6 +264,36 @@ def test_small_lu_variants_ties_bitexact(variant, monkeypatch):
     with pytest.raises(fsigpu.SingularBlockError) as e:
         fsigpu.DenseBlocks.from_dense([np.eye(40), np.ones((50, 50))], labels=["ok", "fs-solid-dp-7"])
     assert e.value.label == "fs-solid-dp-7"
+
+
+@pytest.mark.parametrize("variant", ["blocked", "single_cta"])
+def test_large_block_lu_bitexact(variant, monkeypatch):
+    """Blocks above 164 rows (config-4 Vanka patches): the blocked LU
+    (32-column panels, 64x64 trailing tiles) and the single-CTA kernel give
+    DenseFactorization's factors bit for bit, with pivoting, partial panels
+    and tiles, mixed sizes in one batch, and a singular block's label."""
+    monkeypatch.setenv("FSIGPU_LU_BIG_OLD", "1" if variant == "single_cta" else "0")
+    rng = np.random.default_rng(21)
+    sizes = [165, 230, 257, 320, 401]
+    mats = [rng.uniform(-1, 1, (m, m)) for m in sizes]
+    B = fsigpu.DenseBlocks.from_dense(mats)
+    for a, (lu, piv) in zip(mats, B.lu(sizes)):
+        lo, po = O.dense_factor(a)
+        assert np.array_equal(piv, po), f"pivots differ (m={a.shape[0]})"
+        assert np.array_equal(lu, lo), f"LU not bit-identical (m={a.shape[0]})"
+    rhs = rng.uniform(-1, 1, sum(sizes))
+    x = B.solve(rhs)
+    o = 0
+    for a in mats:
+        m = a.shape[0]
+        lo, po = O.dense_factor(a)
+        assert rel(x[o:o + m], O.dense_solve(lo, po, rhs[o:o + m])) <= 1e-12
+        o += m
+    sing = rng.uniform(-1, 1, (200, 200))
+    sing[:, 7] = 0.0
+    with pytest.raises(fsigpu.SingularBlockError) as e:
+        fsigpu.DenseBlocks.from_dense([mats[0], sing], labels=["ok", "as-vanka-9"])
+    assert e.value.label == "as-vanka-9"
 
 
 def test_singular_block_label():
