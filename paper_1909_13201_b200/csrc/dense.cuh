@@ -1294,7 +1294,7 @@ __global__ void __launch_bounds__(256, 2) lu_big_panel_kernel(const int* __restr
 
 // A22 -= L21 * U12 for panel k0 (full panels only: the last, partial panel
 // has no trailing block). grid = (tiles_r * tiles_c, blocks).
-__global__ void __launch_bounds__(256) lu_big_update_kernel(const int* __restrict__ blist,
+__global__ void __launch_bounds__(256, 3) lu_big_update_kernel(const int* __restrict__ blist,
                                                             const int* __restrict__ msz,
                                                             const long long* __restrict__ lu_off, double* work,
                                                             const int* __restrict__ bad, int k0, int tiles_c) {
@@ -1317,38 +1317,35 @@ __global__ void __launch_bounds__(256) lu_big_update_kernel(const int* __restric
     Us[k][j] = c0 + j < m ? A[(size_t)(c0 + j) * m + k0 + k] : 0.0;
   }
   __syncthreads();
-  const int tx = t & 15, ty = t >> 4;  // 4x4 entries per thread: rows ty*4.., cols tx*4..
-  double acc[4][4];
+  // thread = one row x 16 columns of the tile: the 32 rows of a warp are
+  // consecutive (coalesced column-major loads/stores of A22), the warp's
+  // U12 reads are broadcasts, its L21 reads conflict-free
+  const int ri = t & (kBigTile - 1), cg = t / kBigTile;  // row, 16-column group
+  const int r = r0 + ri;
+  constexpr int TC = kBigTile / 4;
+  double acc[TC];
 #pragma unroll
-  for (int jj = 0; jj < 4; ++jj) {
-    const int c = c0 + tx * 4 + jj;
-#pragma unroll
-    for (int ii = 0; ii < 4; ++ii) {
-      const int r = r0 + ty * 4 + ii;
-      acc[ii][jj] = (r < m && c < m) ? A[(size_t)c * m + r] : 0.0;
-    }
+  for (int jj = 0; jj < TC; ++jj) {
+    const int c = c0 + cg * TC + jj;
+    acc[jj] = (r < m && c < m) ? A[(size_t)c * m + r] : 0.0;
   }
 #pragma unroll 4
   for (int k = 0; k < kBigNB; ++k) {
-    const double2 l01 = *reinterpret_cast<const double2*>(&Ls[k][ty * 4]);
-    const double2 l23 = *reinterpret_cast<const double2*>(&Ls[k][ty * 4 + 2]);
-    const double2 u01 = *reinterpret_cast<const double2*>(&Us[k][tx * 4]);
-    const double2 u23 = *reinterpret_cast<const double2*>(&Us[k][tx * 4 + 2]);
-    const double l[4] = {l01.x, l01.y, l23.x, l23.y};
-    const double u[4] = {u01.x, u01.y, u23.x, u23.y};
+    const double l = Ls[k][ri];
+    double u[TC];
 #pragma unroll
-    for (int ii = 0; ii < 4; ++ii)
+    for (int q = 0; q < TC; q += 2) {
+      const double2 uu = *reinterpret_cast<const double2*>(&Us[k][cg * TC + q]);
+      u[q] = uu.x;
+      u[q + 1] = uu.y;
+    }
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = sub_rn(acc[ii][jj], mul_rn(l[ii], u[jj]));
+    for (int jj = 0; jj < TC; ++jj) acc[jj] = sub_rn(acc[jj], mul_rn(l, u[jj]));
   }
 #pragma unroll
-  for (int jj = 0; jj < 4; ++jj) {
-    const int c = c0 + tx * 4 + jj;
-#pragma unroll
-    for (int ii = 0; ii < 4; ++ii) {
-      const int r = r0 + ty * 4 + ii;
-      if (r < m && c < m) A[(size_t)c * m + r] = acc[ii][jj];
-    }
+  for (int jj = 0; jj < TC; ++jj) {
+    const int c = c0 + cg * TC + jj;
+    if (r < m && c < m) A[(size_t)c * m + r] = acc[jj];
   }
 }
 
