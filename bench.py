@@ -278,7 +278,7 @@ def run_ours(args, ws, rank, local):
     # sensitivity studies only; 0 by default)
     _pad = torch.empty(int(os.environ.get("FSI_PAD_MB", "0")) * (1 << 20), dtype=torch.uint8, device="cuda")
     t0 = time.time()
-    G = fsigpu.GmgPreconditioner(P.levels)
+    G = fsigpu.GmgPreconditioner(P.levels, fsigpu.CycleConfig(smoother=args.level_smoother))
     S = fsigpu.GmresSolver(G, P.frame_scale, restart=30)
     torch.cuda.synchronize()
     setup_s = time.time() - t0
@@ -401,7 +401,8 @@ def run_ours(args, ws, rank, local):
         "data": "synthetic (reference-assembled rest-state FSI Jacobian, seeded uniform RHS; fixtures from oracle/_ref)",
         "config": {"workload": {"cfg0": WORKLOAD, "cfg2": WORKLOAD_CFG2}.get(args.config, WORKLOAD_CFG2FULL),
                    "n_dofs": n,
-                   "max_iters": max_iters, "smoother": args.smoother, "nnz_fine": P.levels[-1].A.nnz,
+                   "max_iters": max_iters, "smoother": args.smoother,
+                   "level_smoother": args.level_smoother, "nnz_fine": P.levels[-1].A.nnz,
                    "parallelism": "replicas" if ws > 1 else "single", "l2": "flushed (256 MB write) between timed solves",
                    "restart": 30, "rel_tol": 1e-10, "cuda_graphs": "conditional WHILE per restart cycle"},
         "solve_ms": ms, "iterations": int(statistics.median(its)), "v_cycles_per_solve": vcyc_per_step,
@@ -462,6 +463,9 @@ def main():
     ap.add_argument("--no-microbench", action="store_true")
     ap.add_argument("--config", choices=["cfg0", "cfg2", "cfg2full"], default="cfg0")
     ap.add_argument("--smoother", choices=["fs", "as"], default="fs")
+    # sweep around the FS/AS smoother: the reference's damped Richardson
+    # (default) or the GMRES(1) step BASELINE configs[0] names
+    ap.add_argument("--level-smoother", choices=["richardson", "gmres1"], default="richardson")
     ap.add_argument("--max-iters", type=int, default=0)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

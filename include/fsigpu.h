@@ -138,6 +138,15 @@ int fsigpu_set_pdl(int enable);
 int fsigpu_set_stage_cap(int cap);
 long long fsigpu_gmg_persist_bytes(fsigpu_gmg g);
 
+/* Level smoother of every smoothed level: 0 = damped Richardson with the
+ * create() omega (reference richardson_smooth, src/precond.cpp:305-317; the
+ * default), 1 = GMRES(1) minimal-residual step  x += alpha FS(b - A x),
+ * alpha = (w.r)/(w.w), w = A FS r  (BASELINE.json configs[0] "1 pre- and 1
+ * post-step GMRES(1)"; not in the reference). GMRES(1) makes the
+ * V-cycle non-linear: use it under the flexible device solver
+ * (fsigpu_gmres_*). Invalidates graphs captured by existing solvers. */
+int fsigpu_gmg_set_smoother(fsigpu_gmg g, int kind);
+
 /* ---- GMG with additive FS smoothers: GmgPreconditioner (gmg.cpp:178-246),
  *      FsPreconditioner (precond.cpp:119-303, additive per SURVEY §8c),
  *      richardson_smooth (precond.cpp:305-317) ---------------------------- */

@@ -61,6 +61,9 @@ orc_gmg* orc_gmg_create(int n_levels, const orc_level_desc* levels, double omega
 void orc_gmg_destroy(orc_gmg* g);
 /* 'v' (default), 'w' or 'f' (gmg.cpp:215-229) */
 void orc_gmg_set_cycle(orc_gmg* g, char mode);
+/* level smoother: 0 damped Richardson (precond.cpp:305-317, default),
+ * 1 GMRES(1) minimal-residual step (BASELINE configs[0]) */
+void orc_gmg_set_smoother(orc_gmg* g, int kind);
 /* additive FS apply on level l >= 1 (SURVEY §8c recipe) */
 void orc_fs_apply(const orc_gmg* g, int level, const double* r, double* z);
 /* one V-cycle from a zero guess (gmg.cpp:188-246) */
@@ -75,6 +78,12 @@ int orc_gmres(const orc_gmg* g, const double* frame_scale, const double* b, int 
               int max_iters, double rel_tol, double abs_tol, double* x, double* history,
               int* n_history, int* iterations, int* converged, int* breakdown,
               long long* m_applies);
+
+/* Flexible GMRES on the same operators (keeps Z = M V; x += Z y at restart) */
+int orc_fgmres(const orc_gmg* g, const double* frame_scale, const double* b, int restart,
+               int max_iters, double rel_tol, double abs_tol, double* x, double* history,
+               int* n_history, int* iterations, int* converged, int* breakdown,
+               long long* m_applies);
 
 #ifdef __cplusplus
 }

@@ -40,6 +40,9 @@ def lib():
                                 C.POINTER(ip), C.POINTER(ip), C.POINTER(ip), C.POINTER(ip),
                                 C.POINTER(C.c_longlong)]
         L.orc_gmres.restype = ip
+        L.orc_fgmres.argtypes = L.orc_gmres.argtypes
+        L.orc_fgmres.restype = ip
+        L.orc_gmg_set_smoother.argtypes = [vp, ip]
         _lib = L
     return _lib
 
@@ -86,7 +89,9 @@ def extract_block(A, dofs):
 class OracleGmg:
     """GmgPreconditioner with additive FS smoothers (CPU restatement)."""
 
-    def __init__(self, levels: List, omega=0.7, pre=1, post=1, cycle="v"):
+    SMOOTHERS = {"richardson": 0, "gmres1": 1}
+
+    def __init__(self, levels: List, omega=0.7, pre=1, post=1, cycle="v", smoother="richardson"):
         from paper_1909_13201_b200.problem import level_descs
         self.levels = levels
         self._descs = level_descs(levels)
@@ -97,6 +102,7 @@ class OracleGmg:
             raise ZeroDivisionError(f"singular block: level {el.value} block {eb.value}")
         self.h = h
         lib().orc_gmg_set_cycle(h, cycle.encode()[:1])
+        lib().orc_gmg_set_smoother(h, self.SMOOTHERS[smoother])
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -121,14 +127,16 @@ class OracleGmg:
         lib().orc_coarse_solve(self.h, b.ctypes.data, x.ctypes.data)
         return x
 
-    def gmres(self, frame_scale, b, restart=30, max_iters=2000, rel_tol=1e-10, abs_tol=1e-300):
+    def gmres(self, frame_scale, b, restart=30, max_iters=2000, rel_tol=1e-10, abs_tol=1e-300,
+              flexible=False):
         n = len(b)
         b, fsc = _d(b), _d(frame_scale)
         x = np.empty(n)
         hist = np.empty(max_iters + 2)
         nh, it, cv, bk = C.c_int(), C.c_int(), C.c_int(), C.c_int()
         ma = C.c_longlong()
-        rc = lib().orc_gmres(self.h, fsc.ctypes.data, b.ctypes.data, restart, max_iters, rel_tol,
+        fn = lib().orc_fgmres if flexible else lib().orc_gmres
+        rc = fn(self.h, fsc.ctypes.data, b.ctypes.data, restart, max_iters, rel_tol,
                              abs_tol, x.ctypes.data, hist.ctypes.data, C.byref(nh), C.byref(it),
                              C.byref(cv), C.byref(bk), C.byref(ma))
         if rc:

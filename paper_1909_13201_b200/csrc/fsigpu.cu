@@ -28,6 +28,7 @@
 #include "krylov.cuh"
 #include "mega.cuh"
 #include "sparse.cuh"
+#include "mr.cuh"
 
 namespace fsigpu {
 
@@ -738,6 +739,7 @@ struct Level {
   DevBuf<int> aus_ptr, aus_col;
   DevBuf<double> aus_val;
   DevBuf<double> delta, bbuf, xbuf, rbuf;
+  DevBuf<double> mr_z, mr_w;  // GMRES(1) smoother: z = FS r, w = A z
   bool assembled = false;  // FS smoother as one sparse operator (kModeAssembled)
   Csr FS;
   Csr AP;  // A * diag(!col_mask) * P : fused prolongation + post-smoothing residual
@@ -783,6 +785,13 @@ struct Gmg {
   double omega = 0.7;
   int pre = 1, post = 1;
   char cyc = 'v';
+  // level smoother: 0 damped Richardson (precond.cpp:305-317), 1 GMRES(1)
+  // minimal-residual step (mr.cuh); `version` bumps on every change so a
+  // solver's captured graphs are rebuilt
+  int smoother = 0;
+  int version = 0;
+  DevBuf<double> mr_part, mr_alpha;
+  DevBuf<unsigned int> mr_ticket;
   DevBuf<double> coarse_inv;  // equilibrated explicit inverse, row-major
   cudaStream_t s = nullptr;
   DevBuf<double> tmp_in, tmp_out;
@@ -828,10 +837,68 @@ struct Gmg {
     else
       L.FS.launch(GatherPlain{r}, EpiAxpy{omega, L.x}, s);
   }
+  void set_smoother(int kind) {
+    if (kind == 1 && !mr_part.p) {
+      mr_part.alloc(2 * kMrCtas);
+      mr_alpha.alloc(1);
+      mr_ticket.alloc(1);
+      FSI_CUDA(cudaMemsetAsync(mr_ticket.p, 0, sizeof(unsigned int), s));
+      for (size_t l = 1; l < lv.size(); ++l) {
+        lv[l].mr_z.alloc(lv[l].n);
+        lv[l].mr_w.alloc(lv[l].n);
+      }
+      FSI_CUDA(cudaStreamSynchronize(s));
+    }
+    smoother = kind;
+    ++version;
+  }
+  // z = FS r (the additive FS smoother applied once, no damping)
+  void fs_into(int l, const double* r, double* z) {
+    Level& L = lv[l];
+    if (L.assembled) {
+      ProfScope ps(FSIGPU_K_BLOCK_SOLVE, L.FS.bytes(false), s);
+      L.FS.launch(GatherPlain{r}, EpiSetScaled{1.0, z}, s);
+      return;
+    }
+    smooth_solve(l, r);
+    ProfScope ps(FSIGPU_K_COMBINE, L.combine_bytes, s);
+    launch_k(fs_combine_kernel, dim3(ceil_div(L.n, 256)), dim3(256), 0, s, L.n, L.g1, L.n_us,
+             (const int*)L.inv_ptr.p, (const int*)L.inv_idx.p, (const double*)L.delta.p, r,
+             (const double*)L.lumped.p, 1.0, z, 1);
+    FSI_CHECK_LAUNCH();
+    counted();
+  }
+  // one GMRES(1) sweep (mr.cuh): r = b - A x, z = FS r, w = A z,
+  // alpha = (w.r)/(w.w), x += alpha z
+  void mr_sweep(int l, int x_zero, bool r_ready, bool mask_out) {
+    Level& L = lv[l];
+    const double* r = L.b;  // x == 0: r = b exactly (precond.cpp:312-313)
+    if (!x_zero) {
+      if (!r_ready) resid(l, L.rbuf.p);
+      r = L.rbuf.p;
+    }
+    fs_into(l, r, L.mr_z.p);
+    {
+      ProfScope ps(FSIGPU_K_SPMV, L.A.bytes(false), s);
+      L.A.launch(GatherPlain{L.mr_z.p}, EpiPlain{L.mr_w.p}, s);
+    }
+    ProfScope ps(FSIGPU_K_COMBINE, 32.0 * L.n, s);
+    launch_k(k_mr_alpha, dim3(kMrCtas), dim3(kMrThreads), 0, s, L.n, (const double*)L.mr_w.p, r, mr_part.p,
+             mr_ticket.p, mr_alpha.p);
+    FSI_CHECK_LAUNCH();
+    launch_k(k_mr_update, dim3(ceil_div(L.n, 256)), dim3(256), 0, s, L.n, (const double*)mr_alpha.p,
+             (const double*)L.mr_z.p, L.x, x_zero, (const unsigned char*)(mask_out ? L.cmask.p : nullptr));
+    FSI_CHECK_LAUNCH();
+    counted(2);
+  }
   // one FS-preconditioned Richardson sweep; x_zero: x == 0 on entry;
   // r_ready: rbuf already holds b - A x (fused prolongation kernel)
   void sweep(int l, int x_zero, bool r_ready = false, bool mask_out = false) {
     Level& L = lv[l];
+    if (smoother == 1) {
+      mr_sweep(l, x_zero, r_ready, mask_out);
+      return;
+    }
     if (L.assembled) {
       if (x_zero) {
         fs_spmv(l, L.b, 1);  // res = b - A*0 = b (precond.cpp:312-313)
@@ -888,8 +955,9 @@ struct Gmg {
       L.R.launch(GatherPlain{L.rbuf.p}, EpiRestrict{B.rmask.p, B.b}, s);
     }
     // the last visit of level l-1 masks its output iff that level ends in a
-    // kernel that can (a post sweep of an assembled level, or the coarse GEMV)
-    const bool fused_mask = L.AP.rows && post > 0 && (l - 1 == 0 || (B.assembled && post > 0));
+    // kernel that can (a post sweep of an assembled level or of the GMRES(1)
+    // smoother, or the coarse GEMV)
+    const bool fused_mask = L.AP.rows && post > 0 && (l - 1 == 0 || ((B.assembled || smoother == 1) && post > 0));
     switch (mode) {
       case 'v': cycle(l - 1, 'v', 1, fused_mask); break;
       case 'w': cycle(l - 1, 'w', 1); cycle(l - 1, 'w', 0, fused_mask); break;
@@ -1043,6 +1111,19 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
   require(d.nc == g.lv[l - 1].n, "gmg: transfer size does not match the coarser level");
   L.P.create(d.n, d.nc, d.p_ptr, d.p_idx, d.p_val, s);
   L.R.create(d.nc, d.n, d.r_ptr, d.r_idx, d.r_val, s);
+  // restriction rows are short (~14 entries): on large coarse levels paired
+  // 16-byte loads with two lanes per row hold a whole row in one batch. Cold
+  // sweeps on config 2 (profiles/r01_tune_restrict_cfg2.txt): 313k rows
+  // 30.7 -> 24.4 us, 78k rows 13.9 -> 12.1; 20k rows: 8 lanes, batch 8.
+  if (!std::getenv("FSIGPU_SPMV_PAIR")) {
+    if (d.nc >= 65536) {
+      L.R.lpr = 2;
+      L.R.unroll = 24;
+    } else if (d.nc >= 16384) {
+      L.R.lpr = 8;
+      L.R.unroll = 8;
+    }
+  }
   {
     // AP_m = A * diag(!col_mask) * P (Gustavson, sorted rows)
     std::vector<int> app(d.n + 1, 0), api;
@@ -1290,6 +1371,7 @@ struct Gmres {
   int hist_cap = 0;
   cudaGraphExec_t cycle_exec = nullptr;
   cudaGraph_t cycle_graph = nullptr;
+  int graph_version = -1;  // Gmg::version the graph was captured at
   // persistent cooperative restart-cycle kernel (inverse-mode V-cycles)
   bool mega = false;
   bool force_mega = false;
@@ -1421,7 +1503,7 @@ struct Gmres {
 
   void setup_mega() {
     Gmg& G = *g;
-    mega = G.cyc == 'v' && (int)G.lv.size() <= kMegaMaxLevels && G.lv.size() >= 2;
+    mega = G.cyc == 'v' && G.smoother == 0 && (int)G.lv.size() <= kMegaMaxLevels && G.lv.size() >= 2;
     for (size_t l = 1; l < G.lv.size(); ++l) mega = mega && G.lv[l].blocks.mode == kModeInverse;
     // opt-in (measured slower than the graph path on config 0: its phases
     // are latency-bound at 2 CTAs/SM)
@@ -1534,7 +1616,7 @@ struct Gmres {
     h0.rel_tol = rel_tol;
     h0.abs_tol = abs_tol;
     FSI_CUDA(cudaMemcpyAsync(st.p, &h0, sizeof(KState), cudaMemcpyHostToDevice, s));
-    if (mega && !g_prof.on) {
+    if (mega && g->smoother == 0 && !g_prof.on) {
       launch_mega(1);
       KState h = read_state();
       check_bar();
@@ -1560,7 +1642,16 @@ struct Gmres {
     KState h = read_state();
     long long cycles = 0;
     const bool use_graph = graphs && !g_prof.on;
-    if (use_graph && !cycle_exec) build_graph();
+    if (cycle_exec && graph_version != g->version) {
+      cudaGraphExecDestroy(cycle_exec);
+      cudaGraphDestroy(cycle_graph);
+      cycle_exec = nullptr;
+      cycle_graph = nullptr;
+    }
+    if (use_graph && !cycle_exec) {
+      build_graph();
+      graph_version = g->version;
+    }
     while (!h.converged && h.its < max_iters) {
       const int its_before = h.its;
       if (use_graph) {
@@ -1651,6 +1742,15 @@ int fsigpu_gmg_set_launch(fsigpu_gmg h, int level, int which, int lpr, int unrol
     Csr* c = which == 0 ? &L.A : which == 1 ? &L.FS : which == 2 ? &L.AP : which == 3 ? &L.P : &L.R;
     c->lpr = lpr;
     c->unroll = unroll;
+  });
+}
+// Level smoother: 0 damped Richardson (the reference's richardson_smooth,
+// precond.cpp:305-317), 1 GMRES(1) minimal-residual step (mr.cuh).
+int fsigpu_gmg_set_smoother(fsigpu_gmg h, int kind) {
+  return guarded([&] {
+    require(h != nullptr, "gmg: null");
+    require(kind == 0 || kind == 1, "smoother must be 0 (richardson) or 1 (gmres1)");
+    h->g.set_smoother(kind);
   });
 }
 int fsigpu_gmg_set_staging(fsigpu_gmg h, int level, int which, int cap) {

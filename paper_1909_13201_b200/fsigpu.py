@@ -108,6 +108,7 @@ def lib():
             "fsigpu_coarse_solve": ([vp, vp, vp], ip),
             "fsigpu_gmg_destroy": ([vp], None),
             "fsigpu_gmg_set_launch": ([vp, ip, ip, ip, ip], ip),
+            "fsigpu_gmg_set_smoother": ([vp, ip], ip),
             "fsigpu_gmg_set_staging": ([vp, ip, ip, ip], ip),
             "fsigpu_set_stage_cap": ([ip], ip),
             "fsigpu_gmg_time_kernel": ([vp, ip, ip, ip, ip, C.POINTER(d), C.POINTER(d)], ip),
@@ -281,6 +282,9 @@ class CycleConfig:
     pre: int = 1
     post: int = 1
     omega: float = 0.7
+    # "richardson" (precond.cpp:305-317) or "gmres1" (minimal-residual step,
+    # BASELINE configs[0]; non-linear, use under the flexible device solver)
+    smoother: str = "richardson"
 
 
 class GmgPreconditioner:
@@ -300,6 +304,13 @@ class GmgPreconditioner:
         _check(rc)
         self.h = h
         self.n = levels[-1].n
+        if cfg.smoother != "richardson":
+            self.set_smoother(cfg.smoother)
+
+    SMOOTHERS = {"richardson": 0, "gmres1": 1}
+
+    def set_smoother(self, kind: str):
+        _check(lib().fsigpu_gmg_set_smoother(self.h, self.SMOOTHERS[kind]))
 
     def size(self) -> int:
         return self.n

@@ -499,3 +499,61 @@ def test_staged_spmv_opt_in(cfg0):
     assert abs(res.iterations - int(g["gmres_add/iterations"][0])) <= 1
     with pytest.raises(ValueError):
         G.set_staging(1, "FS", -5)
+
+
+# ---------------------------------------------------------------- GMRES(1) smoother
+@pytest.fixture(scope="module")
+def cfg0_mr_oracle(cfg0):
+    OG = O.OracleGmg(cfg0.levels, smoother="gmres1")
+    r = cfg0.golden["golden/vcycle_r"]
+    f = OG.gmres(cfg0.frame_scale, cfg0.b, restart=30, max_iters=400, rel_tol=1e-10, flexible=True)
+    return OG.apply(r), f
+
+
+@MODES
+def test_gmres1_smoother_cfg0(cfg0, cfg0_mr_oracle, mode):
+    """GMRES(1) level smoother (BASELINE configs[0]) against the oracle
+    restatement: one V-cycle within 1e-9, FGMRES iterations within +-1 and
+    the final relative residual within 1e-8 of the oracle's FGMRES."""
+    fsigpu.set_block_mode(mode)
+    try:
+        G = fsigpu.GmgPreconditioner(cfg0.levels, fsigpu.CycleConfig(smoother="gmres1"))
+    finally:
+        fsigpu.set_block_mode(fsigpu.MODE_ASSEMBLED)
+    z_ref, f = cfg0_mr_oracle
+    assert rel(G.apply(cfg0.golden["golden/vcycle_r"]), z_ref) <= 1e-9
+    cfg = fsigpu.KrylovConfig(restart=30, max_iters=400, rel_tol=1e-10, abs_tol=1e-300)
+    res = fsigpu.gmres(G, cfg0.frame_scale, cfg0.b, cfg)
+    assert res.converged
+    assert abs(res.iterations - f["iterations"]) <= 1, (res.iterations, f["iterations"])
+    ref_rel = f["history"][-1] / f["history"][0]
+    assert abs(res.true_residual / res.history[0] - ref_rel) <= 1e-8
+
+
+@pytest.mark.parametrize("cycle,pre,post", [("v", 2, 1), ("w", 1, 1), ("f", 1, 2), ("v", 0, 1), ("v", 1, 0)])
+def test_gmres1_smoother_cycle_shapes(chan, cycle, pre, post):
+    cfg = fsigpu.CycleConfig(cycle=cycle, pre=pre, post=post, smoother="gmres1")
+    G = fsigpu.GmgPreconditioner(chan.levels, cfg)
+    OG = O.OracleGmg(chan.levels, cycle=cycle, pre=pre, post=post, smoother="gmres1")
+    r = chan.golden["golden/vcycle_r"]
+    assert rel(G.apply(r), OG.apply(r)) <= 1e-9
+    # alpha = 0 when w = 0: zero residual -> zero correction
+    assert not np.any(G.apply(np.zeros_like(r)))
+
+
+def test_smoother_switch_rebuilds_solver_graph(chan):
+    """Switching the smoother after a solver captured its restart-cycle graph
+    re-captures it (Gmg::version), in both directions."""
+    G = fsigpu.GmgPreconditioner(chan.levels)
+    cfg = fsigpu.KrylovConfig(restart=30, max_iters=300, rel_tol=1e-8, abs_tol=1e-300)
+    S = fsigpu.GmresSolver(G, chan.frame_scale, restart=30)
+    a = S.solve(chan.b, cfg)
+    G.set_smoother("gmres1")
+    b = S.solve(chan.b, cfg)
+    G.set_smoother("richardson")
+    c = S.solve(chan.b, cfg)
+    assert a.iterations == c.iterations and np.array_equal(a.x, c.x)
+    assert b.iterations != a.iterations
+    assert fsigpu.lib().fsigpu_gmg_set_smoother(G.h, 7) != 0
+    with pytest.raises(KeyError):
+        G.set_smoother("bogus")

@@ -179,3 +179,57 @@ def test_as_smoother_chan_matches_reference(chan_as):
     r = G.gmres(chan_as.frame_scale, chan_as.b, restart=30, max_iters=300, rel_tol=1e-8)
     assert r["iterations"] == int(g["gmres_add/iterations"][0])
     assert rel(r["x"], g["gmres_add/x"]) <= 1e-9
+
+
+# ---- FGMRES and the GMRES(1) smoother (BASELINE configs[0])
+def test_fgmres_equals_gmres_for_linear_smoother(chan):
+    """For the linear Richardson V-cycle the flexible variant is the same
+    method: same iteration count, iterate to rounding."""
+    G = O.OracleGmg(chan.levels)
+    a = G.gmres(chan.frame_scale, chan.b, restart=30, max_iters=300, rel_tol=1e-8)
+    f = G.gmres(chan.frame_scale, chan.b, restart=30, max_iters=300, rel_tol=1e-8, flexible=True)
+    assert abs(a["iterations"] - f["iterations"]) <= 1
+    assert f["converged"]
+    # one M apply per Arnoldi step only (no restart-end M(Vy))
+    assert f["m_applies"] == f["iterations"]
+    assert rel(f["x"], a["x"]) <= 1e-8
+
+
+def test_gmres1_smoother_properties(chan, cfg0):
+    """GMRES(1) smoothing is homogeneous of degree 1 (alpha is scale
+    invariant: exactly so for a power-of-two scale) but not additive, and
+    FGMRES converges with it on config 0 (197 iterations; Richardson: 103).
+    On the SI-unit channel it stagnates (relres ~0.5 after 300 its)."""
+    G = O.OracleGmg(chan.levels, smoother="gmres1")
+    r = chan.golden["golden/vcycle_r"]
+    z = G.apply(r)
+    assert np.array_equal(G.apply(4.0 * r), 4.0 * z)
+    rng = np.random.default_rng(7)
+    r2 = rng.uniform(-1, 1, len(r)) * (np.abs(r) > 0)
+    assert rel(G.apply(r + r2), z + G.apply(r2)) > 1e-6
+    # zero input -> zero output (alpha = 0 when w = 0)
+    assert not np.any(G.apply(np.zeros_like(r)))
+    G0 = O.OracleGmg(cfg0.levels, smoother="gmres1")
+    f = G0.gmres(cfg0.frame_scale, cfg0.b, restart=30, max_iters=400, rel_tol=1e-10, flexible=True)
+    assert f["converged"] and 150 <= f["iterations"] <= 250, f["iterations"]
+
+
+def test_gmres1_step_minimises_level_residual(chan):
+    """One GMRES(1) pre-smoothing step from x = 0 (pre=1, post=0 on a
+    2-level hierarchy) never increases the level residual norm, and does no
+    worse than the damped Richardson step."""
+    lv = chan.levels
+    top = lv[-1]
+    r = chan.golden["golden/vcycle_r"]
+    A = top.A.to_scipy()
+    Gm = O.OracleGmg(lv, smoother="gmres1")
+    Gr = O.OracleGmg(lv)
+    z_fs = Gr.fs_apply(len(lv) - 1, r)
+    w = A @ z_fs
+    alpha = (w @ r) / (w @ w)
+    # closed form of the minimal-residual step vs Richardson omega = 0.7
+    res_mr = np.linalg.norm(r - alpha * w)
+    res_rich = np.linalg.norm(r - 0.7 * w)
+    assert res_mr <= np.linalg.norm(r)
+    assert res_mr <= res_rich * (1 + 1e-12)
+    del Gm

@@ -1,7 +1,7 @@
 """Sweep SpMV launch shapes (lanes per row x batch depth) on one hierarchy.
 
 usage: tune_spmv.py [data.fsix] [level ...]   (default: every level >= 1)
-FSI_WARM=1 times back-to-back launches (L2-resident, the in-solve regime of
+FSI_WHICH=A,R limits the sweep to those matrices. FSI_WARM=1 times back-to-back launches (L2-resident, the in-solve regime of
 small hierarchies) instead of launches after an L2 flush.
 """
 import os, sys
@@ -17,7 +17,11 @@ levels = [int(a) for a in sys.argv[2:]] or list(range(1, len(P.levels)))
 cold = os.environ.get("FSI_WARM", "0") != "1"
 for lev in levels:
     L = P.levels[lev]
-    for which, kname in [("A", "residual"), ("FS", "fs_smoother"), ("AP", "prolong_resid")]:
+    kinds = [("A", "residual"), ("FS", "fs_smoother"), ("AP", "prolong_resid"), ("R", "restrict")]
+    only = os.environ.get("FSI_WHICH")
+    for which, kname in kinds:
+        if only and which not in only.split(","):
+            continue
         best, default = None, None
         default = G.time_kernel(kname, lev, reps=10, cold=cold)[0]
         for lpr in [2, 4, 8, 16, 32]:
@@ -26,6 +30,6 @@ for lev in levels:
                 ms, by = G.time_kernel(kname, lev, reps=10, cold=cold)
                 if best is None or ms < best[0]:
                     best = (ms, lpr, u, by)
-        print(f"L{lev} n={L.n:8d} nnz/row={L.A.nnz / L.n:5.1f} {which:3s} default {default*1000:8.2f} us  best lpr={best[1]:2d} u={best[2]} "
+        print(f"L{lev} n={L.n:8d} nnz/row={(L.R.nnz / L.R.rows if which == "R" else L.A.nnz / L.n):5.1f} {which:3s} default {default*1000:8.2f} us  best lpr={best[1]:2d} u={best[2]} "
               f"{best[0]*1000:8.2f} us {best[3]/best[0]/1e6:7.0f} GB/s", flush=True)
         G.set_launch(lev, which, best[1], best[2])
