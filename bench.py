@@ -375,6 +375,14 @@ def run_ours(args, ws, rank, local):
     torch.cuda.synchronize()
     fsigpu.Profile.enable(False)
     cls = {k: v for k, v in fsigpu.Profile.read().items() if v["launches"]}
+    per_level = {}
+    for k in cls:
+        for lvl in range(-1, top + 1):
+            v = fsigpu.Profile.read_level(k, lvl)
+            if v["launches"]:
+                per_level[f"{k}@L{lvl}"] = {"avg_launch_us": 1000.0 * v["ms"] / v["launches"],
+                                            "launches": v["launches"],
+                                            "GBps": v["bytes"] / v["ms"] / 1e6 if v["ms"] > 0 else None}
     insolve = {k: {"ms_total": v["ms"], "launches": v["launches"], "avg_launch_us": 1000.0 * v["ms"] / v["launches"],
                    "bytes_per_launch": v["bytes"] / v["launches"], "GBps": v["bytes"] / v["ms"] / 1e6}
                for k, v in cls.items()}
@@ -388,6 +396,13 @@ def run_ours(args, ws, rank, local):
     per_launch_ms = kt[dom]["ms_cold"]
     achieved = per_launch_bytes / per_launch_ms / 1e6  # GB/s
     share = kt[dom]["ms_cold"] * kt[dom]["per_vcycle"] / sum(v["ms_cold"] * v["per_vcycle"] for v in kt.values())
+    # the same kernel inside the instrumented solve (FS smoother SpMVs are
+    # the block_solve class of their level in the default assembled mode)
+    insolve_dom = None
+    if dom.startswith("fs_smoother@"):
+        v = per_level.get("block_solve@" + dom.split("@")[1])
+        insolve_dom = per_launch_bytes / (v["avg_launch_us"] * 1e3) if v else None  # GB/s
+    achieved_main = insolve_dom if insolve_dom else achieved
     traffic = None
     ncu_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(ncu_path):
@@ -410,16 +425,24 @@ def run_ours(args, ws, rank, local):
         "gpu_launches": launches,
         "e2e": {"value": e2e_value, "unit": "V-cycles/s", "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n + 8 * (r2.iterations + 1), "ms_per_step": e2e_step},
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved_main, "peak": hbm_peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved_main / hbm_peak,
                      "traffic": traffic, "algorithmic_bytes_per_launch": per_launch_bytes,
-                     "avg_launch_us": per_launch_ms * 1000.0, "share_of_vcycle_kernel_time": share,
+                     "avg_launch_us": per_launch_bytes / achieved_main / 1000.0,
+                     "share_of_vcycle_kernel_time": share,
+                     "achieved_cold": achieved, "frac_cold": achieved / hbm_peak,
+                     "avg_launch_us_cold": per_launch_ms * 1000.0,
                      "achieved_warm": per_launch_bytes / kt[dom]["ms_warm"] / 1e6,
                      "frac_warm": per_launch_bytes / kt[dom]["ms_warm"] / 1e6 / hbm_peak,
-                     "timing": "dominant V-cycle kernel timed alone: CUDA events per launch on the library stream, "
-                               "256 MB L2 flush before each (achieved) or back to back (achieved_warm); bytes = "
-                               "algorithmic bytes per launch (DESIGN 3.6)"},
+                     "achieved_insolve": insolve_dom,
+                     "frac_insolve": insolve_dom / hbm_peak if insolve_dom else None,
+                     "timing": "achieved: the dominant V-cycle kernel's launches inside a full solve (graphs off, "
+                               "CUDA events around each launch on the library stream, launch gaps included; "
+                               "the cold-timed value when the kernel has no in-solve class); achieved_cold / "
+                               "achieved_warm: the same kernel timed alone per launch after a 256 MB L2 flush / "
+                               "back to back; bytes = algorithmic bytes per launch (DESIGN 3.6)"},
         "insolve_kernel_classes": insolve,
+        "insolve_per_level": per_level,
         "insolve_timing": "one instrumented solve after the timed region, graphs off, CUDA events around every launch "
                           "(includes launch gaps; per kernel class)",
         "kernel_roofline": kt,

@@ -208,6 +208,8 @@ void fsigpu_gmres_destroy(fsigpu_gmres s);
 #define FSIGPU_K_COUNT 6
 int fsigpu_profile_enable(int enable);
 int fsigpu_profile_read(double* ms, long long* launches, double* bytes);
+/* the same sums restricted to one GMG level (-1: launches outside a cycle) */
+int fsigpu_profile_read_level(int cls, int level, double* ms, long long* launches, double* bytes);
 int fsigpu_profile_reset(void);
 
 #ifdef __cplusplus

@@ -1292,6 +1292,151 @@ __global__ void __launch_bounds__(256, 2) lu_big_panel_kernel(const int* __restr
   }
 }
 
+// Shared-memory panel variant of lu_big_panel_kernel (default for m <= 880):
+// rows k0..m-1 of the panel's kb columns are staged in dynamic shared memory
+// (column-major, ld = m - k0; 200 KB at m = 780), so the 32 pivot steps
+// (search, swap, scale, rank-1 update of the panel) run out of shared memory
+// instead of making L2 round trips per column. The row swaps of the columns
+// outside the panel are deferred to the end of the panel and applied in k
+// order (no other column is read or written in between, so the result is
+// the same as swapping whole rows immediately); U12 then reads L11 from
+// shared memory. Same rounded operations in the same order: bit-identical.
+constexpr int kBigPanelMaxM = 880;
+__global__ void __launch_bounds__(256, 1)
+    lu_big_panel_smem_kernel(const int* __restrict__ blist, const int* __restrict__ msz,
+                             const long long* __restrict__ lu_off, const long long* __restrict__ row_off,
+                             double* work, double* rowmax, int* __restrict__ piv, int* bad, int* __restrict__ fail,
+                             int k0) {
+  extern __shared__ __align__(16) double P[];
+  const int bi = blockIdx.x;
+  const int b = blist[bi];
+  const int m = msz[b];
+  if (k0 >= m || bad[bi]) return;
+  const long long off = lu_off[b], ro = row_off[b];
+  double* A = work + off;
+  double* rm = rowmax + ro;
+  const int kb = min(kBigNB, m - k0);
+  const int ld = m - k0;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  __shared__ double s_v[8];
+  __shared__ int s_i[8];
+  __shared__ int s_p, s_bad;
+  __shared__ int s_perm[kBigNB];
+  for (int e = t; e < ld * kb; e += blockDim.x) {
+    const int q = e / ld, i = e - q * ld;
+    P[e] = A[(size_t)(k0 + q) * m + k0 + i];
+  }
+  __syncthreads();
+  for (int k = k0; k < k0 + kb; ++k) {
+    const int kq = k - k0;
+    double* Pk = P + (size_t)kq * ld;  // column k; local row i - k0
+    double best = -1.0;
+    int bidx = m;
+    for (int i = k + t; i < m; i += blockDim.x) {
+      const double v = fabs(Pk[i - k0]);
+      if (v > best) {
+        best = v;
+        bidx = i;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(kFull, best, o);
+      const int oi = __shfl_xor_sync(kFull, bidx, o);
+      if (ob > best || (ob == best && oi < bidx)) {
+        best = ob;
+        bidx = oi;
+      }
+    }
+    if (lane == 0) {
+      s_v[warp] = best;
+      s_i[warp] = bidx;
+    }
+    __syncthreads();
+    if (t == 0) {
+      double bv = s_v[0];
+      int bx = s_i[0];
+      for (int w = 1; w < 8; ++w)
+        if (s_v[w] > bv || (s_v[w] == bv && s_i[w] < bx)) {
+          bv = s_v[w];
+          bx = s_i[w];
+        }
+      int p = bx < m ? bx : k;
+      if (!(fabs(Pk[kq]) < bv)) p = k;
+      s_p = p;
+      const double pivot = Pk[p - k0];
+      const int bd = fabs(pivot) <= 1e-14 * fmax(rm[p], 1e-300);
+      s_bad = bd;
+      piv[ro + k] = p;
+      s_perm[kq] = p;
+      if (!bd && p != k) {
+        const double r0 = rm[k];
+        rm[k] = rm[p];
+        rm[p] = r0;
+      }
+    }
+    __syncthreads();
+    if (s_bad) {
+      if (t == 0) {
+        bad[bi] = 1;
+        atomicMin(fail, b);
+      }
+      return;
+    }
+    const int p = s_p;
+    if (p != k && t < kb) {
+      double* c = P + (size_t)t * ld;
+      const double a0 = c[kq];
+      c[kq] = c[p - k0];
+      c[p - k0] = a0;
+    }
+    __syncthreads();
+    const double inv = 1.0 / Pk[kq];
+    for (int i = k + 1 + t; i < m; i += blockDim.x) Pk[i - k0] = mul_rn(Pk[i - k0], inv);
+    __syncthreads();
+    const int nc = k0 + kb - (k + 1);
+    const int nr = m - (k + 1);
+    for (int e = t; e < nc * nr; e += blockDim.x) {
+      const int jq = kq + 1 + e / nr, i = k + 1 - k0 + e % nr;
+      double* c = P + (size_t)jq * ld;
+      c[i] = sub_rn(c[i], mul_rn(Pk[i], c[kq]));
+    }
+    __syncthreads();
+  }
+  for (int e = t; e < ld * kb; e += blockDim.x) {
+    const int q = e / ld, i = e - q * ld;
+    A[(size_t)(k0 + q) * m + k0 + i] = P[e];
+  }
+  // deferred row swaps of the columns left and right of the panel, in k order
+  for (int j = t; j < m - kb; j += blockDim.x) {
+    const int jc = j < k0 ? j : j + kb;
+    double* col = A + (size_t)jc * m;
+    for (int q = 0; q < kb; ++q) {
+      const int p = s_perm[q];
+      if (p != k0 + q) {
+        const double a0 = col[k0 + q];
+        col[k0 + q] = col[p];
+        col[p] = a0;
+      }
+    }
+  }
+  __syncthreads();
+  // U12: panel rows of the trailing columns, L11 from shared memory
+  for (int j = k0 + kb + t; j < m; j += blockDim.x) {
+    double u[kBigNB];
+#pragma unroll
+    for (int q = 0; q < kBigNB; ++q) u[q] = q < kb ? A[(size_t)j * m + k0 + q] : 0.0;
+#pragma unroll
+    for (int i = 1; i < kBigNB; ++i)
+#pragma unroll
+      for (int q = 0; q < i; ++q)
+        if (i < kb) u[i] = sub_rn(u[i], mul_rn(P[(size_t)q * ld + i], u[q]));
+#pragma unroll
+    for (int q = 1; q < kBigNB; ++q)
+      if (q < kb) A[(size_t)j * m + k0 + q] = u[q];
+  }
+}
+
 // A22 -= L21 * U12 for panel k0 (full panels only: the last, partial panel
 // has no trailing block). grid = (tiles_r * tiles_c, blocks).
 __global__ void __launch_bounds__(256, 3) lu_big_update_kernel(const int* __restrict__ blist,

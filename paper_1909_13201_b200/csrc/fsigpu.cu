@@ -65,7 +65,14 @@ struct Profiler {
     int cls;
     double bytes;
     cudaEvent_t a, b;
+    int lvl;
   };
+  // GMG level the current launches belong to (set by Gmg::cycle; -1 outside)
+  int level = -1;
+  static constexpr int kLv = 32;
+  double lv_ms[FSIGPU_K_COUNT][kLv + 1] = {};
+  long long lv_launches[FSIGPU_K_COUNT][kLv + 1] = {};
+  double lv_bytes[FSIGPU_K_COUNT][kLv + 1] = {};
   std::vector<Rec> recs;
   std::vector<cudaEvent_t> pool;
   double ms[FSIGPU_K_COUNT] = {0};
@@ -83,7 +90,7 @@ struct Profiler {
   }
   int begin(int cls, double by, cudaStream_t s) {
     if (!on) return -1;
-    Rec r{cls, by, get(), get()};
+    Rec r{cls, by, get(), get(), level};
     FSI_CUDA(cudaEventRecord(r.a, s));
     recs.push_back(r);
     return (int)recs.size() - 1;
@@ -100,6 +107,10 @@ struct Profiler {
       ms[r.cls] += t;
       launches[r.cls] += 1;
       bytes[r.cls] += r.bytes;
+      const int li = (r.lvl >= 0 && r.lvl < kLv) ? r.lvl + 1 : 0;
+      lv_ms[r.cls][li] += t;
+      lv_launches[r.cls][li] += 1;
+      lv_bytes[r.cls][li] += r.bytes;
       pool.push_back(r.a);
       pool.push_back(r.b);
     }
@@ -243,7 +254,34 @@ struct Csr {
   }
   size_t stage_smem() const { return 8 * (size_t)((cap + 3) & ~1) + 4 * (size_t)(cap + 8); }
   double bytes(bool resid) const {
-    return 12.0 * nnz + 4.0 * (rows + 1) + 8.0 * cols + 8.0 * rows + (resid ? 8.0 * rows : 0.0);
+    const double ib = c16 ? 2.0 * nnz + 16.0 * rows : 4.0 * nnz;  // index stream (+ window bases)
+    return 8.0 * nnz + ib + 4.0 * (rows + 1) + 8.0 * cols + 8.0 * rows + (resid ? 8.0 * rows : 0.0);
+  }
+  // CSR16 (sparse.cuh): 16-bit window codes + 4 window bases per row instead
+  // of 32-bit columns. The 32-bit idx is released; only the vector kernel
+  // runs on it (no staged / paired variants).
+  bool c16 = false;
+  DevBuf<unsigned short> code16;
+  DevBuf<int4> bases16;
+  bool compress16(cudaStream_t s) {
+    if (!rows || nstage) return false;
+    DevBuf<unsigned short> code;
+    DevBuf<int4> bs;
+    DevBuf<int> fail;
+    code.alloc((size_t)nnz + 4);
+    bs.alloc((size_t)rows);
+    fail.alloc(1);
+    FSI_CUDA(cudaMemsetAsync(fail.p, 0, sizeof(int), s));
+    c16_compress_kernel<<<ceil_div(rows, 256), 256, 0, s>>>(rows, ptr.p, idx.p, code.p, bs.p, fail.p);
+    FSI_CHECK_LAUNCH();
+    int h_fail = 0;
+    FSI_CUDA(cudaMemcpyAsync(&h_fail, fail.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    FSI_CUDA(cudaStreamSynchronize(s));
+    if (h_fail) return false;
+    code16 = std::move(code);
+    bases16 = std::move(bs);
+    c16 = true;
+    return true;
   }
   int unroll = 4;  // entries per lane per predicated batch (4 or 8); 22/24: paired loads, 2/4 pairs
   template <class G, class E>
@@ -255,6 +293,27 @@ struct Csr {
     }
     const long long threads = (long long)rows * lpr;
     const int grid = ceil_div(threads, 256);
+    if (c16) {
+#define FSI_C16(LP, UU) launch_k(csr16_kernel<LP, G, E, UU>, dim3(grid), dim3(256), 0, s, rows, (const int*)ptr.p, (const unsigned short*)code16.p, (const int4*)bases16.p, (const double*)val.p, g, e)
+#define FSI_C16_L(UU)                \
+  switch (lpr) {                     \
+    case 2: FSI_C16(2, UU); break;   \
+    case 4: FSI_C16(4, UU); break;   \
+    case 8: FSI_C16(8, UU); break;   \
+    case 16: FSI_C16(16, UU); break; \
+    default: FSI_C16(32, UU); break; \
+  }
+      if (unroll == 8) {
+        FSI_C16_L(8)
+      } else {
+        FSI_C16_L(4)
+      }
+#undef FSI_C16_L
+#undef FSI_C16
+      FSI_CHECK_LAUNCH();
+      counted();
+      return;
+    }
 #define FSI_CSR(LP, UU) launch_k(csr_kernel<LP, G, E, UU>, dim3(grid), dim3(256), 0, s, rows, (const int*)ptr.p, (const int*)idx.p, (const double*)val.p, g, e)
 #define FSI_CSRP(LP, UU) launch_k(csr_pair_kernel<LP, G, E, UU>, dim3(grid), dim3(256), 0, s, rows, (const int*)ptr.p, (const int*)idx.p, (const double*)val.p, g, e)
     if (unroll == 22 || unroll == 24) {  // paired loads, 2 or 4 pairs per lane per batch
@@ -564,9 +623,18 @@ struct Blocks {
           if (big_rowmax.n < (size_t)total_rows) big_rowmax.alloc((size_t)total_rows);
           if (big_bad.n < (size_t)grid) big_bad.alloc((size_t)grid);
           lu_big_init_kernel<<<grid, 256, 0, s>>>(bl, m.p, lu_off.p, row_off.p, src, lu.p, big_rowmax.p, big_bad.p);
+          const char* pg = std::getenv("FSIGPU_LU_PANEL_GLOBAL");
+          const bool smem_panel = mx <= kBigPanelMaxM && !(pg && std::atoi(pg) != 0);
+          if (smem_panel)
+            FSI_CUDA(cudaFuncSetAttribute(lu_big_panel_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)((size_t)mx * kBigNB * 8)));
           for (int k0 = 0; k0 < mx; k0 += kBigNB) {
-            lu_big_panel_kernel<<<grid, 256, 0, s>>>(bl, m.p, lu_off.p, row_off.p, lu.p, big_rowmax.p, piv.p,
-                                                     big_bad.p, fail.p, k0);
+            if (smem_panel)
+              lu_big_panel_smem_kernel<<<grid, 256, (size_t)(mx - k0) * kBigNB * 8, s>>>(
+                  bl, m.p, lu_off.p, row_off.p, lu.p, big_rowmax.p, piv.p, big_bad.p, fail.p, k0);
+            else
+              lu_big_panel_kernel<<<grid, 256, 0, s>>>(bl, m.p, lu_off.p, row_off.p, lu.p, big_rowmax.p, piv.p,
+                                                       big_bad.p, fail.p, k0);
             if (k0 + kBigNB < mx) {
               const int tiles = ceil_div(mx - k0 - kBigNB, kBigTile);
               lu_big_update_kernel<<<dim3(tiles * tiles, grid), 256, 0, s>>>(bl, m.p, lu_off.p, lu.p, big_bad.p,
@@ -941,6 +1009,7 @@ struct Gmg {
   // visit of a coarse level, so its final kernel may write the iterate with
   // the constrained columns already zeroed (the caller's ec mask).
   void cycle(int l, char mode, int x_zero, bool mask_out = false) {
+    g_prof.level = l;
     if (l == 0) {
       coarse(x_zero, mask_out);
       return;
@@ -964,6 +1033,7 @@ struct Gmg {
       case 'f': cycle(l - 1, 'f', 1); cycle(l - 1, 'v', 0, fused_mask); break;
       default: throw Error(FSIGPU_ERR_INVALID, "gmg: unknown cycle type");
     }
+    g_prof.level = l;
     if (post > 0 && L.AP.rows) {
       // x += P ec ; r = r_pre - AP ec  (one kernel; rbuf holds r_pre)
       ProfScope ps(FSIGPU_K_TRANSFER, L.P.bytes(false) + L.AP.bytes(false) + 24.0 * L.n + L.n + L.nc, s);
@@ -980,6 +1050,9 @@ struct Gmg {
   }
   // z = M r on device pointers
   void apply(const double* r, double* z) {
+    struct LevelReset {
+      ~LevelReset() { g_prof.level = -1; }
+    } reset_level;
     Level& T = lv.back();
     T.b = const_cast<double*>(r);
     T.x = z;
@@ -1076,6 +1149,12 @@ static void assemble_fs(Level& L, const fsigpu_level_desc& d, const std::vector<
   FSI_CUDA(cudaStreamSynchronize(s));
   L.FS.adopt(L.n, L.n, std::move(ptr), std::move(cols), std::move(fv));
   L.assembled = true;
+  // window-compressed column codes (sparse.cuh CSR16), opt-in with
+  // FSIGPU_FS_C16=1: measured slower (config 0 8.1 -> 9.8 ms per solve,
+  // config-2 L2 FS 44 -> 70 us), and the fine config-2 rows need more than
+  // 4 windows (DESIGN 3.4)
+  const char* e = std::getenv("FSIGPU_FS_C16");
+  if (e && std::atoi(e) == 1) L.FS.compress16(s);
 }
 
 // Build one level from its descriptor (host arrays).
@@ -2474,6 +2553,17 @@ int fsigpu_profile_read(double* ms, long long* launches, double* bytes) {
     }
   });
 }
+int fsigpu_profile_read_level(int cls, int level, double* ms, long long* launches, double* bytes) {
+  return guarded([&] {
+    require(cls >= 0 && cls < FSIGPU_K_COUNT, "profile: bad class");
+    require(level >= -1 && level < Profiler::kLv, "profile: bad level");
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof.flush();
+    if (ms) *ms = g_prof.lv_ms[cls][level + 1];
+    if (launches) *launches = g_prof.lv_launches[cls][level + 1];
+    if (bytes) *bytes = g_prof.lv_bytes[cls][level + 1];
+  });
+}
 int fsigpu_profile_reset(void) {
   return guarded([&] {
     std::lock_guard<std::mutex> lk(g_prof_mu);
@@ -2482,6 +2572,11 @@ int fsigpu_profile_reset(void) {
       g_prof.ms[i] = 0;
       g_prof.launches[i] = 0;
       g_prof.bytes[i] = 0;
+      for (int l = 0; l <= Profiler::kLv; ++l) {
+        g_prof.lv_ms[i][l] = 0;
+        g_prof.lv_launches[i][l] = 0;
+        g_prof.lv_bytes[i][l] = 0;
+      }
     }
   });
 }

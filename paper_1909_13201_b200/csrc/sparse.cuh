@@ -137,6 +137,82 @@ __global__ void __launch_bounds__(256) csr_kernel(int rows, const int* __restric
   if (ok && lane == 0) epi(row, s, pe);
 }
 
+// Segment-compressed column indices ("CSR16"): the assembled FS operator's
+// rows are unions of element-patch dof sets, so their columns fall in at
+// most a few short windows of the frame (one per field section the patch
+// touches: e.g. u^f, p^f and the u^s coupling columns). Each row stores up
+// to 4 window bases (int4, 16 B per row) and each entry a 16-bit code: the
+// top 2 bits select the base, the low 14 bits are the offset in the window.
+// 12 -> 10 bytes per entry (+16 per row) on an HBM-bound stream; same
+// arithmetic in the same order as csr_kernel (bit-identical results).
+constexpr int kC16Bits = 14;
+constexpr int kC16Win = 1 << kC16Bits;
+__device__ __forceinline__ int c16_col(const int4& b, unsigned int code) {
+  const unsigned int sel = code >> kC16Bits;
+  const int base = sel == 0 ? b.x : sel == 1 ? b.y : sel == 2 ? b.z : b.w;
+  return base + (int)(code & (kC16Win - 1));
+}
+
+template <int LPR, class Gather, class Epi, int U = 4>
+__global__ void __launch_bounds__(256) csr16_kernel(int rows, const int* __restrict__ ptr,
+                                                    const unsigned short* __restrict__ code,
+                                                    const int4* __restrict__ bases,
+                                                    const double* __restrict__ val, Gather gx, Epi epi) {
+  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = (int)(gt / LPR);
+  const int lane = threadIdx.x & (LPR - 1);
+  const bool ok = row < rows;
+  pdl_trigger();
+  const int k0 = ok ? __ldg(ptr + row) : 0, k1 = ok ? __ldg(ptr + row + 1) : 0;  // setup data
+  const int4 bs = ok ? __ldg(bases + row) : make_int4(0, 0, 0, 0);
+  pdl_wait();
+  EpiPre pe{0.0, 0};
+  if (ok && lane == 0) pe = epi.pre(row);
+  double s = 0.0;
+  for (int kb = k0 + lane; kb < k1; kb += U * LPR) {
+    int c[U];
+    double v[U], xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = kb + u * LPR;
+      const bool in = k < k1;
+      c[u] = in ? c16_col(bs, __ldg(code + k)) : -1;
+      v[u] = in ? __ldg(val + k) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = c[u] >= 0 ? gx(c[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) s = fma(v[u], xv[u], s);
+  }
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, LPR);
+  if (ok && lane == 0) epi(row, s, pe);
+}
+
+// One thread per row: split the row's sorted columns into windows of
+// kC16Win starting at the first column of each window; more than 4
+// windows sets *fail (the matrix then keeps 32-bit indices).
+__global__ void c16_compress_kernel(int rows, const int* __restrict__ ptr, const int* __restrict__ idx,
+                                    unsigned short* __restrict__ code, int4* __restrict__ bases,
+                                    int* __restrict__ fail) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  int b[4] = {0, 0, 0, 0};
+  int nb = 0;
+  for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+    const int c = idx[k];
+    if (nb == 0 || c - b[nb - 1] >= kC16Win) {
+      if (nb == 4) {
+        atomicExch(fail, 1);
+        return;
+      }
+      b[nb++] = c;
+    }
+    code[k] = (unsigned short)(((nb - 1) << kC16Bits) | (c - b[nb - 1]));
+  }
+  bases[i] = make_int4(b[0], b[1], b[2], b[3]);
+}
+
 // Shared-memory staged CSR ("CSR-stream"). CTA b owns rows [rb[b], rb[b+1])
 // whose entries [ptr[rb[b]], ptr[rb[b+1]]) are contiguous in idx / val, at
 // most `cap` of them. One thread brings both slices into shared memory with

@@ -121,6 +121,7 @@ def lib():
             "fsigpu_gmres_destroy": ([vp], None),
             "fsigpu_profile_enable": ([ip], ip),
             "fsigpu_profile_read": ([vp, vp, vp], ip),
+            "fsigpu_profile_read_level": ([ip, ip, vp, vp, vp], ip),
             "fsigpu_profile_reset": ([], ip),
         }
         for name, (args, res) in sig.items():
@@ -500,3 +501,12 @@ class Profile:
         _check(lib().fsigpu_profile_read(ms.ctypes.data, n.ctypes.data, by.ctypes.data))
         return {k: dict(ms=float(ms[i]), launches=int(n[i]), bytes=float(by[i]))
                 for i, k in enumerate(KERNEL_CLASSES)}
+
+    @staticmethod
+    def read_level(cls: str, level: int):
+        """Sums of one kernel class on one GMG level (in-solve per-launch events)."""
+        ms, by = C.c_double(), C.c_double()
+        n = C.c_longlong()
+        _check(lib().fsigpu_profile_read_level(KERNEL_CLASSES.index(cls), level, C.byref(ms), C.byref(n),
+                                               C.byref(by)))
+        return dict(ms=ms.value, launches=n.value, bytes=by.value)

@@ -266,15 +266,17 @@ def test_small_lu_variants_ties_bitexact(variant, monkeypatch):
     assert e.value.label == "fs-solid-dp-7"
 
 
-@pytest.mark.parametrize("variant", ["blocked", "single_cta"])
+@pytest.mark.parametrize("variant", ["blocked", "blocked_global_panel", "single_cta"])
 def test_large_block_lu_bitexact(variant, monkeypatch):
     """Blocks above 164 rows (config-4 Vanka patches): the blocked LU
-    (32-column panels, 64x64 trailing tiles) and the single-CTA kernel give
-    DenseFactorization's factors bit for bit, with pivoting, partial panels
-    and tiles, mixed sizes in one batch, and a singular block's label."""
+    (32-column panels staged in shared memory or factored in global memory,
+    64x64 trailing tiles) and the single-CTA kernel give DenseFactorization's
+    factors bit for bit, with pivoting, partial panels and tiles, mixed sizes
+    in one batch (up to the config-4 size 780), and a singular block's label."""
     monkeypatch.setenv("FSIGPU_LU_BIG_OLD", "1" if variant == "single_cta" else "0")
+    monkeypatch.setenv("FSIGPU_LU_PANEL_GLOBAL", "1" if variant == "blocked_global_panel" else "0")
     rng = np.random.default_rng(21)
-    sizes = [165, 230, 257, 320, 401]
+    sizes = [165, 230, 257, 320, 401, 780]
     mats = [rng.uniform(-1, 1, (m, m)) for m in sizes]
     B = fsigpu.DenseBlocks.from_dense(mats)
     for a, (lu, piv) in zip(mats, B.lu(sizes)):
@@ -557,3 +559,28 @@ def test_smoother_switch_rebuilds_solver_graph(chan):
     assert fsigpu.lib().fsigpu_gmg_set_smoother(G.h, 7) != 0
     with pytest.raises(KeyError):
         G.set_smoother("bogus")
+
+
+def test_fs_operator_c16_bitidentical(cfg0, monkeypatch):
+    """The window-compressed (16-bit code) FS operator (opt-in) gives
+    bit-identical FS applies, V-cycles and solves to the 32-bit-index one."""
+    g = cfg0.golden
+    r = g["golden/vcycle_r"]
+    top = len(cfg0.levels) - 1
+    G32 = fsigpu.GmgPreconditioner(cfg0.levels)
+    monkeypatch.setenv("FSIGPU_FS_C16", "1")  # opt-in (measured slower, DESIGN 3.4)
+    G16 = fsigpu.GmgPreconditioner(cfg0.levels)
+    monkeypatch.delenv("FSIGPU_FS_C16")
+    for lvl in range(1, top + 1):
+        rr = np.random.default_rng(lvl).uniform(-1, 1, cfg0.levels[lvl].n)
+        assert np.array_equal(G16.fs_apply(lvl, rr), G32.fs_apply(lvl, rr))
+    assert np.array_equal(G16.apply(r), G32.apply(r))
+    assert rel(G16.fs_apply(top, g["golden/fs_r"]), g["golden/fs_z_add"]) <= 1e-12
+    cfg = fsigpu.KrylovConfig(restart=30, max_iters=2000, rel_tol=1e-10, abs_tol=1e-300)
+    a = fsigpu.gmres(G16, cfg0.frame_scale, cfg0.b, cfg)
+    b = fsigpu.gmres(G32, cfg0.frame_scale, cfg0.b, cfg)
+    assert a.iterations == b.iterations and np.array_equal(a.x, b.x)
+    # the compressed stream is smaller: 10 B/entry + 16 B/row vs 12 B/entry
+    ms16, by16 = G16.time_kernel("fs_smoother", top, reps=3)
+    ms32, by32 = G32.time_kernel("fs_smoother", top, reps=3)
+    assert by16 < by32
