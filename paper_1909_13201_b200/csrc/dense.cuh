@@ -1301,7 +1301,7 @@ __global__ void __launch_bounds__(256, 2) lu_big_panel_kernel(const int* __restr
 // order (no other column is read or written in between, so the result is
 // the same as swapping whole rows immediately); U12 then reads L11 from
 // shared memory. Same rounded operations in the same order: bit-identical.
-constexpr int kBigPanelMaxM = 880;
+constexpr int kBigPanelMaxM = 850;  // panel (m * 32 doubles) + row maxima (m) <= 227 KB
 __global__ void __launch_bounds__(256, 1)
     lu_big_panel_smem_kernel(const int* __restrict__ blist, const int* __restrict__ msz,
                              const long long* __restrict__ lu_off, const long long* __restrict__ row_off,
@@ -1322,10 +1322,33 @@ __global__ void __launch_bounds__(256, 1)
   __shared__ int s_i[8];
   __shared__ int s_p, s_bad;
   __shared__ int s_perm[kBigNB];
-  for (int e = t; e < ld * kb; e += blockDim.x) {
-    const int q = e / ld, i = e - q * ld;
-    P[e] = A[(size_t)(k0 + q) * m + k0 + i];
+  // (loops are column-outer / row-inner: no per-element integer division)
+  // the remaining rows' original maxima (singular test) follow the panel, so
+  // the per-step test and swap never wait on a global load
+  double* R = P + (size_t)ld * kb;
+  // panel columns arrive by TMA bulk copies (one per column, one mbarrier)
+  // when every column start is 16-byte aligned (even m and block offset);
+  // ncu showed the per-thread loads of the panel as the top stall at one
+  // CTA per SM. Otherwise plain loads.
+  __shared__ __align__(8) unsigned long long s_bar;
+  const bool bulk = ((off | m) & 1) == 0;
+  if (bulk) {
+    if (t == 0) {
+      mbar_init(&s_bar, 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    if (t == 0) {
+      mbar_arrive_expect_tx(&s_bar, (unsigned)(ld * kb * 8));
+      for (int q = 0; q < kb; ++q)
+        tma_bulk_g2s(P + (size_t)q * ld, A + (size_t)(k0 + q) * m + k0, (unsigned)(ld * 8), &s_bar);
+    }
+  } else {
+    for (int q = 0; q < kb; ++q)
+      for (int i = t; i < ld; i += blockDim.x) P[(size_t)q * ld + i] = A[(size_t)(k0 + q) * m + k0 + i];
   }
+  for (int i = t; i < ld; i += blockDim.x) R[i] = rm[k0 + i];
+  if (bulk) mbar_wait(&s_bar, 0);
   __syncthreads();
   for (int k = k0; k < k0 + kb; ++k) {
     const int kq = k - k0;
@@ -1365,14 +1388,14 @@ __global__ void __launch_bounds__(256, 1)
       if (!(fabs(Pk[kq]) < bv)) p = k;
       s_p = p;
       const double pivot = Pk[p - k0];
-      const int bd = fabs(pivot) <= 1e-14 * fmax(rm[p], 1e-300);
+      const int bd = fabs(pivot) <= 1e-14 * fmax(R[p - k0], 1e-300);
       s_bad = bd;
       piv[ro + k] = p;
       s_perm[kq] = p;
       if (!bd && p != k) {
-        const double r0 = rm[k];
-        rm[k] = rm[p];
-        rm[p] = r0;
+        const double r0 = R[kq];
+        R[kq] = R[p - k0];
+        R[p - k0] = r0;
       }
     }
     __syncthreads();
@@ -1394,19 +1417,29 @@ __global__ void __launch_bounds__(256, 1)
     const double inv = 1.0 / Pk[kq];
     for (int i = k + 1 + t; i < m; i += blockDim.x) Pk[i - k0] = mul_rn(Pk[i - k0], inv);
     __syncthreads();
-    const int nc = k0 + kb - (k + 1);
-    const int nr = m - (k + 1);
-    for (int e = t; e < nc * nr; e += blockDim.x) {
-      const int jq = kq + 1 + e / nr, i = k + 1 - k0 + e % nr;
+    // rank-1 update of the panel columns right of k: each thread keeps the
+    // multipliers of its rows in registers across the columns
+    constexpr int kRows = (kBigPanelMaxM + 255) / 256;
+    double lr[kRows];
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+      const int i = kq + 1 + t + r * 256;
+      lr[r] = i < ld ? Pk[i] : 0.0;
+    }
+    for (int jq = kq + 1; jq < kb; ++jq) {
       double* c = P + (size_t)jq * ld;
-      c[i] = sub_rn(c[i], mul_rn(Pk[i], c[kq]));
+      const double u = c[kq];
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) {
+        const int i = kq + 1 + t + r * 256;
+        if (i < ld) c[i] = sub_rn(c[i], mul_rn(lr[r], u));
+      }
     }
     __syncthreads();
   }
-  for (int e = t; e < ld * kb; e += blockDim.x) {
-    const int q = e / ld, i = e - q * ld;
-    A[(size_t)(k0 + q) * m + k0 + i] = P[e];
-  }
+  for (int q = 0; q < kb; ++q)
+    for (int i = t; i < ld; i += blockDim.x) A[(size_t)(k0 + q) * m + k0 + i] = P[(size_t)q * ld + i];
+  for (int i = t; i < ld; i += blockDim.x) rm[k0 + i] = R[i];
   // deferred row swaps of the columns left and right of the panel, in k order
   for (int j = t; j < m - kb; j += blockDim.x) {
     const int jc = j < k0 ? j : j + kb;
@@ -1491,6 +1524,84 @@ __global__ void __launch_bounds__(256, 3) lu_big_update_kernel(const int* __rest
   for (int jj = 0; jj < TC; ++jj) {
     const int c = c0 + cg * TC + jj;
     if (r < m && c < m) A[(size_t)c * m + r] = acc[jj];
+  }
+}
+
+// Row-strip variant of lu_big_update_kernel (default): a CTA owns 64 rows of
+// A22 and walks all its 64-column tiles, keeping the L21 strip in shared
+// memory and prefetching the next tile (its A22 values into registers, its
+// U12 slice into registers, stored to shared memory after the current
+// tile's math), so the global loads overlap the fp64 work instead of every
+// 64x64 tile paying a full load latency with nothing to hide it. Same
+// per-entry operations in the same k order: bit-identical.
+// grid = (tiles_r, blocks).
+__global__ void __launch_bounds__(256, 2) lu_big_update_strip_kernel(const int* __restrict__ blist,
+                                                                  const int* __restrict__ msz,
+                                                                  const long long* __restrict__ lu_off,
+                                                                  double* work, const int* __restrict__ bad, int k0) {
+  const int bi = blockIdx.y;
+  const int b = blist[bi];
+  const int m = msz[b];
+  const int r0 = k0 + kBigNB + blockIdx.x * kBigTile;
+  const int cbeg = k0 + kBigNB;
+  if (r0 >= m || cbeg >= m || bad[bi]) return;
+  double* A = work + lu_off[b];
+  __shared__ __align__(16) double Ls[kBigNB][kBigTile];
+  __shared__ __align__(16) double Us[kBigNB][kBigTile];
+  const int t = threadIdx.x;
+  const int ri = t & (kBigTile - 1), cg = t / kBigTile;
+  const int r = r0 + ri;
+  constexpr int TC = kBigTile / 4;
+  constexpr int UPT = kBigNB * kBigTile / 256;  // U12 values per thread per tile
+  for (int e = t; e < kBigNB * kBigTile; e += 256) {
+    const int k = e / kBigTile, i = e % kBigTile;
+    Ls[k][i] = r0 + i < m ? A[(size_t)(k0 + k) * m + r0 + i] : 0.0;
+  }
+  double nxt[TC], un[UPT];
+  auto load_tile = [&](int c0) {
+#pragma unroll
+    for (int jj = 0; jj < TC; ++jj) {
+      const int c = c0 + cg * TC + jj;
+      nxt[jj] = (r < m && c < m) ? A[(size_t)c * m + r] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < UPT; ++q) {
+      const int e = t + q * 256;
+      const int j = e / kBigNB, k = e % kBigNB;  // coalesced over k
+      un[q] = c0 + j < m ? A[(size_t)(c0 + j) * m + k0 + k] : 0.0;
+    }
+  };
+  load_tile(cbeg);
+  for (int c0 = cbeg; c0 < m; c0 += kBigTile) {
+    __syncthreads();  // previous tile's Us reads are done
+#pragma unroll
+    for (int q = 0; q < UPT; ++q) {
+      const int e = t + q * 256;
+      Us[e % kBigNB][e / kBigNB] = un[q];
+    }
+    double acc[TC];
+#pragma unroll
+    for (int jj = 0; jj < TC; ++jj) acc[jj] = nxt[jj];
+    __syncthreads();
+    if (c0 + kBigTile < m) load_tile(c0 + kBigTile);  // in flight during the math below
+#pragma unroll 4
+    for (int k = 0; k < kBigNB; ++k) {
+      const double l = Ls[k][ri];
+      double u[TC];
+#pragma unroll
+      for (int q = 0; q < TC; q += 2) {
+        const double2 uu = *reinterpret_cast<const double2*>(&Us[k][cg * TC + q]);
+        u[q] = uu.x;
+        u[q + 1] = uu.y;
+      }
+#pragma unroll
+      for (int jj = 0; jj < TC; ++jj) acc[jj] = sub_rn(acc[jj], mul_rn(l, u[jj]));
+    }
+#pragma unroll
+    for (int jj = 0; jj < TC; ++jj) {
+      const int c = c0 + cg * TC + jj;
+      if (r < m && c < m) A[(size_t)c * m + r] = acc[jj];
+    }
   }
 }
 

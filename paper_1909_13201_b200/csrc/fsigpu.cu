@@ -627,18 +627,23 @@ struct Blocks {
           const bool smem_panel = mx <= kBigPanelMaxM && !(pg && std::atoi(pg) != 0);
           if (smem_panel)
             FSI_CUDA(cudaFuncSetAttribute(lu_big_panel_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)((size_t)mx * kBigNB * 8)));
+                                          (int)((size_t)mx * (kBigNB + 1) * 8)));
           for (int k0 = 0; k0 < mx; k0 += kBigNB) {
             if (smem_panel)
-              lu_big_panel_smem_kernel<<<grid, 256, (size_t)(mx - k0) * kBigNB * 8, s>>>(
+              lu_big_panel_smem_kernel<<<grid, 256, (size_t)(mx - k0) * (kBigNB + 1) * 8, s>>>(
                   bl, m.p, lu_off.p, row_off.p, lu.p, big_rowmax.p, piv.p, big_bad.p, fail.p, k0);
             else
               lu_big_panel_kernel<<<grid, 256, 0, s>>>(bl, m.p, lu_off.p, row_off.p, lu.p, big_rowmax.p, piv.p,
                                                        big_bad.p, fail.p, k0);
             if (k0 + kBigNB < mx) {
               const int tiles = ceil_div(mx - k0 - kBigNB, kBigTile);
-              lu_big_update_kernel<<<dim3(tiles * tiles, grid), 256, 0, s>>>(bl, m.p, lu_off.p, lu.p, big_bad.p,
-                                                                             k0, tiles);
+              const char* ut = std::getenv("FSIGPU_LU_UPDATE_TILES");
+              if (ut && std::atoi(ut) != 0)
+                lu_big_update_kernel<<<dim3(tiles * tiles, grid), 256, 0, s>>>(bl, m.p, lu_off.p, lu.p,
+                                                                               big_bad.p, k0, tiles);
+              else
+                lu_big_update_strip_kernel<<<dim3(tiles, grid), 256, 0, s>>>(bl, m.p, lu_off.p, lu.p, big_bad.p,
+                                                                             k0);
             }
           }
           const size_t smf = (size_t)(mx + (mx + 1) / 2 + 32 * kTileLd + 8) * 8;
