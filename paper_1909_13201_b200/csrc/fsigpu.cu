@@ -319,6 +319,7 @@ struct Csr {
     if (unroll == 22 || unroll == 24) {  // paired loads, 2 or 4 pairs per lane per batch
       if (unroll == 22) {
         switch (lpr) {
+          case 1: FSI_CSRP(1, 2); break;
           case 2: FSI_CSRP(2, 2); break;
           case 4: FSI_CSRP(4, 2); break;
           case 8: FSI_CSRP(8, 2); break;
@@ -327,6 +328,7 @@ struct Csr {
         }
       } else {
         switch (lpr) {
+          case 1: FSI_CSRP(1, 4); break;
           case 2: FSI_CSRP(2, 4); break;
           case 4: FSI_CSRP(4, 4); break;
           case 8: FSI_CSRP(8, 4); break;
@@ -1819,7 +1821,8 @@ long long fsigpu_gmg_persist_bytes(fsigpu_gmg g) { return g ? (long long)g->g.pe
 int fsigpu_gmg_set_launch(fsigpu_gmg h, int level, int which, int lpr, int unroll) {
   return guarded([&] {
     require(h != nullptr && level >= 0 && level < (int)h->g.lv.size(), "launch: bad level");
-    require(lpr == 2 || lpr == 4 || lpr == 8 || lpr == 16 || lpr == 32, "launch: lpr must be 2..32");
+    require(lpr == 2 || lpr == 4 || lpr == 8 || lpr == 16 || lpr == 32 || (lpr == 1 && (unroll == 22 || unroll == 24)),
+            "launch: lpr must be 2..32 (1 with paired loads)");
     require(unroll == 4 || unroll == 8 || unroll == 22 || unroll == 24,
             "launch: unroll must be 4 or 8 (22/24: paired loads, 2/4 pairs)");
     Level& L = h->g.lv[level];

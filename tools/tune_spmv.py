@@ -24,8 +24,10 @@ for lev in levels:
             continue
         best, default = None, None
         default = G.time_kernel(kname, lev, reps=10, cold=cold)[0]
-        for lpr in [2, 4, 8, 16, 32]:
+        for lpr in [1, 2, 4, 8, 16, 32]:
             for u in [4, 8, 22, 24]:
+                if lpr == 1 and u < 22:
+                    continue
                 G.set_launch(lev, which, lpr, u)
                 ms, by = G.time_kernel(kname, lev, reps=10, cold=cold)
                 if best is None or ms < best[0]:
