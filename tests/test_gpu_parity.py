@@ -585,3 +585,27 @@ def test_fs_operator_c16_bitidentical(cfg0, monkeypatch):
     ms16, by16 = G16.time_kernel("fs_smoother", top, reps=3)
     ms32, by32 = G32.time_kernel("fs_smoother", top, reps=3)
     assert by16 < by32
+
+
+@MODES
+def test_vcycle_properties(cfg0, mode):
+    """Size-independent properties (tests/unit_gmg.cpp:335-364 pattern;
+    tests/unit_solver.cpp additive linearity): the additive FS smoother and the
+    V(1,1) cycle are linear maps (<=1e-12 rel.), map zero to exactly zero, and
+    repeat bit-identically run to run (deterministic gather-reduce, no atomics)."""
+    G = gmg(cfg0.levels, mode)
+    n = cfg0.levels[-1].n
+    rng = np.random.default_rng(11)
+    r1, r2 = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    a, b = 0.75, -2.5
+    top = len(cfg0.levels) - 1
+    for f in (G.apply, lambda r: G.fs_apply(top, r)):
+        z1, z2 = f(r1), f(r2)
+        zc = f(a * r1 + b * r2)
+        assert rel(zc, a * z1 + b * z2) <= 1e-12
+        assert not np.any(f(np.zeros(n)))
+        assert np.array_equal(f(r1), z1)
+    cfg = fsigpu.KrylovConfig(restart=30, max_iters=2000, rel_tol=1e-10, abs_tol=1e-300)
+    s1 = fsigpu.gmres(G, cfg0.frame_scale, cfg0.b, cfg)
+    s2 = fsigpu.gmres(G, cfg0.frame_scale, cfg0.b, cfg)
+    assert s1.iterations == s2.iterations and np.array_equal(s1.x, s2.x)
