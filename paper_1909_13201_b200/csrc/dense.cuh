@@ -1605,6 +1605,96 @@ __global__ void __launch_bounds__(256, 2) lu_big_update_strip_kernel(const int* 
   }
 }
 
+// Row-strip update with a 4-row x 8-column register tile per thread (default).
+// lu_big_update_strip_kernel's 1 x 16 tile is shared-memory bound (ncu: L1/TEX
+// 86%, 10 wavefronts per k for 16 mul/sub pairs per lane); here a warp is 16
+// row lanes x 2 column groups, so per k it reads 4 L21 values (16 distinct
+// doubles each, one wavefront) and 4 double2 U12 broadcasts (two addresses
+// in disjoint banks, one wavefront): 8 wavefronts for 32 pairs per lane.
+// Same per-entry operations in the same k order: bit-identical.
+// grid = (tiles_r, blocks), 128 threads.
+__global__ void __launch_bounds__(128, 2) lu_big_update_r4_kernel(const int* __restrict__ blist,
+                                                               const int* __restrict__ msz,
+                                                               const long long* __restrict__ lu_off,
+                                                               double* work, const int* __restrict__ bad, int k0) {
+  constexpr int NT = 128, RT = 4, CT = 8;
+  const int bi = blockIdx.y;
+  const int b = blist[bi];
+  const int m = msz[b];
+  const int r0 = k0 + kBigNB + blockIdx.x * kBigTile;
+  const int cbeg = k0 + kBigNB;
+  if (r0 >= m || cbeg >= m || bad[bi]) return;
+  double* A = work + lu_off[b];
+  __shared__ __align__(16) double Ls[kBigNB][kBigTile];
+  __shared__ __align__(16) double Us[kBigNB][kBigTile];
+  const int t = threadIdx.x;
+  const int rl = t & 15, cg = t >> 4;  // row lane, 8-column group
+  constexpr int UPT = kBigNB * kBigTile / NT;
+  for (int e = t; e < kBigNB * kBigTile; e += NT) {
+    const int k = e / kBigTile, i = e % kBigTile;
+    Ls[k][i] = r0 + i < m ? A[(size_t)(k0 + k) * m + r0 + i] : 0.0;
+  }
+  double nxt[RT][CT], un[UPT];
+  auto load_tile = [&](int c0) {
+#pragma unroll
+    for (int jj = 0; jj < CT; ++jj) {
+      const int c = c0 + cg * CT + jj;
+#pragma unroll
+      for (int i = 0; i < RT; ++i) {
+        const int r = r0 + rl + 16 * i;
+        nxt[i][jj] = (r < m && c < m) ? A[(size_t)c * m + r] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < UPT; ++q) {
+      const int e = t + q * NT;
+      const int j = e / kBigNB, k = e % kBigNB;  // coalesced over k
+      un[q] = c0 + j < m ? A[(size_t)(c0 + j) * m + k0 + k] : 0.0;
+    }
+  };
+  load_tile(cbeg);
+  for (int c0 = cbeg; c0 < m; c0 += kBigTile) {
+    __syncthreads();  // previous tile's Us reads are done
+#pragma unroll
+    for (int q = 0; q < UPT; ++q) {
+      const int e = t + q * NT;
+      Us[e % kBigNB][e / kBigNB] = un[q];
+    }
+    double acc[RT][CT];
+#pragma unroll
+    for (int i = 0; i < RT; ++i)
+#pragma unroll
+      for (int jj = 0; jj < CT; ++jj) acc[i][jj] = nxt[i][jj];
+    __syncthreads();
+    if (c0 + kBigTile < m) load_tile(c0 + kBigTile);  // in flight during the math below
+#pragma unroll 2
+    for (int k = 0; k < kBigNB; ++k) {
+      double l[RT], u[CT];
+#pragma unroll
+      for (int i = 0; i < RT; ++i) l[i] = Ls[k][rl + 16 * i];
+#pragma unroll
+      for (int q = 0; q < CT; q += 2) {
+        const double2 uu = *reinterpret_cast<const double2*>(&Us[k][cg * CT + q]);
+        u[q] = uu.x;
+        u[q + 1] = uu.y;
+      }
+#pragma unroll
+      for (int i = 0; i < RT; ++i)
+#pragma unroll
+        for (int jj = 0; jj < CT; ++jj) acc[i][jj] = sub_rn(acc[i][jj], mul_rn(l[i], u[jj]));
+    }
+#pragma unroll
+    for (int jj = 0; jj < CT; ++jj) {
+      const int c = c0 + cg * CT + jj;
+#pragma unroll
+      for (int i = 0; i < RT; ++i) {
+        const int r = r0 + rl + 16 * i;
+        if (r < m && c < m) A[(size_t)c * m + r] = acc[i][jj];
+      }
+    }
+  }
+}
+
 // Outputs of the blocked LU: gather map from the pivots, optional LU copy,
 // solve format (lu_write_outputs on the factor in global memory).
 // dynamic smem (doubles): [scratch: m][perm: m ints][S: 32*kTileLd]

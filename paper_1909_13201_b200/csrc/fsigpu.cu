@@ -640,9 +640,13 @@ struct Blocks {
             if (k0 + kBigNB < mx) {
               const int tiles = ceil_div(mx - k0 - kBigNB, kBigTile);
               const char* ut = std::getenv("FSIGPU_LU_UPDATE_TILES");
+              const char* u1 = std::getenv("FSIGPU_LU_UPDATE_R1");
               if (ut && std::atoi(ut) != 0)
                 lu_big_update_kernel<<<dim3(tiles * tiles, grid), 256, 0, s>>>(bl, m.p, lu_off.p, lu.p,
                                                                                big_bad.p, k0, tiles);
+              else if (!u1 || std::atoi(u1) == 0)
+                lu_big_update_r4_kernel<<<dim3(tiles, grid), 128, 0, s>>>(bl, m.p, lu_off.p, lu.p, big_bad.p,
+                                                                          k0);
               else
                 lu_big_update_strip_kernel<<<dim3(tiles, grid), 256, 0, s>>>(bl, m.p, lu_off.p, lu.p, big_bad.p,
                                                                              k0);
