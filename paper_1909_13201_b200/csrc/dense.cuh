@@ -1302,7 +1302,10 @@ __global__ void __launch_bounds__(256, 2) lu_big_panel_kernel(const int* __restr
 // the same as swapping whole rows immediately); U12 then reads L11 from
 // shared memory. Same rounded operations in the same order: bit-identical.
 constexpr int kBigPanelMaxM = 850;  // panel (m * 32 doubles) + row maxima (m) <= 227 KB
-__global__ void __launch_bounds__(256, 1)
+// 256 threads (measured: 512 threads slow the panel launch from 289 to 355 us,
+// the longer barriers outweigh the shorter per-thread row loops)
+constexpr int kPanelThreads = 256;
+__global__ void __launch_bounds__(kPanelThreads, 1)
     lu_big_panel_smem_kernel(const int* __restrict__ blist, const int* __restrict__ msz,
                              const long long* __restrict__ lu_off, const long long* __restrict__ row_off,
                              double* work, double* rowmax, int* __restrict__ piv, int* bad, int* __restrict__ fail,
@@ -1318,8 +1321,8 @@ __global__ void __launch_bounds__(256, 1)
   const int kb = min(kBigNB, m - k0);
   const int ld = m - k0;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  __shared__ double s_v[8];
-  __shared__ int s_i[8];
+  __shared__ double s_v[kPanelThreads / 32];
+  __shared__ int s_i[kPanelThreads / 32];
   __shared__ int s_p, s_bad;
   __shared__ int s_perm[kBigNB];
   // (loops are column-outer / row-inner: no per-element integer division)
@@ -1379,7 +1382,7 @@ __global__ void __launch_bounds__(256, 1)
     if (t == 0) {
       double bv = s_v[0];
       int bx = s_i[0];
-      for (int w = 1; w < 8; ++w)
+      for (int w = 1; w < kPanelThreads / 32; ++w)
         if (s_v[w] > bv || (s_v[w] == bv && s_i[w] < bx)) {
           bv = s_v[w];
           bx = s_i[w];
@@ -1419,11 +1422,11 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     // rank-1 update of the panel columns right of k: each thread keeps the
     // multipliers of its rows in registers across the columns
-    constexpr int kRows = (kBigPanelMaxM + 255) / 256;
+    constexpr int kRows = (kBigPanelMaxM + kPanelThreads - 1) / kPanelThreads;
     double lr[kRows];
 #pragma unroll
     for (int r = 0; r < kRows; ++r) {
-      const int i = kq + 1 + t + r * 256;
+      const int i = kq + 1 + t + r * kPanelThreads;
       lr[r] = i < ld ? Pk[i] : 0.0;
     }
     for (int jq = kq + 1; jq < kb; ++jq) {
@@ -1431,7 +1434,7 @@ __global__ void __launch_bounds__(256, 1)
       const double u = c[kq];
 #pragma unroll
       for (int r = 0; r < kRows; ++r) {
-        const int i = kq + 1 + t + r * 256;
+        const int i = kq + 1 + t + r * kPanelThreads;
         if (i < ld) c[i] = sub_rn(c[i], mul_rn(lr[r], u));
       }
     }

@@ -632,7 +632,7 @@ struct Blocks {
                                           (int)((size_t)mx * (kBigNB + 1) * 8)));
           for (int k0 = 0; k0 < mx; k0 += kBigNB) {
             if (smem_panel)
-              lu_big_panel_smem_kernel<<<grid, 256, (size_t)(mx - k0) * (kBigNB + 1) * 8, s>>>(
+              lu_big_panel_smem_kernel<<<grid, kPanelThreads, (size_t)(mx - k0) * (kBigNB + 1) * 8, s>>>(
                   bl, m.p, lu_off.p, row_off.p, lu.p, big_rowmax.p, piv.p, big_bad.p, fail.p, k0);
             else
               lu_big_panel_kernel<<<grid, 256, 0, s>>>(bl, m.p, lu_off.p, row_off.p, lu.p, big_rowmax.p, piv.p,
