@@ -644,9 +644,12 @@ struct Blocks {
               if (ut && std::atoi(ut) != 0)
                 lu_big_update_kernel<<<dim3(tiles * tiles, grid), 256, 0, s>>>(bl, m.p, lu_off.p, lu.p,
                                                                                big_bad.p, k0, tiles);
-              else if (!u1 || std::atoi(u1) == 0)
-                lu_big_update_r4_kernel<<<dim3(tiles, grid), 128, 0, s>>>(bl, m.p, lu_off.p, lu.p, big_bad.p,
-                                                                          k0);
+              else if (u1 && std::atoi(u1) == 4)  // 4x8 tile, 128 threads (A/B)
+                lu_big_update_r4_kernel<4><<<dim3(tiles, grid), 128, 0, s>>>(bl, m.p, lu_off.p, lu.p, big_bad.p,
+                                                                             k0);
+              else if (!u1 || std::atoi(u1) == 0)  // 2x8 tile, 256 threads (default)
+                lu_big_update_r4_kernel<2><<<dim3(tiles, grid), 256, 0, s>>>(bl, m.p, lu_off.p, lu.p, big_bad.p,
+                                                                             k0);
               else
                 lu_big_update_strip_kernel<<<dim3(tiles, grid), 256, 0, s>>>(bl, m.p, lu_off.p, lu.p, big_bad.p,
                                                                              k0);

@@ -267,7 +267,7 @@ def test_small_lu_variants_ties_bitexact(variant, monkeypatch):
 
 
 @pytest.mark.parametrize("variant", ["blocked", "blocked_global_panel", "blocked_tile_update", "blocked_strip_r1",
-                                     "single_cta"])
+                                     "blocked_r4", "single_cta"])
 def test_large_block_lu_bitexact(variant, monkeypatch):
     """Blocks above 164 rows (config-4 Vanka patches): the blocked LU
     (32-column panels staged in shared memory or factored in global memory,
@@ -277,7 +277,7 @@ def test_large_block_lu_bitexact(variant, monkeypatch):
     monkeypatch.setenv("FSIGPU_LU_BIG_OLD", "1" if variant == "single_cta" else "0")
     monkeypatch.setenv("FSIGPU_LU_PANEL_GLOBAL", "1" if variant == "blocked_global_panel" else "0")
     monkeypatch.setenv("FSIGPU_LU_UPDATE_TILES", "1" if variant == "blocked_tile_update" else "0")
-    monkeypatch.setenv("FSIGPU_LU_UPDATE_R1", "1" if variant == "blocked_strip_r1" else "0")
+    monkeypatch.setenv("FSIGPU_LU_UPDATE_R1", {"blocked_strip_r1": "1", "blocked_r4": "4"}.get(variant, "0"))
     rng = np.random.default_rng(21)
     sizes = [165, 230, 257, 320, 401, 780]
     mats = [rng.uniform(-1, 1, (m, m)) for m in sizes]
