@@ -1616,7 +1616,8 @@ __global__ void __launch_bounds__(256, 2) lu_big_update_strip_kernel(const int* 
 // in disjoint banks, one wavefront): 8 wavefronts for 32 pairs per lane.
 // Same per-entry operations in the same k order: bit-identical.
 // grid = (tiles_r, blocks), 512 / RT threads. RT = 2 (default, 124 registers,
-// 16 warps per SM) measured 1% faster than RT = 4 (242 registers, 8 warps).
+// 16 warps per SM) measured 1% faster than RT = 4 (242 registers, 8 warps);
+// RT = 2 at 3 CTAs per SM (80 registers, spills) 12% slower.
 template <int RT>
 __global__ void __launch_bounds__(512 / RT, 2) lu_big_update_r4_kernel(const int* __restrict__ blist,
                                                                const int* __restrict__ msz,
