@@ -1173,12 +1173,44 @@ __global__ void __launch_bounds__(256) lu_big_init_kernel(const int* __restrict_
   const int b = blist[bi];
   const int m = msz[b];
   const long long off = lu_off[b], ro = row_off[b];
-  if (src != work)
-    for (long long e = threadIdx.x; e < (long long)m * m; e += blockDim.x) work[off + e] = src[off + e];
-  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+  // one pass over the block: a warp takes 32 consecutive rows (coalesced
+  // columns) over one of 8 column slices, copies them and folds |a_ij| into
+  // the row maximum; the slices combine by an integer max on the bit
+  // patterns (non-negative doubles order as unsigned), exact and
+  // order-independent like fmax
+  unsigned long long* rmu = reinterpret_cast<unsigned long long*>(rowmax + ro);
+  for (int i = threadIdx.x; i < m; i += blockDim.x) rmu[i] = 0ull;
+  __syncthreads();
+  constexpr int S = 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int chunks = (m + 31) / 32;
+  for (int it = warp; it < chunks * S; it += nw) {
+    const int i = (it / S) * 32 + lane, s = it % S;
+    if (i >= m) continue;
+    const int j0 = s * m / S, j1 = (s + 1) * m / S;
     double mx = 0.0;
-    for (int j = 0; j < m; ++j) mx = fmax(mx, fabs(src[off + (size_t)j * m + i]));
-    rowmax[ro + i] = mx;
+    const double* sp = src + off + i;
+    double* wp = work + off + i;
+    // 8 loads in flight before their stores (src may alias work, so the
+    // compiler cannot hoist loads over the stores by itself)
+    constexpr int U = 8;
+    int j = j0;
+    for (; j + U <= j1; j += U) {
+      double v[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) v[q] = sp[(size_t)(j + q) * m];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        if (src != work) wp[(size_t)(j + q) * m] = v[q];
+        mx = fmax(mx, fabs(v[q]));
+      }
+    }
+    for (; j < j1; ++j) {
+      const double v = sp[(size_t)j * m];
+      if (src != work) wp[(size_t)j * m] = v;
+      mx = fmax(mx, fabs(v));
+    }
+    atomicMax(rmu + i, (unsigned long long)__double_as_longlong(mx));
   }
   if (threadIdx.x == 0) bad[bi] = 0;
 }
