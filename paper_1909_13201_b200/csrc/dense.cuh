@@ -1706,7 +1706,7 @@ __global__ void __launch_bounds__(512 / RT, 2) lu_big_update_r4_kernel(const int
       for (int jj = 0; jj < CT; ++jj) acc[i][jj] = nxt[i][jj];
     __syncthreads();
     if (c0 + kBigTile < m) load_tile(c0 + kBigTile);  // in flight during the math below
-#pragma unroll 2
+#pragma unroll 8
     for (int k = 0; k < kBigNB; ++k) {
       double l[RT], u[CT];
 #pragma unroll
