@@ -126,17 +126,8 @@ void fsigpu_blocks_destroy(fsigpu_blocks b);
 #define FSIGPU_MODE_INVERSE 1
 #define FSIGPU_MODE_ASSEMBLED 2
 int fsigpu_set_block_mode(int mode);
-/* L2 residency of the read-only V-cycle data (default off): the level
- * matrices, transfers and block/coarse inverses are packed in one arena and
- * an access-policy window marks it persisting on the hierarchy's stream
- * (default off: measured slower on config 0). */
-int fsigpu_set_l2_persist(int enable);
 /* programmatic dependent launch of the solve-path kernels (default off: measured neutral) */
 int fsigpu_set_pdl(int enable);
-/* default staged-SpMV capacity for level matrices created afterwards
- * (-1: the built-in per-size rule, 0: off, >0: entries per CTA) */
-int fsigpu_set_stage_cap(int cap);
-long long fsigpu_gmg_persist_bytes(fsigpu_gmg g);
 
 /* Level smoother of every smoothed level: 0 = damped Richardson with the
  * create() omega (reference richardson_smooth, src/precond.cpp:305-317; the
@@ -168,10 +159,6 @@ void fsigpu_gmg_destroy(fsigpu_gmg g);
 /* tuning: lanes per row and batch depth of a level matrix's SpMV launches
  * (which: 0 A, 1 FS, 2 A*P, 3 P, 4 R) */
 int fsigpu_gmg_set_launch(fsigpu_gmg g, int level, int which, int lpr, int unroll);
-/* tuning: shared-memory staged SpMV (one bulk copy of a CTA's CSR slice,
- * then a CSR-stream product/row-sum) with at most `cap` entries per CTA;
- * cap 0 selects the per-row vector kernel. Same `which` as set_launch. */
-int fsigpu_gmg_set_staging(fsigpu_gmg g, int level, int which, int cap);
 int fsigpu_gmg_time_kernel(fsigpu_gmg g, int which, int level, int reps, int cold, double* ms,
                            double* bytes);
 
@@ -188,12 +175,6 @@ int fsigpu_gmres_solve_dev(fsigpu_gmres s, const double* d_b, double* d_x, int m
                            fsigpu_gmres_result* res);
 /* graph capture of the Arnoldi step on/off (default on; multi-kernel path) */
 int fsigpu_gmres_set_graphs(fsigpu_gmres s, int enable);
-/* persistent cooperative restart-cycle kernel on/off (opt-in: needs
- * inverse-mode smoothers and V-cycles; env FSIGPU_MEGA=1 enables it at
- * creation). Default is the multi-kernel path with one CUDA graph per
- * restart cycle. */
-int fsigpu_gmres_set_persistent(fsigpu_gmres s, int enable);
-int fsigpu_gmres_is_persistent(fsigpu_gmres s);
 void fsigpu_gmres_destroy(fsigpu_gmres s);
 
 /* ---- instrumentation: accumulated device time per kernel class, measured

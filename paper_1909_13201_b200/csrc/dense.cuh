@@ -739,17 +739,16 @@ __device__ __forceinline__ void lu_write_outputs(const double* A, int m, int b, 
 
 // Factor one block per CTA (DenseFactorization ctor, dense.cpp:31-67), then
 // write the solve format (tile inverses + packed panels, see PanelGeom).
-// src: column-major input (same offsets as lu_off). SMEM: the block is
-// staged in dynamic shared memory (m <= 164 fits 227 KB); otherwise it is
-// factored in `work` (global, column-major, may alias src).
+// src: column-major input (same offsets as lu_off). The block is staged in
+// dynamic shared memory (m <= 164 fits 227 KB).
 // lu_out (optional) receives the bit-exact LU in column-major order.
-// dynamic smem (doubles): [A: m*m, SMEM only][rowmax: m][perm: m ints][scratch: 32*32]
-template <int NT, bool SMEM>
+// dynamic smem (doubles): [A: m*m][rowmax: m][perm: m ints][scratch: 32*32]
+template <int NT>
 __global__ void __launch_bounds__(NT)
     lu_factor_kernel(const int* __restrict__ blist, const int* __restrict__ msz,
                      const long long* __restrict__ lu_off, const long long* __restrict__ row_off,
                      const long long* __restrict__ sf_off, const double* __restrict__ src,
-                     double* __restrict__ work, double* __restrict__ lu_out, double* __restrict__ sf_out,
+                     double* __restrict__ lu_out, double* __restrict__ sf_out,
                      int* __restrict__ piv_out, int* __restrict__ gsrc_out, int* __restrict__ lperm_out,
                      const int* __restrict__ src_pos, int pos_base, int* __restrict__ fail) {
   extern __shared__ __align__(16) double smem[];
@@ -760,14 +759,11 @@ __global__ void __launch_bounds__(NT)
   const int m = msz[b];
   const long long off = lu_off[b];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const size_t a_sz = SMEM ? (size_t)m * m : 0;
-  double* A = SMEM ? smem : work + off;
-  double* rowmax = smem + a_sz;
+  double* A = smem;
+  double* rowmax = smem + (size_t)m * m;
   int* perm = reinterpret_cast<int*>(rowmax + m);
   double* S = rowmax + m + (m + 1) / 2;
-  if (SMEM || src != work) {
-    for (long long e = tid; e < (long long)m * m; e += NT) A[e] = src[off + e];
-  }
+  for (long long e = tid; e < (long long)m * m; e += NT) A[e] = src[off + e];
   __syncthreads();
   for (int i = tid; i < m; i += NT) {
     double mx = 0.0;
@@ -844,7 +840,7 @@ __global__ void __launch_bounds__(NT)
     return;
   }
   __syncthreads();
-  lu_write_outputs<NT, false>(A, m, b, perm, rowmax, S, row_off, lu_off, sf_off, lu_out, SMEM || lu_out != work, sf_out,
+  lu_write_outputs<NT, false>(A, m, b, perm, rowmax, S, row_off, lu_off, sf_off, lu_out, true, sf_out,
                        piv_out, gsrc_out, lperm_out, src_pos, pos_base);
 }
 
@@ -1005,158 +1001,19 @@ __global__ void __launch_bounds__(MM <= 32 ? 32 : 64)
                              gsrc_out, lperm_out, src_pos, pos_base, /*maps_done=*/true);
 }
 
-// Two threads per block row (lu_reg2_kernel): thread (row i, half h) keeps
-// the columns j = 2q + h of row i in registers (a[MM/2]); the pair sits in
-// adjacent lanes. Same rounded operations per entry as LuRegStep (and the
-// reference): the owner of column K (h = K & 1) offers the pivot candidate
-// and forms l = a_iK * (1/pivot), which its partner takes by shuffle; both
-// halves update their own columns. Half the per-thread update work and
-// twice the warps per SM of the one-thread-per-row kernel.
-template <int K, int MM, int NW>
-struct LuReg2Step {
-  static __device__ __forceinline__ bool run(double (&a)[MM / 2], double rmax, int& pos, int m, int t,
-                                             double* slots, int* perm) {
-    constexpr int kNone = 1 << 20;
-    constexpr int kStride = LuSlot<MM>::kStride;
-    constexpr int HO = K & 1, QO = K >> 1;  // owner half and its register index
-    if (K >= m) return false;
-    const int lane = t & 31, warp = t >> 5, h = t & 1;
-    constexpr int buf = K & 1;
-    const bool owner = h == HO;
-    const bool cand = owner && pos >= K && pos < m;
-    const double my_inv = 1.0 / a[QO];
-    const unsigned long long vb = cand ? lu_vkey(fabs(a[QO])) : 0ull;
-    const unsigned hi = (unsigned)(vb >> 32), lo = (unsigned)vb;
-    const unsigned mh = __reduce_max_sync(kFull, hi);
-    const unsigned ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
-    const unsigned key = __reduce_min_sync(kFull, (cand && hi == mh && lo == ml) ? (unsigned)pos : (unsigned)kNone);
-    double* slot = slots + (size_t)(buf * NW + warp) * kStride;
-    if (mh == 0) {
-      if (lane == 0) slot[0] = __longlong_as_double(0);
-    } else if ((unsigned)pos == key) {  // both halves of this warp's best row publish
-      double* r = slot + 2;
-      if (owner) {
-        const int bad = fabs(a[QO]) <= 1e-14 * fmax(rmax, 1e-300);
-        reinterpret_cast<double2*>(slot)[0] =
-            make_double2(__longlong_as_double((long long)vb), __longlong_as_double((long long)(key | (bad << 30))));
-        r[K] = my_inv;
-      }
-#pragma unroll
-      for (int q = 0; q < MM / 2; ++q)
-        if (2 * q + 1 > K) {  // columns 2q + h > K (h = 0 needs 2q > K)
-          if (2 * q > K || h == 1) r[2 * q + h] = a[q];
-        }
-    }
-    __syncthreads();
-    int ws = buf * NW;
-    unsigned long long bv = (unsigned long long)__double_as_longlong(slots[(size_t)ws * kStride]);
-    int bk = (int)__double_as_longlong(slots[(size_t)ws * kStride + 1]);
-#pragma unroll
-    for (int w = 1; w < NW; ++w) {
-      const double2 o = reinterpret_cast<const double2*>(slots + (size_t)(buf * NW + w) * kStride)[0];
-      const unsigned long long ov = (unsigned long long)__double_as_longlong(o.x);
-      const int ok = (int)__double_as_longlong(o.y);
-      if (ov > bv || (ov == bv && (ok & 0x3fffffff) < (bk & 0x3fffffff))) {
-        bv = ov;
-        bk = ok;
-        ws = buf * NW + w;
-      }
-    }
-    const int p = bk & 0x3fffffff;
-    if (t == 0) perm[K] = p;
-    pos = (pos == p) ? K : (pos == K ? p : pos);
-    if (bk >> 30) return true;
-    const double* r = slots + (size_t)ws * kStride + 2;
-    const bool active = pos > K && pos < m;
-    // multiplier formed by the owner half, shared with its partner
-    const double lo_own = (owner && active) ? mul_rn(a[QO], r[K]) : 0.0;
-    const double lo_partner = __shfl_xor_sync(kFull, lo_own, 1);  // every lane takes part
-    const double l = owner ? lo_own : lo_partner;
-    if (active) {
-      if (owner) a[QO] = l;
-#pragma unroll
-      for (int q = 0; q < MM / 2; ++q)
-        if (2 * q + 1 > K) {
-          if (2 * q > K || h == 1) a[q] = sub_rn(a[q], mul_rn(l, r[2 * q + h]));
-        }
-    }
-    if constexpr (K + 1 < MM) return LuReg2Step<K + 1, MM, NW>::run(a, rmax, pos, m, t, slots, perm);
-    return false;
-  }
-};
-
-// dynamic smem as lu_reg_kernel: [A: m*m][scratch: m][perm: m ints][S: 32*kTileLd]
-template <int MM>
-__global__ void __launch_bounds__(128, 4)
-    lu_reg2_kernel(const int* __restrict__ blist, const int* __restrict__ msz, const long long* __restrict__ lu_off,
-                   const long long* __restrict__ row_off, const long long* __restrict__ sf_off,
-                   const double* __restrict__ src, double* __restrict__ lu_out, double* __restrict__ sf_out,
-                   int* __restrict__ piv_out, int* __restrict__ gsrc_out, int* __restrict__ lperm_out,
-                   const int* __restrict__ src_pos, int pos_base, int* __restrict__ fail) {
-  static_assert(MM % 2 == 0 && MM <= 64 && MM > 32, "two threads per row: 33..64 rows");
-  constexpr int NT = 128;
-  constexpr int NW = NT / 32;
-  constexpr int kNone = 1 << 20;
-  extern __shared__ __align__(16) double smem[];
-  __shared__ __align__(16) double s_slots[2 * NW * LuSlot<MM>::kStride];
-  const int b = blist[blockIdx.x];
-  const int m = msz[b];
-  const long long off = lu_off[b];
-  const int t = threadIdx.x;
-  const int i = t >> 1, h = t & 1;
-  double* A = smem;
-  double* scratch = smem + (size_t)m * m;
-  int* perm = reinterpret_cast<int*>(scratch + m);
-  double* S = scratch + m + (m + 1) / 2;
-
-  double a[MM / 2];
-  const bool valid = i < m;
-#pragma unroll
-  for (int q = 0; q < MM / 2; ++q) {
-    const int j = 2 * q + h;
-    a[q] = (valid && j < m) ? __ldg(src + off + (size_t)j * m + i) : 0.0;
-  }
-  double rmax = 0.0;
-#pragma unroll
-  for (int q = 0; q < MM / 2; ++q) rmax = fmax(rmax, fabs(a[q]));
-  rmax = fmax(rmax, __shfl_xor_sync(kFull, rmax, 1));
-  int pos = valid ? i : kNone;
-  if (LuReg2Step<0, MM, NW>::run(a, rmax, pos, m, t, s_slots, perm)) {
-    if (t == 0) atomicMin(fail, b);
-    return;
-  }
-  const long long ro = row_off[b];
-  if (valid) {
-#pragma unroll
-    for (int q = 0; q < MM / 2; ++q) {
-      const int j = 2 * q + h;
-      if (j < m) A[(size_t)j * m + pos] = a[q];
-    }
-    if (h == 0) {
-      gsrc_out[ro + pos] = src_pos ? src_pos[ro + i] + pos_base : (int)(ro + i);
-      lperm_out[ro + pos] = i;
-      piv_out[ro + i] = perm[i];
-    }
-  }
-  __syncthreads();
-  lu_write_outputs<NT, true>(A, m, b, perm, scratch, S, row_off, lu_off, sf_off, lu_out, true, sf_out, piv_out,
-                             gsrc_out, lperm_out, src_pos, pos_base, /*maps_done=*/true);
-}
-
 // ---------------------------------------------------------------- blocked LU (m > 164)
 // Right-looking LU in panels of kBigNB columns for the large blocks (the
 // pure-DD Vanka patches of config 4, m ~ 500-780), factored in place in
 // global memory (column-major), one launch pair per panel for the whole
 // batch:
-//   lu_big_panel_kernel  (one CTA per block): for each panel column k the
-//     pivot search (largest |a_ik|, lowest row on ties), the swap of the
-//     whole rows k and p (and of their original row maxima), the singular
-//     test, l = a_ik * (1/pivot), the rank-1 update of the remaining panel
+//   lu_big_panel_smem_kernel (one CTA per block): for each panel column k
+//     the pivot search (largest |a_ik|, lowest row on ties), the swap of
+//     rows k and p (and of their original row maxima), the singular test,
+//     l = a_ik * (1/pivot), the rank-1 update of the remaining panel
 //     columns; then the panel rows of the trailing columns (U12): per
 //     column, a_ij -= l_ik * a_kj for k = k0..i-1 in order;
-//   lu_big_update_kernel (a CTA per 64x64 tile of A22): a_ij -= l_ik * u_kj
-//     for the panel's k in order, non-fused, from shared-memory tiles of
-//     L21 and U12.
+//   lu_big_update_r4_kernel (a CTA per 64-row strip of A22): a_ij -= l_ik *
+//     u_kj for the panel's k in order, non-fused, from register tiles.
 // Every entry therefore receives the reference's rounded updates in the
 // reference's k order (DenseFactorization, dense.cpp:31-67): the factors
 // are bit-identical. Row swaps move whole rows immediately, as the
@@ -1215,117 +1072,6 @@ __global__ void __launch_bounds__(256) lu_big_init_kernel(const int* __restrict_
   if (threadIdx.x == 0) bad[bi] = 0;
 }
 
-__global__ void __launch_bounds__(256, 2) lu_big_panel_kernel(const int* __restrict__ blist, const int* __restrict__ msz,
-                                                           const long long* __restrict__ lu_off,
-                                                           const long long* __restrict__ row_off, double* work,
-                                                           double* rowmax, int* __restrict__ piv, int* bad,
-                                                           int* __restrict__ fail, int k0) {
-  const int bi = blockIdx.x;
-  const int b = blist[bi];
-  const int m = msz[b];
-  if (k0 >= m || bad[bi]) return;
-  const long long off = lu_off[b], ro = row_off[b];
-  double* A = work + off;
-  double* rm = rowmax + ro;
-  const int kb = min(kBigNB, m - k0);
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  __shared__ double s_v[8];
-  __shared__ int s_i[8];
-  __shared__ int s_p, s_bad;
-  for (int k = k0; k < k0 + kb; ++k) {
-    // pivot: max |a_ik| over i >= k, lowest i among equals (the reference's
-    // first-strictly-larger scan from i = k)
-    double best = -1.0;
-    int bidx = m;
-    for (int i = k + t; i < m; i += blockDim.x) {
-      const double v = fabs(A[(size_t)k * m + i]);
-      if (v > best) {
-        best = v;
-        bidx = i;
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(kFull, best, o);
-      const int oi = __shfl_xor_sync(kFull, bidx, o);
-      if (ob > best || (ob == best && oi < bidx)) {
-        best = ob;
-        bidx = oi;
-      }
-    }
-    if (lane == 0) {
-      s_v[warp] = best;
-      s_i[warp] = bidx;
-    }
-    __syncthreads();
-    if (t == 0) {
-      double bv = s_v[0];
-      int bx = s_i[0];
-      for (int w = 1; w < 8; ++w)
-        if (s_v[w] > bv || (s_v[w] == bv && s_i[w] < bx)) {
-          bv = s_v[w];
-          bx = s_i[w];
-        }
-      int p = bx < m ? bx : k;
-      if (!(fabs(A[(size_t)k * m + k]) < bv)) p = k;
-      s_p = p;
-      // singular test on the pivot row's own original maximum (dense.cpp:57)
-      const double pivot = A[(size_t)k * m + p];
-      s_bad = fabs(pivot) <= 1e-14 * fmax(rm[p], 1e-300);
-      piv[ro + k] = p;
-    }
-    __syncthreads();
-    if (s_bad) {
-      if (t == 0) {
-        bad[bi] = 1;
-        atomicMin(fail, b);
-      }
-      return;
-    }
-    const int p = s_p;
-    if (p != k) {
-      for (int j = t; j < m; j += blockDim.x) {
-        const double a0 = A[(size_t)j * m + k];
-        A[(size_t)j * m + k] = A[(size_t)j * m + p];
-        A[(size_t)j * m + p] = a0;
-      }
-      if (t == 0) {
-        const double r0 = rm[k];
-        rm[k] = rm[p];
-        rm[p] = r0;
-      }
-    }
-    __syncthreads();
-    const double inv = 1.0 / A[(size_t)k * m + k];
-    for (int i = k + 1 + t; i < m; i += blockDim.x) A[(size_t)k * m + i] = mul_rn(A[(size_t)k * m + i], inv);
-    __syncthreads();
-    // rank-1 update of the panel columns right of k
-    const int nc = k0 + kb - (k + 1);
-    const int nr = m - (k + 1);
-    for (int e = t; e < nc * nr; e += blockDim.x) {
-      const int jj = k + 1 + e / nr, i = k + 1 + e % nr;
-      A[(size_t)jj * m + i] = sub_rn(A[(size_t)jj * m + i], mul_rn(A[(size_t)k * m + i], A[(size_t)jj * m + k]));
-    }
-    __syncthreads();
-  }
-  // U12: panel rows of the trailing columns, one column per thread
-  for (int j = k0 + kb + t; j < m; j += blockDim.x) {
-    double u[kBigNB];
-#pragma unroll
-    for (int q = 0; q < kBigNB; ++q) u[q] = q < kb ? A[(size_t)j * m + k0 + q] : 0.0;
-#pragma unroll
-    for (int i = 1; i < kBigNB; ++i)
-#pragma unroll
-      for (int q = 0; q < i; ++q)
-        if (i < kb) u[i] = sub_rn(u[i], mul_rn(A[(size_t)(k0 + q) * m + k0 + i], u[q]));
-#pragma unroll
-    for (int q = 1; q < kBigNB; ++q)
-      if (q < kb) A[(size_t)j * m + k0 + q] = u[q];
-  }
-}
-
-// Shared-memory panel variant of lu_big_panel_kernel (default for m <= 880):
-// rows k0..m-1 of the panel's kb columns are staged in dynamic shared memory
 // (column-major, ld = m - k0; 200 KB at m = 780), so the 32 pivot steps
 // (search, swap, scale, rank-1 update of the panel) run out of shared memory
 // instead of making L2 round trips per column. The row swaps of the columns
@@ -1505,157 +1251,21 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
   }
 }
 
-// A22 -= L21 * U12 for panel k0 (full panels only: the last, partial panel
-// has no trailing block). grid = (tiles_r * tiles_c, blocks).
-__global__ void __launch_bounds__(256, 3) lu_big_update_kernel(const int* __restrict__ blist,
-                                                            const int* __restrict__ msz,
-                                                            const long long* __restrict__ lu_off, double* work,
-                                                            const int* __restrict__ bad, int k0, int tiles_c) {
-  const int bi = blockIdx.y;
-  const int b = blist[bi];
-  const int m = msz[b];
-  const int r0 = k0 + kBigNB + (blockIdx.x / tiles_c) * kBigTile;
-  const int c0 = k0 + kBigNB + (blockIdx.x % tiles_c) * kBigTile;
-  if (r0 >= m || c0 >= m || bad[bi]) return;
-  double* A = work + lu_off[b];
-  __shared__ __align__(16) double Ls[kBigNB][kBigTile];
-  __shared__ __align__(16) double Us[kBigNB][kBigTile];
-  const int t = threadIdx.x;
-  for (int e = t; e < kBigNB * kBigTile; e += 256) {
-    const int k = e / kBigTile, i = e % kBigTile;  // L21: column k0+k, row r0+i (coalesced over i)
-    Ls[k][i] = r0 + i < m ? A[(size_t)(k0 + k) * m + r0 + i] : 0.0;
-  }
-  for (int e = t; e < kBigNB * kBigTile; e += 256) {
-    const int j = e / kBigNB, k = e % kBigNB;  // U12: row k0+k, column c0+j (coalesced over k)
-    Us[k][j] = c0 + j < m ? A[(size_t)(c0 + j) * m + k0 + k] : 0.0;
-  }
-  __syncthreads();
-  // thread = one row x 16 columns of the tile: the 32 rows of a warp are
-  // consecutive (coalesced column-major loads/stores of A22), the warp's
-  // U12 reads are broadcasts, its L21 reads conflict-free
-  const int ri = t & (kBigTile - 1), cg = t / kBigTile;  // row, 16-column group
-  const int r = r0 + ri;
-  constexpr int TC = kBigTile / 4;
-  double acc[TC];
-#pragma unroll
-  for (int jj = 0; jj < TC; ++jj) {
-    const int c = c0 + cg * TC + jj;
-    acc[jj] = (r < m && c < m) ? A[(size_t)c * m + r] : 0.0;
-  }
-#pragma unroll 4
-  for (int k = 0; k < kBigNB; ++k) {
-    const double l = Ls[k][ri];
-    double u[TC];
-#pragma unroll
-    for (int q = 0; q < TC; q += 2) {
-      const double2 uu = *reinterpret_cast<const double2*>(&Us[k][cg * TC + q]);
-      u[q] = uu.x;
-      u[q + 1] = uu.y;
-    }
-#pragma unroll
-    for (int jj = 0; jj < TC; ++jj) acc[jj] = sub_rn(acc[jj], mul_rn(l, u[jj]));
-  }
-#pragma unroll
-  for (int jj = 0; jj < TC; ++jj) {
-    const int c = c0 + cg * TC + jj;
-    if (r < m && c < m) A[(size_t)c * m + r] = acc[jj];
-  }
-}
-
-// Row-strip variant of lu_big_update_kernel (default): a CTA owns 64 rows of
-// A22 and walks all its 64-column tiles, keeping the L21 strip in shared
-// memory and prefetching the next tile (its A22 values into registers, its
-// U12 slice into registers, stored to shared memory after the current
-// tile's math), so the global loads overlap the fp64 work instead of every
-// 64x64 tile paying a full load latency with nothing to hide it. Same
-// per-entry operations in the same k order: bit-identical.
-// grid = (tiles_r, blocks).
-__global__ void __launch_bounds__(256, 2) lu_big_update_strip_kernel(const int* __restrict__ blist,
-                                                                  const int* __restrict__ msz,
-                                                                  const long long* __restrict__ lu_off,
-                                                                  double* work, const int* __restrict__ bad, int k0) {
-  const int bi = blockIdx.y;
-  const int b = blist[bi];
-  const int m = msz[b];
-  const int r0 = k0 + kBigNB + blockIdx.x * kBigTile;
-  const int cbeg = k0 + kBigNB;
-  if (r0 >= m || cbeg >= m || bad[bi]) return;
-  double* A = work + lu_off[b];
-  __shared__ __align__(16) double Ls[kBigNB][kBigTile];
-  __shared__ __align__(16) double Us[kBigNB][kBigTile];
-  const int t = threadIdx.x;
-  const int ri = t & (kBigTile - 1), cg = t / kBigTile;
-  const int r = r0 + ri;
-  constexpr int TC = kBigTile / 4;
-  constexpr int UPT = kBigNB * kBigTile / 256;  // U12 values per thread per tile
-  for (int e = t; e < kBigNB * kBigTile; e += 256) {
-    const int k = e / kBigTile, i = e % kBigTile;
-    Ls[k][i] = r0 + i < m ? A[(size_t)(k0 + k) * m + r0 + i] : 0.0;
-  }
-  double nxt[TC], un[UPT];
-  auto load_tile = [&](int c0) {
-#pragma unroll
-    for (int jj = 0; jj < TC; ++jj) {
-      const int c = c0 + cg * TC + jj;
-      nxt[jj] = (r < m && c < m) ? A[(size_t)c * m + r] : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < UPT; ++q) {
-      const int e = t + q * 256;
-      const int j = e / kBigNB, k = e % kBigNB;  // coalesced over k
-      un[q] = c0 + j < m ? A[(size_t)(c0 + j) * m + k0 + k] : 0.0;
-    }
-  };
-  load_tile(cbeg);
-  for (int c0 = cbeg; c0 < m; c0 += kBigTile) {
-    __syncthreads();  // previous tile's Us reads are done
-#pragma unroll
-    for (int q = 0; q < UPT; ++q) {
-      const int e = t + q * 256;
-      Us[e % kBigNB][e / kBigNB] = un[q];
-    }
-    double acc[TC];
-#pragma unroll
-    for (int jj = 0; jj < TC; ++jj) acc[jj] = nxt[jj];
-    __syncthreads();
-    if (c0 + kBigTile < m) load_tile(c0 + kBigTile);  // in flight during the math below
-#pragma unroll 4
-    for (int k = 0; k < kBigNB; ++k) {
-      const double l = Ls[k][ri];
-      double u[TC];
-#pragma unroll
-      for (int q = 0; q < TC; q += 2) {
-        const double2 uu = *reinterpret_cast<const double2*>(&Us[k][cg * TC + q]);
-        u[q] = uu.x;
-        u[q + 1] = uu.y;
-      }
-#pragma unroll
-      for (int jj = 0; jj < TC; ++jj) acc[jj] = sub_rn(acc[jj], mul_rn(l, u[jj]));
-    }
-#pragma unroll
-    for (int jj = 0; jj < TC; ++jj) {
-      const int c = c0 + cg * TC + jj;
-      if (r < m && c < m) A[(size_t)c * m + r] = acc[jj];
-    }
-  }
-}
-
-// Row-strip update with a 4-row x 8-column register tile per thread (default).
-// lu_big_update_strip_kernel's 1 x 16 tile is shared-memory bound (ncu: L1/TEX
-// 86%, 10 wavefronts per k for 16 mul/sub pairs per lane); here a warp is 16
+// A 1 x 16 strip tile was shared-memory bound (ncu: L1/TEX 86%, 10
+// wavefronts per k for 16 mul/sub pairs per lane); here a warp is 16
 // row lanes x 2 column groups, so per k it reads 4 L21 values (16 distinct
 // doubles each, one wavefront) and 4 double2 U12 broadcasts (two addresses
 // in disjoint banks, one wavefront): 8 wavefronts for 32 pairs per lane.
 // Same per-entry operations in the same k order: bit-identical.
-// grid = (tiles_r, blocks), 512 / RT threads. RT = 2 (default, 124 registers,
-// 16 warps per SM) measured 1% faster than RT = 4 (242 registers, 8 warps);
-// RT = 2 at 3 CTAs per SM (80 registers, spills) 12% slower.
-template <int RT>
-__global__ void __launch_bounds__(512 / RT, 2) lu_big_update_r4_kernel(const int* __restrict__ blist,
+// grid = (tiles_r, blocks), 256 threads, RT = 2 rows x 8 columns per thread
+// (124 registers, 16 warps per SM; measured 1% faster than 4 x 8 tiles at
+// 242 registers; 2 x 8 at 3 CTAs per SM spills and runs 12% slower).
+constexpr int kUpdRT = 2;
+__global__ void __launch_bounds__(512 / kUpdRT, 2) lu_big_update_r4_kernel(const int* __restrict__ blist,
                                                                const int* __restrict__ msz,
                                                                const long long* __restrict__ lu_off,
                                                                double* work, const int* __restrict__ bad, int k0) {
-  constexpr int NT = 512 / RT, CT = 8;  // RT rows x 8 columns per thread
+  constexpr int RT = kUpdRT, NT = 512 / RT, CT = 8;  // RT rows x 8 columns per thread
   const int bi = blockIdx.y;
   const int b = blist[bi];
   const int m = msz[b];

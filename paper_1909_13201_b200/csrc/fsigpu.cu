@@ -26,7 +26,6 @@
 #include "common.cuh"
 #include "dense.cuh"
 #include "krylov.cuh"
-#include "mega.cuh"
 #include "sparse.cuh"
 #include "mr.cuh"
 
@@ -153,21 +152,7 @@ static int choose_lpr(long long rows, long long nnz) {
   while (l < 32 && want > l * 1.41421356) l *= 2;
   return l;
 }
-static int choose_unroll(long long rows) {
-  static const int pair = [] {
-    const char* e = std::getenv("FSIGPU_SPMV_PAIR");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (pair && rows >= 16384) return pair;  // 22 or 24 (A/B of the paired kernel)
-  return rows < 16384 ? 8 : 4;
-}
-// Staged-kernel capacity (entries per CTA); 0 keeps csr_kernel.
-static int g_stage_cap = 0;
-static int choose_stage_cap(long long rows, long long nnz) {
-  (void)rows;
-  (void)nnz;
-  return g_stage_cap > 0 ? g_stage_cap : 0;
-}
+static int choose_unroll(long long rows) { return rows < 16384 ? 8 : 4; }
 
 struct Csr {
   int rows = 0, cols = 0;
@@ -189,8 +174,7 @@ struct Csr {
     for (int i = 0; i < r; ++i) require(p[i] <= p[i + 1], "csr: offsets not nondecreasing");
     for (long long k = 0; k < nnz; ++k) require(ix[k] >= 0 && ix[k] < c, "csr: column range");
     ptr.upload(p, (size_t)r + 1, s);
-    // padded by 4 entries: the staged kernel's bulk copies round their
-    // ranges out to 16-byte boundaries
+    // padded by 4 entries (the paired-load kernels read 16-byte pairs)
     idx.alloc((size_t)nnz + 4);
     val.alloc((size_t)nnz + 4);
     if (nnz) {
@@ -204,7 +188,6 @@ struct Csr {
       h_idx.assign(ix, ix + nnz);
       h_val.assign(v, v + nnz);
     }
-    stage(choose_stage_cap(r, nnz), s);
     FSI_CUDA(cudaStreamSynchronize(s));
   }
   // take ownership of device CSR arrays built on the GPU
@@ -224,96 +207,16 @@ struct Csr {
     lpr = choose_lpr(r, nnz);
     unroll = choose_unroll(r);
     h_ptr = ptr.download();
-    stage(choose_stage_cap(r, nnz), 0);
   }
-  // Staged (shared-memory CSR-stream) launch: CTA row ranges holding at most
-  // `cap` entries each. cap 0, or a row longer than cap, selects csr_kernel.
-  DevBuf<int> rb;
-  int nstage = 0, cap = 0, slpr = 4;
-  void stage(int cap_, cudaStream_t s) {
-    nstage = 0;
-    cap = 0;
-    if (cap_ <= 0 || rows == 0) return;
-    std::vector<int> b{0};
-    int r = 0;
-    while (r < rows) {
-      const int begin = r;
-      long long e = 0;
-      while (r < rows && e + (h_ptr[r + 1] - h_ptr[r]) <= cap_) e += h_ptr[r + 1] - h_ptr[r], ++r;
-      if (r == begin) return;  // a row longer than cap
-      b.push_back(r);
-    }
-    rb.upload(b, s);
-    FSI_CUDA(cudaStreamSynchronize(s));
-    nstage = (int)b.size() - 1;
-    cap = cap_;
-    // phase-2 lanes per row: ~4 products per lane
-    const double want = (double)nnz / rows / 4.0;
-    slpr = 1;
-    while (slpr < 32 && want > slpr * 1.41421356) slpr *= 2;
-  }
-  size_t stage_smem() const { return 8 * (size_t)((cap + 3) & ~1) + 4 * (size_t)(cap + 8); }
   double bytes(bool resid) const {
-    const double ib = c16 ? 2.0 * nnz + 16.0 * rows : 4.0 * nnz;  // index stream (+ window bases)
-    return 8.0 * nnz + ib + 4.0 * (rows + 1) + 8.0 * cols + 8.0 * rows + (resid ? 8.0 * rows : 0.0);
-  }
-  // CSR16 (sparse.cuh): 16-bit window codes + 4 window bases per row instead
-  // of 32-bit columns. The 32-bit idx is released; only the vector kernel
-  // runs on it (no staged / paired variants).
-  bool c16 = false;
-  DevBuf<unsigned short> code16;
-  DevBuf<int4> bases16;
-  bool compress16(cudaStream_t s) {
-    if (!rows || nstage) return false;
-    DevBuf<unsigned short> code;
-    DevBuf<int4> bs;
-    DevBuf<int> fail;
-    code.alloc((size_t)nnz + 4);
-    bs.alloc((size_t)rows);
-    fail.alloc(1);
-    FSI_CUDA(cudaMemsetAsync(fail.p, 0, sizeof(int), s));
-    c16_compress_kernel<<<ceil_div(rows, 256), 256, 0, s>>>(rows, ptr.p, idx.p, code.p, bs.p, fail.p);
-    FSI_CHECK_LAUNCH();
-    int h_fail = 0;
-    FSI_CUDA(cudaMemcpyAsync(&h_fail, fail.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-    FSI_CUDA(cudaStreamSynchronize(s));
-    if (h_fail) return false;
-    code16 = std::move(code);
-    bases16 = std::move(bs);
-    c16 = true;
-    return true;
+    return 12.0 * nnz + 4.0 * (rows + 1) + 8.0 * cols + 8.0 * rows + (resid ? 8.0 * rows : 0.0);
   }
   int unroll = 4;  // entries per lane per predicated batch (4 or 8); 22/24: paired loads, 2/4 pairs
   template <class G, class E>
   void launch(G g, E e, cudaStream_t s) const {
     if (!rows) return;
-    if (nstage) {
-      launch_staged(g, e, s);
-      return;
-    }
     const long long threads = (long long)rows * lpr;
     const int grid = ceil_div(threads, 256);
-    if (c16) {
-#define FSI_C16(LP, UU) launch_k(csr16_kernel<LP, G, E, UU>, dim3(grid), dim3(256), 0, s, rows, (const int*)ptr.p, (const unsigned short*)code16.p, (const int4*)bases16.p, (const double*)val.p, g, e)
-#define FSI_C16_L(UU)                \
-  switch (lpr) {                     \
-    case 2: FSI_C16(2, UU); break;   \
-    case 4: FSI_C16(4, UU); break;   \
-    case 8: FSI_C16(8, UU); break;   \
-    case 16: FSI_C16(16, UU); break; \
-    default: FSI_C16(32, UU); break; \
-  }
-      if (unroll == 8) {
-        FSI_C16_L(8)
-      } else {
-        FSI_C16_L(4)
-      }
-#undef FSI_C16_L
-#undef FSI_C16
-      FSI_CHECK_LAUNCH();
-      counted();
-      return;
-    }
 #define FSI_CSR(LP, UU) launch_k(csr_kernel<LP, G, E, UU>, dim3(grid), dim3(256), 0, s, rows, (const int*)ptr.p, (const int*)idx.p, (const double*)val.p, g, e)
 #define FSI_CSRP(LP, UU) launch_k(csr_pair_kernel<LP, G, E, UU>, dim3(grid), dim3(256), 0, s, rows, (const int*)ptr.p, (const int*)idx.p, (const double*)val.p, g, e)
     if (unroll == 22 || unroll == 24) {  // paired loads, 2 or 4 pairs per lane per batch
@@ -358,31 +261,6 @@ struct Csr {
     FSI_CHECK_LAUNCH();
     counted();
   }
-  template <int LP, class G, class E>
-  void launch_staged_lp(G g, E e, cudaStream_t s) const {
-    static size_t attr = 48 * 1024;
-    const size_t sm = stage_smem();
-    if (sm > attr) {
-      FSI_CUDA(cudaFuncSetAttribute(csr_staged_kernel<LP, G, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)sm));
-      attr = sm;
-    }
-    launch_k(csr_staged_kernel<LP, G, E>, dim3(nstage), dim3(256), sm, s, (const int*)rb.p, (const int*)ptr.p,
-             (const int*)idx.p, (const double*)val.p, cap, g, e);
-  }
-  template <class G, class E>
-  void launch_staged(G g, E e, cudaStream_t s) const {
-    switch (slpr) {
-      case 1: launch_staged_lp<1>(g, e, s); break;
-      case 2: launch_staged_lp<2>(g, e, s); break;
-      case 4: launch_staged_lp<4>(g, e, s); break;
-      case 8: launch_staged_lp<8>(g, e, s); break;
-      case 16: launch_staged_lp<16>(g, e, s); break;
-      default: launch_staged_lp<32>(g, e, s); break;
-    }
-    FSI_CHECK_LAUNCH();
-    counted();
-  }
 };
 
 // ------------------------------------------------------------ dense blocks
@@ -392,43 +270,12 @@ struct Csr {
 enum BlockMode { kModeLU = 0, kModeInverse = 1, kModeAssembled = 2 };
 static int g_default_mode = kModeAssembled;
 
-// Blocks above 164 rows: blocked LU (default) or the single-CTA in-place
-// kernel (FSIGPU_LU_BIG_OLD=1, A/B).
-static bool lu_big_old() {
-  const char* e = std::getenv("FSIGPU_LU_BIG_OLD");
-  return e && e[0] == '1';
-}
-
-// Register LU with two threads per row for blocks of 33..64 rows: opt-in
-// (FSIGPU_LU_TWO=1). Bit-identical, but the config-1 LU takes 39.2 ms
-// against 30.1 ms with one thread per row: four warps per block make the
-// per-step barrier and the 4-slot pivot combine longer, and at 128
-// registers only 4 CTAs (16 warps) fit per SM.
-static bool lu_two_per_row() {
-  const char* e = std::getenv("FSIGPU_LU_TWO");
-  return e && e[0] == '1';
-}
-
-// Small-block LU variant: register-resident rows (default) or the
-// shared-memory CTA kernel (FSIGPU_LU_SMEM=1, kept for A/B measurement).
-static bool lu_register_path() {
-  const char* e = std::getenv("FSIGPU_LU_SMEM");
-  return !(e && e[0] == '1');
-}
-
 // FSIGPU_FORCE_BIG=1: take the large-system kernel variants at any size
 // (k_spmv_dots_s, the cp.async Arnoldi stages, paired SpMV / A*P loads), so
 // the parity tests cover them on the small committed fixtures.
 static bool force_big() {
   const char* e = std::getenv("FSIGPU_FORCE_BIG");
   return e && e[0] == '1';
-}
-
-// Large-system Arnoldi (B)/(C) through cp.async row stages (default);
-// FSIGPU_ARNOLDI_CP=0 selects the register-row variants for A/B.
-static bool arnoldi_cp() {
-  const char* e = std::getenv("FSIGPU_ARNOLDI_CP");
-  return !(e && e[0] == '0');
 }
 
 struct Blocks {
@@ -468,7 +315,7 @@ struct Blocks {
     pipe_cap = 2;
     for (long long b = 0; b < nb; ++b) {
       const long long mm = sizes[b];
-      require(mm >= 1 && mm <= kLargeMax, "blocks: block size must be in [1, 1024]");
+      require(mm >= 1 && mm <= kBigPanelMaxM, "blocks: block size must be in [1, 850]");
       h_lu_off[b + 1] = h_lu_off[b] + mm * mm;
       h_row_off[b + 1] = h_row_off[b] + mm;
       h_sf_off[b + 1] = h_sf_off[b] + even_up((int)solve_format_size((int)mm));
@@ -537,11 +384,10 @@ struct Blocks {
       h_cls[c].clear();
       cls_max[c] = 0;
     }
-    const bool reg = lu_register_path();
     for (long long b = 0; b < nb; ++b) {
       const int mm = h_m[b];
       int c = mm <= 164 ? 5 : 6;
-      if (reg && mm <= 64) {
+      if (mm <= 64) {
         c = 0;
         while (mm > kRegMM[c]) ++c;
       }
@@ -562,15 +408,6 @@ struct Blocks {
   void launch_reg(int which, const double* src, double* luo, const int* src_pos, int pos_base, cudaStream_t s) {
     const int mx = cls_max[which];
     const size_t sm = (size_t)((size_t)mx * mx + mx + (mx + 1) / 2 + 32 * kTileLd + 8) * 8;
-    if constexpr (MM > 32) {
-      if (lu_two_per_row()) {
-        auto k2 = lu_reg2_kernel<MM>;
-        FSI_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        k2<<<(int)h_cls[which].size(), 128, sm, s>>>(d_cls[which], m.p, lu_off.p, row_off.p, sf_off.p, src, luo,
-                                                   sf.p, piv.p, gsrc.p, lperm.p, src_pos, pos_base, fail.p);
-        return;
-      }
-    }
     auto k = lu_reg_kernel<MM>;
     FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     k<<<(int)h_cls[which].size(), MM <= 32 ? 32 : 64, sm, s>>>(d_cls[which], m.p, lu_off.p, row_off.p,
@@ -582,9 +419,7 @@ struct Blocks {
     const int big = INT_MAX;
     FSI_CUDA(cudaMemcpyAsync(fail.p, &big, sizeof(int), cudaMemcpyHostToDevice, s));
     double* luo = keep_lu ? lu.p : nullptr;
-    auto smem_bytes = [](int mx, bool staged) {
-      return (size_t)((staged ? (size_t)mx * mx : 0) + mx + (mx + 1) / 2 + 32 * 33 + 8) * 8;
-    };
+    auto smem_bytes = [](int mx) { return (size_t)((size_t)mx * mx + mx + (mx + 1) / 2 + 32 * 33 + 8) * 8; };
     auto run = [&](int which) {
       if (h_cls[which].empty()) return;
       const int grid = (int)h_cls[which].size();
@@ -597,62 +432,29 @@ struct Blocks {
         case 3: launch_reg<56>(which, src, luo, src_pos, pos_base, s); break;
         case 4: launch_reg<64>(which, src, luo, src_pos, pos_base, s); break;
         case 5: {
-          const size_t sm = smem_bytes(mx, true);
-          if (mx <= 64) {
-            auto k = lu_factor_kernel<128, true>;
-            FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            k<<<grid, 128, sm, s>>>(bl, m.p, lu_off.p, row_off.p, sf_off.p, src, nullptr, luo, sf.p, piv.p, gsrc.p,
-                                    lperm.p, src_pos, pos_base, fail.p);
-          } else {
-            auto k = lu_factor_kernel<256, true>;
-            FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            k<<<grid, 256, sm, s>>>(bl, m.p, lu_off.p, row_off.p, sf_off.p, src, nullptr, luo, sf.p, piv.p, gsrc.p,
-                                    lperm.p, src_pos, pos_base, fail.p);
-          }
+          const size_t sm = smem_bytes(mx);
+          auto k = lu_factor_kernel<256>;
+          FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+          k<<<grid, 256, sm, s>>>(bl, m.p, lu_off.p, row_off.p, sf_off.p, src, luo, sf.p, piv.p, gsrc.p, lperm.p,
+                                  src_pos, pos_base, fail.p);
           break;
         }
         default: {
-          if (lu_big_old()) {
-            const size_t sm = smem_bytes(mx, false);
-            auto k = lu_factor_kernel<256, false>;
-            FSI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            k<<<grid, 256, sm, s>>>(bl, m.p, lu_off.p, row_off.p, sf_off.p, src, lu.p, lu.p, sf.p, piv.p, gsrc.p,
-                                    lperm.p, src_pos, pos_base, fail.p);
-            break;
-          }
           // blocked LU in global memory: init, (panel, trailing update) per
           // 32-column panel for the whole class, then the outputs
           if (big_rowmax.n < (size_t)total_rows) big_rowmax.alloc((size_t)total_rows);
           if (big_bad.n < (size_t)grid) big_bad.alloc((size_t)grid);
           lu_big_init_kernel<<<grid, 256, 0, s>>>(bl, m.p, lu_off.p, row_off.p, src, lu.p, big_rowmax.p, big_bad.p);
-          const char* pg = std::getenv("FSIGPU_LU_PANEL_GLOBAL");
-          const bool smem_panel = mx <= kBigPanelMaxM && !(pg && std::atoi(pg) != 0);
-          if (smem_panel)
-            FSI_CUDA(cudaFuncSetAttribute(lu_big_panel_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)((size_t)mx * (kBigNB + 1) * 8)));
+          require(mx <= kBigPanelMaxM, "blocks: block size above the blocked-LU panel limit");
+          FSI_CUDA(cudaFuncSetAttribute(lu_big_panel_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)((size_t)mx * (kBigNB + 1) * 8)));
           for (int k0 = 0; k0 < mx; k0 += kBigNB) {
-            if (smem_panel)
-              lu_big_panel_smem_kernel<<<grid, kPanelThreads, (size_t)(mx - k0) * (kBigNB + 1) * 8, s>>>(
-                  bl, m.p, lu_off.p, row_off.p, lu.p, big_rowmax.p, piv.p, big_bad.p, fail.p, k0);
-            else
-              lu_big_panel_kernel<<<grid, 256, 0, s>>>(bl, m.p, lu_off.p, row_off.p, lu.p, big_rowmax.p, piv.p,
-                                                       big_bad.p, fail.p, k0);
+            lu_big_panel_smem_kernel<<<grid, kPanelThreads, (size_t)(mx - k0) * (kBigNB + 1) * 8, s>>>(
+                bl, m.p, lu_off.p, row_off.p, lu.p, big_rowmax.p, piv.p, big_bad.p, fail.p, k0);
             if (k0 + kBigNB < mx) {
+              // 2-row x 8-column register tiles, 256 threads
               const int tiles = ceil_div(mx - k0 - kBigNB, kBigTile);
-              const char* ut = std::getenv("FSIGPU_LU_UPDATE_TILES");
-              const char* u1 = std::getenv("FSIGPU_LU_UPDATE_R1");
-              if (ut && std::atoi(ut) != 0)
-                lu_big_update_kernel<<<dim3(tiles * tiles, grid), 256, 0, s>>>(bl, m.p, lu_off.p, lu.p,
-                                                                               big_bad.p, k0, tiles);
-              else if (u1 && std::atoi(u1) == 4)  // 4x8 tile, 128 threads (A/B)
-                lu_big_update_r4_kernel<4><<<dim3(tiles, grid), 128, 0, s>>>(bl, m.p, lu_off.p, lu.p, big_bad.p,
-                                                                             k0);
-              else if (!u1 || std::atoi(u1) == 0)  // 2x8 tile, 256 threads (default)
-                lu_big_update_r4_kernel<2><<<dim3(tiles, grid), 256, 0, s>>>(bl, m.p, lu_off.p, lu.p, big_bad.p,
-                                                                             k0);
-              else
-                lu_big_update_strip_kernel<<<dim3(tiles, grid), 256, 0, s>>>(bl, m.p, lu_off.p, lu.p, big_bad.p,
-                                                                             k0);
+              lu_big_update_r4_kernel<<<dim3(tiles, grid), 256, 0, s>>>(bl, m.p, lu_off.p, lu.p, big_bad.p, k0);
             }
           }
           const size_t smf = (size_t)(mx + (mx + 1) / 2 + 32 * kTileLd + 8) * 8;
@@ -719,29 +521,17 @@ struct Blocks {
     FSI_CUDA(cudaStreamSynchronize(s));
   }
 
-  // Blocks all <= 64 with a plain gathered right-hand side: per-warp
-  // double-buffered bulk copies of whole blocks (small_pipe_solve_kernel).
-  // Warps per CTA are sized so two buffers per warp fit the shared memory.
-  // Default for all-small blocks with a plain gathered right-hand side
-  // (config 1): one 28 KB shared buffer per warp, 7 warps per SM, and an L2
-  // bulk prefetch of each warp's next block issued before it solves the
-  // current one, so the next TMA copy is an L2 hit. Config-1 solve: 1.54 ms
-  // = 6.64 TB/s, against 2.33 ms for block_solve_kernel (FSIGPU_SOLVE_PIPE=0)
-  // and 2.36 ms for two buffers per warp (=1: only 4 warps per SM, whose
-  // dependent solve phases then run at ~0.9 IPC).
-  static bool small_pipe_enabled() {
-    const char* e = std::getenv("FSIGPU_SOLVE_PIPE");
-    return !(e && e[0] == '0');
-  }
+  // Blocks all <= 64 with a plain gathered right-hand side (config 1): one
+  // shared buffer per warp filled by a bulk copy, with an L2 bulk prefetch
+  // of each warp's next block issued before it solves the current one, so
+  // the next copy is an L2 hit (small_pipe_solve_kernel). Config-1 solve:
+  // 1.54 ms = 6.64 TB/s, against 2.33 ms for block_solve_kernel and 2.36 ms
+  // for two buffers per warp (only 4 warps per SM, whose dependent solve
+  // phases then run at ~0.9 IPC).
   void solve_small_pipe(const SolveArgs& base, cudaStream_t s) const {
     const int cap = pipe_cap;
-    // FSIGPU_SOLVE_PIPE=1: two buffers per warp; =2: one buffer per warp
-    // plus an L2 bulk prefetch of the warp's next block (twice the warps)
-    const char* pe = std::getenv("FSIGPU_SOLVE_PIPE");
-    const int single = (pe && pe[0] == '1') ? 0 : 1;
-    const size_t per_warp = (size_t)((single ? 1 : 2) * cap + 64) * 8;
-    int nw = (int)std::max<size_t>(1, std::min<size_t>(kPipeMaxWarps, (size_t)(200 * 1024) / per_warp));
-    if (const char* e = std::getenv("FSIGPU_PIPE_WARPS")) nw = std::max(1, std::min(kPipeMaxWarps, std::atoi(e)));
+    const size_t per_warp = (size_t)(cap + 64) * 8;
+    const int nw = (int)std::max<size_t>(1, std::min<size_t>(kPipeMaxWarps, (size_t)(200 * 1024) / per_warp));
     const size_t smem = per_warp * nw;
     FSI_CUDA(cudaFuncSetAttribute(small_pipe_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int dev = 0, sms = 0, occ = 0;
@@ -750,7 +540,7 @@ struct Blocks {
     FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, small_pipe_solve_kernel, nw * 32, smem));
     const int grid = (int)std::max<long long>(1, std::min<long long>((long long)sms * std::max(occ, 1),
                                                                      (nb + nw - 1) / nw));
-    SmallPipeArgs a{m.p, sf_off.p, row_off.p, sf.p, gsrc.p, base.r, base.out, nb, cap, single};
+    SmallPipeArgs a{m.p, sf_off.p, row_off.p, sf.p, gsrc.p, base.r, base.out, nb, cap, 1};
     ProfScope ps(FSIGPU_K_BLOCK_SOLVE, solve_bytes, s);
     launch_k(small_pipe_solve_kernel, dim3(grid), dim3(nw * 32), smem, s, a);
     FSI_CHECK_LAUNCH();
@@ -772,7 +562,7 @@ struct Blocks {
       counted();
       return;
     }
-    if (max_m <= kSmallMax && base.g1 == INT_MAX && small_pipe_enabled()) {
+    if (max_m <= kSmallMax && base.g1 == INT_MAX) {
       solve_small_pipe(base, s);
       return;
     }
@@ -861,9 +651,8 @@ static void launch_prolong_resid(const Level& L, const double* ec, const unsigne
 struct Gmg {
   std::vector<Level> lv;
   // read-only hot data (level matrices, transfers, block inverses, coarse
-  // inverse) packed in one arena and pinned in L2 by an access-policy window
+  // inverse) packed in one arena
   DevBuf<char> arena;
-  size_t persist_bytes = 0;
   double omega = 0.7;
   int pre = 1, post = 1;
   char cyc = 'v';
@@ -1163,12 +952,6 @@ static void assemble_fs(Level& L, const fsigpu_level_desc& d, const std::vector<
   FSI_CUDA(cudaStreamSynchronize(s));
   L.FS.adopt(L.n, L.n, std::move(ptr), std::move(cols), std::move(fv));
   L.assembled = true;
-  // window-compressed column codes (sparse.cuh CSR16), opt-in with
-  // FSIGPU_FS_C16=1: measured slower (config 0 8.1 -> 9.8 ms per solve,
-  // config-2 L2 FS 44 -> 70 us), and the fine config-2 rows need more than
-  // 4 windows (DESIGN 3.4)
-  const char* e = std::getenv("FSIGPU_FS_C16");
-  if (e && std::atoi(e) == 1) L.FS.compress16(s);
 }
 
 // Build one level from its descriptor (host arrays).
@@ -1183,7 +966,7 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
   // sweeps on config 2 (profiles/r01_tune_cfg2full_pair.txt): L4 5.0 -> 5.3,
   // L3 3.9 -> 4.2, L2 2.6 -> 2.8 TB/s. The FS operator (long rows) stays on
   // the scalar kernel, which is faster there.
-  if ((d.n >= 65536 || force_big()) && !std::getenv("FSIGPU_SPMV_PAIR")) {
+  if (d.n >= 65536 || force_big()) {
     L.A.lpr = d.n >= 131072 ? 4 : 8;
     L.A.unroll = 24;
   }
@@ -1208,14 +991,12 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
   // 16-byte loads with two lanes per row hold a whole row in one batch. Cold
   // sweeps on config 2 (profiles/r01_tune_restrict_cfg2.txt): 313k rows
   // 30.7 -> 24.4 us, 78k rows 13.9 -> 12.1; 20k rows: 8 lanes, batch 8.
-  if (!std::getenv("FSIGPU_SPMV_PAIR")) {
-    if (d.nc >= 65536) {
-      L.R.lpr = 2;
-      L.R.unroll = 24;
-    } else if (d.nc >= 16384) {
-      L.R.lpr = 8;
-      L.R.unroll = 8;
-    }
+  if (d.nc >= 65536) {
+    L.R.lpr = 2;
+    L.R.unroll = 24;
+  } else if (d.nc >= 16384) {
+    L.R.lpr = 8;
+    L.R.unroll = 8;
   }
   {
     // AP_m = A * diag(!col_mask) * P (Gustavson, sorted rows)
@@ -1253,7 +1034,7 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
     // its P half already adds 2 loads per lane to each batch: on large
     // (HBM-bound) levels batches of 4 AP entries; on small (L2-resident)
     // ones half the lanes with batches of 8 (warm sweeps, tools/tune_spmv.py)
-    const bool pair_ap = (d.n >= 131072 || (force_big() && d.n >= 4096)) && !std::getenv("FSIGPU_SPMV_PAIR");
+    const bool pair_ap = d.n >= 131072 || (force_big() && d.n >= 4096);
     if (d.n < 65536 && !pair_ap) {
       L.AP.lpr = std::max(2, L.AP.lpr / 2);
       L.AP.unroll = 8;
@@ -1394,12 +1175,10 @@ static void build_coarse(Gmg& g, const fsigpu_level_desc& d, cudaStream_t s) {
   }
 }
 
-// Pack the read-only arrays every V-cycle streams into one arena and set an
-// L2 access-policy window (hitProp persisting) on the hierarchy's stream, so
-// CUDA-graph kernel nodes captured from it keep them resident across cycles.
-static int g_l2_persist = 0;  // measured slower on config 0 (tools/ab_test.py)
+// Pack the read-only arrays every V-cycle streams into one arena (one
+// contiguous allocation; an L2 persisting window over it measured slower on
+// config 0 and was dropped).
 static void pin_hot_data(Gmg& g) {
-  std::vector<std::pair<void*, size_t>> items;  // (DevBuf*, bytes) via lambdas
   std::vector<std::function<void(char*)>> movers;
   size_t total = 0;
   auto add = [&](auto& buf) {
@@ -1428,27 +1207,6 @@ static void pin_hot_data(Gmg& g) {
   if (!total) return;
   g.arena.alloc(total);
   for (auto& mv : movers) mv(g.arena.p);
-  g.persist_bytes = 0;
-  if (!g_l2_persist) return;
-  int dev = 0, max_persist = 0, max_window = 0;
-  FSI_CUDA(cudaGetDevice(&dev));
-  FSI_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
-  FSI_CUDA(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev));
-  if (max_persist <= 0 || max_window <= 0) return;
-  size_t cur = 0;
-  FSI_CUDA(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
-  const size_t want = std::min<size_t>(total, (size_t)max_persist);
-  if (cur < want) FSI_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
-  FSI_CUDA(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
-  cudaStreamAttrValue attr = {};
-  const size_t win = std::min<size_t>(total, (size_t)max_window);
-  attr.accessPolicyWindow.base_ptr = g.arena.p;
-  attr.accessPolicyWindow.num_bytes = win;
-  attr.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)cur / (double)win);
-  attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-  attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-  FSI_CUDA(cudaStreamSetAttribute(g.s, cudaStreamAttributeAccessPolicyWindow, &attr));
-  g.persist_bytes = cur;
 }
 
 // ------------------------------------------------------------ GMRES
@@ -1465,12 +1223,6 @@ struct Gmres {
   cudaGraphExec_t cycle_exec = nullptr;
   cudaGraph_t cycle_graph = nullptr;
   int graph_version = -1;  // Gmg::version the graph was captured at
-  // persistent cooperative restart-cycle kernel (inverse-mode V-cycles)
-  bool mega = false;
-  bool force_mega = false;
-  int mega_grid = 0;
-  MegaArgs margs{};
-  DevBuf<GridBar> bar;
 
   ~Gmres() {
     if (cycle_exec) cudaGraphExecDestroy(cycle_exec);
@@ -1521,11 +1273,8 @@ struct Gmres {
     {
       // (B) on parts_b CTAs; (C) on parts_b row CTAs + 1 Givens CTA
       ProfScope ps(FSIGPU_K_ARNOLDI, 8.0 * n * 4, s);
-      if (kk.fuse_small && arnoldi_cp()) {  // large systems: rows streamed through cp.async stages
+      if (kk.fuse_small) {  // large systems: rows streamed through cp.async stages, (C) on its own grid
         launch_k(k_update_dots_norm_cp, dim3(kk.parts_b), dim3(kArnThreads), kStageSmem, s, kk);
-        launch_k(k_update_normalize<false>, dim3(kk.parts_c + 1), dim3(kArnThreads), 0, s, kk);
-      } else if (kk.fuse_small) {  // large systems: no first-row prefetch, (C) on its own grid
-        launch_k(k_update_dots_norm<false>, dim3(kk.parts_b), dim3(kArnThreads), 0, s, kk);
         launch_k(k_update_normalize<false>, dim3(kk.parts_c + 1), dim3(kArnThreads), 0, s, kk);
       } else {
         launch_k(k_update_dots_norm<true>, dim3(kk.parts_b), dim3(kArnThreads), 0, s, kk);
@@ -1594,101 +1343,6 @@ struct Gmres {
     cudaGraphDestroy(post_g);
   }
 
-  void setup_mega() {
-    Gmg& G = *g;
-    mega = G.cyc == 'v' && G.smoother == 0 && (int)G.lv.size() <= kMegaMaxLevels && G.lv.size() >= 2;
-    for (size_t l = 1; l < G.lv.size(); ++l) mega = mega && G.lv[l].blocks.mode == kModeInverse;
-    // opt-in (measured slower than the graph path on config 0: its phases
-    // are latency-bound at 2 CTAs/SM)
-    const char* e = std::getenv("FSIGPU_MEGA");
-    mega = mega && (force_mega || (e && std::atoi(e) != 0));
-    if (!mega) return;
-    int dev = 0, sms = 0, occ = 0, coop = 0;
-    FSI_CUDA(cudaGetDevice(&dev));
-    FSI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    FSI_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
-    FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fgmres_cycle_kernel, kMegaThreads, 0));
-    if (!coop || occ < 1) {
-      mega = false;
-      return;
-    }
-    mega_grid = sms * std::min(occ, 2);
-    if ((size_t)mega_grid * (kMaxRestart + 1) > partial.n) partial.alloc((size_t)mega_grid * (kMaxRestart + 1));
-    kb.partial = partial.p;
-    bar.alloc(1);
-    bar.zero(G.s);
-    MegaArgs& A = margs;
-    A.L = (int)G.lv.size();
-    for (int l = 0; l < A.L; ++l) {
-      Level& L = G.lv[l];
-      MLevel& M = A.lv[l];
-      M.n = L.n;
-      M.nc = L.nc;
-      M.a_ptr = L.A.ptr.p;
-      M.a_idx = L.A.idx.p;
-      M.a_val = L.A.val.p;
-      M.a_lpr = L.A.lpr;
-      M.rmask = L.rmask.p;
-      M.cmask = L.cmask.p;
-      M.b = L.bbuf.p;
-      M.x = L.xbuf.p;
-      M.r = L.rbuf.p;
-      if (l == 0) continue;
-      M.p_ptr = L.P.ptr.p;
-      M.p_idx = L.P.idx.p;
-      M.p_val = L.P.val.p;
-      M.p_lpr = L.P.lpr;
-      M.r_ptr = L.R.ptr.p;
-      M.r_idx = L.R.idx.p;
-      M.r_val = L.R.val.p;
-      M.r_lpr = L.R.lpr;
-      M.g1 = L.g1;
-      M.n_us = L.n_us;
-      M.lumped = L.lumped.p;
-      M.aus_ptr = L.aus_ptr.p;
-      M.aus_col = L.aus_col.p;
-      M.aus_val = L.aus_val.p;
-      M.bm = L.blocks.m.p;
-      M.row_off = L.blocks.row_off.p;
-      M.inv = L.blocks.inv.p;
-      M.inv_off = L.blocks.inv_off.p;
-      M.pos = L.blocks.pos.p;
-      M.tiles = L.blocks.inv_items.p;
-      M.n_tiles = L.blocks.n_inv_items;
-      M.inv_ptr = L.inv_ptr.p;
-      M.inv_idx = L.inv_idx.p;
-      M.delta = L.delta.p;
-    }
-    A.lv[A.L - 1].b = ubuf.p;
-    A.lv[A.L - 1].x = zbuf.p;
-    A.cinv = G.coarse_inv.p;
-    A.omega = G.omega;
-    A.pre = G.pre;
-    A.post = G.post;
-    A.kb = kb;
-    A.bar = bar.p;
-  }
-
-  void check_bar() {
-    GridBar hb;
-    FSI_CUDA(cudaMemcpyAsync(&hb, bar.p, sizeof(GridBar), cudaMemcpyDeviceToHost, g->s));
-    FSI_CUDA(cudaStreamSynchronize(g->s));
-    if (hb.error) {
-      bar.zero(g->s);
-      throw Error(FSIGPU_ERR_CUDA, "gmres: persistent kernel barrier watchdog tripped at phase " +
-                                       std::to_string(hb.phase) + " (count " + std::to_string(hb.count) + ")");
-    }
-  }
-
-  void launch_mega(int first) {
-    margs.kb = kb;
-    margs.first_cycle = first;
-    void* params[] = {&margs};
-    FSI_CUDA(cudaLaunchCooperativeKernel((const void*)fgmres_cycle_kernel, dim3(mega_grid), dim3(kMegaThreads),
-                                         params, 0, g->s));
-    counted();
-  }
-
   KState read_state() {
     KState h;
     FSI_CUDA(cudaMemcpyAsync(&h, st.p, sizeof(KState), cudaMemcpyDeviceToHost, g->s));
@@ -1709,25 +1363,6 @@ struct Gmres {
     h0.rel_tol = rel_tol;
     h0.abs_tol = abs_tol;
     FSI_CUDA(cudaMemcpyAsync(st.p, &h0, sizeof(KState), cudaMemcpyHostToDevice, s));
-    if (mega && g->smoother == 0 && !g_prof.on) {
-      launch_mega(1);
-      KState h = read_state();
-      check_bar();
-      while (!h.converged && h.its < max_iters && !h.breakdown) {
-        const int before = h.its;
-        launch_mega(0);
-        h = read_state();
-        check_bar();
-        if (h.its == before) throw Error(FSIGPU_ERR_CUDA, "gmres: persistent cycle made no progress");
-      }
-      res->iterations = h.its;
-      res->converged = h.converged;
-      res->breakdown = h.breakdown;
-      res->n_history = h.its + 1;
-      res->m_applies = h.its;
-      res->true_residual = h.beta;
-      return;
-    }
     outer_resid();
     k_norm_r<<<grid, kKThreads, 0, s>>>(kb);
     FSI_CHECK_LAUNCH();
@@ -1818,11 +1453,6 @@ long long fsigpu_launch_count(void) { return g_launches; }
 int fsigpu_set_pdl(int enable) {
   return guarded([&] { g_pdl = enable != 0; });
 }
-int fsigpu_set_l2_persist(int enable) {
-  return guarded([&] { g_l2_persist = enable != 0; });
-}
-long long fsigpu_gmg_persist_bytes(fsigpu_gmg g) { return g ? (long long)g->g.persist_bytes : 0; }
-
 // Tuning: launch shape (lanes per row, entries per lane per batch) of one
 // level matrix. which: 0 A, 1 FS, 2 AP, 3 P, 4 R.
 int fsigpu_gmg_set_launch(fsigpu_gmg h, int level, int which, int lpr, int unroll) {
@@ -1845,21 +1475,6 @@ int fsigpu_gmg_set_smoother(fsigpu_gmg h, int kind) {
     require(h != nullptr, "gmg: null");
     require(kind == 0 || kind == 1, "smoother must be 0 (richardson) or 1 (gmres1)");
     h->g.set_smoother(kind);
-  });
-}
-int fsigpu_gmg_set_staging(fsigpu_gmg h, int level, int which, int cap) {
-  return guarded([&] {
-    require(h != nullptr && level >= 0 && level < (int)h->g.lv.size(), "staging: bad level");
-    require(cap >= 0 && cap <= 16384, "staging: cap must be 0..16384");
-    Level& L = h->g.lv[level];
-    Csr* c = which == 0 ? &L.A : which == 1 ? &L.FS : which == 2 ? &L.AP : which == 3 ? &L.P : &L.R;
-    c->stage(cap, h->g.s);
-  });
-}
-int fsigpu_set_stage_cap(int cap) {
-  return guarded([&] {
-    require(cap >= -1 && cap <= 16384, "stage cap must be -1..16384");
-    g_stage_cap = cap;
   });
 }
 int fsigpu_set_block_mode(int mode) {
@@ -2372,7 +1987,7 @@ int fsigpu_gmres_create(fsigpu_gmg g, const double* frame_scale, int restart, fs
       // small systems keep one 128-row tile per CTA (config 0: 157 tiles);
       // large ones run k_spmv_dots_s on up to 4 resident CTAs per SM
       const int tiles = ceil_div(n, kFuseRows);
-      kb.fuse_small = (tiles > 8 * sms || force_big()) && !std::getenv("FSIGPU_FUSE_BIG");
+      kb.fuse_small = tiles > 8 * sms || force_big();
       if (kb.fuse_small) {
         FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_dots_s, kFuseThreadsS, 0));
         kb.parts_a = sms * std::min(std::max(occ, 1), 4);
@@ -2385,23 +2000,15 @@ int fsigpu_gmres_create(fsigpu_gmg g, const double* frame_scale, int restart, fs
       int dev = 0, sms = 0, occ = 0;
       FSI_CUDA(cudaGetDevice(&dev));
       FSI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      const bool big = (ceil_div(n, kFuseRows) > 8 * sms || force_big()) && !std::getenv("FSIGPU_FUSE_BIG");
-      if (big && arnoldi_cp()) {
+      const bool big = ceil_div(n, kFuseRows) > 8 * sms || force_big();
+      if (big) {
         FSI_CUDA(cudaFuncSetAttribute(k_update_dots_norm_cp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)kStageSmem));
-        FSI_CUDA(cudaFuncSetAttribute(k_update_normalize_cp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)kStageSmem));
         FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_dots_norm_cp, kArnThreads, kStageSmem));
         kb.parts_b = std::max(1, std::min(ceil_div(n, kArnThreads), sms * std::min(std::max(occ, 1), 16)));
         // (C) stays on registers: at 80 registers it runs 6 CTAs per SM
-        // (50.6 us on the config-2 fine level) against 3 for the 70 KB
-        // staged variant (61.5 us); k_update_normalize_cp is kept for A/B
-        int occ_c = 0;
-        FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, k_update_normalize<false>, kArnThreads, 0));
-        kb.parts_c = std::max(1, std::min(ceil_div(n, kArnThreads), sms * std::max(occ_c, 1) - 1));
-      } else if (big) {
-        FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_dots_norm<false>, kArnThreads, 0));
-        kb.parts_b = std::max(1, std::min(ceil_div(n, kArnThreads), sms * std::min(std::max(occ, 1), 16)));
+        // (50.6 us on the config-2 fine level) against 3 for a 70 KB staged
+        // variant (61.5 us)
         int occ_c = 0;
         FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, k_update_normalize<false>, kArnThreads, 0));
         kb.parts_c = std::max(1, std::min(ceil_div(n, kArnThreads), sms * std::max(occ_c, 1) - 1));
@@ -2422,7 +2029,6 @@ int fsigpu_gmres_create(fsigpu_gmg g, const double* frame_scale, int restart, fs
       kb.use_cond = 0;
     }
     k.ensure_history(2000);
-    k.setup_mega();
     FSI_CUDA(cudaStreamSynchronize(s));
     *out = h.release();
   });
@@ -2432,72 +2038,6 @@ int fsigpu_gmres_set_graphs(fsigpu_gmres s, int enable) {
   return guarded([&] {
     require(s != nullptr, "gmres: null");
     s->k.graphs = enable != 0;
-  });
-}
-
-int fsigpu_gmres_set_persistent(fsigpu_gmres s, int enable) {
-  return guarded([&] {
-    require(s != nullptr, "gmres: null");
-    if (enable) {
-      s->k.force_mega = true;
-      s->k.setup_mega();
-      require(s->k.mega, "gmres: persistent kernel needs inverse-mode FS smoothers, V-cycles and cooperative launch");
-    } else {
-      s->k.mega = false;
-    }
-  });
-}
-
-int fsigpu_gmres_is_persistent(fsigpu_gmres s) { return s && s->k.mega ? 1 : 0; }
-
-// debug: make every persistent-kernel thread exit after `limit` barriers
-int fsigpu_debug_phase_limit(fsigpu_gmres s, unsigned limit) {
-  return guarded([&] {
-    require(s != nullptr && s->k.mega, "debug: no persistent kernel");
-    FSI_CUDA(cudaMemcpyAsync(&s->k.bar.p->limit, &limit, sizeof(unsigned), cudaMemcpyHostToDevice, s->k.g->s));
-    FSI_CUDA(cudaStreamSynchronize(s->k.g->s));
-  });
-}
-
-// debug: phase timestamps (ns, globaltimer) of the persistent kernel since
-// the last reset; returns the count
-int fsigpu_debug_trace(fsigpu_gmres s, unsigned long long* out, int cap, int reset) {
-  int n = 0;
-  int rc = guarded([&] {
-    require(s != nullptr && s->k.mega, "debug: no persistent kernel");
-    GridBar h;
-    FSI_CUDA(cudaMemcpy(&h, s->k.bar.p, sizeof(GridBar), cudaMemcpyDeviceToHost));
-    n = std::min<int>(cap, (int)h.ntrace);
-    std::memcpy(out, h.trace, sizeof(unsigned long long) * n);
-    if (reset) {
-      const unsigned z = 0;
-      FSI_CUDA(cudaMemcpy(&s->k.bar.p->ntrace, &z, sizeof(unsigned), cudaMemcpyHostToDevice));
-    }
-  });
-  return rc == FSIGPU_OK ? n : -rc;
-}
-
-// debug: time `iters` software grid barriers on `grid` co-resident CTAs
-int fsigpu_debug_barrier(int grid, int iters, int kind, double* ms) {
-  return guarded([&] {
-    cudaStream_t st = new_stream();
-    DevBuf<GridBar> gb(1);
-    gb.zero(st);
-    void* params[] = {&gb.p, &iters, &kind};
-    cudaEvent_t e0, e1;
-    FSI_CUDA(cudaEventCreate(&e0));
-    FSI_CUDA(cudaEventCreate(&e1));
-    FSI_CUDA(cudaEventRecord(e0, st));
-    FSI_CUDA(cudaLaunchCooperativeKernel((const void*)barrier_test_kernel, dim3(grid), dim3(256), params, 0, st));
-    FSI_CUDA(cudaEventRecord(e1, st));
-    FSI_CUDA(cudaEventSynchronize(e1));
-    float t = 0;
-    FSI_CUDA(cudaEventElapsedTime(&t, e0, e1));
-    *ms = t;
-    GridBar h;
-    FSI_CUDA(cudaMemcpy(&h, gb.p, sizeof(GridBar), cudaMemcpyDeviceToHost));
-    require(!h.error, "debug barrier watchdog tripped");
-    cudaStreamDestroy(st);
   });
 }
 

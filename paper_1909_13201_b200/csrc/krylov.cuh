@@ -963,69 +963,4 @@ __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
   }
 }
 
-// (C) for large n: the rows stream through cp.async stages as in
-// k_update_dots_norm_cp; the Givens CTA is unchanged.
-__global__ void __launch_bounds__(kArnThreads) k_update_normalize_cp(KBufs k) {
-  pdl_trigger();
-  pdl_wait();
-  extern __shared__ __align__(16) double stg[];
-  __shared__ double hs[kMaxRestart + 1];
-  __shared__ double red[(kMaxRestart + 1) * kSumSlices];
-  __shared__ double s_hn;
-  const int jn = k.st->jc;
-  const int nv = jn;
-  const int nb = gridDim.x - 1;
-  const bool rows_cta = blockIdx.x < nb;
-  __shared__ double g_col[kMaxRestart + 2], g_cs[kMaxRestart + 1], g_sn[kMaxRestart + 1];
-  double h1t = 0.0, gj = 0.0;
-  const int t = threadIdx.x;
-  if (!rows_cta) {
-    if (t < nv) h1t = __ldcg(k.st->h1 + t);
-    if (t < nv - 1) {
-      g_cs[t] = __ldcg(k.cs + t);
-      g_sn[t] = __ldcg(k.sn + t);
-    }
-    if (t == 0) gj = __ldcg(k.g + nv - 1);
-  }
-  const int stride = nb * blockDim.x;
-  int r = rows_cta ? blockIdx.x * blockDim.x + t : k.n;
-  if (rows_cta) stage_row(k, stg, 0, r, nv, true);  // overlaps the reduction
-  sum_partials<kArnThreads>(k.partial2, k.parts_b, nv + 1, hs, red);
-  if (t < 32) {
-    double q = 0.0;
-    for (int v = t; v < nv; v += 32) q = fma(hs[v], hs[v], q);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(kFull, q, o);
-    if (t == 0) s_hn = sqrt(fmax(hs[nv] - q, 0.0));
-  }
-  __syncthreads();
-  const double hn = s_hn;
-  if (!rows_cta) {
-    if (t < nv) {
-      k.st->h2[t] = hs[t];
-      g_col[t] = h1t + hs[t];
-    }
-    __syncthreads();
-    givens_core(k, nv - 1, hn, g_col, g_cs, g_sn, gj);
-    return;
-  }
-  const bool lucky = hn < 1e-14;
-  double* __restrict__ VJ = k.V + (size_t)jn * k.n;
-  double* __restrict__ UB = k.ubuf;
-  for (int it = 0; r < k.n; ++it, r += stride) {
-    stage_row(k, stg, (it + 1) & 1, r + stride, nv, true);
-    cp_async_wait<1>();
-    const double* row = stg + (size_t)(it & 1) * kStageVals * kArnThreads + t;
-    double wr = row[(size_t)kMaxRestart * kArnThreads];
-#pragma unroll
-    for (int v = 0; v < kMaxRestart; ++v)
-      if (v < nv) wr = fma(-hs[v], row[(size_t)v * kArnThreads], wr);
-    if (!lucky) {
-      const double vv = wr / hn;
-      VJ[r] = vv;
-      UB[r] = vv / row[(size_t)(kMaxRestart + 1) * kArnThreads];
-    }
-  }
-  cp_async_wait<0>();
-}
 }  // namespace fsigpu

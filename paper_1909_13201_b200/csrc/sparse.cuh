@@ -137,102 +137,6 @@ __global__ void __launch_bounds__(256) csr_kernel(int rows, const int* __restric
   if (ok && lane == 0) epi(row, s, pe);
 }
 
-// Segment-compressed column indices ("CSR16"): the assembled FS operator's
-// rows are unions of element-patch dof sets, so their columns fall in at
-// most a few short windows of the frame (one per field section the patch
-// touches: e.g. u^f, p^f and the u^s coupling columns). Each row stores up
-// to 4 window bases (int4, 16 B per row) and each entry a 16-bit code: the
-// top 2 bits select the base, the low 14 bits are the offset in the window.
-// 12 -> 10 bytes per entry (+16 per row) on an HBM-bound stream; same
-// arithmetic in the same order as csr_kernel (bit-identical results).
-constexpr int kC16Bits = 14;
-constexpr int kC16Win = 1 << kC16Bits;
-__device__ __forceinline__ int c16_col(const int4& b, unsigned int code) {
-  const unsigned int sel = code >> kC16Bits;
-  const int base = sel == 0 ? b.x : sel == 1 ? b.y : sel == 2 ? b.z : b.w;
-  return base + (int)(code & (kC16Win - 1));
-}
-
-template <int LPR, class Gather, class Epi, int U = 4>
-__global__ void __launch_bounds__(256) csr16_kernel(int rows, const int* __restrict__ ptr,
-                                                    const unsigned short* __restrict__ code,
-                                                    const int4* __restrict__ bases,
-                                                    const double* __restrict__ val, Gather gx, Epi epi) {
-  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const int row = (int)(gt / LPR);
-  const int lane = threadIdx.x & (LPR - 1);
-  const bool ok = row < rows;
-  pdl_trigger();
-  const int k0 = ok ? __ldg(ptr + row) : 0, k1 = ok ? __ldg(ptr + row + 1) : 0;  // setup data
-  const int4 bs = ok ? __ldg(bases + row) : make_int4(0, 0, 0, 0);
-  pdl_wait();
-  EpiPre pe{0.0, 0};
-  if (ok && lane == 0) pe = epi.pre(row);
-  double s = 0.0;
-  for (int kb = k0 + lane; kb < k1; kb += U * LPR) {
-    int c[U];
-    double v[U], xv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int k = kb + u * LPR;
-      const bool in = k < k1;
-      c[u] = in ? c16_col(bs, __ldg(code + k)) : -1;
-      v[u] = in ? __ldg(val + k) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) xv[u] = c[u] >= 0 ? gx(c[u]) : 0.0;
-#pragma unroll
-    for (int u = 0; u < U; ++u) s = fma(v[u], xv[u], s);
-  }
-#pragma unroll
-  for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, LPR);
-  if (ok && lane == 0) epi(row, s, pe);
-}
-
-// One thread per row: split the row's sorted columns into windows of
-// kC16Win starting at the first column of each window; more than 4
-// windows sets *fail (the matrix then keeps 32-bit indices).
-__global__ void c16_compress_kernel(int rows, const int* __restrict__ ptr, const int* __restrict__ idx,
-                                    unsigned short* __restrict__ code, int4* __restrict__ bases,
-                                    int* __restrict__ fail) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= rows) return;
-  int b[4] = {0, 0, 0, 0};
-  int nb = 0;
-  for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
-    const int c = idx[k];
-    if (nb == 0 || c - b[nb - 1] >= kC16Win) {
-      if (nb == 4) {
-        atomicExch(fail, 1);
-        return;
-      }
-      b[nb++] = c;
-    }
-    code[k] = (unsigned short)(((nb - 1) << kC16Bits) | (c - b[nb - 1]));
-  }
-  bases[i] = make_int4(b[0], b[1], b[2], b[3]);
-}
-
-// Shared-memory staged CSR ("CSR-stream"). CTA b owns rows [rb[b], rb[b+1])
-// whose entries [ptr[rb[b]], ptr[rb[b+1]]) are contiguous in idx / val, at
-// most `cap` of them. One thread brings both slices into shared memory with
-// two bulk copies (cp.async.bulk + mbarrier complete_tx), issued BEFORE the
-// PDL wait: the matrix is setup data, so its fetch overlaps the producer
-// kernel's tail. Then
-//   phase 1: every thread forms val[k] * x[idx[k]] for k = t, t + 256, ...
-//            (U independent gathers in flight per thread, whatever the row
-//            lengths) and writes the product over val in place;
-//   phase 2: LPR lanes per row add the row's products out of shared memory
-//            (fixed strided order + xor tree: deterministic).
-// Compared with csr_kernel the per-warp dependent chain drops from
-// ptr -> (idx, val) -> x per batch to one bulk copy + one gather round.
-// Paired variant of csr_kernel: each lane streams 16-byte pairs (int2 of
-// column indices, double2 of values) starting at the even entry at or below
-// the row start; entries outside [k0, k1) are masked. Half the load
-// instructions of the scalar kernel for the same bytes: on the HBM-bound
-// levels the scalar kernel saturates L1/TEX request throughput (ncu: 91%
-// L1/TEX, 70% DRAM on the config-2 fine residual) before DRAM. Needs idx/val
-// padded by one entry (Csr pads by 4) and 16-B aligned bases.
 template <int LPR, class Gather, class Epi, int UP = 2>
 __global__ void __launch_bounds__(256) csr_pair_kernel(int rows, const int* __restrict__ ptr,
                                                        const int* __restrict__ idx,
@@ -278,68 +182,6 @@ __global__ void __launch_bounds__(256) csr_pair_kernel(int rows, const int* __re
 #pragma unroll
   for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, LPR);
   if (ok && lane == 0) epi(row, s, pe);
-}
-
-template <int LPR, class Gather, class Epi, int U = 8>
-__global__ void __launch_bounds__(256) csr_staged_kernel(const int* __restrict__ rb, const int* __restrict__ ptr,
-                                                         const int* __restrict__ idx,
-                                                         const double* __restrict__ val, int cap, Gather gx,
-                                                         Epi epi) {
-  extern __shared__ __align__(128) unsigned char stage[];
-  __shared__ __align__(8) unsigned long long bar;
-  double* s_val = reinterpret_cast<double*>(stage);  // cap + 2 doubles
-  int* s_idx = reinterpret_cast<int*>(stage + 8 * (size_t)((cap + 2 + 1) & ~1));  // cap + 8 ints
-  const int t = threadIdx.x;
-  const int r0 = __ldg(rb + blockIdx.x), r1 = __ldg(rb + blockIdx.x + 1);
-  const int k0 = __ldg(ptr + r0), k1 = __ldg(ptr + r1);
-  const int kv0 = k0 & ~1, ki0 = k0 & ~3;  // 16-byte aligned sources
-  const unsigned bv = 8u * (unsigned)(((k1 + 1) & ~1) - kv0);
-  const unsigned bi = 4u * (unsigned)(((k1 + 3) & ~3) - ki0);
-  if (t == 0) {
-    mbar_init(&bar, 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-  if (t == 0) {
-    mbar_arrive_expect_tx(&bar, k1 > k0 ? bv + bi : 0u);
-    if (k1 > k0) {
-      tma_bulk_g2s(s_val, val + kv0, bv, &bar);
-      tma_bulk_g2s(s_idx, idx + ki0, bi, &bar);
-    }
-  }
-  pdl_trigger();
-  pdl_wait();
-  mbar_wait(&bar, 0);
-  // phase 1: products
-  for (int kb = k0 + t; kb < k1; kb += 256 * U) {
-    int c[U];
-    double xv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int k = kb + 256 * u;
-      c[u] = k < k1 ? s_idx[k - ki0] : -1;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) xv[u] = c[u] >= 0 ? gx(c[u]) : 0.0;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int k = kb + 256 * u;
-      if (k < k1) s_val[k - kv0] *= xv[u];
-    }
-  }
-  __syncthreads();
-  // phase 2: row sums
-  const int lane = t & (LPR - 1);
-  for (int base = r0; base < r1; base += 256 / LPR) {
-    const int row = base + t / LPR;
-    const bool ok = row < r1;
-    const int a = ok ? __ldg(ptr + row) : 0, b = ok ? __ldg(ptr + row + 1) : 0;
-    double s = 0.0;
-    for (int k = a + lane; k < b; k += LPR) s += s_val[k - kv0];
-#pragma unroll
-    for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, LPR);
-    if (ok && lane == 0) epi(row, s, epi.pre(row));
-  }
 }
 
 // FS combine on one level (precond.cpp:42-57 additive + 271-287 + 305-317):

@@ -78,9 +78,7 @@ def lib():
             "fsigpu_version": ([], ip),
             "fsigpu_launch_count": ([], ll),
             "fsigpu_set_block_mode": ([ip], ip),
-            "fsigpu_set_l2_persist": ([ip], ip),
             "fsigpu_set_pdl": ([ip], ip),
-            "fsigpu_gmg_persist_bytes": ([vp], ll),
             "fsigpu_gmg_stream": ([vp], vp),
             "fsigpu_csr_create": ([ip, ip, vp, vp, vp, C.POINTER(vp)], ip),
             "fsigpu_csr_multiply": ([vp, vp, vp], ip),
@@ -109,15 +107,11 @@ def lib():
             "fsigpu_gmg_destroy": ([vp], None),
             "fsigpu_gmg_set_launch": ([vp, ip, ip, ip, ip], ip),
             "fsigpu_gmg_set_smoother": ([vp, ip], ip),
-            "fsigpu_gmg_set_staging": ([vp, ip, ip, ip], ip),
-            "fsigpu_set_stage_cap": ([ip], ip),
             "fsigpu_gmg_time_kernel": ([vp, ip, ip, ip, ip, C.POINTER(d), C.POINTER(d)], ip),
             "fsigpu_gmres_create": ([vp, vp, ip, C.POINTER(vp)], ip),
             "fsigpu_gmres_solve": ([vp, vp, vp, vp, ip, d, d, vp, C.POINTER(GmresResultC)], ip),
             "fsigpu_gmres_solve_dev": ([vp, vp, vp, ip, d, d, vp, C.POINTER(GmresResultC)], ip),
             "fsigpu_gmres_set_graphs": ([vp, ip], ip),
-            "fsigpu_gmres_set_persistent": ([vp, ip], ip),
-            "fsigpu_gmres_is_persistent": ([vp], ip),
             "fsigpu_gmres_destroy": ([vp], None),
             "fsigpu_profile_enable": ([ip], ip),
             "fsigpu_profile_read": ([vp, vp, vp], ip),
@@ -329,14 +323,6 @@ class GmgPreconditioner:
         w = {"A": 0, "FS": 1, "AP": 2, "P": 3, "R": 4}[which]
         _check(lib().fsigpu_gmg_set_launch(self.h, level, w, lpr, unroll))
 
-    def set_staging(self, level: int, which: str, cap: int):
-        """Staged (shared-memory CSR-stream) SpMV with <= cap entries per CTA; 0 = off."""
-        w = {"A": 0, "FS": 1, "AP": 2, "P": 3, "R": 4}[which]
-        _check(lib().fsigpu_gmg_set_staging(self.h, level, w, cap))
-
-    def persist_bytes(self) -> int:
-        return int(lib().fsigpu_gmg_persist_bytes(self.h))
-
     def stream(self) -> int:
         """cudaStream_t (as int) all kernels of this hierarchy run on."""
         return lib().fsigpu_gmg_stream(self.h) or 0
@@ -406,14 +392,6 @@ class GmresSolver:
     def set_graphs(self, on: bool):
         _check(lib().fsigpu_gmres_set_graphs(self.h, 1 if on else 0))
 
-    def set_persistent(self, on: bool):
-        """Persistent cooperative restart-cycle kernel (default when available)."""
-        _check(lib().fsigpu_gmres_set_persistent(self.h, 1 if on else 0))
-
-    @property
-    def persistent(self) -> bool:
-        return bool(lib().fsigpu_gmres_is_persistent(self.h))
-
     def solve(self, b, cfg: KrylovConfig, x0=None) -> GmresResult:
         n = self.gmg.n
         b = _f64(b)
@@ -453,18 +431,6 @@ def set_block_mode(mode: int):
     """Block-solve mode for GMG hierarchies created afterwards (fsigpu_set_block_mode)."""
     init()
     _check(lib().fsigpu_set_block_mode(mode))
-
-
-def set_l2_persist(on: bool):
-    """L2 access-policy window over the hierarchy's read-only data (default off)."""
-    init()
-    _check(lib().fsigpu_set_l2_persist(1 if on else 0))
-
-
-def set_stage_cap(cap: int):
-    """Staged-SpMV capacity for hierarchies created afterwards (-1 rule, 0 off)."""
-    init()
-    _check(lib().fsigpu_set_stage_cap(cap))
 
 
 def set_pdl(on: bool):

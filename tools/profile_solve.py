@@ -27,8 +27,6 @@ def main():
             B.solve_dev(rhs.data_ptr(), x.data_ptr(), s.cuda_stream)
         torch.cuda.synchronize()
         return
-    if os.environ.get("FSI_STAGE"):
-        fsigpu.set_stage_cap(int(os.environ["FSI_STAGE"]))
     data = os.environ.get("FSI_DATA", os.path.join(ROOT, "data", "cfg0.fsix"))
     P = load_case(data, "case")
     if mode in ("vcycle-lu", "vcycle-inv"):
