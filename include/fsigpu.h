@@ -13,7 +13,11 @@
  * Error behaviour mirrors the reference's exceptions:
  *   FSIGPU_ERR_INVALID   <- std::invalid_argument (bad sizes / config)
  *   FSIGPU_ERR_SINGULAR  <- fsi::SingularBlockError (label via
- *                           fsigpu_last_singular_block(): lowest failing block)
+ *                           fsigpu_last_singular_block(): lowest failing block
+ *                           of the batch, and fsigpu_last_singular_level():
+ *                           its GMG level; block -1 = a non-block failure
+ *                           named by the message, e.g. "gmg-coarse" or
+ *                           "fs lumped mass row <i>", precond.cpp:239-241)
  *   FSIGPU_ERR_CUDA      <- device failure (no reference analogue)
  * GMRES non-convergence is reported in fsigpu_gmres_result, not as an error
  * (krylov.hpp:49-55).
@@ -75,6 +79,7 @@ typedef struct {
 /* ---- runtime ------------------------------------------------------- */
 const char* fsigpu_last_error(void);
 int fsigpu_last_singular_block(void);
+int fsigpu_last_singular_level(void);
 int fsigpu_init(int device);
 int fsigpu_version(void);
 /* number of libfsigpu kernel launches issued so far (graph replays included) */

@@ -53,6 +53,9 @@
 #include "fsi/precond.hpp"
 #include "fsi/sparse.hpp"
 #include "fsi/sparse_lu.hpp"
+#ifdef FSI_ADAPTER_CHECK
+#include "../../tests/cpp/gpu_solve_adapter.cpp"
+#endif
 
 using namespace fsi;
 
@@ -100,12 +103,16 @@ struct Archive {
   }
   void put_sets(const std::string& n, const std::vector<const IndexSet*>& sets) {
     std::vector<int> ptr{0}, idx;
+    std::vector<std::uint8_t> labels;  // IndexSet labels, '\n'-separated
     for (auto* s : sets) {
       idx.insert(idx.end(), s->indices.begin(), s->indices.end());
       ptr.push_back(static_cast<int>(idx.size()));
+      labels.insert(labels.end(), s->label.begin(), s->label.end());
+      labels.push_back('\n');
     }
     put(n + "/ptr", ptr);
     put(n + "/idx", idx);
+    put(n + "/labels", labels);
   }
 };
 
@@ -244,6 +251,24 @@ LevelStack make_stack(const CaseDef& c) {
 // --smoother as: the AS (Vanka, J1) smoother (precond.cpp:99-117) instead of FS
 static bool g_as = false;
 
+// body(i) for i in [0, n), one std::thread per index (n is a few levels).
+// The first exception is rethrown on the calling thread.
+void parallel_for(int n, const std::function<void(int)>& body) {
+  std::vector<std::thread> th;
+  std::vector<std::exception_ptr> err(n);
+  for (int i = 0; i < n; ++i)
+    th.emplace_back([&, i]() {
+      try {
+        body(i);
+      } catch (...) {
+        err[i] = std::current_exception();
+      }
+    });
+  for (auto& t : th) t.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
+}
+
 // Additive FS smoother from the reference's own classes (SURVEY §8c recipe).
 struct AdditiveFs final : LinearOperator {
   int n = 0, g1 = 0, g2 = 0, n_us = 0;
@@ -348,16 +373,18 @@ std::unique_ptr<Problem> build_problem(const std::string& name, unsigned long lo
   for (int l = top - 1; l >= 0; --l)
     xl[l] = restrict_state(st.hier, l + 1, st.spaces[l], st.spaces[l + 1], xl[l + 1]);
 
+  // the levels are independent objects of the reference (no shared mutable
+  // state), so they are assembled on one host thread each
   P->frame.resize(L);
   SparseMatrix jac_top;
-  for (int l = 0; l <= top; ++l) {
+  parallel_for(L, [&](int l) {
     st.assemblers[l]->assemble(xl[l], xo[l], xo[l], stab[l], t, true);
     SparseMatrix jl = st.assemblers[l]->jacobian();
     std::vector<double> rl = st.assemblers[l]->residual();
     apply_dirichlet(jl, rl, P->cs[l], xl[l]);
     P->frame[l] = (g_as ? st.orderings[l].j1 : st.orderings[l].j2).apply(jl);
     if (l == top) jac_top = std::move(jl);
-  }
+  });
   P->setup_assembly_s = now_s() - t0;
 
   t0 = now_s();
@@ -370,18 +397,19 @@ std::unique_ptr<Problem> build_problem(const std::string& name, unsigned long lo
                                                        &P->cmask[l]);
     P->fs_add[l] = std::make_unique<AdditiveFs>(*P->as_mult[l], P->frame[l]);
   }
-  for (int l = 1; l <= top && !g_as; ++l) {
-    FieldSplitPlan p1{P->def.epb1, P->def.overlap};
-    P->fs[l] = std::make_unique<FsPreconditioner>(P->frame[l], st.orderings[l].j2, st.spaces[l], p1,
-                                                  &P->cmask[l]);
-    const FsPreconditioner* as2src = P->fs[l].get();
-    if (P->def.epb2 != P->def.epb1) {
-      FieldSplitPlan p2{P->def.epb2, P->def.overlap};
-      P->fs_as2[l] = std::make_unique<FsPreconditioner>(P->frame[l], st.orderings[l].j2,
-                                                        st.spaces[l], p2, &P->cmask[l]);
-      as2src = P->fs_as2[l].get();
-    }
-    P->fs_add[l] = std::make_unique<AdditiveFs>(*P->fs[l], *as2src);
+  // FS instances (level x {epb1, epb2}) built on one host thread each
+  if (!g_as) {
+    const bool two = P->def.epb2 != P->def.epb1;
+    parallel_for(2 * L, [&](int task) {
+      const int l = task / 2;
+      if (l == 0 || (task % 2 == 1 && !two)) return;
+      const int epb = task % 2 == 0 ? P->def.epb1 : P->def.epb2;
+      auto f = std::make_unique<FsPreconditioner>(P->frame[l], st.orderings[l].j2, st.spaces[l],
+                                                  FieldSplitPlan{epb, P->def.overlap}, &P->cmask[l]);
+      (task % 2 == 0 ? P->fs[l] : P->fs_as2[l]) = std::move(f);
+    });
+    for (int l = 1; l <= top; ++l)
+      P->fs_add[l] = std::make_unique<AdditiveFs>(*P->fs[l], two ? *P->fs_as2[l] : *P->fs[l]);
   }
   P->setup_fs_s = now_s() - t0;
 
@@ -632,6 +660,15 @@ int cmd_export(const Args& a) {
     ar.put_d("gmres/rel_tol", a.rtol);
     auto sa = run_gmres(*P, true, kc);
     put_solve(ar, "gmres_add", sa);
+    // the reference's default KrylovConfig (restart 60, krylov.hpp:42-47),
+    // the configuration the drop-in sees from the driver (config.hpp:61)
+    if (a.max_iters >= 500) {
+      const KrylovConfig kd{};
+      auto sd = run_gmres(*P, true, kd);
+      put_solve(ar, "gmres_default", sd);
+      std::printf("%s additive default KrylovConfig (restart %d): its=%d conv=%d relres=%.3e\n", name.c_str(),
+                  kd.restart, sd.res.iterations, (int)sd.res.converged, sd.true_res / sd.res.history.front());
+    }
     std::printf("%s additive %s: its=%d conv=%d M=%lld %.3fs relres=%.3e\n", name.c_str(), g_as ? "AS" : "FS",
                 sa.res.iterations, (int)sa.res.converged, sa.m_applies, sa.seconds,
                 sa.true_res / sa.res.history.front());
@@ -795,6 +832,65 @@ int cmd_time_blocks(const Args& a) {
   return 0;
 }
 
+#ifdef FSI_ADAPTER_CHECK
+// The drop-in adapter (tests/cpp/gpu_solve_adapter.cpp) driven like the
+// reference driver's solve block (driver.cpp:242-272): GpuGmg from the
+// GmgLevels + per-level FsPreconditioners, gpu_gmres with the reference's
+// default KrylovConfig, against the reference's own gmres on the additive
+// FS hierarchy with the same config. JSON on stdout.
+int cmd_gpu_adapter(const Args& a) {
+  if (a.pos.size() < 2) throw std::invalid_argument("gpu-adapter <case>");
+  auto P = build_problem(a.pos[1], a.seed, false);
+  const int L = P->st.n_levels();
+  std::vector<const FsPreconditioner*> fs(L, nullptr);
+  for (int l = 1; l < L; ++l) fs[l] = P->fs[l].get();
+  const CycleConfig cyc{'v', 1, 1, 0.7};
+  GpuGmg gpu(P->levels_add, fs, cyc);
+  // one V-cycle through the LinearOperator interface
+  std::mt19937_64 rng(a.seed + 5);
+  auto r = seeded(P->n, rng);
+  std::vector<double> zg(P->n), zr(P->n);
+  gpu.apply(r.data(), zg.data());
+  P->gmg_add->apply(r.data(), zr.data());
+  double num = 0, den = 0;
+  for (int i = 0; i < P->n; ++i) {
+    num += (zg[i] - zr[i]) * (zg[i] - zr[i]);
+    den += zr[i] * zr[i];
+  }
+  const KrylovConfig kc{};
+  auto ref = run_gmres(*P, true, kc);
+  const GmresResult g = gpu_gmres(gpu, P->frame_scale, P->b, kc);
+  auto ax = P->a_scaled.multiply(g.x);
+  double s2 = 0;
+  for (int i = 0; i < P->n; ++i) s2 += (P->b[i] - ax[i]) * (P->b[i] - ax[i]);
+  // a singular FS block surfaces as SingularBlockError with the reference label
+  std::string label, expected;
+  {
+    std::vector<GmgLevel> bad = P->levels_add;
+    SparseMatrix broken = P->frame[L - 1];
+    const IndexSet& s0 = P->fs[L - 1]->fluid_block_dofs(3);
+    const int row = P->fs[L - 1]->group1_size() + s0.indices[0];
+    // the lowest AS2 block holding that dof is the one reported
+    for (int b = 0; b < P->fs[L - 1]->n_fluid_blocks() && expected.empty(); ++b)
+      if (P->fs[L - 1]->fluid_block_dofs(b).contains(s0.indices[0])) expected = P->fs[L - 1]->fluid_block_dofs(b).label;
+    for (int k = broken.row_offsets()[row]; k < broken.row_offsets()[row + 1]; ++k) broken.values()[k] = 0.0;
+    bad[L - 1].a = &broken;
+    try {
+      GpuGmg g2(bad, fs, cyc);
+    } catch (const SingularBlockError& e) {
+      label = e.label();
+    }
+  }
+  std::printf("{\"case\": \"%s\", \"restart\": %d, \"vcycle_rel\": %.3e, \"ref_iterations\": %d, "
+              "\"ref_converged\": %d, \"ref_relres\": %.6e, \"gpu_iterations\": %d, \"gpu_converged\": %d, "
+              "\"gpu_relres\": %.6e, \"singular_label\": \"%s\", \"expected_label\": \"%s\"}\n",
+              a.pos[1].c_str(), kc.restart, std::sqrt(num / den), ref.res.iterations, (int)ref.res.converged,
+              ref.true_res / ref.res.history.front(), g.iterations, (int)g.converged,
+              std::sqrt(s2) / g.history.front(), label.c_str(), expected.c_str());
+  return 0;
+}
+#endif
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -809,6 +905,9 @@ int main(int argc, char** argv) {
     if (c == "solve") return cmd_solve(a);
     if (c == "blocks") return cmd_blocks(a);
     if (c == "time-blocks") return cmd_time_blocks(a);
+#ifdef FSI_ADAPTER_CHECK
+    if (c == "gpu-adapter") return cmd_gpu_adapter(a);
+#endif
     std::fprintf(stderr, "unknown command %s\n", c.c_str());
     return 2;
   } catch (const std::exception& e) {

@@ -11,6 +11,7 @@
 #include <functional>
 #include <memory>
 #include <type_traits>
+#include <atomic>
 #include <mutex>
 #include <cstdlib>
 #include <string>
@@ -26,6 +27,7 @@
 #include "common.cuh"
 #include "dense.cuh"
 #include "krylov.cuh"
+#include "krylov_wide.cuh"
 #include "sparse.cuh"
 #include "mr.cuh"
 
@@ -35,7 +37,7 @@ namespace fsigpu {
 // Solve-path kernels are launched with programmatic stream serialization
 // (PDL): inside the captured graphs consecutive kernels overlap launch and
 // prologue with the predecessor's tail (kernels call pdl_trigger/pdl_wait).
-static bool g_pdl = false;  // measured neutral on config 0 (tools/ab_test.py); opt-in
+static std::atomic<bool> g_pdl{false};  // measured neutral on config 0; opt-in
 template <typename... KArgs, typename... Args>
 static void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                      Args&&... args) {
@@ -56,6 +58,7 @@ static void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
 // ------------------------------------------------------------ errors
 static thread_local std::string g_err;
 static thread_local int g_bad_block = -1;
+static thread_local int g_bad_level = -1;  // GMG level of the failing block (-1: standalone batch)
 
 // ------------------------------------------------------------ profiler
 struct Profiler {
@@ -133,7 +136,7 @@ struct ProfScope {
 
 // Host-side count of our kernel launches (graph replays are added from the
 // per-graph counts taken at capture time).
-static long long g_launches = 0;
+static std::atomic<long long> g_launches{0};
 static inline void counted(int k = 1) { g_launches += k; }
 
 // ------------------------------------------------------------ CSR
@@ -268,7 +271,7 @@ struct Csr {
 // Block solve modes: LU forward/back substitution (tiled, tile inverses) or
 // explicit block inverse (computed at setup from the bit-exact LU).
 enum BlockMode { kModeLU = 0, kModeInverse = 1, kModeAssembled = 2 };
-static int g_default_mode = kModeAssembled;
+static std::atomic<int> g_default_mode{kModeAssembled};
 
 // FSIGPU_FORCE_BIG=1: take the large-system kernel variants at any size
 // (k_spmv_dots_s, the cp.async Arnoldi stages, paired SpMV / A*P loads), so
@@ -666,6 +669,11 @@ struct Gmg {
   DevBuf<double> coarse_inv;  // equilibrated explicit inverse, row-major
   cudaStream_t s = nullptr;
   DevBuf<double> tmp_in, tmp_out;
+  // Every entry point that launches on this hierarchy holds the lock: the
+  // V-cycle rewires the top level's b/x pointers and shares per-level
+  // scratch, so concurrent callers of one handle are serialised (the
+  // reference's const apply is re-entrant, precond.cpp:45,61).
+  std::mutex mu;
 
   int size() const { return lv.back().n; }
 
@@ -794,6 +802,15 @@ struct Gmg {
       combine(l, L.rbuf.p, 0);
     }
   }
+  // x (+)= A0^-1 rhs through the equilibrated explicit inverse
+  void coarse_gemv(const double* rhs, double* x, int accumulate, const unsigned char* mask_out) {
+    Level& L = lv[0];
+    ProfScope ps(FSIGPU_K_COARSE, 8.0 * L.n * L.n + 16.0 * L.n, s);
+    launch_k(gemv_kernel, dim3(L.n), dim3(kGemvThreads), 0, s, L.n, (const double*)coarse_inv.p, rhs, x,
+             accumulate, mask_out);
+    FSI_CHECK_LAUNCH();
+    counted();
+  }
   void coarse(int x_zero, bool mask_out = false) {
     Level& L = lv[0];
     const double* rhs = L.b;
@@ -801,12 +818,7 @@ struct Gmg {
       resid(0, L.rbuf.p);
       rhs = L.rbuf.p;
     }
-    ProfScope ps(FSIGPU_K_COARSE, 8.0 * L.n * L.n + 16.0 * L.n, s);
-    launch_k(gemv_kernel, dim3(L.n), dim3(kGemvThreads), 0, s, L.n,
-             (const double*)coarse_inv.p, rhs, L.x, x_zero ? 0 : 1,
-             (const unsigned char*)(mask_out ? L.cmask.p : nullptr));
-    FSI_CHECK_LAUNCH();
-    counted();
+    coarse_gemv(rhs, L.x, x_zero ? 0 : 1, mask_out ? L.cmask.p : nullptr);
   }
   // GmgPreconditioner::cycle (gmg.cpp:188-239). mask_out: this is the last
   // visit of a coarse level, so its final kernel may write the iterate with
@@ -1093,6 +1105,7 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
     try {
       B.factor(dense.p, B.pos.p, 0, s);
     } catch (Error& e) {
+      if (e.code == FSIGPU_ERR_SINGULAR) g_bad_level = l;
       throw Error(e.code, std::string(e.what()) + " (level " + std::to_string(l) + ")");
     }
   }
@@ -1123,7 +1136,13 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
   L.aus_ptr.upload(ap, s);
   L.aus_col.upload(ac.empty() ? std::vector<int>{0} : ac, s);
   L.aus_val.upload(av.empty() ? std::vector<double>{0.0} : av, s);
-  for (int i = 0; i < d.n_us; ++i) require(d.lumped[i] != 0.0, "fs: zero lumped mass entry");
+  // the reference rejects a non-positive lumped row sum (precond.cpp:239-241)
+  for (int i = 0; i < d.n_us; ++i)
+    if (!(d.lumped[i] > 0.0)) {
+      g_bad_block = -1;
+      g_bad_level = l;
+      throw Error(FSIGPU_ERR_SINGULAR, "singular block: fs lumped mass row " + std::to_string(i));
+    }
   FSI_CUDA(cudaStreamSynchronize(s));
   if (g_default_mode == kModeAssembled) assemble_fs(L, d, pos, cnt, ap, ac, av, s);
 }
@@ -1171,6 +1190,7 @@ static void build_coarse(Gmg& g, const fsigpu_level_desc& d, cudaStream_t s) {
   FSI_CUDA(cudaStreamSynchronize(s));
   if (bad) {
     g_bad_block = -1;
+    g_bad_level = 0;
     throw Error(FSIGPU_ERR_SINGULAR, "singular block: gmg-coarse");
   }
 }
@@ -1215,7 +1235,7 @@ struct Gmres {
   int n = 0, mr = 30;
   int grid = 0;
   bool graphs = true;
-  DevBuf<double> scale, V, Z, w, zbuf, ubuf, r, x, b, H, cs, sn, gv, hist, partial, partial2;
+  DevBuf<double> scale, V, Z, w, zbuf, ubuf, r, x, b, H, cs, sn, gv, hist, partial, partial2, partialw;
   DevBuf<unsigned int> ticket;
   DevBuf<KState> st;
   KBufs kb{};
@@ -1254,8 +1274,29 @@ struct Gmres {
     ProfScope ps(FSIGPU_K_SPMV, T.A.bytes(true) + 8.0 * n, g->s);
     T.A.launch(GatherPlain{x.p}, EpiResidScaled{b.p, scale.p, r.p}, g->s);
   }
+  // restart > 32: the chunked five-kernel step of krylov_wide.cuh
+  void arnoldi_wide(const KBufs& kk) {
+    cudaStream_t s = g->s;
+    const int pw = kk.parts_w;
+    const int chunks = ceil_div(mr, kRegRestart);
+    {
+      ProfScope ps(FSIGPU_K_SPMV, g->lv.back().A.bytes(false) + 8.0 * n * 3, s);
+      launch_k(k_wide_spmv, dim3(pw), dim3(kWideThreads), 0, s, kk);
+    }
+    ProfScope ps(FSIGPU_K_ARNOLDI, 8.0 * n * 6, s);
+    launch_k(k_wide_dots<false>, dim3(pw, chunks), dim3(kWideThreads), 0, s, kk);
+    launch_k(k_wide_update, dim3(pw), dim3(kWideThreads), 0, s, kk);
+    launch_k(k_wide_dots<true>, dim3(pw, chunks), dim3(kWideThreads), 0, s, kk);
+    launch_k(k_wide_normalize, dim3(pw + 1), dim3(kWideThreads), 0, s, kk);
+    FSI_CHECK_LAUNCH();
+    counted(5);
+  }
   // outer SpMV + CGS2 Arnoldi + Givens + normalisation: 3 fused kernels
   void arnoldi_fused(const KBufs& kk) {
+    if (mr > kRegRestart) {
+      arnoldi_wide(kk);
+      return;
+    }
     cudaStream_t s = g->s;
     Level& T = g->lv.back();
     const int gs = kk.parts_a;
@@ -1448,6 +1489,7 @@ extern "C" {
 
 const char* fsigpu_last_error(void) { return g_err.c_str(); }
 int fsigpu_last_singular_block(void) { return g_bad_block; }
+int fsigpu_last_singular_level(void) { return g_bad_level; }
 int fsigpu_version(void) { return 1; }
 long long fsigpu_launch_count(void) { return g_launches; }
 int fsigpu_set_pdl(int enable) {
@@ -1474,6 +1516,7 @@ int fsigpu_gmg_set_smoother(fsigpu_gmg h, int kind) {
   return guarded([&] {
     require(h != nullptr, "gmg: null");
     require(kind == 0 || kind == 1, "smoother must be 0 (richardson) or 1 (gmres1)");
+    std::lock_guard<std::mutex> lk(h->g.mu);
     h->g.set_smoother(kind);
   });
 }
@@ -1559,6 +1602,7 @@ void fsigpu_csr_destroy(fsigpu_csr a) {
 int fsigpu_blocks_factor_csr(fsigpu_csr a, int n_blocks, const int* block_ptr, const int* block_idx,
                              fsigpu_blocks* out) {
   g_bad_block = -1;
+  g_bad_level = -1;
   return guarded([&] {
     require(a != nullptr && n_blocks >= 0, "blocks: bad args");
     require(a->a.rows == a->a.cols, "schwarz: matrix not square");
@@ -1591,6 +1635,7 @@ int fsigpu_blocks_factor_csr(fsigpu_csr a, int n_blocks, const int* block_ptr, c
 
 int fsigpu_blocks_factor_dense(int n_blocks, const int* sizes, const double* mats, fsigpu_blocks* out) {
   g_bad_block = -1;
+  g_bad_level = -1;
   return guarded([&] {
     require(n_blocks >= 0, "blocks: bad args");
     auto h = std::make_unique<fsigpu_blocks_t>();
@@ -1617,6 +1662,7 @@ int fsigpu_blocks_factor_dense(int n_blocks, const int* sizes, const double* mat
 
 int fsigpu_blocks_generate_dominant(long long n54, long long n59, unsigned long long seed, fsigpu_blocks* out) {
   g_bad_block = -1;
+  g_bad_level = -1;
   return guarded([&] {
     require(n54 >= 0 && n59 >= 0, "blocks: bad counts");
     auto h = std::make_unique<fsigpu_blocks_t>();
@@ -1700,6 +1746,7 @@ int fsigpu_blocks_solve(fsigpu_blocks b, const double* rhs, double* x) {
 
 int fsigpu_blocks_refactor(fsigpu_blocks b, void* stream) {
   g_bad_block = -1;
+  g_bad_level = -1;
   return guarded([&] {
     require(b != nullptr && b->have_orig, "blocks: no retained matrices");
     cudaStream_t s = stream ? (cudaStream_t)stream : b->s;
@@ -1736,6 +1783,7 @@ void fsigpu_blocks_destroy(fsigpu_blocks b) {
 int fsigpu_gmg_create(int n_levels, const fsigpu_level_desc* levels, double omega, int pre, int post, char cycle,
                       fsigpu_gmg* out) {
   g_bad_block = -1;
+  g_bad_level = -1;
   return guarded([&] {
     require(n_levels >= 1 && levels != nullptr, "gmg: no levels");
     require(pre >= 0 && post >= 0 && !(pre == 0 && post == 0 && n_levels > 1), "gmg: need at least one smoothing sweep");
@@ -1764,6 +1812,7 @@ int fsigpu_gmg_apply_dev(fsigpu_gmg g, const double* d_r, double* d_z, void* str
   return guarded([&] {
     require(g != nullptr, "gmg: null");
     require(stream == nullptr || stream == (void*)g->g.s, "gmg: use the handle stream (NULL)");
+    std::lock_guard<std::mutex> lk(g->g.mu);
     g->g.apply(d_r, d_z);
     if (g_prof.on) g_prof.flush();
   });
@@ -1773,6 +1822,7 @@ int fsigpu_gmg_apply(fsigpu_gmg g, const double* r, double* z) {
   return guarded([&] {
     require(g != nullptr, "gmg: null");
     Gmg& G = g->g;
+    std::lock_guard<std::mutex> lk(G.mu);
     const int n = G.size();
     FSI_CUDA(cudaMemcpyAsync(G.tmp_in.p, r, sizeof(double) * n, cudaMemcpyHostToDevice, G.s));
     G.apply(G.tmp_in.p, G.tmp_out.p);
@@ -1787,22 +1837,11 @@ int fsigpu_fs_apply(fsigpu_gmg g, int level, const double* r, double* z) {
     require(g != nullptr, "gmg: null");
     Gmg& G = g->g;
     require(level >= 1 && level < (int)G.lv.size(), "fs: level must be a smoothed level (>= 1)");
+    std::lock_guard<std::mutex> lk(G.mu);
     Level& L = G.lv[level];
     DevBuf<double> dr, dz(L.n);
     dr.upload(r, (size_t)L.n, G.s);
-    double* sx = L.x;
-    L.x = dz.p;
-    // z = M r  ==  one sweep with omega = 1 from x = 0
-    const double om = G.omega;
-    G.omega = 1.0;
-    if (L.assembled) {
-      G.fs_spmv(level, dr.p, 1);
-    } else {
-      G.smooth_solve(level, dr.p);
-      G.combine(level, dr.p, 1);
-    }
-    G.omega = om;
-    L.x = sx;
+    G.fs_into(level, dr.p, dz.p);  // z = M r (the smoother applied once, no damping)
     FSI_CUDA(cudaMemcpyAsync(z, dz.p, sizeof(double) * L.n, cudaMemcpyDeviceToHost, G.s));
     FSI_CUDA(cudaStreamSynchronize(G.s));
   });
@@ -1812,16 +1851,11 @@ int fsigpu_coarse_solve(fsigpu_gmg g, const double* b, double* x) {
   return guarded([&] {
     require(g != nullptr, "gmg: null");
     Gmg& G = g->g;
+    std::lock_guard<std::mutex> lk(G.mu);
     Level& L = G.lv[0];
     DevBuf<double> db, dx(L.n);
     db.upload(b, (size_t)L.n, G.s);
-    double* sb = L.b;
-    double* sx = L.x;
-    L.b = db.p;
-    L.x = dx.p;
-    G.coarse(1);
-    L.b = sb;
-    L.x = sx;
+    G.coarse_gemv(db.p, dx.p, 0, nullptr);
     FSI_CUDA(cudaMemcpyAsync(x, dx.p, sizeof(double) * L.n, cudaMemcpyDeviceToHost, G.s));
     FSI_CUDA(cudaStreamSynchronize(G.s));
   });
@@ -1837,6 +1871,7 @@ int fsigpu_gmg_time_kernel(fsigpu_gmg h, int which, int level, int reps, int col
   return guarded([&] {
     require(h != nullptr && reps > 0, "time: bad args");
     Gmg& G = h->g;
+    std::lock_guard<std::mutex> lk(G.mu);
     require(level >= 0 && level < (int)G.lv.size(), "time: bad level");
     Level& L = G.lv[level];
     cudaStream_t s = G.s;
@@ -1932,7 +1967,7 @@ void fsigpu_gmg_destroy(fsigpu_gmg g) {
 int fsigpu_gmres_create(fsigpu_gmg g, const double* frame_scale, int restart, fsigpu_gmres* out) {
   return guarded([&] {
     require(g != nullptr && frame_scale != nullptr, "gmres: null args");
-    require(restart >= 1 && restart <= kMaxRestart, "gmres: restart must be in [1, 32]");
+    require(restart >= 1 && restart <= kMaxRestart, "gmres: restart must be in [1, 128]");
     auto h = std::make_unique<fsigpu_gmres_t>();
     Gmres& k = h->k;
     k.g = &g->g;
@@ -1955,8 +1990,8 @@ int fsigpu_gmres_create(fsigpu_gmg g, const double* frame_scale, int restart, fs
     k.sn.alloc(restart);
     k.gv.alloc(restart + 1);
     k.grid = std::max(1, std::min(ceil_div(n, kKThreads), 2 * 148));
-    k.partial.alloc((size_t)std::max(std::max(k.grid, ceil_div(n, kFuseRows)), 4 * 148) * (kMaxRestart + 1));
-    k.partial2.alloc((size_t)(n > 8 * 148 * kFuseRows ? 16 : 4) * 148 * (kMaxRestart + 1));  // (B) grid <= 16 (big) / 4 CTAs per SM
+    k.partial.alloc((size_t)std::max(std::max(k.grid, ceil_div(n, kFuseRows)), 4 * 148) * kPartLd);
+    k.partial2.alloc((size_t)(n > 8 * 148 * kFuseRows ? 16 : 4) * 148 * kPartLd);  // (B) grid <= 16 (big) / 4 CTAs per SM
     k.ticket.alloc(1);
     k.ticket.zero(s);
     k.st.alloc(1);
@@ -1978,6 +2013,12 @@ int fsigpu_gmres_create(fsigpu_gmg g, const double* frame_scale, int restart, fs
     kb.g = k.gv.p;
     kb.partial = k.partial.p;
     kb.partial2 = k.partial2.p;
+    if (restart > kRegRestart) {
+      // wide path: one wave of 256-thread CTAs (<= 2 per SM)
+      kb.parts_w = std::max(1, std::min(ceil_div(n, kWideThreads), 2 * 148));
+      k.partialw.alloc((size_t)ceil_div(restart, kRegRestart) * kb.parts_w * kPartLd);
+      kb.partialw = k.partialw.p;
+    }
     {
       // resident CTAs of k_spmv_dots (1024 threads): the tile loop's grid
       int dev = 0, sms = 0, occ = 0;
@@ -2046,6 +2087,7 @@ int fsigpu_gmres_solve_dev(fsigpu_gmres s, const double* d_b, double* d_x, int m
   return guarded([&] {
     require(s != nullptr && d_b != nullptr && d_x != nullptr, "gmres: null args");
     Gmres& k = s->k;
+    std::lock_guard<std::mutex> lk(k.g->mu);
     cudaStream_t st = k.g->s;
     const size_t nb = sizeof(double) * k.n;
     FSI_CUDA(cudaMemcpyAsync(k.b.p, d_b, nb, cudaMemcpyDeviceToDevice, st));
@@ -2066,6 +2108,7 @@ int fsigpu_gmres_solve(fsigpu_gmres s, const double* b, const double* x0, double
   return guarded([&] {
     require(s != nullptr && b != nullptr && x != nullptr, "gmres: null args");
     Gmres& k = s->k;
+    std::lock_guard<std::mutex> lk(k.g->mu);
     cudaStream_t st = k.g->s;
     const size_t nb = sizeof(double) * k.n;
     FSI_CUDA(cudaMemcpyAsync(k.b.p, b, nb, cudaMemcpyHostToDevice, st));
@@ -2086,7 +2129,9 @@ int fsigpu_gmres_solve(fsigpu_gmres s, const double* b, const double* x0, double
 
 void fsigpu_gmres_destroy(fsigpu_gmres s) {
   if (!s) return;
-  cudaStreamSynchronize(s->k.g->s);
+  // the solver must not touch its hierarchy here: a garbage collector may
+  // destroy the hierarchy first (its stream then no longer exists)
+  cudaDeviceSynchronize();
   delete s;
 }
 

@@ -20,7 +20,10 @@
 
 namespace fsigpu {
 
-constexpr int kMaxRestart = 32;  // restart <= 32 (V_{0..j} dots held in registers)
+constexpr int kRegRestart = 32;   // restart <= 32: the V_{0..j} dots of a row held in registers
+constexpr int kMaxRestart = 128;  // larger restarts (the reference default is 60) take the
+                                  // chunked path of krylov_wide.cuh
+constexpr int kPartLd = kRegRestart + 1;  // row stride of the per-CTA partial-dot buffers
 constexpr int kKThreads = 128;
 
 struct KState {
@@ -61,12 +64,14 @@ struct KBufs {
   double* sn;
   double* g;
   double* history;      // max_iters + 2
-  double* partial;      // grid x (kMaxRestart+1)
+  double* partial;      // grid x (kRegRestart+1)
   double* partial2;     // second partial buffer of the fused Arnoldi step
   int parts_a;          // CTAs of k_spmv_dots (rows of partial it writes)
   int fuse_small;       // (A) runs as k_spmv_dots_s (large n)
   int parts_b;          // CTAs of k_update_dots_norm (rows of partial2)
   int parts_c;          // row CTAs of k_update_normalize (+1 Givens CTA)
+  double* partialw;     // restart > 32 (krylov_wide.cuh): chunks x parts_w x kPartLd
+  int parts_w;          // row CTAs of the wide-path kernels
   unsigned int* ticket;
   KState* st;
   // fused Arnoldi (3 kernels per step)
@@ -131,7 +136,7 @@ __device__ __forceinline__ void finish_sum(const KBufs& k, int nv, double* dst) 
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const unsigned int b = b0 + 32 * u;
-        pv[u] = b < gridDim.x ? __ldcg(k.partial + (size_t)b * (kMaxRestart + 1) + v) : 0.0;
+        pv[u] = b < gridDim.x ? __ldcg(k.partial + (size_t)b * kPartLd + v) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) s += pv[u];
@@ -141,55 +146,6 @@ __device__ __forceinline__ void finish_sum(const KBufs& k, int nv, double* dst) 
     if (lane == 0) dst[v] = s;
   }
   if (threadIdx.x == 0) *k.ticket = 0;
-}
-
-// h1 = V^T w  (+ Z[j] = zbuf)
-__global__ void __launch_bounds__(kKThreads) k_dots(KBufs k) {
-  __shared__ double sm[kMaxRestart * kKThreads];
-  const int j = k.st->j;
-  const int nv = j + 1;
-  double acc[kMaxRestart];
-#pragma unroll
-  for (int v = 0; v < kMaxRestart; ++v) acc[v] = 0.0;
-  double* zj = k.Z + (size_t)j * k.n;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x) {
-    const double wr = k.w[r];
-    zj[r] = k.zbuf[r];
-#pragma unroll
-    for (int v = 0; v < kMaxRestart; ++v)
-      if (v < nv) acc[v] = fma(k.V[(size_t)v * k.n + r], wr, acc[v]);
-  }
-  block_reduce_vec<kMaxRestart>(acc, nv, sm, k.partial + (size_t)blockIdx.x * (kMaxRestart + 1));
-  if (last_block(k.ticket)) finish_sum(k, nv, k.st->h1);
-}
-
-// w -= V h_in ; h_out = V^T w
-__global__ void __launch_bounds__(kKThreads) k_update_dots(KBufs k) {
-  __shared__ double sm[kMaxRestart * kKThreads];
-  __shared__ double hs[kMaxRestart];
-  const int j = k.st->j;
-  const int nv = j + 1;
-  if (threadIdx.x < nv) hs[threadIdx.x] = k.st->h1[threadIdx.x];
-  __syncthreads();
-  double acc[kMaxRestart];
-#pragma unroll
-  for (int v = 0; v < kMaxRestart; ++v) acc[v] = 0.0;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x) {
-    double vr[kMaxRestart];
-    double wr = k.w[r];
-#pragma unroll
-    for (int v = 0; v < kMaxRestart; ++v)
-      if (v < nv) {
-        vr[v] = k.V[(size_t)v * k.n + r];
-        wr = fma(-hs[v], vr[v], wr);
-      }
-    k.w[r] = wr;
-#pragma unroll
-    for (int v = 0; v < kMaxRestart; ++v)
-      if (v < nv) acc[v] = fma(vr[v], wr, acc[v]);
-  }
-  block_reduce_vec<kMaxRestart>(acc, nv, sm, k.partial + (size_t)blockIdx.x * (kMaxRestart + 1));
-  if (last_block(k.ticket)) finish_sum(k, nv, k.st->h2);
 }
 
 // Givens update of column j on device (krylov.cpp:79-100), staged in
@@ -233,68 +189,13 @@ __device__ void givens_core(const KBufs& k, int j, double hn, double* col, doubl
     k.sn[j] = sj;
   }
   __syncthreads();
-  if (t <= j + 1) k.H[t * mr + j] = col[t];
+  for (int i = t; i <= j + 1; i += blockDim.x) k.H[i * mr + j] = col[i];
   if (t == 0) {
     st->j = j + 1;
     if (k.use_cond) {
       const int go = (!st->stop && j + 1 < mr && st->its < st->max_iters) ? 1 : 0;
       cudaGraphSetConditional(k.cond, go);
     }
-  }
-}
-
-__device__ void givens_step(const KBufs& k, double hn) {
-  __shared__ double col[kMaxRestart + 2], cs[kMaxRestart + 1], sn[kMaxRestart + 1];
-  __shared__ double s_gj;
-  const KState* st = k.st;
-  const int j = st->j;
-  const int t = threadIdx.x;
-  if (t <= j) col[t] = __ldcg(st->h1 + t) + __ldcg(st->h2 + t);
-  if (t < j) {
-    cs[t] = __ldcg(k.cs + t);
-    sn[t] = __ldcg(k.sn + t);
-  }
-  if (t == 0) s_gj = __ldcg(k.g + j);
-  __syncthreads();
-  givens_core(k, j, hn, col, cs, sn, s_gj);
-}
-
-// w -= V h2 ; ||w|| ; Givens
-__global__ void __launch_bounds__(kKThreads) k_update_norm(KBufs k) {
-  __shared__ double sm[kKThreads];
-  __shared__ double hs[kMaxRestart];
-  const int j = k.st->j;
-  const int nv = j + 1;
-  if (threadIdx.x < nv) hs[threadIdx.x] = k.st->h2[threadIdx.x];
-  __syncthreads();
-  double acc[1] = {0.0};
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x) {
-    double wr = k.w[r];
-#pragma unroll
-    for (int v = 0; v < kMaxRestart; ++v)
-      if (v < nv) wr = fma(-hs[v], k.V[(size_t)v * k.n + r], wr);
-    k.w[r] = wr;
-    acc[0] = fma(wr, wr, acc[0]);
-  }
-  block_reduce_vec<1>(acc, 1, sm, k.partial + (size_t)blockIdx.x * (kMaxRestart + 1));
-  if (last_block(k.ticket)) {
-    __shared__ double s_n2;
-    finish_sum(k, 1, &s_n2);
-    __syncthreads();
-    givens_step(k, sqrt(s_n2));
-  }
-}
-
-// v_{j} = w / hn (j already advanced), u = v_j / scale; skipped on breakdown.
-__global__ void k_normalize(KBufs k) {
-  const KState* st = k.st;
-  if (st->hn < 1e-14) return;
-  const double hn = st->hn;
-  double* vj = k.V + (size_t)st->j * k.n;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x) {
-    const double v = k.w[r] / hn;
-    vj[r] = v;
-    k.ubuf[r] = v / k.scale[r];
   }
 }
 
@@ -306,7 +207,7 @@ __global__ void __launch_bounds__(kKThreads) k_norm_r(KBufs k) {
   double acc[1] = {0.0};
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x)
     acc[0] = fma(k.r[r], k.r[r], acc[0]);
-  block_reduce_vec<1>(acc, 1, sm, k.partial + (size_t)blockIdx.x * (kMaxRestart + 1));
+  block_reduce_vec<1>(acc, 1, sm, k.partial + (size_t)blockIdx.x * kPartLd);
   if (last_block(k.ticket)) {
     __shared__ double s_n2;
     finish_sum(k, 1, &s_n2);
@@ -342,25 +243,34 @@ __global__ void k_cycle_start(KBufs k) {
   }
 }
 
-// y = H^{-1} g (back substitution, krylov.cpp:103-109): H staged in
-// shared memory, one thread runs the recurrence.
+// y = H^{-1} g (back substitution, krylov.cpp:103-109): H (j <= 32) staged
+// in shared memory, one thread runs the recurrence; wider restarts read H
+// from global memory (once per restart cycle, off the per-step path).
 __global__ void k_solve_y(KBufs k) {
   pdl_trigger();
   pdl_wait();
-  __shared__ double Hs[kMaxRestart * kMaxRestart];
+  __shared__ double Hs[kRegRestart * kRegRestart];
   __shared__ double gs[kMaxRestart + 1];
+  __shared__ double y[kMaxRestart];
   KState* st = k.st;
   const int j = st->j;
   const int mr = k.mr;
-  for (int e = threadIdx.x; e < j * j; e += blockDim.x) Hs[e] = k.H[(e / j) * mr + (e % j)];
-  if (threadIdx.x < j) gs[threadIdx.x] = k.g[threadIdx.x];
+  const bool staged = j <= kRegRestart;
+  if (staged)
+    for (int e = threadIdx.x; e < j * j; e += blockDim.x) Hs[e] = k.H[(e / j) * mr + (e % j)];
+  for (int i = threadIdx.x; i < j; i += blockDim.x) gs[i] = k.g[i];
   __syncthreads();
-  __shared__ double y[kMaxRestart];
   if (threadIdx.x == 0) {
     for (int i = j - 1; i >= 0; --i) {
       double s = gs[i];
-      for (int q = i + 1; q < j; ++q) s -= Hs[i * j + q] * y[q];
-      y[i] = s / Hs[i * j + i];
+      if (staged) {
+        for (int q = i + 1; q < j; ++q) s -= Hs[i * j + q] * y[q];
+        y[i] = s / Hs[i * j + i];
+      } else {
+        const double* Hi = k.H + (size_t)i * mr;
+        for (int q = i + 1; q < j; ++q) s -= __ldcg(Hi + q) * y[q];
+        y[i] = s / __ldcg(Hi + i);
+      }
     }
     for (int i = 0; i < j; ++i) st->y[i] = y[i];
   }
@@ -373,29 +283,25 @@ __global__ void k_update_x(KBufs k) {
   const KState* st = k.st;
   const int j = st->j;
   __shared__ double ys[kMaxRestart];
-  if (threadIdx.x < j) ys[threadIdx.x] = st->y[threadIdx.x];
+  for (int i = threadIdx.x; i < j; i += blockDim.x) ys[i] = st->y[i];
   __syncthreads();
-  // all j loads of a row issued before its FMA chain (predicated batch of
-  // kMaxRestart; a runtime-bound loop left one DRAM latency per term)
+  // all loads of a row's 32-column chunk issued before its FMA chain
+  // (predicated batch; a runtime-bound loop left one DRAM latency per term)
   const double* __restrict__ Z = k.Z;
   double* __restrict__ X = k.x;
   const size_t n = (size_t)k.n;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x) {
-    double z[kMaxRestart];
-#pragma unroll
-    for (int i = 0; i < kMaxRestart; ++i) z[i] = i < j ? __ldg(Z + (size_t)i * n + r) : 0.0;
     double s = 0.0;
+    for (int c0 = 0; c0 < j; c0 += kRegRestart) {
+      double z[kRegRestart];
 #pragma unroll
-    for (int i = 0; i < kMaxRestart; ++i)
-      if (i < j) s = fma(ys[i], z[i], s);
+      for (int i = 0; i < kRegRestart; ++i) z[i] = c0 + i < j ? __ldg(Z + (size_t)(c0 + i) * n + r) : 0.0;
+#pragma unroll
+      for (int i = 0; i < kRegRestart; ++i)
+        if (c0 + i < j) s = fma(ys[c0 + i], z[i], s);
+    }
     X[r] += s;
   }
-}
-
-// Device-side continue flag for the conditional WHILE node of a cycle.
-__global__ void k_set_continue(const KState* st, cudaGraphConditionalHandle h, int mr) {
-  const int go = (!st->stop && st->j < mr && st->its < st->max_iters) ? 1 : 0;
-  cudaGraphSetConditional(h, go);
 }
 
 }  // namespace fsigpu
@@ -480,7 +386,7 @@ __global__ void __launch_bounds__(kFuseThreads) k_spmv_dots_1(KBufs k) {
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-  if (lane == 0 && v < nv) k.partial[(size_t)blockIdx.x * (kMaxRestart + 1) + v] = s;
+  if (lane == 0 && v < nv) k.partial[(size_t)blockIdx.x * kPartLd + v] = s;
 }
 
 // Grid-stride over 128-row tiles with the grid capped at the resident CTA
@@ -536,7 +442,7 @@ __global__ void __launch_bounds__(kFuseThreads) k_spmv_dots(KBufs k) {
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-  if (lane == 0 && v < nv) k.partial[(size_t)blockIdx.x * (kMaxRestart + 1) + v] = s;
+  if (lane == 0 && v < nv) k.partial[(size_t)blockIdx.x * kPartLd + v] = s;
 }
 
 // Per-CTA sums of 32 per-thread values plus one extra: a butterfly
@@ -572,15 +478,15 @@ __device__ __forceinline__ void cta_reduce_t32(double (&a)[32], double extra, in
 }
 
 // Fixed-order sum of `nparts` per-CTA partial rows (row stride
-// kMaxRestart+1) for values 0..nv-1 (nv <= kMaxRestart+1) into dst[]:
+// kRegRestart+1) for values 0..nv-1 (nv <= kRegRestart+1) into dst[]:
 // lanes own values, warps own CTA slices, slices added in order. Every CTA
 // of the consumer kernel runs it on the producer's partials, so no CTA of
 // the producer has to finish the reduction (no last-CTA tail).
 constexpr int kSumSlices = 16;
 template <int T>
 __device__ __forceinline__ void sum_partials(const double* __restrict__ part, int nparts, int nv, double* dst,
-                                             double* red /* kSumSlices x (kMaxRestart+1) */) {
-  constexpr int LD = kMaxRestart + 1;
+                                             double* red /* kSumSlices x (kRegRestart+1) */) {
+  constexpr int LD = kRegRestart + 1;
   // thread t -> value t % nv of CTA slice t / nv (ns slices, fixed for a
   // given nv, so the summation order is deterministic)
   const int ns = min(kSumSlices, T / nv);
@@ -609,46 +515,6 @@ __device__ __forceinline__ void sum_partials(const double* __restrict__ part, in
   __syncthreads();
 }
 
-// fused_row with 16-byte index/value pairs (see csr_pair_kernel), UP pairs
-// per lane per batch. Not used by default: in k_spmv_dots_s (LPR 8, UP 5)
-// its 80 registers cost a CTA per SM and the config-2 step went 243 -> 265 us.
-template <int LPR, int UP>
-__device__ __forceinline__ double fused_row_pair(const KBufs& k, int row, int lane) {
-  const int k0 = row >= 0 ? __ldg(k.a_ptr + row) : 0, k1 = row >= 0 ? __ldg(k.a_ptr + row + 1) : 0;
-  double s = 0.0;
-  for (int kb = (k0 & ~1) + 2 * lane; kb < k1; kb += 2 * UP * LPR) {
-    int2 c[UP];
-    double2 v[UP];
-#pragma unroll
-    for (int u = 0; u < UP; ++u) {
-      const int kk = kb + 2 * u * LPR;
-      if (kk < k1) {
-        c[u] = __ldg(reinterpret_cast<const int2*>(k.a_idx + kk));
-        v[u] = __ldg(reinterpret_cast<const double2*>(k.a_val + kk));
-        if (kk < k0) c[u].x = -1;
-        if (kk + 1 >= k1) c[u].y = -1;
-      } else {
-        c[u] = make_int2(-1, -1);
-        v[u] = make_double2(0.0, 0.0);
-      }
-    }
-    double x0[UP], x1[UP];
-#pragma unroll
-    for (int u = 0; u < UP; ++u) {
-      x0[u] = c[u].x >= 0 ? k.zbuf[c[u].x] : 0.0;
-      x1[u] = c[u].y >= 0 ? k.zbuf[c[u].y] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < UP; ++u) {
-      s = fma(v[u].x, x0[u], s);
-      s = fma(v[u].y, x1[u], s);
-    }
-  }
-#pragma unroll
-  for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, LPR);
-  return s;
-}
-
 // Large-n variant of (A): 256-thread CTAs on 32-row tiles (8 lanes per
 // row, one pass), several CTAs per SM, grid-stride over tiles with the grid
 // at the resident CTA count. With one 1024-thread CTA per SM (k_spmv_dots)
@@ -666,7 +532,7 @@ __global__ void __launch_bounds__(kFuseThreadsS) k_spmv_dots_s(KBufs k) {
   const int t = threadIdx.x;
   const int warp = t >> 5, lane = t & 31;
   constexpr int LPR = 8;
-  constexpr int NQ = kMaxRestart / (kFuseThreadsS / 32);  // vectors per warp
+  constexpr int NQ = kRegRestart / (kFuseThreadsS / 32);  // vectors per warp
   const int ntiles = (k.n + kFuseRowsS - 1) / kFuseRowsS;
   double s[NQ];
 #pragma unroll
@@ -707,7 +573,7 @@ __global__ void __launch_bounds__(kFuseThreadsS) k_spmv_dots_s(KBufs k) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
     const int v = warp + 8 * q;
-    if (lane == 0 && v < nv) k.partial[(size_t)blockIdx.x * (kMaxRestart + 1) + v] = x;
+    if (lane == 0 && v < nv) k.partial[(size_t)blockIdx.x * kPartLd + v] = x;
   }
 }
 
@@ -720,18 +586,18 @@ template <bool PF>
 __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm(KBufs k) {
   pdl_trigger();
   pdl_wait();
-  __shared__ double sm[(kMaxRestart + 1) * (kArnThreads / 32)];
-  __shared__ double hs[kMaxRestart + 1];
-  __shared__ double red[(kMaxRestart + 1) * kSumSlices];
+  __shared__ double sm[kPartLd * (kArnThreads / 32)];
+  __shared__ double hs[kRegRestart + 1];
+  __shared__ double red[kPartLd * kSumSlices];
   const int j = k.st->j;
   const int nv = j + 1;
   // this thread's first row is loaded before the h1 reduction (independent
   // of it), so the two latencies overlap
   const int r0 = blockIdx.x * blockDim.x + threadIdx.x;
-  double w0 = 0.0, v0[PF ? kMaxRestart : 1];
+  double w0 = 0.0, v0[PF ? kRegRestart : 1];
   if constexpr (PF) {
 #pragma unroll
-    for (int v = 0; v < kMaxRestart; ++v) v0[v] = (r0 < k.n && v < nv) ? k.V[(size_t)v * k.n + r0] : 0.0;
+    for (int v = 0; v < kRegRestart; ++v) v0[v] = (r0 < k.n && v < nv) ? k.V[(size_t)v * k.n + r0] : 0.0;
     if (r0 < k.n) w0 = k.w[r0];
   }
   sum_partials<kArnThreads>(k.partial, k.parts_a, nv, hs, red);
@@ -739,18 +605,18 @@ __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm(KBufs k) {
     if (threadIdx.x < nv) k.st->h1[threadIdx.x] = hs[threadIdx.x];
     if (threadIdx.x == 0) k.st->jc = j + 1;
   }
-  double acc[kMaxRestart];
+  double acc[kRegRestart];
 #pragma unroll
-  for (int v = 0; v < kMaxRestart; ++v) acc[v] = 0.0;
+  for (int v = 0; v < kRegRestart; ++v) acc[v] = 0.0;
   double n2 = 0.0;
   if (PF && r0 < k.n) {
     double wr = w0;
 #pragma unroll
-    for (int v = 0; v < kMaxRestart; ++v)
+    for (int v = 0; v < kRegRestart; ++v)
       if (v < nv) wr = fma(-hs[v], v0[PF ? v : 0], wr);
     k.w[r0] = wr;
 #pragma unroll
-    for (int v = 0; v < kMaxRestart; ++v)
+    for (int v = 0; v < kRegRestart; ++v)
       if (v < nv) acc[v] = fma(v0[PF ? v : 0], wr, acc[v]);
     n2 = fma(wr, wr, n2);
   }
@@ -758,11 +624,11 @@ __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm(KBufs k) {
     for (int r = r0 + gridDim.x * blockDim.x; r < k.n; r += gridDim.x * blockDim.x) {
       double wr = k.w[r];
   #pragma unroll
-      for (int v = 0; v < kMaxRestart; ++v)
+      for (int v = 0; v < kRegRestart; ++v)
         if (v < nv) wr = fma(-hs[v], k.V[(size_t)v * k.n + r], wr);
       k.w[r] = wr;
   #pragma unroll
-      for (int v = 0; v < kMaxRestart; ++v)
+      for (int v = 0; v < kRegRestart; ++v)
         if (v < nv) acc[v] = fma(k.V[(size_t)v * k.n + r], wr, acc[v]);  // L1 hits
       n2 = fma(wr, wr, n2);
     }
@@ -773,23 +639,23 @@ __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm(KBufs k) {
     double* __restrict__ W = k.w;
     const size_t n = (size_t)k.n;
     for (int r = PF ? r0 + gridDim.x * blockDim.x : r0; r < k.n; r += gridDim.x * blockDim.x) {
-      double vr[kMaxRestart];
+      double vr[kRegRestart];
 #pragma unroll
-      for (int v = 0; v < kMaxRestart; ++v) vr[v] = v < nv ? __ldg(V + (size_t)v * n + r) : 0.0;
+      for (int v = 0; v < kRegRestart; ++v) vr[v] = v < nv ? __ldg(V + (size_t)v * n + r) : 0.0;
       double wr = W[r];
 #pragma unroll
-      for (int v = 0; v < kMaxRestart; ++v)
+      for (int v = 0; v < kRegRestart; ++v)
         if (v < nv) wr = fma(-hs[v], vr[v], wr);
       W[r] = wr;
 #pragma unroll
-      for (int v = 0; v < kMaxRestart; ++v)
+      for (int v = 0; v < kRegRestart; ++v)
         if (v < nv) acc[v] = fma(vr[v], wr, acc[v]);
       n2 = fma(wr, wr, n2);
     }
   }
   // partial2[cta][0..nv) = h2 dots, partial2[cta][nv] = ||w||^2
-  static_assert(kMaxRestart == 32, "cta_reduce_t32 holds one slot per Krylov vector");
-  cta_reduce_t32<kArnThreads>(acc, n2, nv, sm, k.partial2 + (size_t)blockIdx.x * (kMaxRestart + 1));
+  static_assert(kRegRestart == 32, "cta_reduce_t32 holds one slot per Krylov vector");
+  cta_reduce_t32<kArnThreads>(acc, n2, nv, sm, k.partial2 + (size_t)blockIdx.x * kPartLd);
 }
 
 // Large-n variants of (B) and (C): each thread streams its rows' operands
@@ -799,7 +665,7 @@ __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm(KBufs k) {
 // chain runs, without holding them in registers. A thread reads back only
 // what it copied itself, so cp.async.wait_group alone orders the stages.
 // Slots: stage s, value q, thread t at stg[(s * kStageVals + q) * kArnThreads + t].
-constexpr int kStageVals = kMaxRestart + 2;
+constexpr int kStageVals = kRegRestart + 2;
 constexpr size_t kStageSmem = 2 * kStageVals * kArnThreads * sizeof(double);
 
 __device__ __forceinline__ void stage_row(const KBufs& k, double* stg, int st, int r, int nv, bool with_scale) {
@@ -807,8 +673,8 @@ __device__ __forceinline__ void stage_row(const KBufs& k, double* stg, int st, i
   if (r < k.n) {
     double* base = stg + (size_t)st * kStageVals * kArnThreads + t;
     for (int v = 0; v < nv; ++v) cp_async8(base + (size_t)v * kArnThreads, k.V + (size_t)v * k.n + r);
-    cp_async8(base + (size_t)kMaxRestart * kArnThreads, k.w + r);
-    if (with_scale) cp_async8(base + (size_t)(kMaxRestart + 1) * kArnThreads, k.scale + r);
+    cp_async8(base + (size_t)kRegRestart * kArnThreads, k.w + r);
+    if (with_scale) cp_async8(base + (size_t)kPartLd * kArnThreads, k.scale + r);
   }
   cp_async_commit();
 }
@@ -817,9 +683,9 @@ __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm_cp(KBufs k) {
   pdl_trigger();
   pdl_wait();
   extern __shared__ __align__(16) double stg[];
-  __shared__ double sm[(kMaxRestart + 1) * (kArnThreads / 32)];
-  __shared__ double hs[kMaxRestart + 1];
-  __shared__ double red[(kMaxRestart + 1) * kSumSlices];
+  __shared__ double sm[kPartLd * (kArnThreads / 32)];
+  __shared__ double hs[kRegRestart + 1];
+  __shared__ double red[kPartLd * kSumSlices];
   const int j = k.st->j;
   const int nv = j + 1;
   const int t = threadIdx.x;
@@ -831,27 +697,27 @@ __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm_cp(KBufs k) {
     if (t < nv) k.st->h1[t] = hs[t];
     if (t == 0) k.st->jc = j + 1;
   }
-  double acc[kMaxRestart];
+  double acc[kRegRestart];
 #pragma unroll
-  for (int v = 0; v < kMaxRestart; ++v) acc[v] = 0.0;
+  for (int v = 0; v < kRegRestart; ++v) acc[v] = 0.0;
   double n2 = 0.0;
   double* __restrict__ W = k.w;
   for (int it = 0; r < k.n; ++it, r += stride) {
     stage_row(k, stg, (it + 1) & 1, r + stride, nv, false);
     cp_async_wait<1>();
     const double* row = stg + (size_t)(it & 1) * kStageVals * kArnThreads + t;
-    double wr = row[(size_t)kMaxRestart * kArnThreads];
+    double wr = row[(size_t)kRegRestart * kArnThreads];
 #pragma unroll
-    for (int v = 0; v < kMaxRestart; ++v)
+    for (int v = 0; v < kRegRestart; ++v)
       if (v < nv) wr = fma(-hs[v], row[(size_t)v * kArnThreads], wr);
     W[r] = wr;
 #pragma unroll
-    for (int v = 0; v < kMaxRestart; ++v)
+    for (int v = 0; v < kRegRestart; ++v)
       if (v < nv) acc[v] = fma(row[(size_t)v * kArnThreads], wr, acc[v]);
     n2 = fma(wr, wr, n2);
   }
   cp_async_wait<0>();
-  cta_reduce_t32<kArnThreads>(acc, n2, nv, sm, k.partial2 + (size_t)blockIdx.x * (kMaxRestart + 1));
+  cta_reduce_t32<kArnThreads>(acc, n2, nv, sm, k.partial2 + (size_t)blockIdx.x * kPartLd);
 }
 
 // (C) every CTA sums (B)'s partials into h2 and ||w||^2 and forms
@@ -864,15 +730,15 @@ template <bool PF>
 __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
   pdl_trigger();
   pdl_wait();
-  __shared__ double hs[kMaxRestart + 1];
-  __shared__ double red[(kMaxRestart + 1) * kSumSlices];
+  __shared__ double hs[kRegRestart + 1];
+  __shared__ double red[kPartLd * kSumSlices];
   __shared__ double s_hn;
   const int jn = k.st->jc;  // = j + 1; st->j itself is advanced by the Givens CTA
   const int nv = jn;
   const int nb = gridDim.x - 1;
   const bool rows_cta = blockIdx.x < nb;
   // Givens CTA: its inputs other than h2 are loaded before the reduction
-  __shared__ double g_col[kMaxRestart + 2], g_cs[kMaxRestart + 1], g_sn[kMaxRestart + 1];
+  __shared__ double g_col[kRegRestart + 2], g_cs[kRegRestart + 1], g_sn[kRegRestart + 1];
   double h1t = 0.0, gj = 0.0;
   if (!rows_cta) {
     const int t = threadIdx.x;
@@ -886,10 +752,10 @@ __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
   // first row prefetched before the reduction (see k_update_dots_norm)
   const int r0 = blockIdx.x * blockDim.x + threadIdx.x;
   const bool has0 = rows_cta && r0 < k.n;
-  double w0 = 0.0, v0[PF ? kMaxRestart : 1];
+  double w0 = 0.0, v0[PF ? kRegRestart : 1];
   if constexpr (PF) {
 #pragma unroll
-    for (int v = 0; v < kMaxRestart; ++v) v0[v] = (has0 && v < nv) ? k.V[(size_t)v * k.n + r0] : 0.0;
+    for (int v = 0; v < kRegRestart; ++v) v0[v] = (has0 && v < nv) ? k.V[(size_t)v * k.n + r0] : 0.0;
     if (has0) w0 = k.w[r0];
   }
   sum_partials<kArnThreads>(k.partial2, k.parts_b, nv + 1, hs, red);
@@ -916,7 +782,7 @@ __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
   if (PF && has0) {
     double wr = w0;
 #pragma unroll
-    for (int v = 0; v < kMaxRestart; ++v)
+    for (int v = 0; v < kRegRestart; ++v)
       if (v < nv) wr = fma(-hs[v], v0[PF ? v : 0], wr);
     if (!lucky) {
       const double vv = wr / hn;
@@ -928,7 +794,7 @@ __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
     for (int r = r0 + nb * blockDim.x; r < k.n; r += nb * blockDim.x) {
       double wr = k.w[r];
   #pragma unroll
-      for (int v = 0; v < kMaxRestart; ++v)
+      for (int v = 0; v < kRegRestart; ++v)
         if (v < nv) wr = fma(-hs[v], k.V[(size_t)v * k.n + r], wr);
       if (!lucky) {
         const double vv = wr / hn;
@@ -946,13 +812,13 @@ __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
     double* __restrict__ UB = k.ubuf;
     const size_t n = (size_t)k.n;
     for (int r = PF ? r0 + nb * blockDim.x : (rows_cta ? r0 : k.n); r < k.n; r += nb * blockDim.x) {
-      double vr[kMaxRestart];
+      double vr[kRegRestart];
 #pragma unroll
-      for (int v = 0; v < kMaxRestart; ++v) vr[v] = v < nv ? __ldg(V + (size_t)v * n + r) : 0.0;
+      for (int v = 0; v < kRegRestart; ++v) vr[v] = v < nv ? __ldg(V + (size_t)v * n + r) : 0.0;
       double wr = W[r];
       const double sc = S[r];
 #pragma unroll
-      for (int v = 0; v < kMaxRestart; ++v)
+      for (int v = 0; v < kRegRestart; ++v)
         if (v < nv) wr = fma(-hs[v], vr[v], wr);
       if (!lucky) {
         const double vv = wr / hn;

@@ -74,6 +74,7 @@ def lib():
         sig = {
             "fsigpu_last_error": ([], C.c_char_p),
             "fsigpu_last_singular_block": ([], ip),
+            "fsigpu_last_singular_level": ([], ip),
             "fsigpu_init": ([ip], ip),
             "fsigpu_version": ([], ip),
             "fsigpu_launch_count": ([], ll),
@@ -294,6 +295,11 @@ class GmgPreconditioner:
         rc = lib().fsigpu_gmg_create(len(levels), C.addressof(self._descs), cfg.omega, cfg.pre, cfg.post,
                                      cfg.cycle.encode()[:1], C.byref(h))
         if rc == FSIGPU_ERR_SINGULAR:
+            # the failing block's reference label (precond.cpp:182,224,265)
+            b, lvl = lib().fsigpu_last_singular_block(), lib().fsigpu_last_singular_level()
+            labels = levels[lvl].labels if 0 <= lvl < len(levels) else None
+            if labels is not None and 0 <= b < len(labels):
+                raise SingularBlockError(labels[b])
             msg = lib().fsigpu_last_error().decode()
             raise SingularBlockError(msg.replace("singular block: ", ""))
         _check(rc)
@@ -379,8 +385,8 @@ class GmresSolver:
     """Device-resident FGMRES on diag(frame_scale) A_top, M = GMG(r / frame_scale)."""
 
     def __init__(self, gmg: GmgPreconditioner, frame_scale, restart: int = 30, graphs: bool = True):
-        if restart < 1 or restart > 32:
-            raise ValueError("gmres: restart must be in [1, 32]")
+        if restart < 1 or restart > 128:
+            raise ValueError("gmres: restart must be in [1, 128]")
         self.gmg = gmg
         self.restart = restart
         self._scale = _f64(frame_scale)

@@ -70,6 +70,7 @@ class Level:
     lumped: Optional[np.ndarray] = None
     as1: Optional[BlockSets] = None
     as2: Optional[BlockSets] = None
+    labels: Optional[List[str]] = None  # reference IndexSet labels, AS1 then AS2 blocks
 
 
 @dataclass
@@ -102,6 +103,9 @@ def load_case(path: str, name: str = "") -> Problem:
             lv.lumped = a[p + "/lumped"].astype(np.float64)
             lv.as1 = BlockSets(a[p + "/as1/ptr"].astype(np.int32), a[p + "/as1/idx"].astype(np.int32))
             lv.as2 = BlockSets(a[p + "/as2/ptr"].astype(np.int32), a[p + "/as2/idx"].astype(np.int32))
+            if p + "/as1/labels" in a:
+                lv.labels = [t for k in ("as1", "as2")
+                             for t in bytes(a[f"{p}/{k}/labels"]).decode().split("\n")[:-1]]
         levels.append(lv)
     golden = {k: v for k, v in a.items() if k.startswith(("golden/", "gmres_", "setup/"))}
     return Problem(name=name or path, levels=levels, frame_scale=a["frame_scale"].astype(np.float64),

@@ -46,6 +46,32 @@ def cfg0():
     return load_case(path, "cfg0")
 
 
+DATA_CFG2 = os.path.join(ROOT, "data_cfg2")
+
+
+def ensure_cfg2(case: str) -> str:
+    """Path of the config-2 solve inputs (bulge case),
+    exported on demand by the prebuilt reference exporter
+    (oracle/_ref/fsi_ref_harness, the unmodified reference library): the
+    archives (0.4 GB at 4 levels, 1.6 GB at 5) are too large for the
+    repository, so the GPU box regenerates them (~30 s / ~2 min, one host
+    thread per level and FS instance). The export is deterministic: the
+    committed goldens (tests/golden/<case>_gmres.fsix) carry checksums of
+    the system they were taken on."""
+    import subprocess
+    path = os.path.join(DATA_CFG2, case + ".fsix")
+    if os.path.exists(path):
+        return path
+    exe = os.path.join(ROOT, "oracle", "_ref", "fsi_ref_harness")
+    if not os.path.exists(exe):
+        pytest.fail(f"{exe} missing: cannot export {case} (build it with `make -C oracle ref`)")
+    os.makedirs(DATA_CFG2, exist_ok=True)
+    tmp = path + ".part"
+    subprocess.run([exe, "export", case, tmp, "--no-mult", "--no-gmres"], check=True, stdout=subprocess.DEVNULL)
+    os.replace(tmp, path)
+    return path
+
+
 @pytest.fixture(scope="session")
 def golden_blocks():
     from paper_1909_13201_b200 import fsix

@@ -4,7 +4,10 @@
 // own headers (proj/include/fsi) and the fsigpu C ABI. It is what a
 // maintainer adds to the reference tree to replace the solve block of
 // FsiSolver::newton_step (proj/src/driver.cpp:257-272). tests/test_abi.py
-// syntax-checks it here and, with a GPU, links it against libfsigpu.so.
+// syntax-checks it here; oracle/Makefile `adapter` links it with the
+// reference library and libfsigpu.so into oracle/_ref/fsi_adapter_check
+// (the harness's `gpu-adapter` command), which tests/test_gpu_parity.py
+// runs on the GPU against the reference's own gmres.
 #include <map>
 #include <stdexcept>
 #include <string>
@@ -20,11 +23,27 @@
 namespace fsi {
 namespace {
 
-void check(int rc) {
+// Status -> the reference's exceptions. A singular block is named by the
+// reference IndexSet label of the failing block (labels[level][block],
+// e.g. "fs-fluid-up-12", precond.cpp:182,224,265); non-block failures
+// ("gmg-coarse", "fs lumped mass row <i>") come with the message. Device
+// faults are NOT SolverError: the driver catches SolverError as a
+// non-converged Newton step and retries with dt halved (driver.cpp:369),
+// which must not happen on a dead CUDA context.
+void check(int rc, const std::map<int, std::vector<std::string>>* labels = nullptr) {
   if (rc == FSIGPU_OK) return;
-  if (rc == FSIGPU_ERR_SINGULAR) throw SingularBlockError(fsigpu_last_error());
-  if (rc == FSIGPU_ERR_INVALID) throw std::invalid_argument(fsigpu_last_error());
-  throw SolverError(fsigpu_last_error());
+  const std::string msg = fsigpu_last_error();
+  if (rc == FSIGPU_ERR_SINGULAR) {
+    const int b = fsigpu_last_singular_block(), l = fsigpu_last_singular_level();
+    if (labels && b >= 0) {
+      auto it = labels->find(l);
+      if (it != labels->end() && b < static_cast<int>(it->second.size())) throw SingularBlockError(it->second[b]);
+    }
+    const std::string prefix = "singular block: ";
+    throw SingularBlockError(msg.compare(0, prefix.size(), prefix) == 0 ? msg.substr(prefix.size()) : msg);
+  }
+  if (rc == FSIGPU_ERR_INVALID) throw std::invalid_argument(msg);
+  throw std::runtime_error("fsigpu device failure: " + msg);
 }
 
 void flatten(const std::vector<const IndexSet*>& sets, std::vector<int>& ptr, std::vector<int>& idx) {
@@ -70,6 +89,8 @@ class GpuGmg final : public LinearOperator {
       std::vector<const IndexSet*> s1, s2;
       for (int b = 0; b < f.as1().n_blocks(); ++b) s1.push_back(&f.as1().block_dofs(b));
       for (int b = 0; b < f.n_fluid_blocks(); ++b) s2.push_back(&f.fluid_block_dofs(b));
+      for (const IndexSet* is : s1) labels_[static_cast<int>(l)].push_back(is->label);
+      for (const IndexSet* is : s2) labels_[static_cast<int>(l)].push_back(is->label);
       flatten(s1, as1_ptr_[l], as1_idx_[l]);
       flatten(s2, as2_ptr_[l], as2_idx_[l]);
       x.as1_n = static_cast<int>(as1_ptr_[l].size()) - 1;
@@ -79,7 +100,8 @@ class GpuGmg final : public LinearOperator {
       x.as2_ptr = as2_ptr_[l].data();
       x.as2_idx = as2_idx_[l].data();
     }
-    check(fsigpu_gmg_create(static_cast<int>(d.size()), d.data(), cfg.omega, cfg.pre, cfg.post, cfg.cycle, &h_));
+    check(fsigpu_gmg_create(static_cast<int>(d.size()), d.data(), cfg.omega, cfg.pre, cfg.post, cfg.cycle, &h_),
+          &labels_);
   }
   ~GpuGmg() override { fsigpu_gmg_destroy(h_); }
   int size() const override { return fsigpu_gmg_size(h_); }
@@ -89,6 +111,7 @@ class GpuGmg final : public LinearOperator {
  private:
   fsigpu_gmg h_ = nullptr;
   std::map<size_t, std::vector<int>> as1_ptr_, as1_idx_, as2_ptr_, as2_idx_;
+  std::map<int, std::vector<std::string>> labels_;  // per level: AS1 then AS2 block labels
 };
 
 // Drop-in for gmres(aop, mop, b, cfg) at driver.cpp:262-272.
