@@ -30,10 +30,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 METRIC = "FGMRES-GMG(FS-AS) solve time & V-cycles/s at 1 B200; AS/SpMV HBM GB/s vs roofline"
 DATA = os.path.join(ROOT, "data", "cfg0.fsix")
+# config 2 (0.4 / 1.6 GB archives) is exported on the box by the prebuilt
+# reference exporter when absent (tests/conftest.py:ensure_cfg2)
 DATA_CFG2 = os.path.join(ROOT, "data_cfg2", "cfg2l4.fsix")
-# full config 2 (1.59 GB) exceeds the gpurun snapshot: generate it on the box
-# first with the prebuilt reference exporter (a separate step, not bench.py):
-#   oracle/_ref/fsi_ref_harness export cfg2 data_cfg2/cfg2.fsix --no-mult --max-iters 30 --block-stride 997
 DATA_CFG2FULL = os.path.join(ROOT, "data_cfg2", "cfg2.fsix")
 WORKLOAD_CFG2FULL = ("config2: 2D aneurysm-like FSI (bulge case, 1 coarse wall row), Q2/P1disc 16->256 (5 GMG levels), "
                      "1,249,284 dofs, 81.9M nnz, FGMRES(30), AS1 epb=4 / AS2 epb=16, V(1,1) additive FS omega=0.7")
@@ -42,6 +41,22 @@ WORKLOAD_CFG2 = ("config2 at 4 levels (fits the 512 MiB gpurun snapshot): bulge 
 HARNESS = os.path.join(ROOT, "oracle", "_ref", "fsi_ref_harness")
 WORKLOAD = ("config0: 2D FSI first-Newton Jacobian, unit square Q2/P1disc 8->16->32 (3 GMG levels), "
             "19,972 dofs, FGMRES(30) rtol 1e-10, V(1,1) additive FS smoother omega=0.7")
+
+
+def bench_config(args):
+    """The workload description both arms print (same dict, so the driver
+    sees the same config); run-specific numbers go outside it."""
+    wl = {"cfg0": WORKLOAD, "cfg2": WORKLOAD_CFG2}.get(args.config, WORKLOAD_CFG2FULL)
+    return {"workload": wl, "smoother": args.smoother, "level_smoother": args.level_smoother,
+            "restart": 30, "rel_tol": 1e-10,
+            "parallelism": "replicas" if args.gpus > 1 else "single",
+            "l2": "flushed (256 MB write) between timed solves"}
+
+
+def ensure_cfg2(case):
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from conftest import ensure_cfg2 as _e
+    return _e(case)
 
 
 def peaks():
@@ -163,6 +178,15 @@ def run_reference(args, ws, rank):
     out = subprocess.run(cmd, capture_output=True, text=True, check=True).stdout
     wall = time.time() - t0
     d = json.loads(out.strip().splitlines()[-1])
+    # time to solution of the same system: the additive variant our arm
+    # runs, and the as-shipped multiplicative FS smoother (precond.cpp:271-303)
+    tts = {}
+    for mode in ("add", "mult"):
+        o = subprocess.run([HARNESS, "solve", "cfg0", "--mode", mode, "--reps", "1"], capture_output=True,
+                           text=True, check=True).stdout
+        s0 = json.loads(o.strip().splitlines()[-1])["solves"][0]
+        tts[mode] = {"iterations": s0["iterations"], "v_cycles": s0["m_applies"], "solve_s": s0["seconds"],
+                     "relres": s0["relres"], "converged": bool(s0["converged"])}
     solves = d["solves"][args.warmup:]
     secs = sum(s["seconds"] for s in solves)
     vcyc = sum(s["m_applies"] for s in solves)
@@ -174,7 +198,8 @@ def run_reference(args, ws, rank):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * secs / len(solves), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference-assembled rest-state Jacobian, seeded RHS)",
-        "config": {"workload": WORKLOAD, "parallelism": "replicas", "setup_s": d.get("setup_s")},
+        "config": bench_config(args), "setup_s": d.get("setup_s"),
+        "time_to_solution": tts,
         "cpu_baseline": {"value": value, "unit": "V-cycles/s", "cores": 1, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": "V-cycles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -198,7 +223,23 @@ def cpu_baseline_port(P):
             "solve_s": secs, "iterations": r["iterations"]}
 
 
-def as_microbench(fsigpu, torch, hbm_peak, n54=262144, n59=131072, solves=100):
+def config1_cpu_baseline(threads, n54=16384, n59=8192, nsolve=10):
+    """The reference's DenseFactorization ctor + solve (oracle/_ref
+    fsi_ref_harness time-blocks) on a 1/16 sample of config 1, on `threads`
+    host threads (the per-block loop split across std::threads; the
+    factorizations are immutable)."""
+    if not os.path.exists(HARNESS):
+        return None
+    o = subprocess.run([HARNESS, "time-blocks", str(n54), str(n59), str(nsolve), "--threads", str(threads)],
+                       capture_output=True, text=True, check=True).stdout
+    d = json.loads(o.strip().splitlines()[-1])
+    nb = n54 + n59
+    return {"cores": threads, "kind": "reference", "blocks": nb,
+            "lu_blocks_per_s": nb / d["lu_s"], "solve_blocks_per_s": nb / d["solve_s_per_pass"],
+            "sample": f"{n54} x m=54 + {n59} x m=59 blocks (1/16 of config 1), one LU each and {nsolve} solve passes"}
+
+
+def as_microbench(fsigpu, torch, hbm_peak, n54=262144, n59=131072, solves=100, cpu=True):
     """Config 1: 262,144 x m=54 + 131,072 x m=59 dense fp64 blocks; one batched
     LU, then `solves` batched solves (bytes: SURVEY §8d)."""
     t0 = time.time()
@@ -247,7 +288,14 @@ def as_microbench(fsigpu, torch, hbm_peak, n54=262144, n59=131072, solves=100):
         xo = O.dense_solve(lu, piv, rh[offs[b]:offs[b + 1]])
         worst = max(worst, float(np.linalg.norm(xh[offs[b]:offs[b + 1]] - xo) / np.linalg.norm(xo)))
     del sizes
+    cpu_base = None
+    if cpu:
+        ncores = os.cpu_count() or 1
+        cpu_base = {"1_thread": config1_cpu_baseline(1), f"{ncores}_threads": config1_cpu_baseline(ncores)}
     return {
+        "cpu_baseline": cpu_base,
+        "gpu_lu_blocks_per_s": (n54 + n59) / (lu_ms / 1000.0),
+        "gpu_solve_blocks_per_s": (n54 + n59) / (solve_ms / 1000.0),
         "blocks": n54 + n59, "factor_GB": fbytes / 1e9, "gen_s": gen_s,
         "lu_ms": lu_ms, "lu_GBps": lu_bytes / lu_ms / 1e6, "lu_TFLOPs": lu_flops / lu_ms / 1e9,
         "solve_ms": solve_ms, "solve_GBps": solve_bytes / solve_ms / 1e6,
@@ -353,14 +401,7 @@ def run_ours(args, ws, rank, local):
     # the library stream, L2 flushed before every launch (HBM-bound view);
     # the dominant kernel is the one with the largest share of a V-cycle
     top = len(P.levels) - 1
-    kt = {}
-    kern = [(nm, lvl, pc) for lvl in range(top, 0, -1)
-            for nm, pc in [("fs_smoother", 2), ("residual", 1), ("prolong_resid", 1), ("restrict", 1)]]
-    for name, lvl, per_cycle in kern + [("coarse", 0, 1)]:
-        ms_c, by = G.time_kernel(name, lvl, reps=20, cold=True)
-        ms_w, _ = G.time_kernel(name, lvl, reps=50, cold=False)
-        kt[f"{name}@L{lvl}"] = {"ms_cold": ms_c, "ms_warm": ms_w, "bytes": by, "per_vcycle": per_cycle,
-                                "GBps_cold": by / ms_c / 1e6, "GBps_warm": by / ms_w / 1e6}
+    kt = kernel_table(G, top)
     # ---- in-solve view: one instrumented solve right after the timed
     # region (same inputs, same L2 flush before it), graphs off, CUDA events
     # around every launch on the library stream; per kernel class the
@@ -414,12 +455,9 @@ def run_ours(args, ws, rank, local):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference-assembled rest-state FSI Jacobian, seeded uniform RHS; fixtures from oracle/_ref)",
-        "config": {"workload": {"cfg0": WORKLOAD, "cfg2": WORKLOAD_CFG2}.get(args.config, WORKLOAD_CFG2FULL),
-                   "n_dofs": n,
-                   "max_iters": max_iters, "smoother": args.smoother,
-                   "level_smoother": args.level_smoother, "nnz_fine": P.levels[-1].A.nnz,
-                   "parallelism": "replicas" if ws > 1 else "single", "l2": "flushed (256 MB write) between timed solves",
-                   "restart": 30, "rel_tol": 1e-10, "cuda_graphs": "conditional WHILE per restart cycle"},
+        "config": bench_config(args),
+        "run": {"n_dofs": n, "nnz_fine": P.levels[-1].A.nnz, "max_iters": max_iters,
+                "cuda_graphs": "conditional WHILE per restart cycle"},
         "solve_ms": ms, "iterations": int(statistics.median(its)), "v_cycles_per_solve": vcyc_per_step,
         "final_relres": relres, "setup_s": setup_s, "wall_s_timed": t_wall,
         "gpu_launches": launches,
@@ -427,7 +465,9 @@ def run_ours(args, ws, rank, local):
                 "d2h_bytes_per_step": 8 * n + 8 * (r2.iterations + 1), "ms_per_step": e2e_step},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved_main, "peak": hbm_peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved_main / hbm_peak,
-                     "traffic": traffic, "algorithmic_bytes_per_launch": per_launch_bytes,
+                     "traffic": traffic,
+                     "traffic_source": "stored ncu --set full capture (profiles/ncu_summary.json), not this run",
+                     "algorithmic_bytes_per_launch": per_launch_bytes,
                      "avg_launch_us": per_launch_bytes / achieved_main / 1000.0,
                      "share_of_vcycle_kernel_time": share,
                      "achieved_cold": achieved, "frac_cold": achieved / hbm_peak,
@@ -452,16 +492,116 @@ def run_ours(args, ws, rank, local):
     # whole V-cycle against the HBM floor: algorithmic bytes of every V-cycle
     # kernel (all levels) / measured peak, against the measured time per
     # FGMRES step (one V-cycle + one Arnoldi step)
-    vb = sum(v["bytes"] * v["per_vcycle"] for v in kt.values())
-    out["vcycle_roofline"] = {"bytes": vb, "floor_ms": vb / hbm_peak / 1e6,
-                              "kernels_ms_cold": sum(v["ms_cold"] * v["per_vcycle"] for v in kt.values()),
-                              "step_ms": ms / max(statistics.median(its), 1),
-                              "frac_of_step": vb / hbm_peak / 1e6 / (ms / max(statistics.median(its), 1))}
+    out["vcycle_roofline"] = step_roofline(kt, P, hbm_peak, ms / max(statistics.median(its), 1))
     out["clocks"] = clk.summary()
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and args.config == "cfg0":
         out["cpu_baseline"] = cpu_baseline_port(P)
     if rank == 0 and not args.no_microbench:
-        out["as_microbench"] = as_microbench(fsigpu, torch, hbm_peak)
+        out["as_microbench"] = as_microbench(fsigpu, torch, hbm_peak, cpu=not args.no_cpu_baseline)
+    if rank == 0 and args.config == "cfg0" and not args.no_config2:
+        del S, S_prof, G
+        torch.cuda.empty_cache()
+        out["config2"] = config2_bench(fsigpu, torch, hbm_peak)
+    return out
+
+
+def arnoldi_bytes(n, nnz, mr=30):
+    """Algorithmic bytes of one Arnoldi step, averaged over the
+    j = 0..mr-1 steps of a restart cycle: (A) the outer SpMV (12 nnz + 4(n+1)
+    + gather of z) with the scale, w and Z[j] streams and V_{0..j}^T w; (B)
+    V_{0..j} and w read, w written; (C) V_{0..j}, w and the scale read,
+    v_{j+1} and u written."""
+    tot = 0.0
+    for j in range(mr):
+        nv = j + 1
+        a = 12.0 * nnz + 4.0 * (n + 1) + 8.0 * n + 8.0 * n + 8.0 * n + 8.0 * n + 8.0 * n * nv
+        b = 8.0 * n * nv + 16.0 * n
+        c = 8.0 * n * nv + 16.0 * n + 16.0 * n
+        tot += a + b + c
+    return tot / mr
+
+
+def step_roofline(kt, P, hbm_peak, step_ms):
+    """One FGMRES step (one V-cycle + one Arnoldi step) against the HBM
+    floor: algorithmic bytes of every V-cycle kernel (all levels) plus the
+    Arnoldi step's, over the measured peak, against the measured time."""
+    vb = sum(v["bytes"] * v["per_vcycle"] for v in kt.values())
+    ab = arnoldi_bytes(P.n, P.levels[-1].A.nnz)
+    return {"vcycle_bytes": vb, "arnoldi_bytes": ab, "bytes": vb + ab, "floor_ms": (vb + ab) / hbm_peak / 1e6,
+            "kernels_ms_cold": sum(v["ms_cold"] * v["per_vcycle"] for v in kt.values()),
+            "step_ms": step_ms, "frac_of_step": (vb + ab) / hbm_peak / 1e6 / step_ms}
+
+
+def kernel_table(G, top, reps_cold=20, reps_warm=50):
+    kt = {}
+    kern = [(nm, lvl, pc) for lvl in range(top, 0, -1)
+            for nm, pc in [("fs_smoother", 2), ("residual", 1), ("prolong_resid", 1), ("restrict", 1)]]
+    for name, lvl, per_cycle in kern + [("coarse", 0, 1)]:
+        ms_c, by = G.time_kernel(name, lvl, reps=reps_cold, cold=True)
+        ms_w, _ = G.time_kernel(name, lvl, reps=reps_warm, cold=False)
+        kt[f"{name}@L{lvl}"] = {"ms_cold": ms_c, "ms_warm": ms_w, "bytes": by, "per_vcycle": per_cycle,
+                                "GBps_cold": by / ms_c / 1e6, "GBps_warm": by / ms_w / 1e6}
+    return kt
+
+
+def config2_bench(fsigpu, torch, hbm_peak, steps=3, max_iters=60):
+    """Config 2 (the HBM-roofline config: bulge case, 5 levels,
+    1,249,284 dofs, 81.9 M fine nnz): FGMRES(30) for a fixed budget of
+    `max_iters` Arnoldi steps per timed solve (the additive smoother needs
+    hundreds of iterations there, the reference's relres after 300 is 0.95),
+    L2 flushed between solves, plus the per-step HBM floor, the dominant
+    kernel's cold roofline and the history against the reference's
+    (tests/golden/cfg2_gmres.fsix)."""
+    from paper_1909_13201_b200 import fsix
+    from paper_1909_13201_b200.problem import load_case
+    t0 = time.time()
+    path = ensure_cfg2("cfg2")
+    export_s = time.time() - t0
+    P = load_case(path, "cfg2")
+    t0 = time.time()
+    G = fsigpu.GmgPreconditioner(P.levels)
+    S = fsigpu.GmresSolver(G, P.frame_scale, restart=30)
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+    cfg = fsigpu.KrylovConfig(restart=30, max_iters=max_iters, rel_tol=1e-10, abs_tol=1e-300)
+    lib_stream = torch.cuda.ExternalStream(G.stream())
+    b = torch.from_numpy(P.b).cuda()
+    x = torch.zeros(P.n, dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    S.solve_dev(b.data_ptr(), x.data_ptr(), cfg)  # warm-up (graph capture)
+    per, vc = [], 0
+    for _ in range(steps):
+        flush.fill_(1.0)
+        x.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(lib_stream)
+        res = S.solve_dev(b.data_ptr(), x.data_ptr(), cfg)
+        e1.record(lib_stream)
+        e1.synchronize()
+        per.append(e0.elapsed_time(e1))
+        vc += res.m_applies
+    ms = sum(per) / len(per)
+    top = len(P.levels) - 1
+    kt = kernel_table(G, top, reps_cold=5, reps_warm=10)
+    dom = max(kt, key=lambda k: kt[k]["ms_cold"] * kt[k]["per_vcycle"])
+    hist = S.solve(P.b, cfg).history
+    gold = fsix.load(os.path.join(ROOT, "tests", "golden", "cfg2_gmres.fsix"))["gmres_add/history"]
+    k = min(len(hist), len(gold))
+    out = {"workload": WORKLOAD_CFG2FULL, "value": vc / len(per) / (ms / 1000.0), "unit": "V-cycles/s",
+           "ms_per_solve": ms, "arnoldi_steps_per_solve": max_iters, "steps": steps,
+           "ms_per_fgmres_step": ms / max_iters,
+           "step_roofline": step_roofline(kt, P, hbm_peak, ms / max_iters),
+           "roofline": {"bound": "hbm", "kernel": dom, "achieved": kt[dom]["GBps_cold"], "peak": hbm_peak,
+                        "unit": "GB/s", "frac": kt[dom]["GBps_cold"] / hbm_peak,
+                        "algorithmic_bytes_per_launch": kt[dom]["bytes"],
+                        "avg_launch_us": 1000.0 * kt[dom]["ms_cold"],
+                        "timing": "kernel alone, CUDA events per launch after a 256 MB L2 flush"},
+           "kernel_roofline": kt,
+           "history_vs_reference_max_rel": float(np.max(np.abs(hist[:k] - gold[:k]) / gold[:k])),
+           "export_s": export_s, "setup_s": setup_s}
+    del S, G, P, b, x, flush
+    torch.cuda.empty_cache()
     return out
 
 
@@ -484,6 +624,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-microbench", action="store_true")
+    ap.add_argument("--no-config2", action="store_true", help="skip the config-2 sub-object (exports 1.6 GB)")
     ap.add_argument("--config", choices=["cfg0", "cfg2", "cfg2full"], default="cfg0")
     ap.add_argument("--smoother", choices=["fs", "as"], default="fs")
     # sweep around the FS/AS smoother: the reference's damped Richardson

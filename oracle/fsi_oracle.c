@@ -189,11 +189,147 @@ static void sweep_apply_additive(const orc_sweep* s, const double* r, double* z)
     if (s->cover[i] > 1.0) z[i] /= s->cover[i];
 }
 
+/* CSC of the sub-matrix A[base:base+dim, base:base+dim] of a frame CSR
+ * (SparseCsc::from_csr of the group matrix, precond.cpp:36,139) */
+typedef struct {
+  int dim;
+  int* ptr;
+  int* row;
+  double* val;
+} orc_csc;
+
+static void csc_build(orc_csc* c, int base, int dim, const int* a_ptr, const int* a_idx, const double* a_val) {
+  c->dim = dim;
+  c->ptr = (int*)calloc((size_t)dim + 1, sizeof(int));
+  for (int i = 0; i < dim; ++i)
+    for (int k = a_ptr[base + i]; k < a_ptr[base + i + 1]; ++k) {
+      const int j = a_idx[k] - base;
+      if (j >= 0 && j < dim) c->ptr[j + 1]++;
+    }
+  for (int j = 0; j < dim; ++j) c->ptr[j + 1] += c->ptr[j];
+  const int tot = c->ptr[dim];
+  c->row = (int*)malloc(sizeof(int) * (size_t)(tot > 0 ? tot : 1));
+  c->val = (double*)malloc(sizeof(double) * (size_t)(tot > 0 ? tot : 1));
+  int* next = (int*)malloc(sizeof(int) * (size_t)(dim > 0 ? dim : 1));
+  for (int j = 0; j < dim; ++j) next[j] = c->ptr[j];
+  for (int i = 0; i < dim; ++i) /* rows in order: each column's rows ascend */
+    for (int k = a_ptr[base + i]; k < a_ptr[base + i + 1]; ++k) {
+      const int j = a_idx[k] - base;
+      if (j >= 0 && j < dim) {
+        c->row[next[j]] = i;
+        c->val[next[j]++] = a_val[k];
+      }
+    }
+  free(next);
+}
+
+static void csc_free(orc_csc* c) {
+  free(c->ptr);
+  free(c->row);
+  free(c->val);
+}
+
+/* SchwarzSweep::apply, multiplicative branch (precond.cpp:59-77): every
+ * block sees the residual updated by all previous block corrections, the
+ * update walking the corrected columns of the CSC. The blocks are visited
+ * in `order` (NULL: their index order, which is the reference's). res is
+ * updated in place, z accumulated. */
+static void sweep_apply_mult(const orc_sweep* s, const orc_csc* a, const int* order, double* res, double* z) {
+  double rhs[1024], delta[1024];
+  for (int q = 0; q < s->n_blocks; ++q) {
+    const int b = order ? order[q] : q;
+    const int m = s->ptr[b + 1] - s->ptr[b];
+    const int* d = s->idx + s->ptr[b];
+    for (int i = 0; i < m; ++i) rhs[i] = res[d[i]];
+    orc_dense_solve(m, s->lu + s->lu_off[b], s->piv + s->ptr[b], rhs, delta);
+    for (int i = 0; i < m; ++i) {
+      const int c = d[i];
+      z[c] += delta[i];
+      const double dv = delta[i];
+      if (dv == 0.0) continue;
+      for (int k = a->ptr[c]; k < a->ptr[c + 1]; ++k) res[a->row[k]] -= a->val[k] * dv;
+    }
+  }
+}
+
+/* Multicolour ordering of the blocks of one sweep (the order the GPU's
+ * multiplicative smoother runs them in, one kernel per colour). Blocks b
+ * and b' conflict when they share a dof or the sweep matrix stores an entry
+ * coupling them in either direction (A[i,j] or A[j,i], i in b, j in b');
+ * greedy in block order: colour(b) = the smallest colour no conflicting
+ * earlier block has. Same-colour blocks then neither overlap nor see each
+ * other's corrections, so running them in parallel equals running them in
+ * sequence. Returns the colour count; order[] = blocks sorted by (colour,
+ * index). */
+static int colour_blocks(const orc_sweep* s, const orc_csc* a, int* order) {
+  const int nb = s->n_blocks, dim = s->dim;
+  /* dof -> blocks holding it */
+  int* dptr = (int*)calloc((size_t)dim + 1, sizeof(int));
+  for (int k = 0; k < s->ptr[nb]; ++k) dptr[s->idx[k] + 1]++;
+  for (int i = 0; i < dim; ++i) dptr[i + 1] += dptr[i];
+  int* dblk = (int*)malloc(sizeof(int) * (size_t)(s->ptr[nb] > 0 ? s->ptr[nb] : 1));
+  int* nx = (int*)malloc(sizeof(int) * (size_t)(dim > 0 ? dim : 1));
+  for (int i = 0; i < dim; ++i) nx[i] = dptr[i];
+  for (int b = 0; b < nb; ++b)
+    for (int k = s->ptr[b]; k < s->ptr[b + 1]; ++k) dblk[nx[s->idx[k]]++] = b;
+  /* row pattern of the sweep matrix = the transpose of its CSC */
+  int* rptr = (int*)calloc((size_t)dim + 1, sizeof(int));
+  for (int k = 0; k < a->ptr[dim]; ++k) rptr[a->row[k] + 1]++;
+  for (int i = 0; i < dim; ++i) rptr[i + 1] += rptr[i];
+  int* rcol = (int*)malloc(sizeof(int) * (size_t)(a->ptr[dim] > 0 ? a->ptr[dim] : 1));
+  for (int i = 0; i < dim; ++i) nx[i] = rptr[i];
+  for (int j = 0; j < dim; ++j)
+    for (int k = a->ptr[j]; k < a->ptr[j + 1]; ++k) rcol[nx[a->row[k]]++] = j;
+  int* colour = (int*)malloc(sizeof(int) * (size_t)(nb > 0 ? nb : 1));
+  int* seen = (int*)malloc(sizeof(int) * (size_t)(nb + 1));  /* colour -> last block marking it */
+  for (int c = 0; c <= nb; ++c) seen[c] = -1;
+  int ncol = 0;
+#define ORC_MARK(j)                                                             \
+  for (int q = dptr[j]; q < dptr[(j) + 1]; ++q) {                               \
+    const int o = dblk[q];                                                      \
+    if (o < b) seen[colour[o]] = b;                                             \
+  }
+  for (int b = 0; b < nb; ++b) {
+    for (int k = s->ptr[b]; k < s->ptr[b + 1]; ++k) {
+      const int i = s->idx[k];
+      ORC_MARK(i)
+      for (int e = rptr[i]; e < rptr[i + 1]; ++e) {
+        const int j = rcol[e];
+        ORC_MARK(j)
+      }
+      for (int e = a->ptr[i]; e < a->ptr[i + 1]; ++e) {
+        const int j = a->row[e];
+        ORC_MARK(j)
+      }
+    }
+    int c = 0;
+    while (seen[c] == b) ++c;
+    colour[b] = c;
+    if (c + 1 > ncol) ncol = c + 1;
+  }
+#undef ORC_MARK
+  int q = 0;
+  for (int c = 0; c < ncol; ++c)
+    for (int b = 0; b < nb; ++b)
+      if (colour[b] == c) order[q++] = b;
+  free(dptr);
+  free(dblk);
+  free(nx);
+  free(rptr);
+  free(rcol);
+  free(colour);
+  free(seen);
+  return ncol;
+}
+
 /* ------------------------------------------------------------ GMG */
 
 typedef struct {
   orc_level_desc d;
   orc_sweep as1, as2;
+  orc_csc csc1, csc2;      /* A_g1, A_g2 (multiplicative sweeps) */
+  int *order1, *order2;    /* multicolour block orders */
+  int ncol1, ncol2;
   /* CSC of group 2 restricted to the u^s columns [0, n_us): the Jacobi
    * residual update walks these columns (precond.cpp:281-287) */
   int* us_ptr;
@@ -208,6 +344,9 @@ struct orc_gmg {
   double omega;
   int pre, post;
   int smoother; /* 0 richardson (precond.cpp:305-317), 1 GMRES(1) */
+  int fs_mode;  /* 0 additive, 1 multiplicative in multicolour
+                   order (the GPU's), 2 multiplicative in the reference's
+                   block order (FsPreconditioner::apply as shipped) */
   /* coarse: equilibrated dense LU */
   int n0;
   double* c_lu;
@@ -245,7 +384,35 @@ static void build_us_csc(orc_level* l) {
 
 /* Additive FS apply: z1 = AS1_add(r1);
  * z2[:n_us] = r2/l; res2 = r2 - A_g2[:, :n_us] z2; z2 += AS2_add(res2) */
+/* FsPreconditioner::apply (precond.cpp:271-303), the shipped multiplicative
+ * smoother: z1 = AS1_mult(r1); z2[:n_us] = r2/l with the residual update of
+ * those columns; AS2 fluid blocks multiplicative on the updated residual.
+ * coloured: blocks in multicolour order instead of index order. */
+static void fs_apply_mult(const orc_gmg* g, int level, const double* r, double* z, int coloured) {
+  const orc_level* l = &g->lv[level];
+  const int n = l->d.n, g1 = l->d.g1, g2 = n - g1, n_us = l->d.n_us;
+  memset(z, 0, sizeof(double) * (size_t)n);
+  double* res = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  memcpy(res, r, sizeof(double) * (size_t)n);
+  sweep_apply_mult(&l->as1, &l->csc1, coloured ? l->order1 : NULL, res, z);
+  double* res2 = res + g1;
+  double* z2 = z + g1;
+  for (int i = 0; i < n_us; ++i) {
+    const double d = r[g1 + i] / l->d.lumped[i];
+    z2[i] = d;
+    if (d == 0.0) continue;
+    for (int k = l->csc2.ptr[i]; k < l->csc2.ptr[i + 1]; ++k) res2[l->csc2.row[k]] -= l->csc2.val[k] * d;
+  }
+  (void)g2;
+  sweep_apply_mult(&l->as2, &l->csc2, coloured ? l->order2 : NULL, res2, z2);
+  free(res);
+}
+
 void orc_fs_apply(const orc_gmg* g, int level, const double* r, double* z) {
+  if (g->fs_mode != 0) {
+    fs_apply_mult(g, level, r, z, g->fs_mode == 1);
+    return;
+  }
   const orc_level* l = &g->lv[level];
   const int n = l->d.n, g1 = l->d.g1, g2 = n - g1, n_us = l->d.n_us;
   memset(z, 0, sizeof(double) * (size_t)n);
@@ -419,6 +586,12 @@ orc_gmg* orc_gmg_create(int n_levels, const orc_level_desc* levels, double omega
       return NULL;
     }
     build_us_csc(lv);
+    csc_build(&lv->csc1, 0, d->g1, d->a_ptr, d->a_idx, d->a_val);
+    csc_build(&lv->csc2, d->g1, d->n - d->g1, d->a_ptr, d->a_idx, d->a_val);
+    lv->order1 = (int*)malloc(sizeof(int) * (size_t)(d->as1_n > 0 ? d->as1_n : 1));
+    lv->order2 = (int*)malloc(sizeof(int) * (size_t)(d->as2_n > 0 ? d->as2_n : 1));
+    lv->ncol1 = colour_blocks(&lv->as1, &lv->csc1, lv->order1);
+    lv->ncol2 = colour_blocks(&lv->as2, &lv->csc2, lv->order2);
   }
   /* coarse: equilibrate like sparse_lu.cpp:104-121, dense LU */
   const orc_level_desc* c = &levels[0];
@@ -456,12 +629,20 @@ orc_gmg* orc_gmg_create(int n_levels, const orc_level_desc* levels, double omega
 
 void orc_gmg_set_cycle(orc_gmg* g, char mode) { g->mode = mode; }
 void orc_gmg_set_smoother(orc_gmg* g, int kind) { g->smoother = kind; }
+void orc_gmg_set_fs_mode(orc_gmg* g, int mode) { g->fs_mode = mode; }
+int orc_gmg_colours(const orc_gmg* g, int level, int group) {
+  return group == 1 ? g->lv[level].ncol1 : g->lv[level].ncol2;
+}
 
 void orc_gmg_destroy(orc_gmg* g) {
   if (!g) return;
   for (int l = 1; l < g->L; ++l) {
     sweep_free(&g->lv[l].as1);
     sweep_free(&g->lv[l].as2);
+    csc_free(&g->lv[l].csc1);
+    csc_free(&g->lv[l].csc2);
+    free(g->lv[l].order1);
+    free(g->lv[l].order2);
     free(g->lv[l].us_ptr);
     free(g->lv[l].us_row);
     free(g->lv[l].us_val);

@@ -64,7 +64,13 @@ void orc_gmg_set_cycle(orc_gmg* g, char mode);
 /* level smoother: 0 damped Richardson (precond.cpp:305-317, default),
  * 1 GMRES(1) minimal-residual step (BASELINE configs[0]) */
 void orc_gmg_set_smoother(orc_gmg* g, int kind);
-/* additive FS apply on level l >= 1 (SURVEY §8c recipe) */
+/* FS variant: 0 additive (default), 1 multiplicative in the
+ * multicolour block order the GPU runs, 2 multiplicative in the
+ * reference's block order (FsPreconditioner::apply, precond.cpp:271-303) */
+void orc_gmg_set_fs_mode(orc_gmg* g, int mode);
+/* colours of the AS1 (group 1) or AS2 (group 2) blocks of a level */
+int orc_gmg_colours(const orc_gmg* g, int level, int group);
+/* FS apply on level l >= 1 in the current variant */
 void orc_fs_apply(const orc_gmg* g, int level, const double* r, double* z);
 /* one V-cycle from a zero guess (gmg.cpp:188-246) */
 void orc_gmg_apply(const orc_gmg* g, const double* r, double* z);

@@ -43,6 +43,9 @@ def lib():
         L.orc_fgmres.argtypes = L.orc_gmres.argtypes
         L.orc_fgmres.restype = ip
         L.orc_gmg_set_smoother.argtypes = [vp, ip]
+        L.orc_gmg_set_fs_mode.argtypes = [vp, ip]
+        L.orc_gmg_colours.argtypes = [vp, ip, ip]
+        L.orc_gmg_colours.restype = ip
         _lib = L
     return _lib
 
@@ -87,11 +90,16 @@ def extract_block(A, dofs):
 
 
 class OracleGmg:
-    """GmgPreconditioner with additive FS smoothers (CPU restatement)."""
+    """GmgPreconditioner with FS smoothers (CPU restatement). fs: "additive"
+    (default), "multicolour" (multiplicative in the multicolour
+    block order the GPU runs) or "multiplicative" (the shipped
+    FsPreconditioner::apply, blocks in the reference's order)."""
 
     SMOOTHERS = {"richardson": 0, "gmres1": 1}
+    FS_MODES = {"additive": 0, "multicolour": 1, "multiplicative": 2}
 
-    def __init__(self, levels: List, omega=0.7, pre=1, post=1, cycle="v", smoother="richardson"):
+    def __init__(self, levels: List, omega=0.7, pre=1, post=1, cycle="v", smoother="richardson",
+                 fs="additive"):
         from paper_1909_13201_b200.problem import level_descs
         self.levels = levels
         self._descs = level_descs(levels)
@@ -103,6 +111,11 @@ class OracleGmg:
         self.h = h
         lib().orc_gmg_set_cycle(h, cycle.encode()[:1])
         lib().orc_gmg_set_smoother(h, self.SMOOTHERS[smoother])
+        lib().orc_gmg_set_fs_mode(h, self.FS_MODES[fs])
+
+    def colours(self, level, group):
+        """Colour count of the AS1 (group 1) or AS2 (group 2) blocks of a level."""
+        return lib().orc_gmg_colours(self.h, level, group)
 
     def __del__(self):
         if getattr(self, "h", None):
