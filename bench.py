@@ -498,6 +498,8 @@ def run_ours(args, ws, rank, local):
         out["cpu_baseline"] = cpu_baseline_port(P)
     if rank == 0 and not args.no_microbench:
         out["as_microbench"] = as_microbench(fsigpu, torch, hbm_peak, cpu=not args.no_cpu_baseline)
+    if rank == 0 and args.config == "cfg0" and args.smoother == "fs":
+        out["multiplicative_fs"] = mult_time_to_solution(fsigpu, torch, P, steps=max(3, args.steps // 2))
     if rank == 0 and args.config == "cfg0" and not args.no_config2:
         del S, S_prof, G
         torch.cuda.empty_cache()
@@ -603,6 +605,39 @@ def config2_bench(fsigpu, torch, hbm_peak, steps=3, max_iters=60):
     del S, G, P, b, x, flush
     torch.cuda.empty_cache()
     return out
+
+
+def mult_time_to_solution(fsigpu, torch, P, steps=5):
+    """Config 0 with the reference's shipped multiplicative FS smoother
+    (precond.cpp:271-303) in multicolour order (mult.cuh): FGMRES(30) to
+    rtol 1e-10, L2 flushed between solves. The reference's own
+    multiplicative solve is timed by the reference arm (time_to_solution)."""
+    G = fsigpu.GmgPreconditioner(P.levels, fsigpu.CycleConfig(schwarz="multiplicative"))
+    S = fsigpu.GmresSolver(G, P.frame_scale, restart=30)
+    cfg = fsigpu.KrylovConfig(restart=30, max_iters=2000, rel_tol=1e-10, abs_tol=1e-300)
+    lib_stream = torch.cuda.ExternalStream(G.stream())
+    b = torch.from_numpy(P.b).cuda()
+    x = torch.zeros(P.n, dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    l0 = fsigpu.launch_count()
+    res = S.solve_dev(b.data_ptr(), x.data_ptr(), cfg)
+    launches = fsigpu.launch_count() - l0
+    per = []
+    for _ in range(steps):
+        flush.fill_(1.0)
+        x.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(lib_stream)
+        res = S.solve_dev(b.data_ptr(), x.data_ptr(), cfg)
+        e1.record(lib_stream)
+        e1.synchronize()
+        per.append(e0.elapsed_time(e1))
+    ms = sum(per) / len(per)
+    return {"schwarz": "multiplicative (multicolour order)", "iterations": res.iterations,
+            "converged": res.converged, "final_relres": res.true_residual / float(np.linalg.norm(P.b)),
+            "solve_ms": ms, "v_cycles_per_s": res.m_applies / (ms / 1000.0), "launches_per_solve": launches,
+            "steps": steps}
 
 
 def S_solve_host(fsigpu, S, bh, xh, cfg):

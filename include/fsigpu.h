@@ -148,6 +148,17 @@ int fsigpu_gmg_set_smoother(fsigpu_gmg g, int kind);
  *      richardson_smooth (precond.cpp:305-317) ---------------------------- */
 int fsigpu_gmg_create(int n_levels, const fsigpu_level_desc* levels, double omega, int pre,
                       int post, char cycle, fsigpu_gmg* out);
+/* The same with the Schwarz mode of the FS smoothers (SchwarzMode,
+ * include/fsi/precond.hpp): additive (the default above) or
+ * multiplicative, the reference's shipped FsPreconditioner::apply
+ * (precond.cpp:59-77,271-303) with the blocks run in multicolour order:
+ * same-colour blocks share no dof and do not couple, so each colour is one
+ * parallel step (block order differs from the reference's; the CPU
+ * restatement runs the same order). */
+#define FSIGPU_SCHWARZ_ADDITIVE 0
+#define FSIGPU_SCHWARZ_MULTIPLICATIVE 1
+int fsigpu_gmg_create_ex(int n_levels, const fsigpu_level_desc* levels, double omega, int pre,
+                         int post, char cycle, int schwarz, fsigpu_gmg* out);
 int fsigpu_gmg_size(fsigpu_gmg g);
 /* the cudaStream_t every GMG / GMRES kernel of this handle is launched on */
 void* fsigpu_gmg_stream(fsigpu_gmg g);

@@ -30,6 +30,7 @@
 #include "krylov_wide.cuh"
 #include "sparse.cuh"
 #include "mr.cuh"
+#include "mult.cuh"
 
 namespace fsigpu {
 
@@ -616,6 +617,13 @@ struct Level {
   DevBuf<double> delta, bbuf, xbuf, rbuf;
   DevBuf<double> mr_z, mr_w;  // GMRES(1) smoother: z = FS r, w = A z
   bool assembled = false;  // FS smoother as one sparse operator (kModeAssembled)
+  // multiplicative FS (mult.cuh): group-restricted matrix, blocks by colour
+  bool mult = false;
+  Csr AG;
+  DevBuf<int> col_blocks;
+  std::vector<int> h_col_off;  // colour c = col_blocks[h_col_off[c] .. h_col_off[c+1])
+  DevBuf<double> mz;           // FS(r) of the sweep
+  double mult_bytes = 0;
   Csr FS;
   Csr AP;  // A * diag(!col_mask) * P : fused prolongation + post-smoothing residual
   double* b = nullptr;  // level rhs (top level: external)
@@ -731,9 +739,29 @@ struct Gmg {
     smoother = kind;
     ++version;
   }
-  // z = FS r (the additive FS smoother applied once, no damping)
+  // multiplicative FS (mult.cuh): z = FS_mult r; x (optional) += omega z
+  void mult_apply(int l, const double* r, double* z, double* x, int x_zero) {
+    Level& L = lv[l];
+    ProfScope ps(FSIGPU_K_BLOCK_SOLVE, L.mult_bytes, s);
+    launch_k(mult_init_kernel, dim3(std::max(1, std::min(ceil_div(L.n, 256), 4 * 148))), dim3(256), 0, s, L.n, L.g1,
+             L.n_us, r, (const double*)L.lumped.p, z, x, omega, x_zero);
+    MultArgs a{L.col_blocks.p, L.blocks.m.p, L.blocks.row_off.p, L.blocks.pos.p, L.blocks.inv.p,
+               L.blocks.inv_off.p, L.AG.ptr.p, L.AG.idx.p, L.AG.val.p, r, z, x, omega};
+    const int nc = (int)L.h_col_off.size() - 1;
+    for (int c = 0; c < nc; ++c) {
+      const int cnt = L.h_col_off[c + 1] - L.h_col_off[c];
+      if (cnt) launch_k(mult_colour_kernel, dim3(cnt), dim3(kMultThreads), 0, s, a, L.h_col_off[c]);
+    }
+    FSI_CHECK_LAUNCH();
+    counted(1 + nc);
+  }
+  // z = FS r (the FS smoother applied once, no damping)
   void fs_into(int l, const double* r, double* z) {
     Level& L = lv[l];
+    if (L.mult) {
+      mult_apply(l, r, z, nullptr, 1);
+      return;
+    }
     if (L.assembled) {
       ProfScope ps(FSIGPU_K_BLOCK_SOLVE, L.FS.bytes(false), s);
       L.FS.launch(GatherPlain{r}, EpiSetScaled{1.0, z}, s);
@@ -776,6 +804,15 @@ struct Gmg {
     Level& L = lv[l];
     if (smoother == 1) {
       mr_sweep(l, x_zero, r_ready, mask_out);
+      return;
+    }
+    if (L.mult) {
+      const double* r = L.b;  // x == 0: res = b exactly (precond.cpp:312-313)
+      if (!x_zero) {
+        if (!r_ready) resid(l, L.rbuf.p);
+        r = L.rbuf.p;
+      }
+      mult_apply(l, r, L.mz.p, L.x, x_zero);
       return;
     }
     if (L.assembled) {
@@ -966,8 +1003,114 @@ static void assemble_fs(Level& L, const fsigpu_level_desc& d, const std::vector<
   L.assembled = true;
 }
 
+// Multicolour order of the blocks of one group of the multiplicative FS
+// smoother (mult.cuh). Blocks b, b' conflict when they share a dof or the
+// group matrix A[base:base+dim, base:base+dim] stores an entry coupling them
+// in either direction; greedy in block order, colour(b) = the smallest colour
+// no conflicting earlier block has. Same rule as the oracle's colour_blocks
+// (oracle/fsi_oracle.c). bidx: group-local positions. Returns the count.
+static int colour_group(int nb, const int* bptr, const int* bidx, int base, int dim, const fsigpu_level_desc& d,
+                        std::vector<int>& colour) {
+  colour.assign(nb, 0);
+  if (nb == 0) return 0;
+  std::vector<int> rp(dim + 1, 0), rc;
+  for (int i = 0; i < dim; ++i) {
+    for (int k = d.a_ptr[base + i]; k < d.a_ptr[base + i + 1]; ++k) {
+      const int j = d.a_idx[k] - base;
+      if (j >= 0 && j < dim) rc.push_back(j);
+    }
+    rp[i + 1] = (int)rc.size();
+  }
+  std::vector<int> cp(dim + 1, 0), cr(rc.size());
+  for (int j : rc) cp[j + 1]++;
+  for (int j = 0; j < dim; ++j) cp[j + 1] += cp[j];
+  {
+    std::vector<int> nx(cp.begin(), cp.end() - 1);
+    for (int i = 0; i < dim; ++i)
+      for (int k = rp[i]; k < rp[i + 1]; ++k) cr[nx[rc[k]]++] = i;
+  }
+  std::vector<int> dptr(dim + 1, 0), dblk(bptr[nb]);
+  for (int k = 0; k < bptr[nb]; ++k) dptr[bidx[k] + 1]++;
+  for (int i = 0; i < dim; ++i) dptr[i + 1] += dptr[i];
+  {
+    std::vector<int> nx(dptr.begin(), dptr.end() - 1);
+    for (int b = 0; b < nb; ++b)
+      for (int k = bptr[b]; k < bptr[b + 1]; ++k) dblk[nx[bidx[k]]++] = b;
+  }
+  std::vector<int> seen(nb + 1, -1);
+  int ncol = 0;
+  for (int b = 0; b < nb; ++b) {
+    auto mark = [&](int j) {
+      for (int q = dptr[j]; q < dptr[j + 1]; ++q)
+        if (dblk[q] < b) seen[colour[dblk[q]]] = b;
+    };
+    for (int k = bptr[b]; k < bptr[b + 1]; ++k) {
+      const int i = bidx[k];
+      mark(i);
+      for (int e = rp[i]; e < rp[i + 1]; ++e) mark(rc[e]);
+      for (int e = cp[i]; e < cp[i + 1]; ++e) mark(cr[e]);
+    }
+    int c = 0;
+    while (seen[c] == b) ++c;
+    colour[b] = c;
+    ncol = std::max(ncol, c + 1);
+  }
+  return ncol;
+}
+
+// Multiplicative FS data of a level: the group-restricted matrix
+// blockdiag(A_g1, A_g2) and the AS1 / AS2 blocks sorted by colour (merged:
+// colour c = the AS1 blocks of colour c, then the AS2 blocks of colour c;
+// the groups never couple, precond.cpp:137-139).
+static void build_mult(Level& L, const fsigpu_level_desc& d, cudaStream_t s) {
+  const int n = d.n, g1 = d.g1;
+  std::vector<int> c1, c2;
+  const int n1 = colour_group(d.as1_n, d.as1_ptr, d.as1_idx, 0, g1, d, c1);
+  const int n2 = colour_group(d.as2_n, d.as2_ptr, d.as2_idx, g1, n - g1, d, c2);
+  const int nc = std::max(n1, n2);
+  std::vector<int> order;
+  L.h_col_off.assign(1, 0);
+  for (int c = 0; c < nc; ++c) {
+    for (int b = 0; b < d.as1_n; ++b)
+      if (c1[b] == c) order.push_back(b);
+    for (int b = 0; b < d.as2_n; ++b)
+      if (c2[b] == c) order.push_back(d.as1_n + b);
+    L.h_col_off.push_back((int)order.size());
+  }
+  L.col_blocks.upload(order.empty() ? std::vector<int>{0} : order, s);
+  std::vector<int> ap(n + 1, 0), ai;
+  std::vector<double> av;
+  for (int i = 0; i < n; ++i) {
+    for (int k = d.a_ptr[i]; k < d.a_ptr[i + 1]; ++k)
+      if ((i < g1) == (d.a_idx[k] < g1)) {
+        ai.push_back(d.a_idx[k]);
+        av.push_back(d.a_val[k]);
+      }
+    ap[i + 1] = (int)ai.size();
+  }
+  if (ai.empty()) {
+    ai.push_back(0);
+    av.push_back(0.0);
+  }
+  L.AG.create(n, n, ap.data(), ai.data(), av.data(), s);
+  L.mz.alloc(n);
+  double by = 40.0 * n;  // init: r, lumped, z and x
+  const Blocks& B = L.blocks;
+  for (long long b = 0; b < B.nb; ++b) {
+    const int m = B.h_m[b];
+    by += 8.0 * even_up(m) * m + 36.0 * m;  // inverse, pos, r, z and x updates
+  }
+  for (int b = 0; b < d.as1_n; ++b)
+    for (int k = d.as1_ptr[b]; k < d.as1_ptr[b + 1]; ++k) by += 20.0 * (ap[d.as1_idx[k] + 1] - ap[d.as1_idx[k]]);
+  for (int b = 0; b < d.as2_n; ++b)
+    for (int k = d.as2_ptr[b]; k < d.as2_ptr[b + 1]; ++k)
+      by += 20.0 * (ap[g1 + d.as2_idx[k] + 1] - ap[g1 + d.as2_idx[k]]);
+  L.mult_bytes = by;
+  L.mult = true;
+}
+
 // Build one level from its descriptor (host arrays).
-static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t s) {
+static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t s, bool mult) {
   Level& L = g.lv[l];
   require(d.n > 0, "gmg: empty level");
   L.n = d.n;
@@ -1091,7 +1234,8 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
   }
   L.n_as1 = nb1;
   Blocks& B = L.blocks;
-  B.mode = g_default_mode == kModeLU ? kModeLU : kModeInverse;  // assembled builds on the inverses
+  // assembled and multiplicative smoothers build on the inverses
+  B.mode = (g_default_mode == kModeLU && !mult) ? kModeLU : kModeInverse;
   B.layout(sizes, s);
   B.pos.upload(pos, s);
   DevBuf<double> dense((size_t)std::max<long long>(B.h_lu_off[B.nb], 1));
@@ -1144,7 +1288,10 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
       throw Error(FSIGPU_ERR_SINGULAR, "singular block: fs lumped mass row " + std::to_string(i));
     }
   FSI_CUDA(cudaStreamSynchronize(s));
-  if (g_default_mode == kModeAssembled) assemble_fs(L, d, pos, cnt, ap, ac, av, s);
+  if (mult)
+    build_mult(L, d, s);
+  else if (g_default_mode == kModeAssembled)
+    assemble_fs(L, d, pos, cnt, ap, ac, av, s);
 }
 
 // Coarse operator: equilibrate (sparse_lu.cpp:104-121), Gauss-Jordan
@@ -1782,9 +1929,16 @@ void fsigpu_blocks_destroy(fsigpu_blocks b) {
 // ---- GMG
 int fsigpu_gmg_create(int n_levels, const fsigpu_level_desc* levels, double omega, int pre, int post, char cycle,
                       fsigpu_gmg* out) {
+  return fsigpu_gmg_create_ex(n_levels, levels, omega, pre, post, cycle, FSIGPU_SCHWARZ_ADDITIVE, out);
+}
+
+int fsigpu_gmg_create_ex(int n_levels, const fsigpu_level_desc* levels, double omega, int pre, int post, char cycle,
+                         int schwarz, fsigpu_gmg* out) {
   g_bad_block = -1;
   g_bad_level = -1;
   return guarded([&] {
+    require(schwarz == FSIGPU_SCHWARZ_ADDITIVE || schwarz == FSIGPU_SCHWARZ_MULTIPLICATIVE,
+            "fs: schwarz mode must be 0 (additive) or 1 (multiplicative)");
     require(n_levels >= 1 && levels != nullptr, "gmg: no levels");
     require(pre >= 0 && post >= 0 && !(pre == 0 && post == 0 && n_levels > 1), "gmg: need at least one smoothing sweep");
     require(omega >= 0.0 && omega < 2.0, "richardson: omega outside [0,2)");
@@ -1797,7 +1951,7 @@ int fsigpu_gmg_create(int n_levels, const fsigpu_level_desc* levels, double omeg
     g.post = post;
     g.cyc = cycle;
     g.lv.resize(n_levels);
-    for (int l = 0; l < n_levels; ++l) build_level(g, l, levels[l], g.s);
+    for (int l = 0; l < n_levels; ++l) build_level(g, l, levels[l], g.s, schwarz == FSIGPU_SCHWARZ_MULTIPLICATIVE);
     build_coarse(g, levels[0], g.s);
     pin_hot_data(g);
     g.tmp_in.alloc(g.size());

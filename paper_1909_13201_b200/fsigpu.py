@@ -100,6 +100,7 @@ def lib():
             "fsigpu_blocks_get_lu": ([vp, vp, vp], ip),
             "fsigpu_blocks_destroy": ([vp], None),
             "fsigpu_gmg_create": ([ip, vp, d, ip, ip, C.c_char, C.POINTER(vp)], ip),
+            "fsigpu_gmg_create_ex": ([ip, vp, d, ip, ip, C.c_char, ip, C.POINTER(vp)], ip),
             "fsigpu_gmg_size": ([vp], ip),
             "fsigpu_gmg_apply": ([vp, vp, vp], ip),
             "fsigpu_gmg_apply_dev": ([vp, vp, vp, vp], ip),
@@ -281,10 +282,14 @@ class CycleConfig:
     # "richardson" (precond.cpp:305-317) or "gmres1" (minimal-residual step,
     # BASELINE configs[0]; non-linear, use under the flexible device solver)
     smoother: str = "richardson"
+    # SchwarzMode of the FS blocks (include/fsi/precond.hpp): "additive"
+    # (default) or "multiplicative" (the shipped
+    # FsPreconditioner::apply, precond.cpp:271-303, blocks in multicolour order)
+    schwarz: str = "additive"
 
 
 class GmgPreconditioner:
-    """GMG V/W/F cycle with additive FS smoothers on the device."""
+    """GMG V/W/F cycle with FS smoothers on the device."""
 
     def __init__(self, levels: List[Level], cfg: CycleConfig = CycleConfig()):
         init()
@@ -292,8 +297,8 @@ class GmgPreconditioner:
         self._descs = level_descs(levels)
         self.labels = []
         h = C.c_void_p()
-        rc = lib().fsigpu_gmg_create(len(levels), C.addressof(self._descs), cfg.omega, cfg.pre, cfg.post,
-                                     cfg.cycle.encode()[:1], C.byref(h))
+        rc = lib().fsigpu_gmg_create_ex(len(levels), C.addressof(self._descs), cfg.omega, cfg.pre, cfg.post,
+                                        cfg.cycle.encode()[:1], self.SCHWARZ[cfg.schwarz], C.byref(h))
         if rc == FSIGPU_ERR_SINGULAR:
             # the failing block's reference label (precond.cpp:182,224,265)
             b, lvl = lib().fsigpu_last_singular_block(), lib().fsigpu_last_singular_level()
@@ -309,6 +314,7 @@ class GmgPreconditioner:
             self.set_smoother(cfg.smoother)
 
     SMOOTHERS = {"richardson": 0, "gmres1": 1}
+    SCHWARZ = {"additive": 0, "multiplicative": 1}
 
     def set_smoother(self, kind: str):
         _check(lib().fsigpu_gmg_set_smoother(self.h, self.SMOOTHERS[kind]))
