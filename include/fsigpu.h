@@ -131,7 +131,8 @@ void fsigpu_blocks_destroy(fsigpu_blocks b);
 #define FSIGPU_MODE_INVERSE 1
 #define FSIGPU_MODE_ASSEMBLED 2
 int fsigpu_set_block_mode(int mode);
-/* programmatic dependent launch of the solve-path kernels (default off: measured neutral) */
+/* programmatic dependent launch of the solve-path kernels (default on: each kernel fetches its
+ * setup data before griddepcontrol.wait; config 0: 8.45 -> 7.96 ms per solve) */
 int fsigpu_set_pdl(int enable);
 
 /* Level smoother of every smoothed level: 0 = damped Richardson with the

@@ -389,6 +389,8 @@ __device__ __forceinline__ void small_solve_smem(const double* blk, int m, doubl
 
 constexpr int kPipeMaxWarps = 8;
 __global__ void __launch_bounds__(kPipeMaxWarps * 32) small_pipe_solve_kernel(SmallPipeArgs a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(16) double dsm[];
   __shared__ unsigned long long bars[kPipeMaxWarps][2];
   const int NW = blockDim.x >> 5;

@@ -38,7 +38,10 @@ namespace fsigpu {
 // Solve-path kernels are launched with programmatic stream serialization
 // (PDL): inside the captured graphs consecutive kernels overlap launch and
 // prologue with the predecessor's tail (kernels call pdl_trigger/pdl_wait).
-static std::atomic<bool> g_pdl{false};  // measured neutral on config 0; opt-in
+// on by default: the kernels fetch their setup data (matrix rows) before
+// griddepcontrol.wait, which overlaps it with the predecessor's tail
+// (config 0: 8.45 -> 7.96 ms per solve, tools/ab_pdl.py)
+static std::atomic<bool> g_pdl{true};
 template <typename... KArgs, typename... Args>
 static void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                      Args&&... args) {

@@ -343,13 +343,35 @@ __device__ __forceinline__ double fused_row(const KBufs& k, int row, int lane) {
 // on config 0.
 template <int LPR>
 __global__ void __launch_bounds__(kFuseThreads) k_spmv_dots_1(KBufs k) {
+  static_assert(kFuseThreads / LPR >= kFuseRows, "one row pass per CTA");
   pdl_trigger();
-  pdl_wait();
   __shared__ double ws[kFuseRows];
-  const int j = k.st->j;
-  const int nv = j + 1;
   const int r0 = blockIdx.x * kFuseRows;
   const int t = threadIdx.x;
+  // setup data first (the outer operator's row and its first batch, the
+  // frame scale: never written by the solve), so under programmatic
+  // dependent launch it overlaps the V-cycle's last kernel
+  const int rl = t / LPR, ln = t & (LPR - 1);
+  const int row = r0 + rl;
+  const bool ok = rl < kFuseRows && row < k.n;
+  const bool head = ok && ln == 0;
+  const double sc = head ? __ldg(k.scale + row) : 0.0;
+  constexpr int U = 8;
+  const int k0 = ok ? __ldg(k.a_ptr + row) : 0, k1 = ok ? __ldg(k.a_ptr + row + 1) : 0;
+  int c[U];
+  double av[U];
+  auto load = [&](int kb) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int kk = kb + u * LPR;
+      c[u] = kk < k1 ? __ldg(k.a_idx + kk) : -1;
+      av[u] = kk < k1 ? __ldg(k.a_val + kk) : 0.0;
+    }
+  };
+  load(k0 + ln);
+  pdl_wait();
+  const int j = k.st->j;
+  const int nv = j + 1;
   // operands that do not depend on w are loaded before the SpMV so their
   // latency overlaps it: the V entries of the partial dots (warp v, lanes
   // over the CTA's 128 rows, 4 each) and z_j for the copy into Z[j]
@@ -357,19 +379,26 @@ __global__ void __launch_bounds__(kFuseThreads) k_spmv_dots_1(KBufs k) {
   double vv[kFuseRows / 32];
 #pragma unroll
   for (int q = 0; q < kFuseRows / 32; ++q) {
-    const int row = r0 + lane + 32 * q;
-    vv[q] = (v < nv && row < k.n) ? k.V[(size_t)v * k.n + row] : 0.0;
+    const int rr = r0 + lane + 32 * q;
+    vv[q] = (v < nv && rr < k.n) ? k.V[(size_t)v * k.n + rr] : 0.0;
   }
   const bool zc = t < kFuseRows && r0 + t < k.n;
   const double zj = zc ? k.zbuf[r0 + t] : 0.0;
-  constexpr int RPP = kFuseThreads / LPR;  // rows per pass
-  for (int p = 0; p < kFuseRows; p += RPP) {
-    const int rl = p + t / LPR;
-    const int row = r0 + rl;
-    const bool ok = rl < kFuseRows && row < k.n;
-    const bool head = ok && (t & (LPR - 1)) == 0;
-    const double sc = head ? k.scale[row] : 0.0;
-    const double s = fused_row<LPR>(k, ok ? row : -1, t & (LPR - 1));
+  {
+    double s = 0.0;
+    for (int kb = k0 + ln; kb < k1; kb += U * LPR) {
+      double xv[U], vc[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        xv[u] = c[u] >= 0 ? k.zbuf[c[u]] : 0.0;
+        vc[u] = av[u];
+      }
+      if (kb + U * LPR < k1) load(kb + U * LPR);
+#pragma unroll
+      for (int u = 0; u < U; ++u) s = fma(vc[u], xv[u], s);
+    }
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, LPR);
     if (head) {
       const double w = sc * s;
       k.w[row] = w;

@@ -22,6 +22,8 @@ constexpr int kMrCtas = 296;  // 2 per SM; fixed so the summation order never ch
 __global__ void __launch_bounds__(kMrThreads) k_mr_alpha(int n, const double* __restrict__ w,
                                                          const double* __restrict__ r, double* part,
                                                          unsigned int* ticket, double* alpha) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ double s_wr[kMrThreads / 32], s_ww[kMrThreads / 32];
   double wr = 0.0, ww = 0.0;
   for (int i = blockIdx.x * kMrThreads + threadIdx.x; i < n; i += kMrCtas * kMrThreads) {
@@ -78,6 +80,8 @@ __global__ void __launch_bounds__(kMrThreads) k_mr_alpha(int n, const double* __
 __global__ void __launch_bounds__(256) k_mr_update(int n, const double* __restrict__ alpha,
                                                    const double* __restrict__ z, double* __restrict__ x,
                                                    int x_zero, const unsigned char* __restrict__ mask) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * 256 + threadIdx.x;
   if (i >= n) return;
   const double a = __ldg(alpha);

@@ -110,27 +110,40 @@ __global__ void __launch_bounds__(256) csr_kernel(int rows, const int* __restric
   // full-mask shuffle waits on an exited lane
   const bool ok = row < rows;
   pdl_trigger();
-  const int k0 = ok ? __ldg(ptr + row) : 0, k1 = ok ? __ldg(ptr + row + 1) : 0;  // setup data
+  // The matrix is setup data (never written by the solve): its row bounds
+  // and first batch are fetched before the dependency wait, so under
+  // programmatic dependent launch they overlap the predecessor's tail and
+  // only the gathers of the vector remain on the critical path.
+  const int k0 = ok ? __ldg(ptr + row) : 0, k1 = ok ? __ldg(ptr + row + 1) : 0;
+  int c[U];
+  double v[U];
+  auto load = [&](int kb) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = kb + u * LPR;
+      const bool in = k < k1;
+      c[u] = in ? __ldg(idx + k) : -1;
+      v[u] = in ? __ldg(val + k) : 0.0;
+    }
+  };
+  load(k0 + lane);
   pdl_wait();
   EpiPre pe{0.0, 0};
   if (ok && lane == 0) pe = epi.pre(row);
   double s = 0.0;
-  // predicated batches of U entries per lane: all index/value loads of a
-  // batch are in flight before the dependent x gathers (no early exits)
+  // predicated batches of U entries per lane: a batch's index/value loads
+  // are in flight before its dependent x gathers, and the next batch's are
+  // issued behind those gathers (no early exits)
   for (int kb = k0 + lane; kb < k1; kb += U * LPR) {
-    int c[U];
-    double v[U], xv[U];
+    double xv[U], vc[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int k = kb + u * LPR;
-      const bool ok = k < k1;
-      c[u] = ok ? __ldg(idx + k) : -1;
-      v[u] = ok ? __ldg(val + k) : 0.0;
+      xv[u] = c[u] >= 0 ? gx(c[u]) : 0.0;
+      vc[u] = v[u];
     }
+    if (kb + U * LPR < k1) load(kb + U * LPR);
 #pragma unroll
-    for (int u = 0; u < U; ++u) xv[u] = c[u] >= 0 ? gx(c[u]) : 0.0;
-#pragma unroll
-    for (int u = 0; u < U; ++u) s = fma(v[u], xv[u], s);
+    for (int u = 0; u < U; ++u) s = fma(vc[u], xv[u], s);
   }
 #pragma unroll
   for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, LPR);
@@ -146,7 +159,27 @@ __global__ void __launch_bounds__(256) csr_pair_kernel(int rows, const int* __re
   const int lane = threadIdx.x & (LPR - 1);
   const bool ok = row < rows;
   pdl_trigger();
-  const int k0 = ok ? __ldg(ptr + row) : 0, k1 = ok ? __ldg(ptr + row + 1) : 0;  // setup data
+  // setup data (row bounds, first pair batch) before the dependency wait,
+  // as in csr_kernel
+  const int k0 = ok ? __ldg(ptr + row) : 0, k1 = ok ? __ldg(ptr + row + 1) : 0;
+  int2 cn[UP];
+  double2 vn[UP];
+  auto load = [&](int kb) {
+#pragma unroll
+    for (int u = 0; u < UP; ++u) {
+      const int k = kb + 2 * u * LPR;
+      if (k < k1) {
+        cn[u] = __ldg(reinterpret_cast<const int2*>(idx + k));
+        vn[u] = __ldg(reinterpret_cast<const double2*>(val + k));
+        if (k < k0) cn[u].x = -1;
+        if (k + 1 >= k1) cn[u].y = -1;
+      } else {
+        cn[u] = make_int2(-1, -1);
+        vn[u] = make_double2(0.0, 0.0);
+      }
+    }
+  };
+  load((k0 & ~1) + 2 * lane);
   pdl_wait();
   EpiPre pe{0.0, 0};
   if (ok && lane == 0) pe = epi.pre(row);
@@ -156,17 +189,10 @@ __global__ void __launch_bounds__(256) csr_pair_kernel(int rows, const int* __re
     double2 v[UP];
 #pragma unroll
     for (int u = 0; u < UP; ++u) {
-      const int k = kb + 2 * u * LPR;
-      if (k < k1) {
-        c[u] = __ldg(reinterpret_cast<const int2*>(idx + k));
-        v[u] = __ldg(reinterpret_cast<const double2*>(val + k));
-        if (k < k0) c[u].x = -1;
-        if (k + 1 >= k1) c[u].y = -1;
-      } else {
-        c[u] = make_int2(-1, -1);
-        v[u] = make_double2(0.0, 0.0);
-      }
+      c[u] = cn[u];
+      v[u] = vn[u];
     }
+    if (kb + 2 * UP * LPR < k1) load(kb + 2 * UP * LPR);
     double x0[UP], x1[UP];
 #pragma unroll
     for (int u = 0; u < UP; ++u) {
@@ -223,26 +249,36 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(int n, const double*
   const int row = blockIdx.x;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   pdl_trigger();
-  pdl_wait();
+  // the inverse and the mask are setup data: the row's first batch is
+  // fetched before the dependency wait (see csr_kernel)
   const double* Mr = M + (size_t)row * n;
-  double xo = 0.0;
-  unsigned char mo = 0;
-  if (t == 0) {
-    if (accumulate) xo = x[row];
-    if (mask_out) mo = mask_out[row];
-  }
-  double s = 0.0;
   constexpr int U = 8;
-  for (int jb = t; jb < n; jb += kGemvThreads * U) {
-    double mv[U], bv[U];
+  double mv[U];
+  auto load = [&](int jb) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int j = jb + kGemvThreads * u;
       mv[u] = j < n ? __ldg(Mr + j) : 0.0;
-      bv[u] = j < n ? __ldg(b + j) : 0.0;
     }
+  };
+  load(t);
+  unsigned char mo = 0;
+  if (t == 0 && mask_out) mo = __ldg(mask_out + row);
+  pdl_wait();
+  double xo = 0.0;
+  if (t == 0 && accumulate) xo = x[row];
+  double s = 0.0;
+  for (int jb = t; jb < n; jb += kGemvThreads * U) {
+    double bv[U], mc[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) s = fma(mv[u], bv[u], s);
+    for (int u = 0; u < U; ++u) {
+      const int j = jb + kGemvThreads * u;
+      bv[u] = j < n ? __ldg(b + j) : 0.0;
+      mc[u] = mv[u];
+    }
+    if (jb + kGemvThreads * U < n) load(jb + kGemvThreads * U);
+#pragma unroll
+    for (int u = 0; u < U; ++u) s = fma(mc[u], bv[u], s);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
@@ -397,7 +433,7 @@ __global__ void __launch_bounds__(256) prolong_resid_kernel(int rows, const int*
   const int lane = threadIdx.x & (LPR - 1);
   const bool ok = row < rows;
   pdl_trigger();
-  pdl_wait();
+  // setup data (P, AP, the masks) before the dependency wait (see csr_kernel)
   int p0 = 0, p1 = 0, a0 = 0, a1 = 0;
   if (ok) {
     p0 = __ldg(pp + row);
@@ -405,36 +441,38 @@ __global__ void __launch_bounds__(256) prolong_resid_kernel(int rows, const int*
     a0 = __ldg(ap + row);
     a1 = __ldg(ap + row + 1);
   }
-  // the row's own operands, loaded before the dot products (see EpiPre)
   unsigned char cm = 1;
+  if (ok && lane == 0) cm = __ldg(cmask + row);
+  double s1 = 0.0, s2 = 0.0;
+  int kp = p0 + lane, ka = a0 + lane;
+  int c[UP + UA];
+  double v[UP + UA];
+#pragma unroll
+  for (int u = 0; u < UP; ++u) {
+    const int k = kp + u * LPR;
+    const bool in = k < p1;
+    c[u] = in ? __ldg(pi + k) : -1;
+    v[u] = in ? __ldg(pv + k) : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < UA; ++u) {
+    const int k = ka + u * LPR;
+    const bool in = k < a1;
+    c[UP + u] = in ? __ldg(ai + k) : -1;
+    v[UP + u] = in ? __ldg(av + k) : 0.0;
+  }
+  pdl_wait();
+  // the row's own operands, loaded before the dot products (see EpiPre)
   double xo = 0.0, rp = 0.0;
   if (ok && lane == 0) {
-    cm = cmask[row];
     xo = x[row];
     rp = r_pre[row];
   }
   auto gather = [&](int c) -> double {
     return c >= 0 ? ((cmask_coarse && __ldg(cmask_coarse + c)) ? 0.0 : __ldg(ec + c)) : 0.0;
   };
-  double s1 = 0.0, s2 = 0.0;
-  int kp = p0 + lane, ka = a0 + lane;
   {
-    int c[UP + UA];
-    double v[UP + UA], xv[UP + UA];
-#pragma unroll
-    for (int u = 0; u < UP; ++u) {
-      const int k = kp + u * LPR;
-      const bool in = k < p1;
-      c[u] = in ? __ldg(pi + k) : -1;
-      v[u] = in ? __ldg(pv + k) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < UA; ++u) {
-      const int k = ka + u * LPR;
-      const bool in = k < a1;
-      c[UP + u] = in ? __ldg(ai + k) : -1;
-      v[UP + u] = in ? __ldg(av + k) : 0.0;
-    }
+    double xv[UP + UA];
 #pragma unroll
     for (int u = 0; u < UP + UA; ++u) xv[u] = gather(c[u]);
 #pragma unroll
@@ -483,7 +521,7 @@ __global__ void __launch_bounds__(256) prolong_resid_pair_kernel(
   const int lane = threadIdx.x & (LPR - 1);
   const bool ok = row < rows;
   pdl_trigger();
-  pdl_wait();
+  // setup data (P, AP, the masks) before the dependency wait (see csr_kernel)
   int p0 = 0, p1 = 0, a0 = 0, a1 = 0;
   if (ok) {
     p0 = __ldg(pp + row);
@@ -492,12 +530,7 @@ __global__ void __launch_bounds__(256) prolong_resid_pair_kernel(
     a1 = __ldg(ap + row + 1);
   }
   unsigned char cm = 1;
-  double xo = 0.0, rp = 0.0;
-  if (ok && lane == 0) {
-    cm = cmask[row];
-    xo = x[row];
-    rp = r_pre[row];
-  }
+  if (ok && lane == 0) cm = __ldg(cmask + row);
   auto gather = [&](int c) -> double {
     return c >= 0 ? ((cmask_coarse && __ldg(cmask_coarse + c)) ? 0.0 : __ldg(ec + c)) : 0.0;
   };
@@ -516,7 +549,7 @@ __global__ void __launch_bounds__(256) prolong_resid_pair_kernel(
       }
     }
   };
-  double s1 = 0.0, s2 = 0.0;
+  double s1 = 0.0, s2 = 0.0, xo = 0.0, rp = 0.0;
   int kp = p0 + lane, ka = (a0 & ~1) + 2 * lane;
   {
     int cp[UP];
@@ -531,6 +564,11 @@ __global__ void __launch_bounds__(256) prolong_resid_pair_kernel(
     int2 c[UA];
     double2 v[UA];
     load_pairs(ka, c, v);
+    pdl_wait();
+    if (ok && lane == 0) {
+      xo = x[row];
+      rp = r_pre[row];
+    }
     double xp[UP], x0[UA], x1[UA];
 #pragma unroll
     for (int u = 0; u < UP; ++u) xp[u] = gather(cp[u]);
