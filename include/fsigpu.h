@@ -179,6 +179,43 @@ int fsigpu_gmg_set_launch(fsigpu_gmg g, int level, int which, int lpr, int unrol
 int fsigpu_gmg_time_kernel(fsigpu_gmg g, int which, int level, int reps, int cold, double* ms,
                            double* bytes);
 
+/* ---- block sets built on the device: FsPreconditioner's field-split
+ *      sets (precond.cpp:119-269) and the Vanka sets of the pure-DD smoother
+ *      (build_vanka_blocks, ordering.cpp:77-115, as AsPreconditioner maps
+ *      them, precond.cpp:99-117), from the mesh-side index maps in the
+ *      solver's frame. Replaces constructing (and CPU-factorising) the
+ *      reference FsPreconditioner / AsPreconditioner to obtain the sets. --- */
+typedef struct fsigpu_sets_t* fsigpu_sets;
+typedef struct {
+  int n_elements;
+  int n_nodes;                      /* Q2 nodes (DofMap::n_q2_nodes)                  */
+  int nodes_per_element;            /* 9 (2D Q2) or 27 (3D Q2)                        */
+  int dim;                          /* components of d and u (2 or 3)                 */
+  int p_per_element;                /* P1disc modes per element (3 in 2D, 4 in 3D)    */
+  const int* element_nodes;         /* n_elements x nodes_per_element                 */
+  const unsigned char* elem_solid;  /* FieldLayout::elem_solid                        */
+  const unsigned char* node_solid;  /* FieldLayout::node_solid                        */
+  const int* d_pos;                 /* n_nodes x dim: frame_of(d_dof(node, i))        */
+  const int* u_pos;                 /* n_nodes x dim: frame_of(u_dof(node, i))        */
+  const int* p_pos;                 /* n_elements x p_per_element: frame_of(p_dof)    */
+  const unsigned char* drop;        /* constrained_positions (precond.cpp:90-97), or NULL */
+} fsigpu_mesh_desc;
+/* level: n, a_* (frame matrix), g1, n_us are read (the sets are ignored).
+ * AS1: solid [d^s,p^s] chunks of epb_as1 elements, then fluid d^f chunks of
+ * epb_as1 grown by overlap_layers rings; AS2: fluid [u^f,p^f] chunks of
+ * epb_as2 (group-2 local); lumped u^s mass (precond.cpp:231-245; a
+ * non-positive row sum -> FSIGPU_ERR_SINGULAR "fs lumped mass row <i>"). */
+int fsigpu_fs_sets_build(const fsigpu_level_desc* level, const fsigpu_mesh_desc* mesh, int epb_as1,
+                         int epb_as2, int overlap_layers, fsigpu_sets* out);
+/* Vanka sets (J1 frame positions) as AS1 blocks of a one-group level */
+int fsigpu_vanka_sets_build(int n, const fsigpu_mesh_desc* mesh, int epb, fsigpu_sets* out);
+int fsigpu_sets_counts(fsigpu_sets s, int* as1_n, int* as1_len, int* as2_n, int* as2_len, int* n_us);
+int fsigpu_sets_copy(fsigpu_sets s, int* as1_ptr, int* as1_idx, int* as2_ptr, int* as2_idx,
+                     double* lumped);
+/* the reference label of block b (AS1 then AS2): fs-solid-dp-<start>, ... */
+const char* fsigpu_sets_label(fsigpu_sets s, int block);
+void fsigpu_sets_destroy(fsigpu_sets s);
+
 /* ---- outer solver: gmres (krylov.cpp:20-126) on the row-equilibrated
  *      frame operator diag(frame_scale) A_top with M(r) = GMG(r/frame_scale)
  *      (driver.cpp:259-272).  Implemented as FGMRES(restart) with CGS2

@@ -558,6 +558,39 @@ std::vector<double> seeded(int n, std::mt19937_64& rng) {
   return v;
 }
 
+// The mesh-side inputs of the FS / Vanka block construction
+// (FsPreconditioner ctor, precond.cpp:119-269; build_vanka_blocks +
+// AsPreconditioner, ordering.cpp:77-115, precond.cpp:99-117) in the
+// solver's frame: element -> Q2 nodes, the region flags, the frame
+// positions of every d, u and p dof (OrderingPlan::frame_of) and the
+// dropped positions (constrained_positions, precond.cpp:90-97), so the GPU
+// can build the block sets itself (fsigpu_fs_sets_build).
+void put_mesh(Archive& ar, const std::string& pre, const Problem& P, int l) {
+  const Space& sp = P.st.spaces[l];
+  const FieldLayout& fl = sp.layout;
+  const OrderingPlan& plan = g_as ? P.st.orderings[l].j1 : P.st.orderings[l].j2;
+  std::vector<int> en, dpos, upos, ppos;
+  for (int e = 0; e < fl.n_elements; ++e)
+    for (int a = 0; a < 9; ++a) en.push_back(sp.dofmap.element_nodes[e][a]);
+  for (int q = 0; q < fl.n_q2_nodes; ++q)
+    for (int i = 0; i < 2; ++i) {
+      dpos.push_back(plan.frame_of(fl.d_dof(q, i)));
+      upos.push_back(plan.frame_of(fl.u_dof(q, i)));
+    }
+  for (int e = 0; e < fl.n_elements; ++e)
+    for (int m = 0; m < 3; ++m) ppos.push_back(plan.frame_of(fl.p_dof(e, m)));
+  ar.put(pre + "/element_nodes", en);
+  ar.put(pre + "/elem_solid", fl.elem_solid);
+  ar.put(pre + "/node_solid", fl.node_solid);
+  ar.put(pre + "/d_pos", dpos);
+  ar.put(pre + "/u_pos", upos);
+  ar.put(pre + "/p_pos", ppos);
+  ar.put(pre + "/drop", constrained_positions(plan, P.cmask[l]));
+  ar.put_i(pre + "/epb_as1", P.def.epb1);
+  ar.put_i(pre + "/epb_as2", P.def.epb2);
+  ar.put_i(pre + "/overlap", P.def.overlap);
+}
+
 int cmd_export(const Args& a) {
   if (a.pos.size() < 3) throw std::invalid_argument("export <case> <out>");
   const std::string name = a.pos[1];
@@ -568,6 +601,7 @@ int cmd_export(const Args& a) {
   ar.put_i("seed", static_cast<long long>(a.seed % 2147483647ull));
   for (int l = 0; l < L; ++l) {
     const std::string p = "L" + std::to_string(l);
+    put_mesh(ar, p + "/mesh", *P, l);
     ar.put_csr(p + "/A", P->frame[l]);
     ar.put(p + "/row_mask", P->levels_add[l].constrained_rows);
     ar.put(p + "/col_mask", P->levels_add[l].constrained_cols);
@@ -860,6 +894,21 @@ int cmd_gpu_adapter(const Args& a) {
   const KrylovConfig kc{};
   auto ref = run_gmres(*P, true, kc);
   const GmresResult g = gpu_gmres(gpu, P->frame_scale, P->b, kc);
+  // the same drop-in without any reference FsPreconditioner: block sets and
+  // lumped mass built on the GPU from the Space / J2 plan / masks
+  std::vector<const Space*> sps;
+  std::vector<const OrderingPlan*> plans;
+  std::vector<const ConstraintMasks*> cms;
+  for (int l = 0; l < L; ++l) {
+    sps.push_back(&P->st.spaces[l]);
+    plans.push_back(&P->st.orderings[l].j2);
+    cms.push_back(&P->cmask[l]);
+  }
+  GpuGmg gpu_mesh(P->levels_add, sps, plans, cms, FieldSplitPlan{P->def.epb1, P->def.overlap}, cyc);
+  const GmresResult gm = gpu_gmres(gpu_mesh, P->frame_scale, P->b, kc);
+  std::vector<double> zm(P->n);
+  gpu_mesh.apply(r.data(), zm.data());
+  bool same = gm.iterations == g.iterations && gm.x == g.x && zm == zg;
   auto ax = P->a_scaled.multiply(g.x);
   double s2 = 0;
   for (int i = 0; i < P->n; ++i) s2 += (P->b[i] - ax[i]) * (P->b[i] - ax[i]);
@@ -883,10 +932,11 @@ int cmd_gpu_adapter(const Args& a) {
   }
   std::printf("{\"case\": \"%s\", \"restart\": %d, \"vcycle_rel\": %.3e, \"ref_iterations\": %d, "
               "\"ref_converged\": %d, \"ref_relres\": %.6e, \"gpu_iterations\": %d, \"gpu_converged\": %d, "
-              "\"gpu_relres\": %.6e, \"singular_label\": \"%s\", \"expected_label\": \"%s\"}\n",
+              "\"gpu_relres\": %.6e, \"singular_label\": \"%s\", \"expected_label\": \"%s\", "
+              "\"device_sets_identical\": %d}\n",
               a.pos[1].c_str(), kc.restart, std::sqrt(num / den), ref.res.iterations, (int)ref.res.converged,
               ref.true_res / ref.res.history.front(), g.iterations, (int)g.converged,
-              std::sqrt(s2) / g.history.front(), label.c_str(), expected.c_str());
+              std::sqrt(s2) / g.history.front(), label.c_str(), expected.c_str(), (int)same);
   return 0;
 }
 #endif

@@ -12,6 +12,8 @@
 #include <memory>
 #include <type_traits>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <mutex>
 #include <cstdlib>
 #include <string>
@@ -31,6 +33,7 @@
 #include "sparse.cuh"
 #include "mr.cuh"
 #include "mult.cuh"
+#include "sets.cuh"
 
 namespace fsigpu {
 
@@ -178,8 +181,6 @@ struct Csr {
     cols = c;
     nnz = r ? p[r] : 0;
     require(nnz >= 0 && (r == 0 || p[0] == 0), "csr: bad row offsets");
-    for (int i = 0; i < r; ++i) require(p[i] <= p[i + 1], "csr: offsets not nondecreasing");
-    for (long long k = 0; k < nnz; ++k) require(ix[k] >= 0 && ix[k] < c, "csr: column range");
     ptr.upload(p, (size_t)r + 1, s);
     // padded by 4 entries (the paired-load kernels read 16-byte pairs)
     idx.alloc((size_t)nnz + 4);
@@ -195,7 +196,19 @@ struct Csr {
       h_idx.assign(ix, ix + nnz);
       h_val.assign(v, v + nnz);
     }
+    // offsets and column ranges checked on the device (host loops over
+    // ~1e8 entries took seconds at config 2)
+    int bad = 0;
+    if (r) {
+      DevBuf<int> flag(1);
+      flag.zero(s);
+      csr_check_kernel<<<ceil_div(r, 256), 256, 0, s>>>(r, c, nnz, ptr.p, idx.p, flag.p);
+      FSI_CHECK_LAUNCH();
+      FSI_CUDA(cudaMemcpyAsync(&bad, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    }
     FSI_CUDA(cudaStreamSynchronize(s));
+    require(!(bad & 1), "csr: offsets not nondecreasing");
+    require(!(bad & 2), "csr: column range");
   }
   // take ownership of device CSR arrays built on the GPU
   void adopt(int r, int c, DevBuf<int>&& p, DevBuf<int>&& ix, DevBuf<double>&& v) {
@@ -1112,12 +1125,69 @@ static void build_mult(Level& L, const fsigpu_level_desc& d, cudaStream_t s) {
   L.mult = true;
 }
 
+// AP = A diag(!cmask) P on the device; false if a row overflows the
+// per-CTA product buffer (then the caller runs the host loop)
+static bool build_ap_device(Level& L, cudaStream_t s) {
+  const int n = L.n;
+  DevBuf<int> cnt(n), flag(1);
+  DevBuf<long long> off(n + 1);
+  flag.zero(s);
+  ap_row_kernel<<<n, kApThreads, 0, s>>>(n, L.A.ptr.p, L.A.idx.p, L.A.val.p, L.cmask.p, L.P.ptr.p, L.P.idx.p,
+                                         L.P.val.p, 0, cnt.p, nullptr, nullptr, nullptr, flag.p);
+  FSI_CHECK_LAUNCH();
+  int of = 0;
+  FSI_CUDA(cudaMemcpyAsync(&of, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  FSI_CUDA(cudaStreamSynchronize(s));
+  if (of) return false;
+  std::vector<int> c = cnt.download(s);
+  std::vector<long long> o(n + 1, 0);
+  std::vector<int> p32(n + 1, 0);
+  for (int i = 0; i < n; ++i) o[i + 1] = o[i] + c[i];
+  require(o[n] < INT_MAX, "A*P: too many entries for int32 offsets");
+  for (int i = 0; i <= n; ++i) p32[i] = (int)o[i];
+  off.upload(o, s);
+  const long long nnz = std::max<long long>(o[n], 1);
+  DevBuf<int> ptr, idx(nnz);
+  DevBuf<double> val(nnz);
+  idx.zero(s);
+  val.zero(s);
+  ptr.upload(p32, s);
+  ap_row_kernel<<<n, kApThreads, 0, s>>>(n, L.A.ptr.p, L.A.idx.p, L.A.val.p, L.cmask.p, L.P.ptr.p, L.P.idx.p,
+                                         L.P.val.p, 1, nullptr, off.p, idx.p, val.p, flag.p);
+  FSI_CHECK_LAUNCH();
+  FSI_CUDA(cudaStreamSynchronize(s));
+  L.AP.adopt(n, L.nc, std::move(ptr), std::move(idx), std::move(val));
+  return true;
+}
+
+// FSIGPU_SETUP_TRACE=1: wall time of the setup phases on stderr
+struct SetupTrace {
+  const char* what;
+  int level;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  static bool on() {
+    static const bool v = [] {
+      const char* e = std::getenv("FSIGPU_SETUP_TRACE");
+      return e && e[0] == '1';
+    }();
+    return v;
+  }
+  SetupTrace(const char* w, int l) : what(w), level(l) {}
+  ~SetupTrace() {
+    if (!on()) return;
+    cudaDeviceSynchronize();
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::fprintf(stderr, "[fsigpu setup] L%d %-24s %9.1f ms\n", level, what, ms);
+  }
+};
+
 // Build one level from its descriptor (host arrays).
 static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t s, bool mult) {
   Level& L = g.lv[l];
   require(d.n > 0, "gmg: empty level");
   L.n = d.n;
   require(d.a_ptr && d.a_idx && d.a_val && d.row_mask && d.col_mask, "gmg: null level arrays");
+  std::unique_ptr<SetupTrace> tr(new SetupTrace("A, P, R upload", l));
   L.A.create(d.n, d.n, d.a_ptr, d.a_idx, d.a_val, s);
   // level operators (~65 entries per row) on HBM-bound levels: paired
   // 16-byte index/value loads, 4 pairs per lane (csr_pair_kernel). Cold
@@ -1156,8 +1226,10 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
     L.R.lpr = 8;
     L.R.unroll = 8;
   }
-  {
-    // AP_m = A * diag(!col_mask) * P (Gustavson, sorted rows)
+  tr.reset(new SetupTrace("A*P", l));
+  // AP_m = A * diag(!col_mask) * P on the device (ap_row_kernel); rows with
+  // more than kApCap products (not in the 2D Q2 hierarchies) use the host loop
+  if (!build_ap_device(L, s)) {
     std::vector<int> app(d.n + 1, 0), api;
     std::vector<double> apv, acc(d.nc, 0.0);
     std::vector<int> mark(d.nc, -1), touched;
@@ -1189,6 +1261,8 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
       apv.push_back(0.0);
     }
     L.AP.create(d.n, d.nc, app.data(), api.data(), apv.data(), s);
+  }
+  {
     // its P half already adds 2 loads per lane to each batch: on large
     // (HBM-bound) levels batches of 4 AP entries; on small (L2-resident)
     // ones half the lanes with batches of 8 (warm sweeps, tools/tune_spmv.py)
@@ -1236,6 +1310,7 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
     }
   }
   L.n_as1 = nb1;
+  tr.reset(new SetupTrace("blocks extract + LU", l));
   Blocks& B = L.blocks;
   // assembled and multiplicative smoothers build on the inverses
   B.mode = (g_default_mode == kModeLU && !mult) ? kModeLU : kModeInverse;
@@ -1257,6 +1332,7 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
     }
   }
   // inverse map position -> delta slots in block order (precond.cpp:52-55)
+  tr.reset(new SetupTrace("maps", l));
   std::vector<int> cnt(d.n + 1, 0);
   for (int p : pos) cnt[p + 1]++;
   for (int i = 0; i < d.n; ++i) cnt[i + 1] += cnt[i];
@@ -1291,6 +1367,7 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
       throw Error(FSIGPU_ERR_SINGULAR, "singular block: fs lumped mass row " + std::to_string(i));
     }
   FSI_CUDA(cudaStreamSynchronize(s));
+  tr.reset(new SetupTrace(mult ? "multicolour" : "assembled FS", l));
   if (mult)
     build_mult(L, d, s);
   else if (g_default_mode == kModeAssembled)
@@ -1300,6 +1377,7 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
 // Coarse operator: equilibrate (sparse_lu.cpp:104-121), Gauss-Jordan
 // inverse on the device, fold the scalings into the inverse.
 static void build_coarse(Gmg& g, const fsigpu_level_desc& d, cudaStream_t s) {
+  SetupTrace tr("coarse inverse", 0);
   const int n = d.n;
   std::vector<double> rs(n, 1.0), cs(n, 1.0), cm(n, 0.0);
   for (int i = 0; i < n; ++i) {
@@ -1312,28 +1390,29 @@ static void build_coarse(Gmg& g, const fsigpu_level_desc& d, cudaStream_t s) {
       cm[d.a_idx[k]] = std::max(cm[d.a_idx[k]], std::fabs(d.a_val[k]) * rs[i]);
   for (int j = 0; j < n; ++j)
     if (cm[j] > 0.0) cs[j] = 1.0 / cm[j];
-  std::vector<double> W((size_t)n * 2 * n, 0.0);
-  for (int i = 0; i < n; ++i)
-    for (int k = d.a_ptr[i]; k < d.a_ptr[i + 1]; ++k) {
-      const int j = d.a_idx[k];
-      W[(size_t)i * 2 * n + j] += d.a_val[k] * rs[i] * cs[j];
-    }
-  DevBuf<double> Wd, f, drs, dcs;
-  Wd.upload(W, s);
-  f.alloc(n);
+  // [diag(rs) A diag(cs) | I] built on the device from the level's CSR
+  const Csr& A0 = g.lv[0].A;
+  DevBuf<double> Wd((size_t)n * 2 * n), f(n), drs, dcs;
+  Wd.zero(s);
   drs.upload(rs, s);
   dcs.upload(cs, s);
-  DevBuf<int> fail(1);
+  DevBuf<int> fail(1), piv(n);
   fail.zero(s);
-  gj_init_kernel<<<ceil_div((long long)n * n, 256), 256, 0, s>>>(n, Wd.p);
+  gj_init_kernel<<<ceil_div(n, 256), 256, 0, s>>>(n, A0.ptr.p, A0.idx.p, A0.val.p, drs.p, dcs.p, Wd.p);
   for (int k = 0; k < n; ++k) {
-    gj_pivot_kernel<<<1, 1024, 0, s>>>(n, Wd.p, k, f.p, fail.p);
-    dim3 grid(ceil_div(2LL * n, 256), n);
+    gj_pivot_kernel<<<1, 1024, 0, s>>>(n, Wd.p, k, f.p, fail.p, piv.p);
+    dim3 grid(ceil_div((long long)n, 256), n);
     gj_eliminate_kernel<<<grid, 256, 0, s>>>(n, Wd.p, k, f.p);
   }
   FSI_CHECK_LAUNCH();
+  // the right half's columns, unpermuted: apply the swaps (k <-> piv[k]) in reverse
+  std::vector<int> pv = piv.download(s), col(n);
+  for (int j = 0; j < n; ++j) col[j] = j;
+  for (int k = n - 1; k >= 0; --k) std::swap(col[k], col[pv[k]]);
+  DevBuf<int> dcol;
+  dcol.upload(col, s);
   g.coarse_inv.alloc((size_t)n * n);
-  gj_extract_kernel<<<ceil_div((long long)n * n, 256), 256, 0, s>>>(n, Wd.p, drs.p, dcs.p, g.coarse_inv.p);
+  gj_extract_kernel<<<ceil_div((long long)n * n, 256), 256, 0, s>>>(n, Wd.p, dcol.p, drs.p, dcs.p, g.coarse_inv.p);
   FSI_CHECK_LAUNCH();
   int bad = 0;
   FSI_CUDA(cudaMemcpyAsync(&bad, fail.p, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1606,6 +1685,114 @@ struct Gmres {
 struct fsigpu_gmg_t {
   fsigpu::Gmg g;
 };
+struct fsigpu_sets_t {
+  std::vector<int> as1_ptr{0}, as1_idx, as2_ptr{0}, as2_idx;
+  std::vector<double> lumped;
+  std::vector<std::string> labels;  // AS1 then AS2 blocks
+};
+
+namespace fsigpu {
+
+// Device-side block-set construction (sets.cuh). Host side: the element
+// partition by region and the node -> element adjacency (index maps of the
+// mesh, O(elements)), the count scan, and the labels.
+struct SetBuilder {
+  const fsigpu_mesh_desc& m;
+  cudaStream_t s;
+  std::vector<int> solid, fluid;
+  DevBuf<int> d_solid, d_fluid, en, ne_ptr, ne_idx, dpos, upos, ppos, cnt, out, overflow;
+  DevBuf<long long> off;
+  DevBuf<unsigned char> esol, nsol, drop, g1e;
+  SetBuilder(const fsigpu_mesh_desc& mesh, int n_frame, cudaStream_t st) : m(mesh), s(st) {
+    require(m.n_elements >= 0 && m.n_nodes >= 0 && m.nodes_per_element >= 1 && m.nodes_per_element <= 27 &&
+                m.dim >= 1 && m.dim <= 3 && m.p_per_element >= 0 && m.p_per_element <= 4,
+            "sets: bad mesh sizes");
+    require(m.element_nodes && m.elem_solid && m.node_solid && m.d_pos && m.u_pos && m.p_pos, "sets: null mesh arrays");
+    const int E = m.n_elements, N = m.n_nodes, npe = m.nodes_per_element;
+    for (int e = 0; e < E; ++e) (m.elem_solid[e] ? solid : fluid).push_back(e);
+    std::vector<int> np(N + 1, 0), ni((size_t)E * npe);
+    for (long long q = 0; q < (long long)E * npe; ++q) {
+      const int node = m.element_nodes[q];
+      require(node >= 0 && node < N, "sets: element node out of range");
+      np[node + 1]++;
+    }
+    for (int i = 0; i < N; ++i) np[i + 1] += np[i];
+    {
+      std::vector<int> nx(np.begin(), np.end() - 1);
+      for (int e = 0; e < E; ++e)
+        for (int a = 0; a < npe; ++a) ni[nx[m.element_nodes[(size_t)e * npe + a]]++] = e;
+    }
+    for (long long q = 0; q < (long long)N * m.dim; ++q)
+      require(m.d_pos[q] >= 0 && m.d_pos[q] < n_frame && m.u_pos[q] >= 0 && m.u_pos[q] < n_frame,
+              "sets: d/u position out of the frame");
+    for (long long q = 0; q < (long long)E * m.p_per_element; ++q)
+      require(m.p_pos[q] >= 0 && m.p_pos[q] < n_frame, "sets: p position out of the frame");
+    auto up = [&](DevBuf<int>& d, const std::vector<int>& v) { d.upload(v.empty() ? std::vector<int>{0} : v, s); };
+    up(d_solid, solid);
+    up(d_fluid, fluid);
+    en.upload(m.element_nodes, (size_t)std::max<long long>((long long)E * npe, 1), s);
+    up(ne_ptr, np);
+    up(ne_idx, ni);
+    dpos.upload(m.d_pos, (size_t)std::max(N * m.dim, 1), s);
+    upos.upload(m.u_pos, (size_t)std::max(N * m.dim, 1), s);
+    ppos.upload(m.p_pos, (size_t)std::max(E * m.p_per_element, 1), s);
+    esol.upload(m.elem_solid, (size_t)std::max(E, 1), s);
+    nsol.upload(m.node_solid, (size_t)std::max(N, 1), s);
+    if (m.drop) drop.upload(m.drop, (size_t)std::max(n_frame, 1), s);
+    overflow.alloc(1);
+    overflow.zero(s);
+  }
+  // sets of one kind over `list` (element chunks of epb) appended to ptr/idx
+  void run(int kind, const std::vector<int>& list, const DevBuf<int>& dlist, int epb, int overlap, int g1,
+           std::vector<int>& ptr, std::vector<int>& idx) {
+    const int np = list.empty() ? 0 : ceil_div((long long)list.size(), epb);
+    if (np == 0) return;
+    SetArgs a{};
+    a.kind = kind;
+    a.epb = epb;
+    a.overlap = overlap;
+    a.n_list = (int)list.size();
+    a.npe = m.nodes_per_element;
+    a.dim = m.dim;
+    a.ppe = m.p_per_element;
+    a.g1 = g1;
+    a.list = dlist.p;
+    a.en = en.p;
+    a.elem_solid = esol.p;
+    a.node_solid = nsol.p;
+    a.ne_ptr = ne_ptr.p;
+    a.ne_idx = ne_idx.p;
+    a.d_pos = dpos.p;
+    a.u_pos = upos.p;
+    a.p_pos = ppos.p;
+    a.drop = drop.n ? drop.p : nullptr;
+    a.g1_empty = g1e.n ? g1e.p : nullptr;
+    a.overflow = overflow.p;
+    cnt.alloc(np);
+    a.count = cnt.p;
+    set_patch_kernel<<<np, kSetThreads, 0, s>>>(a, 0);
+    FSI_CHECK_LAUNCH();
+    std::vector<int> c = cnt.download(s);
+    int of = 0;
+    FSI_CUDA(cudaMemcpy(&of, overflow.p, sizeof(int), cudaMemcpyDeviceToHost));
+    require(!of, "sets: a patch exceeds the per-CTA capacity (4096 dof positions, 1024 elements)");
+    std::vector<long long> o(np + 1, 0);
+    for (int q = 0; q < np; ++q) o[q + 1] = o[q] + c[q];
+    require(o[np] < INT_MAX, "sets: too many positions");
+    off.upload(o, s);
+    out.alloc((size_t)std::max<long long>(o[np], 1));
+    a.off = off.p;
+    a.out = out.p;
+    set_patch_kernel<<<np, kSetThreads, 0, s>>>(a, 1);
+    FSI_CHECK_LAUNCH();
+    std::vector<int> v = out.download(s);
+    const int base = (int)idx.size();
+    idx.insert(idx.end(), v.begin(), v.begin() + o[np]);
+    for (int q = 0; q < np; ++q) ptr.push_back(base + (int)o[q + 1]);
+  }
+};
+
+}  // namespace fsigpu
 struct fsigpu_gmres_t {
   fsigpu::Gmres k;
 };
@@ -2291,6 +2478,110 @@ void fsigpu_gmres_destroy(fsigpu_gmres s) {
   cudaDeviceSynchronize();
   delete s;
 }
+
+// ---- block sets built on the device (sets.cuh)
+int fsigpu_fs_sets_build(const fsigpu_level_desc* lv, const fsigpu_mesh_desc* mesh, int epb_as1, int epb_as2,
+                         int overlap_layers, fsigpu_sets* out) {
+  g_bad_block = -1;
+  g_bad_level = -1;
+  return guarded([&] {
+    require(lv != nullptr && mesh != nullptr && out != nullptr, "sets: null args");
+    require(epb_as1 >= 1 && epb_as2 >= 1 && overlap_layers >= 0, "fieldsplit: elems_per_block must be >= 1");
+    const fsigpu_level_desc& d = *lv;
+    require(d.n > 0 && d.a_ptr && d.a_idx && d.a_val, "sets: level matrix missing");
+    require(d.g1 >= 0 && d.n_us >= 0 && d.g1 + d.n_us <= d.n, "fs: bad group sizes");
+    cudaStream_t s = new_stream();
+    struct StreamGuard {
+      cudaStream_t s;
+      ~StreamGuard() { cudaStreamDestroy(s); }
+    } sg{s};
+    auto h = std::make_unique<fsigpu_sets_t>();
+    SetBuilder B(*mesh, d.n, s);
+    Csr A;
+    A.create(d.n, d.n, d.a_ptr, d.a_idx, d.a_val, s);
+    B.g1e.alloc((size_t)std::max(d.g1, 1));
+    if (d.g1) {
+      g1_empty_kernel<<<ceil_div(d.g1, 256), 256, 0, s>>>(d.g1, A.ptr.p, A.idx.p, A.val.p, B.g1e.p);
+      FSI_CHECK_LAUNCH();
+    }
+    // AS1: solid [d^s, p^s] chunks, then overlapping fluid d^f chunks
+    B.run(kSetSolidDp, B.solid, B.d_solid, epb_as1, 0, d.g1, h->as1_ptr, h->as1_idx);
+    for (size_t st = 0; st < B.solid.size(); st += epb_as1) h->labels.push_back("fs-solid-dp-" + std::to_string(st));
+    B.run(kSetFluidD, B.fluid, B.d_fluid, epb_as1, overlap_layers, d.g1, h->as1_ptr, h->as1_idx);
+    for (size_t st = 0; st < B.fluid.size(); st += epb_as1) h->labels.push_back("fs-fluid-d-" + std::to_string(st));
+    // AS2: fluid [u^f, p^f] chunks, group-2 local positions
+    B.run(kSetFluidUp, B.fluid, B.d_fluid, epb_as2, 0, d.g1, h->as2_ptr, h->as2_idx);
+    for (size_t st = 0; st < B.fluid.size(); st += epb_as2) h->labels.push_back("fs-fluid-up-" + std::to_string(st));
+    // lumped u^s mass
+    h->lumped.assign(d.n_us, 1.0);
+    if (d.n_us) {
+      DevBuf<double> lm(d.n_us);
+      DevBuf<int> bad(1);
+      const int big = INT_MAX;
+      FSI_CUDA(cudaMemcpyAsync(bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+      lumped_kernel<<<ceil_div(d.n_us, 256), 256, 0, s>>>(d.g1, d.n_us, A.ptr.p, A.idx.p, A.val.p, lm.p, bad.p);
+      FSI_CHECK_LAUNCH();
+      h->lumped = lm.download(s);
+      const int b = bad.download(s)[0];
+      if (b != INT_MAX) throw Error(FSIGPU_ERR_SINGULAR, "singular block: fs lumped mass row " + std::to_string(b));
+    }
+    FSI_CUDA(cudaStreamSynchronize(s));
+    *out = h.release();
+  });
+}
+
+int fsigpu_vanka_sets_build(int n, const fsigpu_mesh_desc* mesh, int epb, fsigpu_sets* out) {
+  return guarded([&] {
+    require(mesh != nullptr && out != nullptr && n > 0, "sets: null args");
+    require(epb >= 1, "vanka: elems_per_block must be >= 1");
+    cudaStream_t s = new_stream();
+    struct StreamGuard {
+      cudaStream_t s;
+      ~StreamGuard() { cudaStreamDestroy(s); }
+    } sg{s};
+    auto h = std::make_unique<fsigpu_sets_t>();
+    SetBuilder B(*mesh, n, s);
+    B.run(kSetVankaSolid, B.solid, B.d_solid, epb, 0, n, h->as1_ptr, h->as1_idx);
+    int k = 0;
+    for (size_t st = 0; st < B.solid.size(); st += epb) h->labels.push_back("vanka-solid-" + std::to_string(k++));
+    B.run(kSetVankaFluid, B.fluid, B.d_fluid, epb, 0, n, h->as1_ptr, h->as1_idx);
+    for (size_t st = 0; st < B.fluid.size(); st += epb) h->labels.push_back("vanka-fluid-" + std::to_string(k++));
+    FSI_CUDA(cudaStreamSynchronize(s));
+    *out = h.release();
+  });
+}
+
+int fsigpu_sets_counts(fsigpu_sets h, int* as1_n, int* as1_len, int* as2_n, int* as2_len, int* n_us) {
+  return guarded([&] {
+    require(h != nullptr, "sets: null");
+    if (as1_n) *as1_n = (int)h->as1_ptr.size() - 1;
+    if (as1_len) *as1_len = (int)h->as1_idx.size();
+    if (as2_n) *as2_n = (int)h->as2_ptr.size() - 1;
+    if (as2_len) *as2_len = (int)h->as2_idx.size();
+    if (n_us) *n_us = (int)h->lumped.size();
+  });
+}
+
+int fsigpu_sets_copy(fsigpu_sets h, int* as1_ptr, int* as1_idx, int* as2_ptr, int* as2_idx, double* lumped) {
+  return guarded([&] {
+    require(h != nullptr, "sets: null");
+    auto cp = [](const auto& v, auto* dst) {
+      if (dst && !v.empty()) std::memcpy(dst, v.data(), sizeof(v[0]) * v.size());
+    };
+    cp(h->as1_ptr, as1_ptr);
+    cp(h->as1_idx, as1_idx);
+    cp(h->as2_ptr, as2_ptr);
+    cp(h->as2_idx, as2_idx);
+    cp(h->lumped, lumped);
+  });
+}
+
+const char* fsigpu_sets_label(fsigpu_sets h, int block) {
+  if (!h || block < 0 || block >= (int)h->labels.size()) return "";
+  return h->labels[block].c_str();
+}
+
+void fsigpu_sets_destroy(fsigpu_sets h) { delete h; }
 
 // ---- profiler
 int fsigpu_profile_enable(int enable) {

@@ -293,10 +293,17 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(int n, const double*
 }
 
 // ---- setup: Gauss-Jordan inverse with partial pivoting on W = [A | I] ----
-// Step k, single CTA: pivot search in column k, row swap, pivot-row scaling,
-// and a copy of column k (the elimination factors) into f.
+// Row k's pivot swap moves only the left columns [k, n) and the right
+// columns [n, n+k) (the dense part); the unit entries of the not yet
+// eliminated rows stay in place, which is the row swap followed by a swap of
+// right-half columns n+k <-> n+p. So at step k the live columns are the
+// contiguous range [k+1, n+k] (half of [A | I]), and the inverse is the right
+// half with its columns unpermuted at the end (gj_extract_kernel, perm from
+// the host).
+// Step k, single CTA: pivot search in column k, the swap, pivot-row scaling
+// of [k+1, n+k], and the elimination factors f = W[:, k] (f[k] = 0).
 __global__ void gj_pivot_kernel(int n, double* __restrict__ W, int k, double* __restrict__ f,
-                                int* __restrict__ fail) {
+                                int* __restrict__ fail, int* __restrict__ piv) {
   __shared__ double sb[32];
   __shared__ int si[32];
   __shared__ int s_p;
@@ -332,48 +339,57 @@ __global__ void gj_pivot_kernel(int n, double* __restrict__ W, int k, double* __
       }
     if (!(best > 1e-14) || bi >= n) *fail = 1;  // equilibrated: entries <= 1
     s_p = bi < n ? bi : k;
+    piv[k] = s_p;
   }
   __syncthreads();
   const int p = s_p;
   if (p != k)
-    for (int j = tid; j < ld; j += blockDim.x) {
+    for (int j = k + tid; j < n + k; j += blockDim.x) {
       const double t = W[(size_t)k * ld + j];
       W[(size_t)k * ld + j] = W[(size_t)p * ld + j];
       W[(size_t)p * ld + j] = t;
     }
   __syncthreads();
   const double inv = 1.0 / W[(size_t)k * ld + k];
-  __syncthreads();
-  for (int j = tid; j < ld; j += blockDim.x) W[(size_t)k * ld + j] *= inv;
+  for (int j = k + 1 + tid; j <= n + k; j += blockDim.x) W[(size_t)k * ld + j] *= inv;
   for (int i = tid; i < n; i += blockDim.x) f[i] = (i == k) ? 0.0 : W[(size_t)i * ld + k];
 }
 
+// rows i != k: W[i, j] -= f_i W[k, j] for the live columns j in [k+1, n+k]
 __global__ void gj_eliminate_kernel(int n, double* __restrict__ W, int k,
                                     const double* __restrict__ f) {
   const int ld = 2 * n;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = k + 1 + blockIdx.x * blockDim.x + threadIdx.x;
   const int i = blockIdx.y;
-  if (j >= ld) return;
+  if (j > n + k) return;
   const double fi = f[i];
   if (fi == 0.0) return;
   W[(size_t)i * ld + j] -= fi * W[(size_t)k * ld + j];
 }
 
-// M[i][j] = cs_i * W[i][n+j] * rs_j  (A^{-1} = Dc Ahat^{-1} Dr)
-__global__ void gj_extract_kernel(int n, const double* __restrict__ W,
+// M[i][j] = cs_i * W[i][n + col[j]] * rs_j  (A^{-1} = Dc Ahat^{-1} Dr, right
+// half unpermuted by col)
+__global__ void gj_extract_kernel(int n, const double* __restrict__ W, const int* __restrict__ col,
                                   const double* __restrict__ rs, const double* __restrict__ cs,
                                   double* __restrict__ M) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (long long)n * n) return;
   const int i = (int)(e / n), j = (int)(e % n);
-  M[e] = cs[i] * W[(size_t)i * 2 * n + n + j] * rs[j];
+  M[e] = cs[i] * W[(size_t)i * 2 * n + n + col[j]] * rs[j];
 }
 
-__global__ void gj_init_kernel(int n, double* __restrict__ W) {
-  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (long long)n * n) return;
-  const int i = (int)(e / n), j = (int)(e % n);
-  W[(size_t)i * 2 * n + n + j] = (i == j) ? 1.0 : 0.0;
+// W = [diag(rs) A diag(cs) | I], W zeroed before
+__global__ void gj_init_kernel(int n, const int* __restrict__ ptr, const int* __restrict__ idx,
+                               const double* __restrict__ val, const double* __restrict__ rs,
+                               const double* __restrict__ cs, double* __restrict__ W) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double* Wi = W + (size_t)i * 2 * n;
+  for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+    const int j = idx[k];
+    Wi[j] += val[k] * rs[i] * cs[j];
+  }
+  Wi[n + i] = 1.0;
 }
 
 }  // namespace fsigpu
@@ -650,5 +666,144 @@ __global__ void coo_cols_kernel(long long nnz, const unsigned long long* __restr
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= nnz) return;
   cols[e] = (int)(keys[e] & 0xffffffffull);
+}
+}  // namespace fsigpu
+
+namespace fsigpu {
+// ---- setup: A*P on the device ---------------------------------------------
+// AP_m = A * diag(!col_mask) * P, one CTA per row: the row's products
+// (c, a_ik * p_kc) are collected in traversal order (k ascending, then the P
+// row), sorted by (column, traversal index) and summed per column in
+// traversal order with separate rounded mul/add: the host Gustavson loop's
+// exact arithmetic (acc += a * p from 0), so AP is bit-identical to it.
+constexpr int kApThreads = 128;
+constexpr int kApCap = 2048;  // products per row (Q2: <= 65 x 9)
+
+// exclusive scan of v[0..n) in shared memory (any n), block-wide; returns the total
+__device__ __forceinline__ int ap_block_scan(int* v, int n, int* part) {
+  const int t = threadIdx.x;
+  const int per = (n + kApThreads - 1) / kApThreads;
+  const int b = t * per, e = min(n, b + per);
+  int s = 0;
+  for (int i = b; i < e; ++i) s += v[i];
+  part[t] = s;
+  __syncthreads();
+  if (t == 0) {
+    int acc = 0;
+    for (int q = 0; q < kApThreads; ++q) {
+      const int x = part[q];
+      part[q] = acc;
+      acc += x;
+    }
+    part[kApThreads] = acc;
+  }
+  __syncthreads();
+  int acc = part[t];
+  for (int i = b; i < e; ++i) {
+    const int x = v[i];
+    v[i] = acc;
+    acc += x;
+  }
+  __syncthreads();
+  return part[kApThreads];
+}
+
+__global__ void __launch_bounds__(kApThreads) ap_row_kernel(int n, const int* __restrict__ ap, const int* __restrict__ ai,
+                                                            const double* __restrict__ av,
+                                                            const unsigned char* __restrict__ cmask,
+                                                            const int* __restrict__ pp, const int* __restrict__ pi,
+                                                            const double* __restrict__ pv, int pass,
+                                                            int* __restrict__ count, const long long* __restrict__ off,
+                                                            int* __restrict__ oi, double* __restrict__ ov,
+                                                            int* overflow) {
+  __shared__ unsigned long long key[kApCap];
+  __shared__ double val[kApCap];
+  __shared__ int len[kApCap];
+  __shared__ int part[kApThreads + 1];
+  const int row = blockIdx.x;
+  const int t = threadIdx.x;
+  const int k0 = ap[row], k1 = ap[row + 1];
+  const int na = k1 - k0;
+  if (na > kApCap) {
+    if (t == 0) atomicExch(overflow, 1);
+    return;
+  }
+  // products in traversal order (k ascending, then the P row): slot base of
+  // A entry k = exclusive prefix of the P row lengths of the unmasked columns
+  for (int q = t; q < na; q += kApThreads) {
+    const int c = ai[k0 + q];
+    len[q] = cmask[c] ? 0 : pp[c + 1] - pp[c];
+  }
+  __syncthreads();
+  const int np = ap_block_scan(len, na, part);
+  if (np > kApCap) {
+    if (t == 0) atomicExch(overflow, 1);
+    return;
+  }
+  for (int q = t; q < na; q += kApThreads) {
+    const int c = ai[k0 + q];
+    if (cmask[c]) continue;
+    const double a = av[k0 + q];
+    int slot = len[q];
+    for (int r = pp[c]; r < pp[c + 1]; ++r, ++slot) {
+      key[slot] = ((unsigned long long)(unsigned)pi[r] << 32) | (unsigned)slot;
+      val[slot] = __dmul_rn(a, pv[r]);
+    }
+  }
+  int n2 = 1;
+  while (n2 < np) n2 <<= 1;
+  for (int i = np + t; i < n2; i += kApThreads) key[i] = ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= n2; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = t; i < n2; i += kApThreads) {
+        const int ij = i ^ j;
+        if (ij > i) {
+          const bool up = (i & k) == 0;
+          const unsigned long long x = key[i], y = key[ij];
+          if ((x > y) == up) {  // values stay put: the slot is the key's low word
+            key[i] = y;
+            key[ij] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  // column runs: head flags -> their output index (exclusive scan), then
+  // each head sums its run in traversal order
+  for (int i = t; i < np; i += kApThreads)
+    len[i] = (i == 0 || (key[i] >> 32) != (key[i - 1] >> 32)) ? 1 : 0;
+  __syncthreads();
+  const int nu = ap_block_scan(len, np, part);
+  if (!pass) {
+    if (t == 0) count[row] = nu;
+    return;
+  }
+  const long long o = off[row];
+  for (int i = t; i < np; i += kApThreads) {
+    const unsigned col = (unsigned)(key[i] >> 32);
+    const bool head = i == 0 || (unsigned)(key[i - 1] >> 32) != col;
+    if (!head) continue;
+    double acc = 0.0;
+    for (int j = i; j < np && (unsigned)(key[j] >> 32) == col; ++j) acc = __dadd_rn(acc, val[(unsigned)key[j]]);
+    oi[o + len[i]] = (int)col;
+    ov[o + len[i]] = acc;
+  }
+}
+
+// CSR sanity on the device (the host loops over ~1e8 entries took seconds):
+// offsets nondecreasing from 0, columns in [0, cols)
+__global__ void csr_check_kernel(int rows, int cols, long long nnz, const int* __restrict__ ptr,
+                                 const int* __restrict__ idx, int* bad) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < rows) {
+    const int a = ptr[i], b = ptr[i + 1];
+    if (a > b || (i == 0 && a != 0) || a < 0 || b > nnz) atomicOr(bad, 1);
+    for (int k = max(a, 0); k < b && k < nnz; ++k)
+      if (idx[k] < 0 || idx[k] >= cols) {
+        atomicOr(bad, 2);
+        break;
+      }
+  }
 }
 }  // namespace fsigpu

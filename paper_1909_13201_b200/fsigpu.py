@@ -31,7 +31,7 @@ from typing import List, Optional, Sequence
 
 import numpy as np
 
-from .problem import Csr, Level, level_descs
+from .problem import BlockSets, Csr, Level, level_descs, mesh_desc
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # FSIGPU_LIB: an alternative in-tree build of the same library (A/B timing
@@ -115,6 +115,13 @@ def lib():
             "fsigpu_gmres_solve_dev": ([vp, vp, vp, ip, d, d, vp, C.POINTER(GmresResultC)], ip),
             "fsigpu_gmres_set_graphs": ([vp, ip], ip),
             "fsigpu_gmres_destroy": ([vp], None),
+            "fsigpu_fs_sets_build": ([vp, vp, ip, ip, ip, C.POINTER(vp)], ip),
+            "fsigpu_vanka_sets_build": ([ip, vp, ip, C.POINTER(vp)], ip),
+            "fsigpu_sets_counts": ([vp, C.POINTER(ip), C.POINTER(ip), C.POINTER(ip), C.POINTER(ip),
+                                    C.POINTER(ip)], ip),
+            "fsigpu_sets_copy": ([vp, vp, vp, vp, vp, vp], ip),
+            "fsigpu_sets_label": ([vp, ip], C.c_char_p),
+            "fsigpu_sets_destroy": ([vp], None),
             "fsigpu_profile_enable": ([ip], ip),
             "fsigpu_profile_read": ([vp, vp, vp], ip),
             "fsigpu_profile_read_level": ([ip, ip, vp, vp, vp], ip),
@@ -434,6 +441,47 @@ class GmresSolver:
         if getattr(self, "h", None) and _lib is not None:
             _lib.fsigpu_gmres_destroy(self.h)
             self.h = None
+
+
+def build_block_sets(level: Level, epb_as1: int = 0, epb_as2: int = 0, overlap: int = -1,
+                     vanka: bool = False):
+    """The level's Schwarz block sets built on the device from its mesh-side
+    index maps (fsigpu_fs_sets_build / fsigpu_vanka_sets_build): returns a copy
+    of the level with as1/as2, lumped and labels replaced (FsPreconditioner's
+    sets, precond.cpp:119-269, or the Vanka sets, ordering.cpp:77-115)."""
+    import copy
+    init()
+    m = level.mesh
+    if m is None:
+        raise ValueError("level has no mesh maps")
+    epb1 = epb_as1 or int(m["epb_as1"][0])
+    epb2 = epb_as2 or int(m["epb_as2"][0])
+    ov = overlap if overlap >= 0 else int(m["overlap"][0])
+    md = mesh_desc(m)
+    h = C.c_void_p()
+    if vanka:
+        _check(lib().fsigpu_vanka_sets_build(level.n, C.byref(md), epb1, C.byref(h)))
+    else:
+        desc = level_descs([level, level])  # entry 1: a smoothed level (g1, n_us filled)
+        _check(lib().fsigpu_fs_sets_build(C.byref(desc[1]), C.byref(md), epb1, epb2, ov, C.byref(h)))
+    try:
+        n1, l1, n2, l2, nus = (C.c_int() for _ in range(5))
+        _check(lib().fsigpu_sets_counts(h, C.byref(n1), C.byref(l1), C.byref(n2), C.byref(l2), C.byref(nus)))
+        p1, i1 = np.zeros(n1.value + 1, np.int32), np.zeros(max(l1.value, 1), np.int32)
+        p2, i2 = np.zeros(n2.value + 1, np.int32), np.zeros(max(l2.value, 1), np.int32)
+        lm = np.zeros(max(nus.value, 1))
+        _check(lib().fsigpu_sets_copy(h, p1.ctypes.data, i1.ctypes.data, p2.ctypes.data, i2.ctypes.data,
+                                      lm.ctypes.data))
+        labels = [lib().fsigpu_sets_label(h, b).decode() for b in range(n1.value + n2.value)]
+    finally:
+        lib().fsigpu_sets_destroy(h)
+    out = copy.copy(level)
+    out.as1 = BlockSets(p1, i1[:l1.value].copy())
+    out.as2 = BlockSets(p2, i2[:l2.value].copy())
+    if not vanka:
+        out.lumped = lm[:nus.value].copy()
+    out.labels = labels
+    return out
 
 
 MODE_LU, MODE_INVERSE, MODE_ASSEMBLED = 0, 1, 2

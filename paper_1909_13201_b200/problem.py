@@ -71,6 +71,8 @@ class Level:
     as1: Optional[BlockSets] = None
     as2: Optional[BlockSets] = None
     labels: Optional[List[str]] = None  # reference IndexSet labels, AS1 then AS2 blocks
+    # mesh-side index maps of the block construction (fsigpu_mesh_desc), if exported
+    mesh: Optional[Dict[str, np.ndarray]] = None
 
 
 @dataclass
@@ -106,6 +108,8 @@ def load_case(path: str, name: str = "") -> Problem:
             if p + "/as1/labels" in a:
                 lv.labels = [t for k in ("as1", "as2")
                              for t in bytes(a[f"{p}/{k}/labels"]).decode().split("\n")[:-1]]
+        if p + "/mesh/element_nodes" in a:
+            lv.mesh = {k[len(p) + 6:]: v for k, v in a.items() if k.startswith(p + "/mesh/")}
         levels.append(lv)
     golden = {k: v for k, v in a.items() if k.startswith(("golden/", "gmres_", "setup/"))}
     return Problem(name=name or path, levels=levels, frame_scale=a["frame_scale"].astype(np.float64),
@@ -127,6 +131,29 @@ class LevelDesc(C.Structure):
         ("as1_n", C.c_int), ("as1_ptr", C.c_void_p), ("as1_idx", C.c_void_p),
         ("as2_n", C.c_int), ("as2_ptr", C.c_void_p), ("as2_idx", C.c_void_p),
     ]
+
+
+class MeshDesc(C.Structure):
+    """C layout of ``fsigpu_mesh_desc`` (include/fsigpu.h)."""
+    _fields_ = [
+        ("n_elements", C.c_int), ("n_nodes", C.c_int), ("nodes_per_element", C.c_int),
+        ("dim", C.c_int), ("p_per_element", C.c_int),
+        ("element_nodes", C.c_void_p), ("elem_solid", C.c_void_p), ("node_solid", C.c_void_p),
+        ("d_pos", C.c_void_p), ("u_pos", C.c_void_p), ("p_pos", C.c_void_p), ("drop", C.c_void_p),
+    ]
+
+
+def mesh_desc(m: Dict[str, np.ndarray], npe: int = 9, dim: int = 2, ppe: int = 3) -> MeshDesc:
+    """MeshDesc over the (kept-alive) arrays of an exported level mesh."""
+    d = MeshDesc()
+    d.n_elements = len(m["elem_solid"])
+    d.n_nodes = len(m["node_solid"])
+    d.nodes_per_element, d.dim, d.p_per_element = npe, dim, ppe
+    d.element_nodes, d.elem_solid, d.node_solid = (m["element_nodes"].ctypes.data, m["elem_solid"].ctypes.data,
+                                                   m["node_solid"].ctypes.data)
+    d.d_pos, d.u_pos, d.p_pos = m["d_pos"].ctypes.data, m["u_pos"].ctypes.data, m["p_pos"].ctypes.data
+    d.drop = m["drop"].ctypes.data if "drop" in m else None
+    return d
 
 
 def _p(a: Optional[np.ndarray]):

@@ -290,6 +290,8 @@ def test_cpp_adapter_linked_against_reference(tmp_path):
     assert abs(r["gpu_iterations"] - r["ref_iterations"]) <= 1, r
     assert abs(r["gpu_relres"] - r["ref_relres"]) <= 1e-8, r
     assert r["singular_label"] == r["expected_label"] and r["singular_label"].startswith("fs-fluid-up-"), r
+    # GpuGmg built without the reference FsPreconditioner (sets on the GPU)
+    assert r["device_sets_identical"] == 1, r
 
 
 # ---------------------------------------------------------------- more cases
@@ -574,6 +576,8 @@ def test_cfg2_parity(cfg2):
     converges (cfg2l4: 309 its) iterations within +-1 and the final relative
     residual within 1e-8; the iterate's strided sample within 1e-5."""
     P, gold = cfg2
+    if P.levels[1].mesh is not None:  # the block sets built on the device equal the exported ones
+        _check_device_sets(P, False)
     ck = _system_checksums(P)
     assert np.allclose(ck, gold["system_checksums"], rtol=1e-13, atol=0), (ck, gold["system_checksums"])
     G = fsigpu.GmgPreconditioner(P.levels)
@@ -616,6 +620,49 @@ def test_as_smoother_cfg0(cfg0_as):
     assert res.converged
     assert abs(res.iterations - int(g["gmres_add/iterations"][0])) <= 1
     assert rel(res.x, g["gmres_add/x"]) <= 1e-6
+
+
+# ---------------------------------------------------------------- block sets on the device
+def _check_device_sets(P, vanka):
+    for l in range(1, len(P.levels)):
+        lv = P.levels[l]
+        d = fsigpu.build_block_sets(lv, vanka=vanka)
+        assert np.array_equal(d.as1.ptr, lv.as1.ptr) and np.array_equal(d.as1.idx, lv.as1.idx), l
+        assert np.array_equal(d.as2.ptr, lv.as2.ptr) and np.array_equal(d.as2.idx, lv.as2.idx), l
+        assert d.labels == lv.labels, l
+        if not vanka:
+            assert np.array_equal(d.lumped, lv.lumped), l
+    return [P.levels[0]] + [fsigpu.build_block_sets(lv, vanka=vanka) for lv in P.levels[1:]]
+
+
+@pytest.mark.parametrize("case,vanka", [("chan", False), ("chan_as", True), ("cfg0", False), ("cfg0_as", True)])
+def test_block_sets_built_on_device(case, vanka, request):
+    """FsPreconditioner's field-split sets (precond.cpp:119-269: solid
+    [d^s,p^s], overlapping fluid d^f, fluid [u^f,p^f]; constrained and empty
+    group-1 rows dropped), the lumped u^s mass (:231-245) and the Vanka sets
+    (ordering.cpp:77-115 as AsPreconditioner maps them), built on the device
+    from the mesh maps, equal the reference's exactly, labels included; a
+    hierarchy built on them solves bit-identically."""
+    P = request.getfixturevalue(case)
+    levels = _check_device_sets(P, vanka)
+    a = fsigpu.gmres(fsigpu.GmgPreconditioner(levels), P.frame_scale, P.b,
+                     fsigpu.KrylovConfig(restart=30, max_iters=200, rel_tol=1e-8, abs_tol=1e-300))
+    b = fsigpu.gmres(fsigpu.GmgPreconditioner(P.levels), P.frame_scale, P.b,
+                     fsigpu.KrylovConfig(restart=30, max_iters=200, rel_tol=1e-8, abs_tol=1e-300))
+    assert a.iterations == b.iterations and np.array_equal(a.x, b.x)
+
+
+def test_block_sets_errors(chan):
+    import copy
+    lv = chan.levels[-1]
+    bad = copy.deepcopy(lv)
+    r = bad.g1  # first u^s row: make its A_g2 row sum negative
+    bad.A.val[bad.A.ptr[r]:bad.A.ptr[r + 1]] *= -1.0
+    with pytest.raises(fsigpu.SingularBlockError) as e:
+        fsigpu.build_block_sets(bad)
+    assert e.value.label.startswith("fs lumped mass row")
+    with pytest.raises(ValueError):
+        fsigpu.build_block_sets(lv, epb_as1=-1)
 
 
 # ---------------------------------------------------------------- multiplicative FS
