@@ -500,6 +500,8 @@ def run_ours(args, ws, rank, local):
         out["as_microbench"] = as_microbench(fsigpu, torch, hbm_peak, cpu=not args.no_cpu_baseline)
     if rank == 0 and args.config == "cfg0" and args.smoother == "fs":
         out["multiplicative_fs"] = mult_time_to_solution(fsigpu, torch, P, steps=max(3, args.steps // 2))
+    if rank == 0 and args.config == "cfg0" and not args.no_config34:
+        out.update(config34_bench(fsigpu, torch, hbm_peak))
     if rank == 0 and args.config == "cfg0" and not args.no_config2:
         del S, S_prof, G
         torch.cuda.empty_cache()
@@ -607,6 +609,100 @@ def config2_bench(fsigpu, torch, hbm_peak, steps=3, max_iters=60):
     return out
 
 
+WORKLOAD_V3 = ("config3 (3D valve-like FSI, harness-generated: Q2 hexes + P1disc pressure, 4^3 -> 16^3, 3 GMG "
+               "levels, 232,006 dofs, two leaflet slabs), FS [d | u,p] with 2x2x2-element patches, FGMRES(30) rtol 1e-10")
+WORKLOAD_V3DD = ("config4 (the same 3D system), pure DD: AS over 2x2x2-element Vanka patches of all fields jointly "
+                 "(blocks up to 782 dofs), FGMRES(30) rtol 1e-10")
+
+
+def fp64_peak():
+    """Measured fp64 non-fused mul+sub peak (the LU's rounded a - l*u) from
+    profiles/r01_fp64_peak.json, else the nominal 37 TFLOP/s."""
+    p = os.path.join(ROOT, "profiles", "r01_fp64_peak.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        for k in ("fp64_mul_sub_tflops",):
+            if k in d:
+                return float(d[k]), "measured (profiles/r01_fp64_peak.json)"
+    except (OSError, ValueError):
+        pass
+    return 35.5, "measured in round 1 (DMUL+DADD, profiles/README.md)"
+
+
+def config34_bench(fsigpu, torch, hbm_peak, steps=3):
+    """Configs 3-4 (BASELINE.json; the 3D system is harness-generated, its
+    solve path checked against the reference's solve classes at 8^3 in
+    tests/test_gpu_parity.py::test_valve3d_parity): per case the GPU setup,
+    the batched LU of the fine level's Schwarz blocks (bit-exact
+    DenseFactorization, blocked LU above 164 rows) against the fp64 peak, and
+    full FGMRES(30) solves to rtol 1e-10 (L2 flushed between solves)."""
+    from paper_1909_13201_b200.problem import load_case
+    out = {}
+    peak, peak_kind = fp64_peak()
+    for case, wl in (("v3", WORKLOAD_V3), ("v3_dd", WORKLOAD_V3DD)):
+        t0 = time.time()
+        path = ensure_cfg2_case(case)
+        export_s = time.time() - t0
+        P = load_case(path, case)
+        top = P.levels[-1]
+        # the fine level's Schwarz blocks alone: extract + bit-exact LU (+ solve format)
+        A = fsigpu.SparseMatrix(top.A)
+        sets = [top.as1.idx[top.as1.ptr[b]:top.as1.ptr[b + 1]] for b in range(top.as1.n)]
+        sizes = np.array([len(x) for x in sets], dtype=np.float64)
+        fsigpu.DenseBlocks.from_csr(A, sets)  # warm-up
+        torch.cuda.synchronize()
+        t0 = time.time()
+        B = fsigpu.DenseBlocks.from_csr(A, sets)
+        torch.cuda.synchronize()
+        lu_s = time.time() - t0
+        flops = float(np.sum(2.0 / 3.0 * sizes ** 3))
+        del B, A
+        t0 = time.time()
+        G = fsigpu.GmgPreconditioner(P.levels)
+        S = fsigpu.GmresSolver(G, P.frame_scale, restart=30)
+        torch.cuda.synchronize()
+        setup_s = time.time() - t0
+        cfg = fsigpu.KrylovConfig(restart=30, max_iters=500, rel_tol=1e-10, abs_tol=1e-300)
+        lib_stream = torch.cuda.ExternalStream(G.stream())
+        b = torch.from_numpy(P.b).cuda()
+        x = torch.zeros(P.n, dtype=torch.float64, device="cuda")
+        flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+        res = S.solve_dev(b.data_ptr(), x.data_ptr(), cfg)
+        per = []
+        for _ in range(steps):
+            flush.fill_(1.0)
+            x.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(lib_stream)
+            res = S.solve_dev(b.data_ptr(), x.data_ptr(), cfg)
+            e1.record(lib_stream)
+            e1.synchronize()
+            per.append(e0.elapsed_time(e1))
+        ms = sum(per) / len(per)
+        out["config3" if case == "v3" else "config4"] = {
+            "workload": wl, "n_dofs": P.n, "nnz_fine": top.A.nnz, "value": res.m_applies / (ms / 1000.0),
+            "unit": "V-cycles/s", "solve_ms": ms, "iterations": res.iterations, "converged": res.converged,
+            "final_relres": res.true_residual / float(np.linalg.norm(P.b)),
+            "fine_blocks": int(top.as1.n), "block_size_max": int(sizes.max()), "block_size_mean": float(sizes.mean()),
+            "lu": {"blocks": int(top.as1.n), "gflop": flops / 1e9, "seconds": lu_s,
+                   "tflops": flops / lu_s / 1e12, "fp64_peak_tflops": peak, "peak_kind": peak_kind,
+                   "frac_of_fp64_peak": flops / lu_s / 1e12 / peak,
+                   "timing": "wall clock of one synchronous fsigpu_blocks_factor_csr (extraction + bit-exact LU + "
+                             "solve format) after a warm-up"},
+            "setup_s": setup_s, "export_s": export_s, "steps": steps}
+        del S, G, P, b, x, flush
+        torch.cuda.empty_cache()
+    return out
+
+
+def ensure_cfg2_case(case):
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from conftest import ensure_case
+    return ensure_case(case)
+
+
 def mult_time_to_solution(fsigpu, torch, P, steps=5):
     """Config 0 with the reference's shipped multiplicative FS smoother
     (precond.cpp:271-303) in multicolour order (mult.cuh): FGMRES(30) to
@@ -660,6 +756,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-microbench", action="store_true")
     ap.add_argument("--no-config2", action="store_true", help="skip the config-2 sub-object (exports 1.6 GB)")
+    ap.add_argument("--no-config34", action="store_true", help="skip the 3D config-3/4 sub-objects")
     ap.add_argument("--config", choices=["cfg0", "cfg2", "cfg2full"], default="cfg0")
     ap.add_argument("--smoother", choices=["fs", "as"], default="fs")
     # sweep around the FS/AS smoother: the reference's damped Richardson

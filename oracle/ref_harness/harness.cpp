@@ -25,6 +25,8 @@
 //   fsi_ref_harness solve  <case> [--mode add|mult] [--reps R] [--max-iters N]
 //   fsi_ref_harness blocks <out.fsix> [--seed S]     (golden dense LU blocks)
 //   fsi_ref_harness time-blocks <n54> <n59> <nsolve> [--threads T] [--seed S]
+//   fsi_ref_harness export3d <v3s|v3s_dd|v3|v3_dd> <out.fsix> [--no-gmres]
+//                          (configs 3-4: 3D valve-like system, valve3d.inc)
 // cases: cfg0 (unit square 8->16->32), sq4 (8->64, 4 levels), chan (reference
 // unit_solver channel nx=4 ny_fluid=2 ny_wall=1, 2 levels), changmg (unit_gmg
 // channel, ny_wall=2, 2 levels), cfg2 (bulge 16->256, 5 levels), cfg2l4 (bulge
@@ -866,6 +868,8 @@ int cmd_time_blocks(const Args& a) {
   return 0;
 }
 
+#include "valve3d.inc"
+
 #ifdef FSI_ADAPTER_CHECK
 // The drop-in adapter (tests/cpp/gpu_solve_adapter.cpp) driven like the
 // reference driver's solve block (driver.cpp:242-272): GpuGmg from the
@@ -955,6 +959,7 @@ int main(int argc, char** argv) {
     if (c == "solve") return cmd_solve(a);
     if (c == "blocks") return cmd_blocks(a);
     if (c == "time-blocks") return cmd_time_blocks(a);
+    if (c == "export3d") return cmd_export3d(a);
 #ifdef FSI_ADAPTER_CHECK
     if (c == "gpu-adapter") return cmd_gpu_adapter(a);
 #endif

@@ -954,35 +954,29 @@ static void assemble_fs(Level& L, const fsigpu_level_desc& d, const std::vector<
     hk.push_back((p << 32) | p);
     hv.push_back(1.0 / d.lumped[k]);
   }
-  std::vector<double> blk;
+  // the coupling entries of the AS2 blocks touching u^s columns, built on
+  // the device (fs_coo_coupling_kernel) in the order the host loop emitted
+  // them: per block its (j, k) couplings, j-major
+  std::vector<int> cblk, clj, clk;
+  std::vector<long long> cloff{0}, coff{0};
   for (long long b = L.n_as1; b < B.nb; ++b) {
     const int m = B.h_m[b];
     const long long ro = B.h_row_off[b];
-    bool touch = false;
-    for (int j = 0; j < m && !touch; ++j) {
+    const size_t before = clj.size();
+    for (int j = 0; j < m; ++j) {
       const int q = pos[ro + j] - g1;
-      touch = ap[q + 1] > ap[q];
-    }
-    if (!touch) continue;
-    const int ld = even_up(m);
-    blk.resize((size_t)ld * m);
-    FSI_CUDA(cudaMemcpy(blk.data(), B.inv.p + B.h_inv_off[b], sizeof(double) * blk.size(), cudaMemcpyDeviceToHost));
-    for (int i = 0; i < m; ++i) {
-      const int pi = pos[ro + i];
-      const int cov = cover_ptr[pi + 1] - cover_ptr[pi];
-      for (int j = 0; j < m; ++j) {
-        const int q = pos[ro + j] - g1;
-        for (int k = ap[q]; k < ap[q + 1]; ++k) {
-          const int c = ac[k];
-          double v = -blk[(size_t)j * ld + i] * av[k] / d.lumped[c];
-          if (cov > 1) v = v / (double)cov;
-          hk.push_back(((unsigned long long)(unsigned)pi << 32) | (unsigned)(g1 + c));
-          hv.push_back(v);
-        }
+      for (int k = ap[q]; k < ap[q + 1]; ++k) {
+        clj.push_back(j);
+        clk.push_back(k);
       }
     }
+    if (clj.size() == before) continue;
+    cblk.push_back((int)b);
+    cloff.push_back((long long)clj.size());
+    coff.push_back(coff.back() + (long long)m * (long long)(clj.size() - before));
   }
-  const long long N = nblk + (long long)hk.size();
+  const long long ncoup = coff.back();
+  const long long N = nblk + (long long)hk.size() + ncoup;
   DevBuf<unsigned long long> keys(N), ukeys(N);
   DevBuf<double> vals(N), uvals(N);
   DevBuf<long long> dco;
@@ -998,6 +992,27 @@ static void assemble_fs(Level& L, const fsigpu_level_desc& d, const std::vector<
   if (!hk.empty()) {
     FSI_CUDA(cudaMemcpyAsync(keys.p + nblk, hk.data(), sizeof(unsigned long long) * hk.size(), cudaMemcpyHostToDevice, s));
     FSI_CUDA(cudaMemcpyAsync(vals.p + nblk, hv.data(), sizeof(double) * hv.size(), cudaMemcpyHostToDevice, s));
+  }
+  if (ncoup) {
+    for (auto& o : coff) o += nblk + (long long)hk.size();
+    DevBuf<int> dblk, dj, dk, dac;
+    DevBuf<long long> dcl, dco;
+    DevBuf<double> dav, dlm;
+    dblk.upload(cblk, s);
+    dj.upload(clj, s);
+    dk.upload(clk, s);
+    dcl.upload(cloff, s);
+    dco.upload(coff, s);
+    dac.upload(ac.empty() ? std::vector<int>{0} : ac, s);
+    dav.upload(av.empty() ? std::vector<double>{0.0} : av, s);
+    dlm.upload(d.lumped, (size_t)std::max(d.n_us, 1), s);
+    DevBuf<int> inv_ptr_c;
+    inv_ptr_c.upload(cover_ptr, s);
+    fs_coo_coupling_kernel<<<(int)cblk.size(), 256, 0, s>>>(dblk.p, B.m.p, B.row_off.p, B.inv.p, B.inv_off.p,
+                                                            B.pos.p, inv_ptr_c.p, dcl.p, dj.p, dk.p, dac.p, dav.p,
+                                                            dlm.p, g1, dco.p, keys.p, vals.p);
+    FSI_CHECK_LAUNCH();
+    FSI_CUDA(cudaStreamSynchronize(s));
   }
   auto pol = thrust::cuda::par.on(s);
   thrust::device_ptr<unsigned long long> kp(keys.p), ukp(ukeys.p);

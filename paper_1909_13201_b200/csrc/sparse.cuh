@@ -655,6 +655,40 @@ __global__ void fs_coo_blocks_kernel(int nb, const int* __restrict__ msz, const 
   }
 }
 
+// The lumped-Jacobi coupling of the AS2 blocks (precond.cpp:281-287):
+// entries (p_i, g1 + c) = -inv(A_b)[i, j] * A_g2[p_j, c] / lumped[c] (/ cover)
+// for every row i and coupling (j, c) of block b, emitted in the host
+// loop's order (i, then the block's couplings j-major), one CTA per block.
+__global__ void fs_coo_coupling_kernel(const int* __restrict__ blk, const int* __restrict__ msz,
+                                       const long long* __restrict__ row_off, const double* __restrict__ inv,
+                                       const long long* __restrict__ inv_off, const int* __restrict__ pos,
+                                       const int* __restrict__ inv_ptr, const long long* __restrict__ cl_off,
+                                       const int* __restrict__ cl_j, const int* __restrict__ cl_k,
+                                       const int* __restrict__ ac, const double* __restrict__ av,
+                                       const double* __restrict__ lumped, int g1, const long long* __restrict__ out_off,
+                                       unsigned long long* __restrict__ keys, double* __restrict__ vals) {
+  const int q = blockIdx.x;
+  const int b = blk[q];
+  const int m = msz[b];
+  const int ld = (m + 1) & ~1;
+  const long long ro = row_off[b];
+  const double* M = inv + inv_off[b];
+  const long long c0 = cl_off[q];
+  const int nc = (int)(cl_off[q + 1] - c0);
+  const long long o = out_off[q];
+  for (long long e = threadIdx.x; e < (long long)m * nc; e += blockDim.x) {
+    const int i = (int)(e / nc), t = (int)(e % nc);
+    const int j = cl_j[c0 + t], k = cl_k[c0 + t];
+    const int pi = pos[ro + i];
+    const int cov = inv_ptr[pi + 1] - inv_ptr[pi];
+    const int c = ac[k];
+    double v = -M[(size_t)j * ld + i] * av[k] / lumped[c];
+    if (cov > 1) v = v / (double)cov;
+    keys[o + e] = ((unsigned long long)(unsigned)pi << 32) | (unsigned)(g1 + c);
+    vals[o + e] = v;
+  }
+}
+
 __global__ void coo_row_count_kernel(long long nnz, const unsigned long long* __restrict__ keys,
                                      int* __restrict__ cnt) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;

@@ -111,7 +111,7 @@ def load_case(path: str, name: str = "") -> Problem:
         if p + "/mesh/element_nodes" in a:
             lv.mesh = {k[len(p) + 6:]: v for k, v in a.items() if k.startswith(p + "/mesh/")}
         levels.append(lv)
-    golden = {k: v for k, v in a.items() if k.startswith(("golden/", "gmres_", "setup/"))}
+    golden = {k: v for k, v in a.items() if k.startswith(("golden/", "gmres_", "gmres/", "setup/"))}
     return Problem(name=name or path, levels=levels, frame_scale=a["frame_scale"].astype(np.float64),
                    b=a["b"].astype(np.float64), golden=golden)
 
@@ -144,7 +144,11 @@ class MeshDesc(C.Structure):
 
 
 def mesh_desc(m: Dict[str, np.ndarray], npe: int = 9, dim: int = 2, ppe: int = 3) -> MeshDesc:
-    """MeshDesc over the (kept-alive) arrays of an exported level mesh."""
+    """MeshDesc over the (kept-alive) arrays of an exported level mesh (2D Q2
+    by default; 3D archives carry nodes_per_element / dim / p_per_element)."""
+    npe = int(m["nodes_per_element"][0]) if "nodes_per_element" in m else npe
+    dim = int(m["dim"][0]) if "dim" in m else dim
+    ppe = int(m["p_per_element"][0]) if "p_per_element" in m else ppe
     d = MeshDesc()
     d.n_elements = len(m["elem_solid"])
     d.n_nodes = len(m["node_solid"])

@@ -49,6 +49,27 @@ def cfg0():
 DATA_CFG2 = os.path.join(ROOT, "data_cfg2")
 
 
+def ensure_case(case: str) -> str:
+    """ensure_cfg2 for every generated case: cfg2 / cfg2l4 (reference
+    exporter) and the 3D valve cases v3s, v3s_dd (with the reference's
+    goldens) and v3, v3_dd (bench size, inputs only)."""
+    import subprocess
+    if case.startswith("cfg2"):
+        return ensure_cfg2(case)
+    path = os.path.join(DATA_CFG2, case + ".fsix")
+    if os.path.exists(path):
+        return path
+    exe = os.path.join(ROOT, "oracle", "_ref", "fsi_ref_harness")
+    if not os.path.exists(exe):
+        pytest.fail(f"{exe} missing: cannot export {case}")
+    os.makedirs(DATA_CFG2, exist_ok=True)
+    tmp = path + ".part"
+    extra = [] if case in ("v3s", "v3s_dd") else ["--no-gmres"]
+    subprocess.run([exe, "export3d", case, tmp] + extra, check=True, stdout=subprocess.DEVNULL)
+    os.replace(tmp, path)
+    return path
+
+
 def ensure_cfg2(case: str) -> str:
     """Path of the config-2 solve inputs (bulge case),
     exported on demand by the prebuilt reference exporter
