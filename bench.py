@@ -427,6 +427,55 @@ def run_ours(args, ws, rank, local):
     insolve = {k: {"ms_total": v["ms"], "launches": v["launches"], "avg_launch_us": 1000.0 * v["ms"] / v["launches"],
                    "bytes_per_launch": v["bytes"] / v["launches"], "GBps": v["bytes"] / v["ms"] / 1e6}
                for k, v in cls.items()}
+    # ---- in-graph view: the SAME captured restart-cycle graphs as the timed
+    # region, with device-clock stamps in the kernels (last CTA exit minus
+    # dependency release, %globaltimer): the only per-kernel duration that
+    # has neither launch gaps (events with graphs off) nor a cold L2 (alone)
+    ingraph = {}
+    ingraph_solve_ms = None
+    if hasattr(fsigpu, "Stamps"):
+        fsigpu.Stamps.enable(True)
+        S.solve_dev(b.data_ptr(), x.data_ptr(), cfg)  # re-captures the graphs with the stamp slots
+        fsigpu.Stamps.enable(True)                    # reset the counters, capture once more
+        S.solve_dev(b.data_ptr(), x.data_ptr(), cfg)
+        fsigpu.Stamps.enable(True)
+        flush.fill_(1.0)
+        x.zero_()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(lib_stream)
+        r3 = S.solve_dev(b.data_ptr(), x.data_ptr(), cfg)
+        e1.record(lib_stream)
+        e1.synchronize()
+        ingraph_solve_ms = e0.elapsed_time(e1)
+        names = {}
+        for lvl in range(0, top + 1):
+            names[f"fs_smoother@L{lvl}"] = ("block_solve", lvl, 0)
+            names[f"residual@L{lvl}"] = ("spmv", lvl, 0)
+            names[f"restrict@L{lvl}"] = ("transfer", lvl, 0)
+            names[f"prolong_resid@L{lvl}"] = ("transfer", lvl, 1)
+        names["coarse@L0"] = ("coarse", 0, 0)
+        names["arnoldi_A_spmv_dots"] = ("arnoldi", -1, 0)
+        names["arnoldi_B_update_dots_norm"] = ("arnoldi", -1, 1)
+        names["arnoldi_C_update_normalize"] = ("arnoldi", -1, 2)
+        tot_us = 0.0
+        for nm, (kcls, lvl, sub) in names.items():
+            v = fsigpu.Stamps.read(kcls, lvl, sub)
+            if v["launches"]:
+                d = {"avg_launch_us": v["us"] / v["launches"], "launches": v["launches"]}
+                if nm in kt:
+                    d["GBps"] = kt[nm]["bytes"] / (d["avg_launch_us"] * 1e3)
+                ingraph[nm] = d
+                tot_us += v["us"]
+        fsigpu.Stamps.enable(False)
+        steps3 = max(r3.iterations, 1)
+        ingraph["_check"] = {"stamped_us_per_step": tot_us / steps3,
+                             "event_timed_us_per_step": 1000.0 * ingraph_solve_ms / steps3,
+                             "iterations": r3.iterations,
+                             "note": "sum of the stamped kernel durations of one solve / its FGMRES steps, against the "
+                                     "same solve timed with CUDA events on the library stream (cycle tails, graph "
+                                     "launches and host syncs make up the difference)"}
     # the roofline object: the V-cycle kernel with the largest share of a
     # V-cycle, timed alone per launch with CUDA events on the library stream
     # after a 256 MB L2 flush (HBM-bound view; the in-solve events above add
@@ -444,6 +493,7 @@ def run_ours(args, ws, rank, local):
         v = per_level.get("block_solve@" + dom.split("@")[1])
         insolve_dom = per_launch_bytes / (v["avg_launch_us"] * 1e3) if v else None  # GB/s
     achieved_main = insolve_dom if insolve_dom else achieved
+    ingraph_dom = ingraph.get(dom, {}).get("GBps")
     traffic = None
     ncu_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(ncu_path):
@@ -476,11 +526,17 @@ def run_ours(args, ws, rank, local):
                      "frac_warm": per_launch_bytes / kt[dom]["ms_warm"] / 1e6 / hbm_peak,
                      "achieved_insolve": insolve_dom,
                      "frac_insolve": insolve_dom / hbm_peak if insolve_dom else None,
+                     "achieved_ingraph": ingraph_dom,
+                     "frac_ingraph": ingraph_dom / hbm_peak if ingraph_dom else None,
+                     "avg_launch_us_ingraph": ingraph.get(dom, {}).get("avg_launch_us"),
                      "timing": "achieved: the dominant V-cycle kernel's launches inside a full solve (graphs off, "
                                "CUDA events around each launch on the library stream, launch gaps included; "
                                "the cold-timed value when the kernel has no in-solve class); achieved_cold / "
                                "achieved_warm: the same kernel timed alone per launch after a 256 MB L2 flush / "
-                               "back to back; bytes = algorithmic bytes per launch (DESIGN 3.6)"},
+                               "back to back; achieved_ingraph: the same launches inside the captured restart-cycle "
+                               "graphs of the timed region, from device-clock stamps in the kernel (last CTA exit "
+                               "minus dependency release); bytes = algorithmic bytes per launch (DESIGN 3.6)"},
+        "ingraph_kernels": ingraph,
         "insolve_kernel_classes": insolve,
         "insolve_per_level": per_level,
         "insolve_timing": "one instrumented solve after the timed region, graphs off, CUDA events around every launch "

@@ -246,6 +246,15 @@ int fsigpu_profile_read(double* ms, long long* launches, double* bytes);
 /* the same sums restricted to one GMG level (-1: launches outside a cycle) */
 int fsigpu_profile_read_level(int cls, int level, double* ms, long long* launches, double* bytes);
 int fsigpu_profile_reset(void);
+/* Device-clock launch stamps: durations of the solve kernels INSIDE the
+ * captured restart-cycle graph (last CTA exit minus dependency release, from
+ * %globaltimer), where CUDA events cannot bracket a launch. No reference
+ * counterpart (bench instrumentation). enable/disable resets the counters and
+ * makes solvers re-capture their graphs. sub: kernel of the class at that
+ * level (SPMV/BLOCK_SOLVE 0; TRANSFER 0 = restriction, 1 = prolongation +
+ * residual; COARSE 0; ARNOLDI at level -1: 0 = (A) SpMV + dots, 1 = (B), 2 = (C)). */
+int fsigpu_stamps_enable(int enable);
+int fsigpu_stamps_read(int cls, int level, int sub, double* us_total, long long* launches);
 
 #ifdef __cplusplus
 }

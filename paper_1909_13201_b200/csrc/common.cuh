@@ -115,6 +115,35 @@ constexpr unsigned kFull = 0xffffffffu;
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// ---- device-clock launch stamps (opt-in profiling of kernels INSIDE a CUDA graph) ----
+// A slot is four u64: {start, end, accumulated ns, launches}. Thread 0 of CTA
+// 0 folds the previous launch of the same graph node into the accumulator on
+// entry, and stamps `start` once the launch's dependencies are resolved
+// (after griddepcontrol.wait); thread 0 of every CTA raises `end` with a
+// fire-and-forget atomic max on exit. Duration = last CTA exit - dependency
+// release. A null slot (the default) costs one predicated branch.
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void stamp_fold(unsigned long long* slot) {
+  if (slot && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    const unsigned long long s0 = slot[0], e0 = *(volatile unsigned long long*)(slot + 1);
+    if (s0 && e0 > s0) {
+      slot[2] += e0 - s0;
+      slot[3] += 1;
+    }
+    slot[0] = 0;
+  }
+}
+__device__ __forceinline__ void stamp_start(unsigned long long* slot) {
+  if (slot && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) slot[0] = global_ns();
+}
+__device__ __forceinline__ void stamp_end(unsigned long long* slot) {
+  if (slot && threadIdx.x == 0) atomicMax(slot + 1, global_ns());
+}
+
 // ---- mbarrier + bulk-copy (TMA, non-tensor) helpers ----
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));

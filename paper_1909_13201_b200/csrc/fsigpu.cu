@@ -129,11 +129,34 @@ struct Profiler {
 static Profiler g_prof;
 static std::mutex g_prof_mu;
 
+// Device-clock launch stamps (common.cuh stamp_*): kernel durations INSIDE
+// the captured restart-cycle graph, where CUDA events cannot bracket a
+// launch. One slot of four u64 per (kernel class, GMG level, kernel of the
+// class); the pointers are baked into the graph at capture, so switching the
+// stamps bumps g_stamp_epoch and every solver re-captures.
+constexpr int kStampSubs = 4;
+static unsigned long long* g_stamp_buf = nullptr;
+static bool g_stamp_on = false;
+static std::atomic<int> g_stamp_epoch{0};
+static thread_local int g_cur_cls = -1;
+static inline size_t stamp_slots() { return (size_t)FSIGPU_K_COUNT * (Profiler::kLv + 1) * kStampSubs; }
+// slot of the kernel being launched under the current ProfScope
+static inline unsigned long long* cur_stamp(int sub = 0) {
+  if (!g_stamp_on || g_cur_cls < 0) return nullptr;
+  const int li = (g_prof.level >= 0 && g_prof.level < Profiler::kLv) ? g_prof.level + 1 : 0;
+  return g_stamp_buf + 4 * (((size_t)g_cur_cls * (Profiler::kLv + 1) + li) * kStampSubs + sub);
+}
+
 struct ProfScope {
   int id;
   cudaStream_t s;
-  ProfScope(int cls, double bytes, cudaStream_t st) : s(st) { id = g_prof.begin(cls, bytes, st); }
+  int prev_cls;
+  ProfScope(int cls, double bytes, cudaStream_t st) : s(st), prev_cls(g_cur_cls) {
+    g_cur_cls = cls;
+    id = g_prof.begin(cls, bytes, st);
+  }
   ~ProfScope() {
+    g_cur_cls = prev_cls;
     try {
       g_prof.end(id, s);
     } catch (...) {
@@ -237,8 +260,8 @@ struct Csr {
     if (!rows) return;
     const long long threads = (long long)rows * lpr;
     const int grid = ceil_div(threads, 256);
-#define FSI_CSR(LP, UU) launch_k(csr_kernel<LP, G, E, UU>, dim3(grid), dim3(256), 0, s, rows, (const int*)ptr.p, (const int*)idx.p, (const double*)val.p, g, e)
-#define FSI_CSRP(LP, UU) launch_k(csr_pair_kernel<LP, G, E, UU>, dim3(grid), dim3(256), 0, s, rows, (const int*)ptr.p, (const int*)idx.p, (const double*)val.p, g, e)
+#define FSI_CSR(LP, UU) launch_k(csr_kernel<LP, G, E, UU>, dim3(grid), dim3(256), 0, s, rows, (const int*)ptr.p, (const int*)idx.p, (const double*)val.p, g, e, cur_stamp(0))
+#define FSI_CSRP(LP, UU) launch_k(csr_pair_kernel<LP, G, E, UU>, dim3(grid), dim3(256), 0, s, rows, (const int*)ptr.p, (const int*)idx.p, (const double*)val.p, g, e, cur_stamp(0))
     if (unroll == 22 || unroll == 24) {  // paired loads, 2 or 4 pairs per lane per batch
       if (unroll == 22) {
         switch (lpr) {
@@ -655,7 +678,7 @@ static void launch_prolong_resid(const Level& L, const double* ec, const unsigne
 #define FSI_PR(K, LP, UA)                                                                                        \
   launch_k(K<LP, UA>, dim3(grid), dim3(256), 0, s, L.n, (const int*)L.P.ptr.p, (const int*)L.P.idx.p,         \
            (const double*)L.P.val.p, (const int*)L.AP.ptr.p, (const int*)L.AP.idx.p, (const double*)L.AP.val.p, \
-           ec, cmask_coarse, (const unsigned char*)L.cmask.p, L.x, r_pre, r)
+           ec, cmask_coarse, (const unsigned char*)L.cmask.p, L.x, r_pre, r, cur_stamp(1))
 #define FSI_PR_L(K, UA)                 \
   switch (L.AP.lpr) {                   \
     case 2: FSI_PR(K, 2, UA); break;    \
@@ -860,7 +883,7 @@ struct Gmg {
     Level& L = lv[0];
     ProfScope ps(FSIGPU_K_COARSE, 8.0 * L.n * L.n + 16.0 * L.n, s);
     launch_k(gemv_kernel, dim3(L.n), dim3(kGemvThreads), 0, s, L.n, (const double*)coarse_inv.p, rhs, x,
-             accumulate, mask_out);
+             accumulate, mask_out, cur_stamp(0));
     FSI_CHECK_LAUNCH();
     counted();
   }
@@ -1487,6 +1510,7 @@ struct Gmres {
   cudaGraphExec_t cycle_exec = nullptr;
   cudaGraph_t cycle_graph = nullptr;
   int graph_version = -1;  // Gmg::version the graph was captured at
+  int graph_stamp_epoch = 0;  // g_stamp_epoch the graph was captured at (stamp pointers are baked in)
 
   ~Gmres() {
     if (cycle_exec) cudaGraphExecDestroy(cycle_exec);
@@ -1536,11 +1560,14 @@ struct Gmres {
     counted(5);
   }
   // outer SpMV + CGS2 Arnoldi + Givens + normalisation: 3 fused kernels
-  void arnoldi_fused(const KBufs& kk) {
+  void arnoldi_fused(const KBufs& kin) {
     if (mr > kRegRestart) {
-      arnoldi_wide(kk);
+      arnoldi_wide(kin);
       return;
     }
+    KBufs kk = kin;
+    // device-clock stamps of (A), (B), (C): class ARNOLDI, no level, subs 0..2
+    kk.stamp = g_stamp_on ? g_stamp_buf + 4 * ((size_t)FSIGPU_K_ARNOLDI * (Profiler::kLv + 1) * kStampSubs) : nullptr;
     cudaStream_t s = g->s;
     Level& T = g->lv.back();
     const int gs = kk.parts_a;
@@ -1655,7 +1682,7 @@ struct Gmres {
     KState h = read_state();
     long long cycles = 0;
     const bool use_graph = graphs && !g_prof.on;
-    if (cycle_exec && graph_version != g->version) {
+    if (cycle_exec && (graph_version != g->version || graph_stamp_epoch != g_stamp_epoch)) {
       cudaGraphExecDestroy(cycle_exec);
       cudaGraphDestroy(cycle_graph);
       cycle_exec = nullptr;
@@ -1664,6 +1691,7 @@ struct Gmres {
     if (use_graph && !cycle_exec) {
       build_graph();
       graph_version = g->version;
+      graph_stamp_epoch = g_stamp_epoch;
     }
     while (!h.converged && h.its < max_iters) {
       const int its_before = h.its;
@@ -2272,7 +2300,7 @@ int fsigpu_gmg_time_kernel(fsigpu_gmg h, int which, int level, int reps, int col
         }
         case 4:
           require(level == 0, "time: coarse GEMV lives on level 0");
-          gemv_kernel<<<L.n, kGemvThreads, 0, s>>>(L.n, G.coarse_inv.p, L.b, L.x, 0);
+          gemv_kernel<<<L.n, kGemvThreads, 0, s>>>(L.n, G.coarse_inv.p, L.b, L.x, 0, nullptr, nullptr);
           by = 8.0 * L.n * L.n + 16.0 * L.n;
           break;
         default:
@@ -2641,6 +2669,38 @@ int fsigpu_profile_reset(void) {
         g_prof.lv_bytes[i][l] = 0;
       }
     }
+  });
+}
+
+// Device-clock launch stamps: durations of the solve kernels inside the
+// captured graphs (see common.cuh stamp_*). Enabling or disabling makes
+// every solver re-capture its graph on the next solve.
+int fsigpu_stamps_enable(int enable) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (enable && !g_stamp_buf) FSI_CUDA(cudaMalloc(&g_stamp_buf, stamp_slots() * 4 * sizeof(unsigned long long)));
+    if (g_stamp_buf) FSI_CUDA(cudaMemset(g_stamp_buf, 0, stamp_slots() * 4 * sizeof(unsigned long long)));
+    g_stamp_on = enable != 0;
+    ++g_stamp_epoch;
+  });
+}
+int fsigpu_stamps_read(int cls, int level, int sub, double* us_total, long long* launches) {
+  return guarded([&] {
+    require(cls >= 0 && cls < FSIGPU_K_COUNT, "stamps: bad class");
+    require(level >= -1 && level < Profiler::kLv, "stamps: bad level");
+    require(sub >= 0 && sub < kStampSubs, "stamps: bad kernel index");
+    require(g_stamp_buf != nullptr, "stamps: not enabled");
+    FSI_CUDA(cudaDeviceSynchronize());
+    unsigned long long h[4];
+    const size_t slot = ((size_t)cls * (Profiler::kLv + 1) + level + 1) * kStampSubs + sub;
+    FSI_CUDA(cudaMemcpy(h, g_stamp_buf + 4 * slot, sizeof(h), cudaMemcpyDeviceToHost));
+    unsigned long long ns = h[2], cnt = h[3];
+    if (h[0] && h[1] > h[0]) {  // the last launch has not been folded yet
+      ns += h[1] - h[0];
+      cnt += 1;
+    }
+    if (us_total) *us_total = (double)ns / 1000.0;
+    if (launches) *launches = (long long)cnt;
   });
 }
 

@@ -80,6 +80,7 @@ struct KBufs {
   const double* a_val;
   int a_lpr;
   cudaGraphConditionalHandle cond;  // WHILE handle of the restart-cycle graph
+  unsigned long long* stamp;        // device-clock stamps of (A), (B), (C): 3 slots of 4 u64, or null
   int use_cond;
 };
 
@@ -343,6 +344,7 @@ __device__ __forceinline__ double fused_row(const KBufs& k, int row, int lane) {
 // on config 0.
 template <int LPR>
 __global__ void __launch_bounds__(kFuseThreads) k_spmv_dots_1(KBufs k) {
+  stamp_fold(k.stamp ? k.stamp + 0 : nullptr);
   static_assert(kFuseThreads / LPR >= kFuseRows, "one row pass per CTA");
   pdl_trigger();
   __shared__ double ws[kFuseRows];
@@ -370,6 +372,7 @@ __global__ void __launch_bounds__(kFuseThreads) k_spmv_dots_1(KBufs k) {
   };
   load(k0 + ln);
   pdl_wait();
+  stamp_start(k.stamp ? k.stamp + 0 : nullptr);
   const int j = k.st->j;
   const int nv = j + 1;
   // operands that do not depend on w are loaded before the SpMV so their
@@ -416,6 +419,7 @@ __global__ void __launch_bounds__(kFuseThreads) k_spmv_dots_1(KBufs k) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
   if (lane == 0 && v < nv) k.partial[(size_t)blockIdx.x * kPartLd + v] = s;
+  stamp_end(k.stamp ? k.stamp + 0 : nullptr);
 }
 
 // Grid-stride over 128-row tiles with the grid capped at the resident CTA
@@ -424,8 +428,10 @@ __global__ void __launch_bounds__(kFuseThreads) k_spmv_dots_1(KBufs k) {
 // tile left 9,761 partials that every CTA of (B) summed, ~1 MB each).
 template <int LPR>
 __global__ void __launch_bounds__(kFuseThreads) k_spmv_dots(KBufs k) {
+  stamp_fold(k.stamp ? k.stamp + 0 : nullptr);
   pdl_trigger();
   pdl_wait();
+  stamp_start(k.stamp ? k.stamp + 0 : nullptr);
   __shared__ double ws[kFuseRows];
   const int j = k.st->j;
   const int nv = j + 1;
@@ -472,6 +478,7 @@ __global__ void __launch_bounds__(kFuseThreads) k_spmv_dots(KBufs k) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
   if (lane == 0 && v < nv) k.partial[(size_t)blockIdx.x * kPartLd + v] = s;
+  stamp_end(k.stamp ? k.stamp + 0 : nullptr);
 }
 
 // Per-CTA sums of 32 per-thread values plus one extra: a butterfly
@@ -553,8 +560,10 @@ __device__ __forceinline__ void sum_partials(const double* __restrict__ part, in
 constexpr int kFuseThreadsS = 256;
 constexpr int kFuseRowsS = 32;
 __global__ void __launch_bounds__(kFuseThreadsS) k_spmv_dots_s(KBufs k) {
+  stamp_fold(k.stamp ? k.stamp + 0 : nullptr);
   pdl_trigger();
   pdl_wait();
+  stamp_start(k.stamp ? k.stamp + 0 : nullptr);
   __shared__ double ws[kFuseRowsS];
   const int j = k.st->j;
   const int nv = j + 1;
@@ -604,6 +613,7 @@ __global__ void __launch_bounds__(kFuseThreadsS) k_spmv_dots_s(KBufs k) {
     const int v = warp + 8 * q;
     if (lane == 0 && v < nv) k.partial[(size_t)blockIdx.x * kPartLd + v] = x;
   }
+  stamp_end(k.stamp ? k.stamp + 0 : nullptr);
 }
 
 // (B) h1 = sum of (A)'s partials (every CTA); w -= V h1 ; partial2 <- V^T w
@@ -613,8 +623,10 @@ __global__ void __launch_bounds__(kFuseThreadsS) k_spmv_dots_s(KBufs k) {
 // streams every row, and the 64 freed registers double the resident warps.
 template <bool PF>
 __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm(KBufs k) {
+  stamp_fold(k.stamp ? k.stamp + 4 : nullptr);
   pdl_trigger();
   pdl_wait();
+  stamp_start(k.stamp ? k.stamp + 4 : nullptr);
   __shared__ double sm[kPartLd * (kArnThreads / 32)];
   __shared__ double hs[kRegRestart + 1];
   __shared__ double red[kPartLd * kSumSlices];
@@ -685,6 +697,7 @@ __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm(KBufs k) {
   // partial2[cta][0..nv) = h2 dots, partial2[cta][nv] = ||w||^2
   static_assert(kRegRestart == 32, "cta_reduce_t32 holds one slot per Krylov vector");
   cta_reduce_t32<kArnThreads>(acc, n2, nv, sm, k.partial2 + (size_t)blockIdx.x * kPartLd);
+  stamp_end(k.stamp ? k.stamp + 4 : nullptr);
 }
 
 // Large-n variants of (B) and (C): each thread streams its rows' operands
@@ -709,8 +722,10 @@ __device__ __forceinline__ void stage_row(const KBufs& k, double* stg, int st, i
 }
 
 __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm_cp(KBufs k) {
+  stamp_fold(k.stamp ? k.stamp + 4 : nullptr);
   pdl_trigger();
   pdl_wait();
+  stamp_start(k.stamp ? k.stamp + 4 : nullptr);
   extern __shared__ __align__(16) double stg[];
   __shared__ double sm[kPartLd * (kArnThreads / 32)];
   __shared__ double hs[kRegRestart + 1];
@@ -747,6 +762,7 @@ __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm_cp(KBufs k) {
   }
   cp_async_wait<0>();
   cta_reduce_t32<kArnThreads>(acc, n2, nv, sm, k.partial2 + (size_t)blockIdx.x * kPartLd);
+  stamp_end(k.stamp ? k.stamp + 4 : nullptr);
 }
 
 // (C) every CTA sums (B)'s partials into h2 and ||w||^2 and forms
@@ -757,8 +773,10 @@ __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm_cp(KBufs k) {
 //     u = v_{j+1} / scale over the rows. Launched with one extra CTA.
 template <bool PF>
 __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
+  stamp_fold(k.stamp ? k.stamp + 8 : nullptr);
   pdl_trigger();
   pdl_wait();
+  stamp_start(k.stamp ? k.stamp + 8 : nullptr);
   __shared__ double hs[kRegRestart + 1];
   __shared__ double red[kPartLd * kSumSlices];
   __shared__ double s_hn;
@@ -804,6 +822,7 @@ __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
     }
     __syncthreads();
     givens_core(k, nv - 1, hn, g_col, g_cs, g_sn, gj);
+    stamp_end(k.stamp ? k.stamp + 8 : nullptr);
     return;
   }
   const bool lucky = hn < 1e-14;
@@ -856,6 +875,7 @@ __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
       }
     }
   }
+  stamp_end(k.stamp ? k.stamp + 8 : nullptr);
 }
 
 }  // namespace fsigpu

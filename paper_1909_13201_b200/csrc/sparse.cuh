@@ -102,7 +102,8 @@ template <int LPR, class Gather, class Epi, int U = 4>
 __global__ void __launch_bounds__(256) csr_kernel(int rows, const int* __restrict__ ptr,
                                                   const int* __restrict__ idx,
                                                   const double* __restrict__ val, Gather gx,
-                                                  Epi epi) {
+                                                  Epi epi, unsigned long long* stamp) {
+  stamp_fold(stamp);
   const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int row = (int)(gt / LPR);
   const int lane = threadIdx.x & (LPR - 1);
@@ -128,6 +129,7 @@ __global__ void __launch_bounds__(256) csr_kernel(int rows, const int* __restric
   };
   load(k0 + lane);
   pdl_wait();
+  stamp_start(stamp);
   EpiPre pe{0.0, 0};
   if (ok && lane == 0) pe = epi.pre(row);
   double s = 0.0;
@@ -148,12 +150,15 @@ __global__ void __launch_bounds__(256) csr_kernel(int rows, const int* __restric
 #pragma unroll
   for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, LPR);
   if (ok && lane == 0) epi(row, s, pe);
+  stamp_end(stamp);
 }
 
 template <int LPR, class Gather, class Epi, int UP = 2>
 __global__ void __launch_bounds__(256) csr_pair_kernel(int rows, const int* __restrict__ ptr,
                                                        const int* __restrict__ idx,
-                                                       const double* __restrict__ val, Gather gx, Epi epi) {
+                                                       const double* __restrict__ val, Gather gx, Epi epi,
+                                                       unsigned long long* stamp) {
+  stamp_fold(stamp);
   const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int row = (int)(gt / LPR);
   const int lane = threadIdx.x & (LPR - 1);
@@ -181,6 +186,7 @@ __global__ void __launch_bounds__(256) csr_pair_kernel(int rows, const int* __re
   };
   load((k0 & ~1) + 2 * lane);
   pdl_wait();
+  stamp_start(stamp);
   EpiPre pe{0.0, 0};
   if (ok && lane == 0) pe = epi.pre(row);
   double s = 0.0;
@@ -208,6 +214,7 @@ __global__ void __launch_bounds__(256) csr_pair_kernel(int rows, const int* __re
 #pragma unroll
   for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, LPR);
   if (ok && lane == 0) epi(row, s, pe);
+  stamp_end(stamp);
 }
 
 // FS combine on one level (precond.cpp:42-57 additive + 271-287 + 305-317):
@@ -244,7 +251,9 @@ constexpr int kGemvThreads = 256;
 __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(int n, const double* __restrict__ M,
                                                             const double* __restrict__ b,
                                                             double* __restrict__ x, int accumulate,
-                                                            const unsigned char* __restrict__ mask_out = nullptr) {
+                                                            const unsigned char* __restrict__ mask_out,
+                                                            unsigned long long* stamp) {
+  stamp_fold(stamp);
   __shared__ double red[kGemvThreads / 32];
   const int row = blockIdx.x;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -265,6 +274,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(int n, const double*
   unsigned char mo = 0;
   if (t == 0 && mask_out) mo = __ldg(mask_out + row);
   pdl_wait();
+  stamp_start(stamp);
   double xo = 0.0;
   if (t == 0 && accumulate) xo = x[row];
   double s = 0.0;
@@ -290,6 +300,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(int n, const double*
     for (int w = 0; w < kGemvThreads / 32; ++w) z += red[w];
     x[row] = mo ? 0.0 : (accumulate ? xo + z : z);
   }
+  stamp_end(stamp);
 }
 
 // ---- setup: Gauss-Jordan inverse with partial pivoting on W = [A | I] ----
@@ -438,7 +449,8 @@ __global__ void __launch_bounds__(256) prolong_resid_kernel(int rows, const int*
                                                             const double* __restrict__ av, const double* ec,
                                                             const unsigned char* __restrict__ cmask_coarse,
                                                             const unsigned char* __restrict__ cmask, double* x,
-                                                            const double* r_pre, double* r) {
+                                                            const double* r_pre, double* r, unsigned long long* stamp) {
+  stamp_fold(stamp);
   // P rows hold <= 9 entries (Q2 natural injection, 3 for the P1disc
   // pressure): size the P batch so one batch covers them at any LPR (at
   // least 2 per lane, the config-0 tuning); the tail loop below then only
@@ -478,6 +490,7 @@ __global__ void __launch_bounds__(256) prolong_resid_kernel(int rows, const int*
     v[UP + u] = in ? __ldg(av + k) : 0.0;
   }
   pdl_wait();
+  stamp_start(stamp);
   // the row's own operands, loaded before the dot products (see EpiPre)
   double xo = 0.0, rp = 0.0;
   if (ok && lane == 0) {
@@ -520,6 +533,7 @@ __global__ void __launch_bounds__(256) prolong_resid_kernel(int rows, const int*
     if (!cm) x[row] = xo + s1;
     r[row] = rp - s2;
   }
+  stamp_end(stamp);
 }
 
 // prolong_resid_kernel with the A*P half streamed as 16-byte pairs (int2
@@ -530,7 +544,8 @@ __global__ void __launch_bounds__(256) prolong_resid_pair_kernel(
     int rows, const int* __restrict__ pp, const int* __restrict__ pi, const double* __restrict__ pv,
     const int* __restrict__ ap, const int* __restrict__ ai, const double* __restrict__ av, const double* ec,
     const unsigned char* __restrict__ cmask_coarse, const unsigned char* __restrict__ cmask, double* x,
-    const double* r_pre, double* r) {
+    const double* r_pre, double* r, unsigned long long* stamp) {
+  stamp_fold(stamp);
   constexpr int UP = (9 + LPR - 1) / LPR;
   const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int row = (int)(gt / LPR);
@@ -581,6 +596,7 @@ __global__ void __launch_bounds__(256) prolong_resid_pair_kernel(
     double2 v[UA];
     load_pairs(ka, c, v);
     pdl_wait();
+    stamp_start(stamp);
     if (ok && lane == 0) {
       xo = x[row];
       rp = r_pre[row];
@@ -627,6 +643,7 @@ __global__ void __launch_bounds__(256) prolong_resid_pair_kernel(
     if (!cm) x[row] = xo + s1;
     r[row] = rp - s2;
   }
+  stamp_end(stamp);
 }
 
 // ---- assembled FS operator (setup): COO entries of

@@ -126,6 +126,8 @@ def lib():
             "fsigpu_profile_read": ([vp, vp, vp], ip),
             "fsigpu_profile_read_level": ([ip, ip, vp, vp, vp], ip),
             "fsigpu_profile_reset": ([], ip),
+            "fsigpu_stamps_enable": ([ip], ip),
+            "fsigpu_stamps_read": ([ip, ip, ip, vp, vp], ip),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -536,3 +538,21 @@ class Profile:
         _check(lib().fsigpu_profile_read_level(KERNEL_CLASSES.index(cls), level, C.byref(ms), C.byref(n),
                                                C.byref(by)))
         return dict(ms=ms.value, launches=n.value, bytes=by.value)
+
+
+class Stamps:
+    """Device-clock launch stamps: kernel durations INSIDE the captured
+    restart-cycle graph (last CTA exit minus dependency release), where CUDA
+    events cannot bracket a launch. enable() resets the counters and makes the
+    solvers re-capture their graphs."""
+
+    @staticmethod
+    def enable(on: bool = True):
+        _check(lib().fsigpu_stamps_enable(1 if on else 0))
+
+    @staticmethod
+    def read(cls: str, level: int, sub: int = 0):
+        us = C.c_double()
+        n = C.c_longlong()
+        _check(lib().fsigpu_stamps_read(KERNEL_CLASSES.index(cls), level, sub, C.byref(us), C.byref(n)))
+        return dict(us=us.value, launches=n.value)
