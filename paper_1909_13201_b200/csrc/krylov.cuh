@@ -154,10 +154,25 @@ __device__ __forceinline__ void finish_sum(const KBufs& k, int nv, double* dst) 
 // use_cond, also sets the restart-cycle WHILE condition. Core: col[0..j]
 // already holds H(:,j) = h1 + h2, cs/sn[0..j) the previous rotations and
 // gj = g[j]; all in shared memory / registers (loaded by the caller).
-__device__ void givens_core(const KBufs& k, int j, double hn, double* col, double* cs, double* sn, double gj) {
+// pre: the solve state's scalars (its, max_iters, target), loaded by the
+// caller before its reduction so their L2 round trip is off the chain.
+struct GivensPre {
+  int its, max_iters;
+  double target;
+};
+__device__ __forceinline__ GivensPre givens_prefetch(const KBufs& k) {
+  GivensPre p;
+  p.its = __ldcg(&k.st->its);
+  p.max_iters = __ldcg(&k.st->max_iters);
+  p.target = __ldcg(&k.st->target);
+  return p;
+}
+__device__ void givens_core(const KBufs& k, int j, double hn, double* col, double* cs, double* sn, double gj,
+                            GivensPre pre) {
   KState* st = k.st;
   const int mr = k.mr;
   const int t = threadIdx.x;
+  int stop = 0;
   if (t == 0) {
     col[j + 1] = hn;
     int lucky = 0;
@@ -181,11 +196,12 @@ __device__ void givens_core(const KBufs& k, int j, double hn, double* col, doubl
     k.g[j + 1] = -sj * gj;
     k.g[j] = c * gj;
     const double rho = fabs(-sj * gj);
-    st->its += 1;
+    st->its = pre.its + 1;
     st->rho = rho;
     st->hn = hn;
-    k.history[st->its] = rho;
-    st->stop = (rho <= st->target || lucky) ? 1 : 0;
+    k.history[pre.its + 1] = rho;
+    stop = (rho <= pre.target || lucky) ? 1 : 0;
+    st->stop = stop;
     k.cs[j] = c;
     k.sn[j] = sj;
   }
@@ -194,7 +210,7 @@ __device__ void givens_core(const KBufs& k, int j, double hn, double* col, doubl
   if (t == 0) {
     st->j = j + 1;
     if (k.use_cond) {
-      const int go = (!st->stop && j + 1 < mr && st->its < st->max_iters) ? 1 : 0;
+      const int go = (!stop && j + 1 < mr && pre.its + 1 < pre.max_iters) ? 1 : 0;
       cudaGraphSetConditional(k.cond, go);
     }
   }
@@ -518,8 +534,12 @@ __device__ __forceinline__ void cta_reduce_t32(double (&a)[32], double extra, in
 // lanes own values, warps own CTA slices, slices added in order. Every CTA
 // of the consumer kernel runs it on the producer's partials, so no CTA of
 // the producer has to finish the reduction (no last-CTA tail).
+// U: loads per thread per round. Small systems (one row per thread, ~160
+// partial rows, 4 slices at nv = 31) take U = 40 so the whole sum is ONE L2
+// round trip: with U = 10 its four dependent rounds were ~3 us of the 4 us
+// of (B) and of the 8 us of (C) on config 0 (device-clock stamps).
 constexpr int kSumSlices = 16;
-template <int T>
+template <int T, int U = 10>
 __device__ __forceinline__ void sum_partials(const double* __restrict__ part, int nparts, int nv, double* dst,
                                              double* red /* kSumSlices x (kRegRestart+1) */) {
   constexpr int LD = kRegRestart + 1;
@@ -529,7 +549,6 @@ __device__ __forceinline__ void sum_partials(const double* __restrict__ part, in
   const int v = threadIdx.x % nv, q = threadIdx.x / nv;
   if (q < ns) {
     double s = 0.0;
-    constexpr int U = 10;
     for (int b0 = q; b0 < nparts; b0 += ns * U) {
       double pv[U];
 #pragma unroll
@@ -641,7 +660,7 @@ __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm(KBufs k) {
     for (int v = 0; v < kRegRestart; ++v) v0[v] = (r0 < k.n && v < nv) ? k.V[(size_t)v * k.n + r0] : 0.0;
     if (r0 < k.n) w0 = k.w[r0];
   }
-  sum_partials<kArnThreads>(k.partial, k.parts_a, nv, hs, red);
+  sum_partials<kArnThreads, PF ? 40 : 10>(k.partial, k.parts_a, nv, hs, red);
   if (blockIdx.x == 0) {
     if (threadIdx.x < nv) k.st->h1[threadIdx.x] = hs[threadIdx.x];
     if (threadIdx.x == 0) k.st->jc = j + 1;
@@ -787,6 +806,7 @@ __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
   // Givens CTA: its inputs other than h2 are loaded before the reduction
   __shared__ double g_col[kRegRestart + 2], g_cs[kRegRestart + 1], g_sn[kRegRestart + 1];
   double h1t = 0.0, gj = 0.0;
+  GivensPre gpre{};
   if (!rows_cta) {
     const int t = threadIdx.x;
     if (t < nv) h1t = __ldcg(k.st->h1 + t);
@@ -795,17 +815,21 @@ __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
       g_sn[t] = __ldcg(k.sn + t);
     }
     if (t == 0) gj = __ldcg(k.g + nv - 1);
+    if (t == 0) gpre = givens_prefetch(k);
   }
   // first row prefetched before the reduction (see k_update_dots_norm)
   const int r0 = blockIdx.x * blockDim.x + threadIdx.x;
   const bool has0 = rows_cta && r0 < k.n;
-  double w0 = 0.0, v0[PF ? kRegRestart : 1];
+  double w0 = 0.0, sc0 = 1.0, v0[PF ? kRegRestart : 1];
   if constexpr (PF) {
 #pragma unroll
     for (int v = 0; v < kRegRestart; ++v) v0[v] = (has0 && v < nv) ? k.V[(size_t)v * k.n + r0] : 0.0;
-    if (has0) w0 = k.w[r0];
+    if (has0) {
+      w0 = k.w[r0];
+      sc0 = k.scale[r0];
+    }
   }
-  sum_partials<kArnThreads>(k.partial2, k.parts_b, nv + 1, hs, red);
+  sum_partials<kArnThreads, PF ? 40 : 10>(k.partial2, k.parts_b, nv + 1, hs, red);
   if (threadIdx.x < 32) {
     double q = 0.0;
     for (int v = threadIdx.x; v < nv; v += 32) q = fma(hs[v], hs[v], q);
@@ -821,7 +845,7 @@ __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
       g_col[threadIdx.x] = h1t + hs[threadIdx.x];
     }
     __syncthreads();
-    givens_core(k, nv - 1, hn, g_col, g_cs, g_sn, gj);
+    givens_core(k, nv - 1, hn, g_col, g_cs, g_sn, gj, gpre);
     stamp_end(k.stamp ? k.stamp + 8 : nullptr);
     return;
   }
@@ -835,7 +859,7 @@ __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
     if (!lucky) {
       const double vv = wr / hn;
       vj[r0] = vv;
-      k.ubuf[r0] = vv / k.scale[r0];
+      k.ubuf[r0] = vv / sc0;
     }
   }
   if constexpr (PF) {

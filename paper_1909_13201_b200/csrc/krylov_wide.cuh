@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_normalize(KBufs k) {
     }
     if (t == 0) s_gj = __ldcg(k.g + nv - 1);
     __syncthreads();
-    givens_core(k, nv - 1, hn, g_col, g_cs, g_sn, s_gj);
+    givens_core(k, nv - 1, hn, g_col, g_cs, g_sn, s_gj, givens_prefetch(k));
     return;
   }
   const bool lucky = hn < 1e-14;
