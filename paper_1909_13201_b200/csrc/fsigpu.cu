@@ -172,20 +172,29 @@ static inline void counted(int k = 1) { g_launches += k; }
 // ------------------------------------------------------------ CSR
 // Lanes per row: the power of two nearest to avg_nnz / target. The entries
 // per lane that hide latency best grow with the level size: ~2 on tiny
-// (L2-resident, launch-bound) levels, 4 below 64k rows, 8 up to 128k, 16 on HBM-bound
-// levels, where fewer lanes per row keep more rows -- hence more independent
-// loads -- in flight per warp. Batch depth 8 only pays on tiny levels. From
-// the per-level sweeps of tools/tune_spmv.py on configs 0 and 2
-// (profiles/r01_tune_spmv_*.txt).
+// levels (< 16k rows), 8 from 16k to 128k rows, 16 on HBM-bound levels, where
+// fewer lanes per row keep more rows -- hence more independent loads -- in
+// flight per warp. Batch depth: tiny levels take the smallest batch that
+// holds a lane's whole share (4 or 8), 16k..64k rows 8, larger levels 4.
+// Levels below 64k rows are tuned on the kernels' IN-GRAPH durations
+// (device-clock stamps inside a config-0 solve, tools/tune_ingraph.py,
+// profiles/r02_tune_ingraph_cfg0.txt: fine FS 7.8 -> 6.6 us, fine A 4.05 ->
+// 3.55, L1 A 2.9 -> 1.5); the isolated cold/warm sweeps of round 1
+// (profiles/r01_tune_spmv_*.txt) had picked 4 entries per lane there. The
+// HBM-bound levels keep the cold-sweep rule.
 static int choose_lpr(long long rows, long long nnz) {
   if (rows <= 0) return 2;
-  const double target = rows < 16384 ? 2.0 : rows < 65536 ? 4.0 : rows < 131072 ? 8.0 : 16.0;
+  const double target = rows < 16384 ? 2.0 : rows < 131072 ? 8.0 : 16.0;
   const double want = (double)nnz / rows / target;
   int l = 2;
   while (l < 32 && want > l * 1.41421356) l *= 2;
   return l;
 }
-static int choose_unroll(long long rows) { return rows < 16384 ? 8 : 4; }
+static int choose_unroll(long long rows, long long nnz, int lpr) {
+  if (rows >= 65536) return 4;
+  if (rows >= 16384) return 8;
+  return rows > 0 && (double)nnz / rows / lpr <= 4.0 ? 4 : 8;
+}
 
 struct Csr {
   int rows = 0, cols = 0;
@@ -213,7 +222,7 @@ struct Csr {
       FSI_CUDA(cudaMemcpyAsync(val.p, v, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
     }
     lpr = choose_lpr(r, nnz);
-    unroll = choose_unroll(r);
+    unroll = choose_unroll(r, nnz, lpr);
     h_ptr.assign(p, p + r + 1);
     if (keep_host) {
       h_idx.assign(ix, ix + nnz);
@@ -248,7 +257,7 @@ struct Csr {
     ix.release();
     v.release();
     lpr = choose_lpr(r, nnz);
-    unroll = choose_unroll(r);
+    unroll = choose_unroll(r, nnz, lpr);
     h_ptr = ptr.download();
   }
   double bytes(bool resid) const {
@@ -882,8 +891,14 @@ struct Gmg {
   void coarse_gemv(const double* rhs, double* x, int accumulate, const unsigned char* mask_out) {
     Level& L = lv[0];
     ProfScope ps(FSIGPU_K_COARSE, 8.0 * L.n * L.n + 16.0 * L.n, s);
-    launch_k(gemv_kernel, dim3(L.n), dim3(kGemvThreads), 0, s, L.n, (const double*)coarse_inv.p, rhs, x,
-             accumulate, mask_out, cur_stamp(0));
+    // 64-thread CTAs (one batch of 22 loads per thread) when 256-thread
+    // CTAs would need a second wave (5 resident per SM)
+    if (L.n > 5 * 148 && L.n <= 64 * 22)
+      launch_k(gemv_kernel<64, 22>, dim3(L.n), dim3(64), 0, s, L.n, (const double*)coarse_inv.p, rhs, x,
+               accumulate, mask_out, cur_stamp(0));
+    else
+      launch_k(gemv_kernel<kGemvThreads, 8>, dim3(L.n), dim3(kGemvThreads), 0, s, L.n,
+               (const double*)coarse_inv.p, rhs, x, accumulate, mask_out, cur_stamp(0));
     FSI_CHECK_LAUNCH();
     counted();
   }
@@ -1263,6 +1278,9 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
   } else if (d.nc >= 16384) {
     L.R.lpr = 8;
     L.R.unroll = 8;
+  } else {  // in-graph sweep on config 0: 1.29 -> 1.10 us (5,124 coarse rows)
+    L.R.lpr = 4;
+    L.R.unroll = 24;
   }
   tr.reset(new SetupTrace("A*P", l));
   // AP_m = A * diag(!col_mask) * P on the device (ap_row_kernel); rows with
@@ -1305,9 +1323,12 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
     // (HBM-bound) levels batches of 4 AP entries; on small (L2-resident)
     // ones half the lanes with batches of 8 (warm sweeps, tools/tune_spmv.py)
     const bool pair_ap = d.n >= 131072 || (force_big() && d.n >= 4096);
-    if (d.n < 65536 && !pair_ap) {
+    if (d.n < 16384 && !pair_ap) {
       L.AP.lpr = std::max(2, L.AP.lpr / 2);
       L.AP.unroll = 8;
+    } else if (d.n < 65536 && !pair_ap) {  // in-graph sweep on config 0 (20k rows): 4.51 -> 4.27 us
+      L.AP.lpr = 8;
+      L.AP.unroll = 22;
     } else if (pair_ap) {
       // HBM-bound levels: the A*P half as 16-byte pairs (cold sweeps on the
       // config-2 hierarchy, profiles/r01_tune_cfg2full_ap.txt: L4 227 -> 190
@@ -1888,6 +1909,7 @@ int fsigpu_gmg_set_launch(fsigpu_gmg h, int level, int which, int lpr, int unrol
     Csr* c = which == 0 ? &L.A : which == 1 ? &L.FS : which == 2 ? &L.AP : which == 3 ? &L.P : &L.R;
     c->lpr = lpr;
     c->unroll = unroll;
+    ++h->g.version;  // captured solver graphs hold the old launch shape
   });
 }
 // Level smoother: 0 damped Richardson (the reference's richardson_smooth,
@@ -2300,7 +2322,7 @@ int fsigpu_gmg_time_kernel(fsigpu_gmg h, int which, int level, int reps, int col
         }
         case 4:
           require(level == 0, "time: coarse GEMV lives on level 0");
-          gemv_kernel<<<L.n, kGemvThreads, 0, s>>>(L.n, G.coarse_inv.p, L.b, L.x, 0, nullptr, nullptr);
+          gemv_kernel<kGemvThreads, 8><<<L.n, kGemvThreads, 0, s>>>(L.n, G.coarse_inv.p, L.b, L.x, 0, nullptr, nullptr);
           by = 8.0 * L.n * L.n + 16.0 * L.n;
           break;
         default:

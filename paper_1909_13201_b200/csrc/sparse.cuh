@@ -244,29 +244,31 @@ __global__ void fs_combine_kernel(int n, int g1, int n_us, const int* __restrict
 }
 
 // Coarse solve x0 (+)= Ainv' b0 with the explicit equilibrated inverse
-// (row-major n0 x n0): one 256-thread CTA per row, so a row of <= 2048
-// columns is ONE predicated batch of loads per thread (latency-bound at
-// these sizes); xor tree per warp, warp sums added in warp order.
+// (row-major n0 x n0): one T-thread CTA per row, U predicated loads per
+// thread per batch, so a row of <= T * U columns is ONE batch (latency-bound
+// at these sizes); xor tree per warp, warp sums added in warp order.
+// <256, 8> is the default; <64, 22> serves coarse levels whose row count
+// would otherwise need a second wave of 256-thread CTAs (config 0: 1,348
+// rows against 5 x 148 resident CTAs; in-graph 3.2 us).
 constexpr int kGemvThreads = 256;
-__global__ void __launch_bounds__(kGemvThreads) gemv_kernel(int n, const double* __restrict__ M,
-                                                            const double* __restrict__ b,
-                                                            double* __restrict__ x, int accumulate,
-                                                            const unsigned char* __restrict__ mask_out,
-                                                            unsigned long long* stamp) {
+template <int T, int U>
+__global__ void __launch_bounds__(T) gemv_kernel(int n, const double* __restrict__ M, const double* __restrict__ b,
+                                                 double* __restrict__ x, int accumulate,
+                                                 const unsigned char* __restrict__ mask_out,
+                                                 unsigned long long* stamp) {
   stamp_fold(stamp);
-  __shared__ double red[kGemvThreads / 32];
+  __shared__ double red[T / 32];
   const int row = blockIdx.x;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   pdl_trigger();
   // the inverse and the mask are setup data: the row's first batch is
   // fetched before the dependency wait (see csr_kernel)
   const double* Mr = M + (size_t)row * n;
-  constexpr int U = 8;
   double mv[U];
   auto load = [&](int jb) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int j = jb + kGemvThreads * u;
+      const int j = jb + T * u;
       mv[u] = j < n ? __ldg(Mr + j) : 0.0;
     }
   };
@@ -278,15 +280,15 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(int n, const double*
   double xo = 0.0;
   if (t == 0 && accumulate) xo = x[row];
   double s = 0.0;
-  for (int jb = t; jb < n; jb += kGemvThreads * U) {
+  for (int jb = t; jb < n; jb += T * U) {
     double bv[U], mc[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int j = jb + kGemvThreads * u;
+      const int j = jb + T * u;
       bv[u] = j < n ? __ldg(b + j) : 0.0;
       mc[u] = mv[u];
     }
-    if (jb + kGemvThreads * U < n) load(jb + kGemvThreads * U);
+    if (jb + T * U < n) load(jb + T * U);
 #pragma unroll
     for (int u = 0; u < U; ++u) s = fma(mc[u], bv[u], s);
   }
@@ -297,7 +299,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(int n, const double*
   if (t == 0) {
     double z = 0.0;
 #pragma unroll
-    for (int w = 0; w < kGemvThreads / 32; ++w) z += red[w];
+    for (int w = 0; w < T / 32; ++w) z += red[w];
     x[row] = mo ? 0.0 : (accumulate ? xo + z : z);
   }
   stamp_end(stamp);
