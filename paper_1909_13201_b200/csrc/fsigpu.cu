@@ -172,7 +172,7 @@ static inline void counted(int k = 1) { g_launches += k; }
 // ------------------------------------------------------------ CSR
 // Lanes per row: the power of two nearest to avg_nnz / target. The entries
 // per lane that hide latency best grow with the level size: ~2 on tiny
-// levels (< 16k rows), 8 from 16k to 128k rows, 16 on HBM-bound levels, where
+// levels (< 16k rows), 8 from 16k to 64k rows, 16 on HBM-bound levels, where
 // fewer lanes per row keep more rows -- hence more independent loads -- in
 // flight per warp. Batch depth: tiny levels take the smallest batch that
 // holds a lane's whole share (4 or 8), 16k..64k rows 8, larger levels 4.
@@ -184,7 +184,7 @@ static inline void counted(int k = 1) { g_launches += k; }
 // HBM-bound levels keep the cold-sweep rule.
 static int choose_lpr(long long rows, long long nnz) {
   if (rows <= 0) return 2;
-  const double target = rows < 16384 ? 2.0 : rows < 131072 ? 8.0 : 16.0;
+  const double target = rows < 16384 ? 2.0 : rows < 65536 ? 8.0 : 16.0;
   const double want = (double)nnz / rows / target;
   int l = 2;
   while (l < 32 && want > l * 1.41421356) l *= 2;
@@ -1247,9 +1247,12 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
   // sweeps on config 2 (profiles/r01_tune_cfg2full_pair.txt): L4 5.0 -> 5.3,
   // L3 3.9 -> 4.2, L2 2.6 -> 2.8 TB/s. The FS operator (long rows) stays on
   // the scalar kernel, which is faster there.
+  // In-graph sweep on config 2 (profiles/r02_tune_ingraph_cfg2.txt): 4 lanes
+  // with 2 pairs per batch on every such level (1.25M rows 237 -> 217 us,
+  // 313k 61 -> 55, 78k 19.4 -> 15.6).
   if (d.n >= 65536 || force_big()) {
-    L.A.lpr = d.n >= 131072 ? 4 : 8;
-    L.A.unroll = 24;
+    L.A.lpr = 4;
+    L.A.unroll = 22;
   }
   L.rmask.upload(d.row_mask, (size_t)d.n, s);
   L.cmask.upload(d.col_mask, (size_t)d.n, s);
@@ -1275,9 +1278,9 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
   if (d.nc >= 65536) {
     L.R.lpr = 2;
     L.R.unroll = 24;
-  } else if (d.nc >= 16384) {
+  } else if (d.nc >= 16384) {  // in-graph on config 2 (20k coarse rows): 3.5 -> 1.6 us with pairs
     L.R.lpr = 8;
-    L.R.unroll = 8;
+    L.R.unroll = 22;
   } else {  // in-graph sweep on config 0: 1.29 -> 1.10 us (5,124 coarse rows)
     L.R.lpr = 4;
     L.R.unroll = 24;
@@ -1322,7 +1325,7 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
     // its P half already adds 2 loads per lane to each batch: on large
     // (HBM-bound) levels batches of 4 AP entries; on small (L2-resident)
     // ones half the lanes with batches of 8 (warm sweeps, tools/tune_spmv.py)
-    const bool pair_ap = d.n >= 131072 || (force_big() && d.n >= 4096);
+    const bool pair_ap = d.n >= 65536 || (force_big() && d.n >= 4096);
     if (d.n < 16384 && !pair_ap) {
       L.AP.lpr = std::max(2, L.AP.lpr / 2);
       L.AP.unroll = 8;
@@ -1333,8 +1336,9 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
       // HBM-bound levels: the A*P half as 16-byte pairs (cold sweeps on the
       // config-2 hierarchy, profiles/r01_tune_cfg2full_ap.txt: L4 227 -> 190
       // us at 2 lanes x 4 pairs, L3 67 -> 60 us at 4 lanes x 2 pairs)
+      // (78k rows, in-graph: 18.1 -> 14.1 us at 4 lanes x 4 pairs)
       L.AP.lpr = d.n >= 1048576 ? 2 : 4;
-      L.AP.unroll = d.n >= 1048576 ? 24 : 22;
+      L.AP.unroll = d.n >= 1048576 || d.n < 131072 ? 24 : 22;
     } else {
       L.AP.unroll = 4;
     }
