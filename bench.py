@@ -543,7 +543,9 @@ def run_ours(args, ws, rank, local):
                                "timed with CUDA events on the library stream. achieved_insolve: the same launches "
                                "with graphs off and CUDA events around each launch (launch gaps included); "
                                "achieved_cold / achieved_warm: the kernel alone per launch after a 256 MB L2 flush / "
-                               "back to back, CUDA events; bytes = algorithmic bytes per launch (DESIGN 3.6)"},
+                               "back to back, CUDA events; bytes = algorithmic bytes per launch (DESIGN 3.6). Inside a "
+                               "solve the 41 MB operator of config 0 is served from the 126 MB L2 (two reads per "
+                               "step), so `frac` against the HBM copy peak (the contract's denominator) can reach 1"},
         "ingraph_kernels": ingraph,
         "insolve_kernel_classes": insolve,
         "insolve_per_level": per_level,
@@ -716,12 +718,16 @@ def config34_bench(fsigpu, torch, hbm_peak, steps=3):
         sizes = np.array([len(x) for x in sets], dtype=np.float64)
         fsigpu.DenseBlocks.from_csr(A, sets)  # warm-up
         torch.cuda.synchronize()
-        t0 = time.time()
-        B = fsigpu.DenseBlocks.from_csr(A, sets)
-        torch.cuda.synchronize()
-        lu_s = time.time() - t0
+        lu_s = None
+        for _ in range(3):  # host-side call (index upload, allocations): the best of 3
+            t0 = time.time()
+            B = fsigpu.DenseBlocks.from_csr(A, sets)
+            torch.cuda.synchronize()
+            dt = time.time() - t0
+            lu_s = dt if lu_s is None else min(lu_s, dt)
+            del B
         flops = float(np.sum(2.0 / 3.0 * sizes ** 3))
-        del B, A
+        del A
         t0 = time.time()
         G = fsigpu.GmgPreconditioner(P.levels)
         S = fsigpu.GmresSolver(G, P.frame_scale, restart=30)
@@ -753,8 +759,8 @@ def config34_bench(fsigpu, torch, hbm_peak, steps=3):
             "lu": {"blocks": int(top.as1.n), "gflop": flops / 1e9, "seconds": lu_s,
                    "tflops": flops / lu_s / 1e12, "fp64_peak_tflops": peak, "peak_kind": peak_kind,
                    "frac_of_fp64_peak": flops / lu_s / 1e12 / peak,
-                   "timing": "wall clock of one synchronous fsigpu_blocks_factor_csr (extraction + bit-exact LU + "
-                             "solve format) after a warm-up"},
+                   "timing": "wall clock of a synchronous fsigpu_blocks_factor_csr (extraction + bit-exact LU + "
+                             "solve format), best of 3 after a warm-up"},
             "setup_s": setup_s, "export_s": export_s, "steps": steps}
         del S, G, P, b, x, flush
         torch.cuda.empty_cache()

@@ -855,3 +855,57 @@ def test_vcycle_properties(cfg0, mode):
     s1 = fsigpu.gmres(G, cfg0.frame_scale, cfg0.b, cfg)
     s2 = fsigpu.gmres(G, cfg0.frame_scale, cfg0.b, cfg)
     assert s1.iterations == s2.iterations and np.array_equal(s1.x, s2.x)
+
+
+def test_device_clock_stamps(cfg0):
+    """fsigpu_stamps_*: kernel durations inside the captured restart-cycle
+    graph. Every kernel of a step is stamped once per FGMRES step (the FS
+    smoother twice per level), the stamped kernels fit inside the solve's own
+    event-timed duration, the iterate is bit-identical with and without the
+    stamps, and disabling them re-captures a graph that runs as before."""
+    import torch
+    P = cfg0
+    G = fsigpu.GmgPreconditioner(P.levels)
+    S = fsigpu.GmresSolver(G, P.frame_scale, restart=30)
+    cfg = fsigpu.KrylovConfig(restart=30, max_iters=2000, rel_tol=1e-10, abs_tol=1e-300)
+    base = S.solve(P.b, cfg)
+    top = len(P.levels) - 1
+    stream = torch.cuda.ExternalStream(G.stream())
+    b = torch.from_numpy(P.b).cuda()
+    x = torch.zeros(P.b.shape[0], dtype=torch.float64, device="cuda")
+    fsigpu.Stamps.enable(True)
+    try:
+        S.solve_dev(b.data_ptr(), x.data_ptr(), cfg)  # re-capture with the stamp slots
+        fsigpu.Stamps.enable(True)                    # reset the counters
+        x.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r = S.solve_dev(b.data_ptr(), x.data_ptr(), cfg)
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        its = r.iterations
+        assert its == base.iterations
+        total_us = 0.0
+        for lvl in range(1, top + 1):
+            fs = fsigpu.Stamps.read("block_solve", lvl, 0)
+            assert fs["launches"] == 2 * its, (lvl, fs)
+            for cls, sub in [("spmv", 0), ("transfer", 0), ("transfer", 1)]:
+                v = fsigpu.Stamps.read(cls, lvl, sub)
+                assert v["launches"] == its and v["us"] > 0, (cls, lvl, sub, v)
+                total_us += v["us"]
+            total_us += fs["us"]
+        co = fsigpu.Stamps.read("coarse", 0, 0)
+        assert co["launches"] == its
+        total_us += co["us"]
+        for sub in range(3):
+            v = fsigpu.Stamps.read("arnoldi", -1, sub)
+            assert v["launches"] == its, (sub, v)
+            total_us += v["us"]
+        assert 0.3 * ms * 1000.0 < total_us < ms * 1000.0, (total_us, ms)
+        assert np.array_equal(x.cpu().numpy(), base.x)
+    finally:
+        fsigpu.Stamps.enable(False)
+    again = S.solve(P.b, cfg)
+    assert again.iterations == base.iterations and np.array_equal(again.x, base.x)
