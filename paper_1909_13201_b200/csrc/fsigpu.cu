@@ -1069,6 +1069,12 @@ static void assemble_fs(Level& L, const fsigpu_level_desc& d, const std::vector<
   FSI_CUDA(cudaMemcpyAsync(fv.p, uvals.p, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
   FSI_CUDA(cudaStreamSynchronize(s));
   L.FS.adopt(L.n, L.n, std::move(ptr), std::move(cols), std::move(fv));
+  // the 3D FS operator's rows are several hundred entries long: 16 lanes with
+  // batches of 8 on large levels (232k rows: 220 -> 211 us in-graph)
+  if (L.n >= 65536 && (double)L.FS.nnz / L.n > 400.0) {
+    L.FS.lpr = 16;
+    L.FS.unroll = 8;
+  }
   L.assembled = true;
 }
 
@@ -1250,9 +1256,12 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
   // In-graph sweep on config 2 (profiles/r02_tune_ingraph_cfg2.txt): 4 lanes
   // with 2 pairs per batch on every such level (1.25M rows 237 -> 217 us,
   // 313k 61 -> 55, 78k 19.4 -> 15.6).
+  // Rows of the 3D hierarchies are longer (~176 entries): 8 lanes and
+  // scalar batches of 8 there (232k rows: 111 -> 90 us, r02_tune_ingraph_3d.txt).
   if (d.n >= 65536 || force_big()) {
-    L.A.lpr = 4;
-    L.A.unroll = 22;
+    const double per_row = (double)L.A.nnz / std::max(1, d.n);
+    L.A.lpr = per_row > 100.0 ? 8 : 4;
+    L.A.unroll = per_row > 100.0 ? 8 : 22;
   }
   L.rmask.upload(d.row_mask, (size_t)d.n, s);
   L.cmask.upload(d.col_mask, (size_t)d.n, s);
@@ -1281,9 +1290,11 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
   } else if (d.nc >= 16384) {  // in-graph on config 2 (20k coarse rows): 3.5 -> 1.6 us with pairs
     L.R.lpr = 8;
     L.R.unroll = 22;
-  } else {  // in-graph sweep on config 0: 1.29 -> 1.10 us (5,124 coarse rows)
-    L.R.lpr = 4;
-    L.R.unroll = 24;
+  } else {
+    // small coarse levels: 32 lanes keep every SM busy (in-graph sweeps: the 3D
+    // hierarchy's 4.6k coarse rows 4.1 -> 1.7 us; config 0 within 0.1 us of its best)
+    L.R.lpr = 32;
+    L.R.unroll = 22;
   }
   tr.reset(new SetupTrace("A*P", l));
   // AP_m = A * diag(!col_mask) * P on the device (ap_row_kernel); rows with
@@ -1329,16 +1340,22 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
     if (d.n < 16384 && !pair_ap) {
       L.AP.lpr = std::max(2, L.AP.lpr / 2);
       L.AP.unroll = 8;
-    } else if (d.n < 65536 && !pair_ap) {  // in-graph sweep on config 0 (20k rows): 4.51 -> 4.27 us
-      L.AP.lpr = 8;
-      L.AP.unroll = 22;
+    } else if (d.n < 65536 && !pair_ap) {
+      // in-graph sweeps: config 0 (20k rows, 35 entries per row) 4.5 -> 4.3-4.4 us
+      // at 8 lanes with pairs; the 3D hierarchy (31k rows) 18.5 -> 13 us at
+      // 8-16 lanes x 4 pairs
+      const double want = (double)L.AP.nnz / std::max(1, d.n) / 4.0;
+      int l = 8;
+      while (l < 32 && want > l * 1.41421356) l *= 2;
+      L.AP.lpr = l;
+      L.AP.unroll = (double)L.AP.nnz / std::max(1, d.n) > 40.0 ? 24 : 22;
     } else if (pair_ap) {
       // HBM-bound levels: the A*P half as 16-byte pairs (cold sweeps on the
       // config-2 hierarchy, profiles/r01_tune_cfg2full_ap.txt: L4 227 -> 190
       // us at 2 lanes x 4 pairs, L3 67 -> 60 us at 4 lanes x 2 pairs)
       // (78k rows, in-graph: 18.1 -> 14.1 us at 4 lanes x 4 pairs)
       L.AP.lpr = d.n >= 1048576 ? 2 : 4;
-      L.AP.unroll = d.n >= 1048576 || d.n < 131072 ? 24 : 22;
+      L.AP.unroll = 24;  // 4 pairs per batch on every such level (232k rows 3D: 82.6 -> 73.1 us)
     } else {
       L.AP.unroll = 4;
     }

@@ -39,6 +39,7 @@ def measure(level, which):
 
 for lev in range(top, 0, -1):
     for which in ["FS", "A", "AP", "R"]:
+        measure(lev, which)  # warm-up: the first measurement after a re-capture reads high
         base = measure(lev, which)
         res = []
         for lpr in [2, 4, 8, 16, 32]:
