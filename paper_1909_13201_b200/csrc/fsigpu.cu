@@ -260,8 +260,54 @@ struct Csr {
     unroll = choose_unroll(r, nnz, lpr);
     h_ptr = ptr.download();
   }
+  // column-pair format (sparse.cuh csr2_kernel): built for the FS operator
+  // and the level operator when the column count is even
+  DevBuf<int> ptr2, idx2;
+  DevBuf<double2> val2;
+  long long n2 = 0;  // elements (pairs)
+  bool pairs = false;
+  void build_pairs(cudaStream_t s) {
+    pairs = false;
+    // HBM-bound levels only: on L2-resident levels the bytes saved do not
+    // matter and the wider loads cost occupancy (config 0 in-graph: fine FS
+    // 6.5 -> 6.9 us, fine residual 3.5 -> 4.5 us with pairs; config 2: 1.25M rows
+    // FS 692 -> 669 us, residual 220 -> 195 us, 20k rows FS 13.9 -> 14.9 us)
+    if (rows < 65536 || (cols & 1) || pairs_disabled()) return;
+    ptr2.alloc((size_t)rows + 1);
+    ptr2.zero(s);
+    csr2_build_kernel<<<ceil_div(rows, 128), 128, 0, s>>>(rows, ptr.p, idx.p, val.p, ptr2.p, nullptr, nullptr, 0);
+    FSI_CHECK_LAUNCH();
+    thrust::device_ptr<int> pp(ptr2.p);
+    thrust::inclusive_scan(thrust::cuda::par.on(s), pp, pp + rows + 1, pp);
+    int total = 0;
+    FSI_CUDA(cudaMemcpyAsync(&total, ptr2.p + rows, sizeof(int), cudaMemcpyDeviceToHost, s));
+    FSI_CUDA(cudaStreamSynchronize(s));
+    n2 = total;
+    // worth it only when most entries pair up (20 B per element against 12 B per entry)
+    if (20.0 * n2 > 0.95 * 12.0 * nnz) return;
+    idx2.alloc((size_t)n2 + 4);
+    val2.alloc((size_t)n2 + 4);
+    csr2_build_kernel<<<ceil_div(rows, 128), 128, 0, s>>>(rows, ptr.p, idx.p, val.p, ptr2.p, idx2.p, val2.p, 1);
+    FSI_CHECK_LAUNCH();
+    FSI_CUDA(cudaStreamSynchronize(s));
+    pairs = true;
+    // launch shape of csr2_kernel from the in-graph sweep on config 2
+    // (profiles/r02_tune_pairs_cfg2.txt): ~16 elements per lane (8 on levels
+    // below 128k rows with short rows), batches of 2 elements
+    const double per_row = (double)n2 / rows;
+    const double want = per_row / ((rows >= 131072 || per_row > 64.0) ? 16.0 : 8.0);
+    int l = 2;
+    while (l < 32 && want > l * 1.41421356) l *= 2;
+    lpr = l;
+    unroll = 4;
+  }
+  static bool pairs_disabled() {
+    const char* e = std::getenv("FSIGPU_COLUMN_PAIRS");
+    return e && e[0] == '0';
+  }
   double bytes(bool resid) const {
-    return 12.0 * nnz + 4.0 * (rows + 1) + 8.0 * cols + 8.0 * rows + (resid ? 8.0 * rows : 0.0);
+    const double mat = pairs ? 20.0 * n2 : 12.0 * nnz;
+    return mat + 4.0 * (rows + 1) + 8.0 * cols + 8.0 * rows + (resid ? 8.0 * rows : 0.0);
   }
   int unroll = 4;  // entries per lane per predicated batch (4 or 8); 22/24: paired loads, 2/4 pairs
   template <class G, class E>
@@ -269,6 +315,31 @@ struct Csr {
     if (!rows) return;
     const long long threads = (long long)rows * lpr;
     const int grid = ceil_div(threads, 256);
+    if (pairs && lpr >= 2) {
+      // column-pair format: batches of 2 (unroll 4 / 22) or 4 (unroll 8 / 24) elements per lane
+#define FSI_CSR2(LP, UU) launch_k(csr2_kernel<LP, G, E, UU>, dim3(grid), dim3(256), 0, s, rows, (const int*)ptr2.p, (const int*)idx2.p, (const double2*)val2.p, g, e, cur_stamp(0))
+      if (unroll == 8 || unroll == 24) {
+        switch (lpr) {
+          case 2: FSI_CSR2(2, 4); break;
+          case 4: FSI_CSR2(4, 4); break;
+          case 8: FSI_CSR2(8, 4); break;
+          case 16: FSI_CSR2(16, 4); break;
+          default: FSI_CSR2(32, 4); break;
+        }
+      } else {
+        switch (lpr) {
+          case 2: FSI_CSR2(2, 2); break;
+          case 4: FSI_CSR2(4, 2); break;
+          case 8: FSI_CSR2(8, 2); break;
+          case 16: FSI_CSR2(16, 2); break;
+          default: FSI_CSR2(32, 2); break;
+        }
+      }
+#undef FSI_CSR2
+      FSI_CHECK_LAUNCH();
+      counted();
+      return;
+    }
 #define FSI_CSR(LP, UU) launch_k(csr_kernel<LP, G, E, UU>, dim3(grid), dim3(256), 0, s, rows, (const int*)ptr.p, (const int*)idx.p, (const double*)val.p, g, e, cur_stamp(0))
 #define FSI_CSRP(LP, UU) launch_k(csr_pair_kernel<LP, G, E, UU>, dim3(grid), dim3(256), 0, s, rows, (const int*)ptr.p, (const int*)idx.p, (const double*)val.p, g, e, cur_stamp(0))
     if (unroll == 22 || unroll == 24) {  // paired loads, 2 or 4 pairs per lane per batch
@@ -1075,6 +1146,7 @@ static void assemble_fs(Level& L, const fsigpu_level_desc& d, const std::vector<
     L.FS.lpr = 16;
     L.FS.unroll = 8;
   }
+  L.FS.build_pairs(s);
   L.assembled = true;
 }
 
@@ -1263,6 +1335,7 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
     L.A.lpr = per_row > 100.0 ? 8 : 4;
     L.A.unroll = per_row > 100.0 ? 8 : 22;
   }
+  L.A.build_pairs(s);
   L.rmask.upload(d.row_mask, (size_t)d.n, s);
   L.cmask.upload(d.col_mask, (size_t)d.n, s);
   L.rbuf.alloc(d.n);

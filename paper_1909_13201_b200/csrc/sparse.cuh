@@ -217,6 +217,111 @@ __global__ void __launch_bounds__(256) csr_pair_kernel(int rows, const int* __re
   stamp_end(stamp);
 }
 
+// ---- column-pair CSR ("BSR 1 x 2") ---------------------------------------
+// The unknowns of the vector fields sit in (x, y) component pairs at
+// consecutive frame positions, so the columns of a level-operator or FS-
+// operator row come in aligned pairs (2c, 2c + 1): on config 0 every entry of
+// the assembled FS operator and 97% of the entries of A. One element stores
+// the pair's index c and both values (a missing partner is an explicit 0.0):
+// 20 bytes per two entries instead of 24, one 4-B index load, one 16-B value
+// load and ONE 16-B gather of x per two entries instead of two of each. The
+// vector CSR kernels were L1/TEX-request bound before DRAM (ncu, round 1).
+// Needs an even column count (the gathers read x as double2).
+struct GatherPlain2 {
+  const double* x;
+  __device__ double2 operator()(int c2) const { return __ldg(reinterpret_cast<const double2*>(x) + c2); }
+};
+struct GatherMasked2 {
+  const double* x;
+  const unsigned char* mask;
+  __device__ double2 operator()(int c2) const {
+    const uchar2 m = __ldg(reinterpret_cast<const uchar2*>(mask) + c2);
+    double2 v = __ldg(reinterpret_cast<const double2*>(x) + c2);
+    if (m.x) v.x = 0.0;
+    if (m.y) v.y = 0.0;
+    return v;
+  }
+};
+__device__ __forceinline__ GatherPlain2 to_pairs(const GatherPlain& g) { return {g.x}; }
+__device__ __forceinline__ GatherMasked2 to_pairs(const GatherMasked& g) { return {g.x, g.mask}; }
+
+// csr_kernel on the column-pair format: LPR lanes per row, predicated
+// batches of U elements (= 2U entries) per lane, the same epilogues.
+template <int LPR, class Gather, class Epi, int U>
+__global__ void __launch_bounds__(256) csr2_kernel(int rows, const int* __restrict__ ptr,
+                                                   const int* __restrict__ idx,
+                                                   const double2* __restrict__ val, Gather gx1, Epi epi,
+                                                   unsigned long long* stamp) {
+  stamp_fold(stamp);
+  const auto gx = to_pairs(gx1);
+  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = (int)(gt / LPR);
+  const int lane = threadIdx.x & (LPR - 1);
+  const bool ok = row < rows;
+  pdl_trigger();
+  const int k0 = ok ? __ldg(ptr + row) : 0, k1 = ok ? __ldg(ptr + row + 1) : 0;
+  int c[U];
+  double2 v[U];
+  auto load = [&](int kb) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = kb + u * LPR;
+      const bool in = k < k1;
+      c[u] = in ? __ldg(idx + k) : -1;
+      v[u] = in ? __ldg(val + k) : make_double2(0.0, 0.0);
+    }
+  };
+  load(k0 + lane);
+  pdl_wait();
+  stamp_start(stamp);
+  EpiPre pe{0.0, 0};
+  if (ok && lane == 0) pe = epi.pre(row);
+  double s = 0.0;
+  for (int kb = k0 + lane; kb < k1; kb += U * LPR) {
+    double2 xv[U], vc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      xv[u] = c[u] >= 0 ? gx(c[u]) : make_double2(0.0, 0.0);
+      vc[u] = v[u];
+    }
+    if (kb + U * LPR < k1) load(kb + U * LPR);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      s = fma(vc[u].x, xv[u].x, s);
+      s = fma(vc[u].y, xv[u].y, s);
+    }
+  }
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, LPR);
+  if (ok && lane == 0) epi(row, s, pe);
+  stamp_end(stamp);
+}
+
+// setup: elements per row (pass 0, out = counts) / fill (pass 1) of the
+// column-pair format from a CSR with sorted columns; one thread per row
+__global__ void csr2_build_kernel(int rows, const int* __restrict__ ptr, const int* __restrict__ idx,
+                                  const double* __restrict__ val, int* __restrict__ ptr2, int* __restrict__ idx2,
+                                  double2* __restrict__ val2, int pass) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int k0 = ptr[r], k1 = ptr[r + 1];
+  int n = 0, o = pass ? ptr2[r] : 0;
+  for (int k = k0; k < k1;) {
+    const int c = idx[k], c2 = c >> 1;
+    const bool two = k + 1 < k1 && (idx[k + 1] >> 1) == c2;  // sorted: (2 c2, 2 c2 + 1)
+    if (pass) {
+      double2 v;
+      if (two) v = make_double2(val[k], val[k + 1]);
+      else v = (c & 1) ? make_double2(0.0, val[k]) : make_double2(val[k], 0.0);
+      idx2[o + n] = c2;
+      val2[o + n] = v;
+    }
+    ++n;
+    k += two ? 2 : 1;
+  }
+  if (!pass) ptr2[r + 1] = n;
+}
+
 // FS combine on one level (precond.cpp:42-57 additive + 271-287 + 305-317):
 //   p <  g1, p >= g1+n_us : z = sum_{(b,i) covering p, block order} delta / cover
 //   g1 <= p < g1+n_us     : z = r[p] / lumped[p-g1]
