@@ -755,6 +755,24 @@ struct Level {
 static void launch_prolong_resid(const Level& L, const double* ec, const unsigned char* cmask_coarse,
                                  const double* r_pre, double* r, cudaStream_t s) {
   const int grid = ceil_div((long long)L.n * L.AP.lpr, 256);
+  if (L.AP.pairs && L.AP.lpr >= 2) {
+#define FSI_PR2(LP, UA)                                                                                         \
+  launch_k(prolong_resid2_kernel<LP, UA>, dim3(grid), dim3(256), 0, s, L.n, (const int*)L.P.ptr.p,             \
+           (const int*)L.P.idx.p, (const double*)L.P.val.p, (const int*)L.AP.ptr2.p, (const int*)L.AP.idx2.p,  \
+           (const double2*)L.AP.val2.p, ec, cmask_coarse, (const unsigned char*)L.cmask.p, L.x, r_pre, r,      \
+           cur_stamp(1))
+    const bool four = L.AP.unroll == 8 || L.AP.unroll == 24;
+    switch (L.AP.lpr) {
+      case 2: if (four) FSI_PR2(2, 4); else FSI_PR2(2, 2); break;
+      case 4: if (four) FSI_PR2(4, 4); else FSI_PR2(4, 2); break;
+      case 8: if (four) FSI_PR2(8, 4); else FSI_PR2(8, 2); break;
+      case 16: if (four) FSI_PR2(16, 4); else FSI_PR2(16, 2); break;
+      default: if (four) FSI_PR2(32, 4); else FSI_PR2(32, 2); break;
+    }
+#undef FSI_PR2
+    FSI_CHECK_LAUNCH();
+    return;
+  }
 #define FSI_PR(K, LP, UA)                                                                                        \
   launch_k(K<LP, UA>, dim3(grid), dim3(256), 0, s, L.n, (const int*)L.P.ptr.p, (const int*)L.P.idx.p,         \
            (const double*)L.P.val.p, (const int*)L.AP.ptr.p, (const int*)L.AP.idx.p, (const double*)L.AP.val.p, \
@@ -1431,6 +1449,15 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
       L.AP.unroll = 24;  // 4 pairs per batch on every such level (232k rows 3D: 82.6 -> 73.1 us)
     } else {
       L.AP.unroll = 4;
+    }
+    // column-pair format of A*P on the large levels (keeps the lane count, 2 elements per batch)
+    {
+      const int keep_lpr = L.AP.lpr;
+      L.AP.build_pairs(s);
+      if (L.AP.pairs) {
+        L.AP.lpr = keep_lpr;
+        L.AP.unroll = 4;
+      }
     }
   }
   require(d.g1 >= 0 && d.n_us >= 0 && d.g1 + d.n_us <= d.n, "fs: bad group sizes");

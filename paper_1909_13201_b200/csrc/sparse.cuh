@@ -643,6 +643,110 @@ __global__ void __launch_bounds__(256) prolong_resid_kernel(int rows, const int*
   stamp_end(stamp);
 }
 
+// prolong_resid_kernel with the A*P half in the column-pair format (one
+// element = columns 2c, 2c + 1 of the coarse iterate: 20 bytes and one
+// 16-byte gather per two entries; large levels), UA elements per lane per
+// batch. The P half stays scalar.
+template <int LPR, int UA>
+__global__ void __launch_bounds__(256) prolong_resid2_kernel(int rows, const int* __restrict__ pp,
+                                                             const int* __restrict__ pi, const double* __restrict__ pv,
+                                                             const int* __restrict__ ap, const int* __restrict__ ai,
+                                                             const double2* __restrict__ av, const double* ec,
+                                                             const unsigned char* __restrict__ cmask_coarse,
+                                                             const unsigned char* __restrict__ cmask, double* x,
+                                                             const double* r_pre, double* r, unsigned long long* stamp) {
+  stamp_fold(stamp);
+  constexpr int UP = (9 + LPR - 1) / LPR > 2 ? (9 + LPR - 1) / LPR : 2;
+  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = (int)(gt / LPR);
+  const int lane = threadIdx.x & (LPR - 1);
+  const bool ok = row < rows;
+  pdl_trigger();
+  int p0 = 0, p1 = 0, a0 = 0, a1 = 0;
+  if (ok) {
+    p0 = __ldg(pp + row);
+    p1 = __ldg(pp + row + 1);
+    a0 = __ldg(ap + row);
+    a1 = __ldg(ap + row + 1);
+  }
+  unsigned char cm = 1;
+  if (ok && lane == 0) cm = __ldg(cmask + row);
+  double s1 = 0.0, s2 = 0.0;
+  int kp = p0 + lane, ka = a0 + lane;
+  int c[UP], c2[UA];
+  double v[UP];
+  double2 v2[UA];
+#pragma unroll
+  for (int u = 0; u < UP; ++u) {
+    const int k = kp + u * LPR;
+    const bool in = k < p1;
+    c[u] = in ? __ldg(pi + k) : -1;
+    v[u] = in ? __ldg(pv + k) : 0.0;
+  }
+  auto load2 = [&](int kb) {
+#pragma unroll
+    for (int u = 0; u < UA; ++u) {
+      const int k = kb + u * LPR;
+      const bool in = k < a1;
+      c2[u] = in ? __ldg(ai + k) : -1;
+      v2[u] = in ? __ldg(av + k) : make_double2(0.0, 0.0);
+    }
+  };
+  load2(ka);
+  pdl_wait();
+  stamp_start(stamp);
+  double xo = 0.0, rp = 0.0;
+  if (ok && lane == 0) {
+    xo = x[row];
+    rp = r_pre[row];
+  }
+  auto gather = [&](int cc) -> double {
+    return cc >= 0 ? ((cmask_coarse && __ldg(cmask_coarse + cc)) ? 0.0 : __ldg(ec + cc)) : 0.0;
+  };
+  auto gather2 = [&](int cc) -> double2 {
+    if (cc < 0) return make_double2(0.0, 0.0);
+    double2 e = __ldg(reinterpret_cast<const double2*>(ec) + cc);
+    if (cmask_coarse) {
+      const uchar2 m = __ldg(reinterpret_cast<const uchar2*>(cmask_coarse) + cc);
+      if (m.x) e.x = 0.0;
+      if (m.y) e.y = 0.0;
+    }
+    return e;
+  };
+  {
+    double xv[UP];
+#pragma unroll
+    for (int u = 0; u < UP; ++u) xv[u] = gather(c[u]);
+#pragma unroll
+    for (int u = 0; u < UP; ++u) s1 = fma(v[u], xv[u], s1);
+  }
+  for (kp += UP * LPR; kp < p1; kp += LPR) s1 = fma(__ldg(pv + kp), gather(__ldg(pi + kp)), s1);
+  for (; ka < a1; ka += UA * LPR) {
+    double2 xv[UA], vc[UA];
+#pragma unroll
+    for (int u = 0; u < UA; ++u) {
+      xv[u] = gather2(c2[u]);
+      vc[u] = v2[u];
+    }
+    if (ka + UA * LPR < a1) load2(ka + UA * LPR);
+#pragma unroll
+    for (int u = 0; u < UA; ++u) {
+      s2 = fma(vc[u].x, xv[u].x, s2);
+      s2 = fma(vc[u].y, xv[u].y, s2);
+    }
+  }
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) {
+    s1 += __shfl_xor_sync(kFull, s1, o, LPR);
+    s2 += __shfl_xor_sync(kFull, s2, o, LPR);
+  }
+  if (ok && lane == 0) {
+    if (!cm) x[row] = xo + s1;
+    r[row] = rp - s2;
+  }
+  stamp_end(stamp);
+}
+
 // prolong_resid_kernel with the A*P half streamed as 16-byte pairs (int2
 // columns, double2 values; see csr_pair_kernel), UA pairs per lane per
 // batch. The P half and the first A*P batch are still fetched together.
