@@ -266,13 +266,13 @@ struct Csr {
   DevBuf<double2> val2;
   long long n2 = 0;  // elements (pairs)
   bool pairs = false;
-  void build_pairs(cudaStream_t s) {
+  void build_pairs(cudaStream_t s, bool any_size = false) {
     pairs = false;
     // HBM-bound levels only: on L2-resident levels the bytes saved do not
     // matter and the wider loads cost occupancy (config 0 in-graph: fine FS
     // 6.5 -> 6.9 us, fine residual 3.5 -> 4.5 us with pairs; config 2: 1.25M rows
     // FS 692 -> 669 us, residual 220 -> 195 us, 20k rows FS 13.9 -> 14.9 us)
-    if (rows < 65536 || (cols & 1) || pairs_disabled()) return;
+    if ((rows < 65536 && !any_size) || !rows || (cols & 1) || pairs_disabled()) return;
     ptr2.alloc((size_t)rows + 1);
     ptr2.zero(s);
     csr2_build_kernel<<<ceil_div(rows, 128), 128, 0, s>>>(rows, ptr.p, idx.p, val.p, ptr2.p, nullptr, nullptr, 0);
@@ -301,12 +301,52 @@ struct Csr {
     lpr = l;
     unroll = 4;
   }
+  // 2 x 2 blocks on top of the column pairs (sparse.cuh bsr22_kernel): the FS
+  // operator of the large levels, where the two component rows of a node
+  // share their pattern
+  DevBuf<int> ptrb, idxb;
+  DevBuf<double2> valb;
+  long long nb22 = 0;
+  bool blocks22 = false;
+  void build_blocks22(cudaStream_t s) {
+    blocks22 = false;
+    const char* e = std::getenv("FSIGPU_BLOCKS22");
+    if (!pairs || (rows & 1) || (e && e[0] == '0')) return;
+    const int rp = rows / 2;
+    ptrb.alloc((size_t)rp + 1);
+    ptrb.zero(s);
+    bsr22_build_kernel<<<ceil_div(rp, 128), 128, 0, s>>>(rp, ptr2.p, idx2.p, val2.p, ptrb.p, nullptr, nullptr, 0);
+    FSI_CHECK_LAUNCH();
+    thrust::device_ptr<int> pp(ptrb.p);
+    thrust::inclusive_scan(thrust::cuda::par.on(s), pp, pp + rp + 1, pp);
+    int total = 0;
+    FSI_CUDA(cudaMemcpyAsync(&total, ptrb.p + rp, sizeof(int), cudaMemcpyDeviceToHost, s));
+    FSI_CUDA(cudaStreamSynchronize(s));
+    nb22 = total;
+    if (36.0 * nb22 > 0.98 * 20.0 * n2) return;  // the row patterns differ too often
+    idxb.alloc((size_t)nb22 + 4);
+    valb.alloc(2 * (size_t)nb22 + 8);
+    bsr22_build_kernel<<<ceil_div(rp, 128), 128, 0, s>>>(rp, ptr2.p, idx2.p, val2.p, ptrb.p, idxb.p, valb.p, 1);
+    FSI_CHECK_LAUNCH();
+    FSI_CUDA(cudaStreamSynchronize(s));
+    blocks22 = true;
+    // launch shape of bsr22_kernel (in-graph sweeps): the HBM-bound levels keep
+    // the pair format's lane count; L2-resident levels take ~3 blocks per lane
+    // (config 0 fine FS: 32 lanes 5.4 us, 8 lanes 22 us)
+    if (rows < 65536) {
+      const double want = (double)nb22 / (rows / 2) / 3.0;
+      int l = 2;
+      while (l < 32 && want > l * 1.41421356) l *= 2;
+      lpr = l;
+      unroll = 4;
+    }
+  }
   static bool pairs_disabled() {
     const char* e = std::getenv("FSIGPU_COLUMN_PAIRS");
     return e && e[0] == '0';
   }
   double bytes(bool resid) const {
-    const double mat = pairs ? 20.0 * n2 : 12.0 * nnz;
+    const double mat = blocks22 ? 36.0 * nb22 : pairs ? 20.0 * n2 : 12.0 * nnz;
     return mat + 4.0 * (rows + 1) + 8.0 * cols + 8.0 * rows + (resid ? 8.0 * rows : 0.0);
   }
   int unroll = 4;  // entries per lane per predicated batch (4 or 8); 22/24: paired loads, 2/4 pairs
@@ -315,6 +355,21 @@ struct Csr {
     if (!rows) return;
     const long long threads = (long long)rows * lpr;
     const int grid = ceil_div(threads, 256);
+    if (blocks22 && lpr >= 2) {
+      const int grid2 = ceil_div((long long)(rows / 2) * lpr, 256);
+#define FSI_BSR(LP, UU) launch_k(bsr22_kernel<LP, G, E, UU>, dim3(grid2), dim3(256), 0, s, rows / 2, (const int*)ptrb.p, (const int*)idxb.p, (const double2*)valb.p, g, e, cur_stamp(0))
+      switch (lpr) {
+        case 2: FSI_BSR(2, 2); break;
+        case 4: FSI_BSR(4, 2); break;
+        case 8: FSI_BSR(8, 2); break;
+        case 16: FSI_BSR(16, 2); break;
+        default: FSI_BSR(32, 2); break;
+      }
+#undef FSI_BSR
+      FSI_CHECK_LAUNCH();
+      counted();
+      return;
+    }
     if (pairs && lpr >= 2) {
       // column-pair format: batches of 2 (unroll 4 / 22) or 4 (unroll 8 / 24) elements per lane
 #define FSI_CSR2(LP, UU) launch_k(csr2_kernel<LP, G, E, UU>, dim3(grid), dim3(256), 0, s, rows, (const int*)ptr2.p, (const int*)idx2.p, (const double2*)val2.p, g, e, cur_stamp(0))
@@ -1164,7 +1219,18 @@ static void assemble_fs(Level& L, const fsigpu_level_desc& d, const std::vector<
     L.FS.lpr = 16;
     L.FS.unroll = 8;
   }
-  L.FS.build_pairs(s);
+  // 2 x 2 blocks from 16k rows up (in-graph: they also pay on the L2-resident
+  // fine level of config 0); the column pairs alone only on HBM-bound levels
+  {
+    const int keep_lpr = L.FS.lpr, keep_unroll = L.FS.unroll;
+    L.FS.build_pairs(s, L.n >= 16384);
+    L.FS.build_blocks22(s);
+    if (!L.FS.blocks22 && L.n < 65536) {  // plain CSR with its own launch shape
+      L.FS.pairs = false;
+      L.FS.lpr = keep_lpr;
+      L.FS.unroll = keep_unroll;
+    }
+  }
   L.assembled = true;
 }
 
@@ -1354,6 +1420,7 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
     L.A.unroll = per_row > 100.0 ? 8 : 22;
   }
   L.A.build_pairs(s);
+  L.A.build_blocks22(s);
   L.rmask.upload(d.row_mask, (size_t)d.n, s);
   L.cmask.upload(d.col_mask, (size_t)d.n, s);
   L.rbuf.alloc(d.n);

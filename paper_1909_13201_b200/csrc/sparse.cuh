@@ -297,6 +297,98 @@ __global__ void __launch_bounds__(256) csr2_kernel(int rows, const int* __restri
   stamp_end(stamp);
 }
 
+// ---- 2 x 2 block CSR on top of the column pairs --------------------------
+// The two component rows (2R, 2R + 1) of a node share their column pattern
+// in the FS operator, so a 2 x 2 block (rows 2R, 2R + 1 x columns 2c, 2c + 1)
+// needs ONE 4-byte index for four values: 36 bytes per four entries (9 per
+// entry against 10 for the column pairs and 12 for CSR), and one 16-byte
+// gather of x serves both rows. val holds {a(2R,2c), a(2R,2c+1)} and
+// {a(2R+1,2c), a(2R+1,2c+1)} as two consecutive double2. Patterns that
+// differ between the two rows are merged (explicit zeros). LPR lanes per ROW
+// PAIR, batches of U blocks per lane.
+template <int LPR, class Gather, class Epi, int U>
+__global__ void __launch_bounds__(256) bsr22_kernel(int row_pairs, const int* __restrict__ ptr,
+                                                    const int* __restrict__ idx,
+                                                    const double2* __restrict__ val, Gather gx1, Epi epi,
+                                                    unsigned long long* stamp) {
+  stamp_fold(stamp);
+  const auto gx = to_pairs(gx1);
+  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int rp = (int)(gt / LPR);
+  const int lane = threadIdx.x & (LPR - 1);
+  const bool ok = rp < row_pairs;
+  pdl_trigger();
+  const int k0 = ok ? __ldg(ptr + rp) : 0, k1 = ok ? __ldg(ptr + rp + 1) : 0;
+  int c[U];
+  double2 v0[U], v1[U];
+  auto load = [&](int kb) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = kb + u * LPR;
+      const bool in = k < k1;
+      c[u] = in ? __ldg(idx + k) : -1;
+      v0[u] = in ? __ldg(val + 2 * (size_t)k) : make_double2(0.0, 0.0);
+      v1[u] = in ? __ldg(val + 2 * (size_t)k + 1) : make_double2(0.0, 0.0);
+    }
+  };
+  load(k0 + lane);
+  pdl_wait();
+  stamp_start(stamp);
+  // lane 0 owns row 2 rp, lane 1 row 2 rp + 1 (their epilogue operands)
+  EpiPre pe{0.0, 0};
+  if (ok && lane < 2) pe = epi.pre(2 * rp + lane);
+  double s0 = 0.0, s1 = 0.0;
+  for (int kb = k0 + lane; kb < k1; kb += U * LPR) {
+    double2 xv[U], a0[U], a1[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      xv[u] = c[u] >= 0 ? gx(c[u]) : make_double2(0.0, 0.0);
+      a0[u] = v0[u];
+      a1[u] = v1[u];
+    }
+    if (kb + U * LPR < k1) load(kb + U * LPR);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      s0 = fma(a0[u].x, xv[u].x, s0);
+      s0 = fma(a0[u].y, xv[u].y, s0);
+      s1 = fma(a1[u].x, xv[u].x, s1);
+      s1 = fma(a1[u].y, xv[u].y, s1);
+    }
+  }
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) {
+    s0 += __shfl_xor_sync(kFull, s0, o, LPR);
+    s1 += __shfl_xor_sync(kFull, s1, o, LPR);
+  }
+  if (ok && lane < 2) epi(2 * rp + lane, lane ? s1 : s0, pe);
+  stamp_end(stamp);
+}
+
+// setup: blocks per row pair (pass 0) / fill (pass 1) from the column-pair
+// format (ptr2/idx2/val2 with sorted pair indices): merge of the two rows
+__global__ void bsr22_build_kernel(int row_pairs, const int* __restrict__ ptr2, const int* __restrict__ idx2,
+                                   const double2* __restrict__ val2, int* __restrict__ ptrb, int* __restrict__ idxb,
+                                   double2* __restrict__ valb, int pass) {
+  const int rp = blockIdx.x * blockDim.x + threadIdx.x;
+  if (rp >= row_pairs) return;
+  int a = ptr2[2 * rp], ae = ptr2[2 * rp + 1], b = ae, be = ptr2[2 * rp + 2];
+  int n = 0;
+  const int o = pass ? ptrb[rp] : 0;
+  while (a < ae || b < be) {
+    const int ca = a < ae ? idx2[a] : 0x7fffffff, cb = b < be ? idx2[b] : 0x7fffffff;
+    const int cmin = ca < cb ? ca : cb;
+    if (pass) {
+      idxb[o + n] = cmin;
+      valb[2 * (size_t)(o + n)] = ca == cmin ? val2[a] : make_double2(0.0, 0.0);
+      valb[2 * (size_t)(o + n) + 1] = cb == cmin ? val2[b] : make_double2(0.0, 0.0);
+    }
+    if (ca == cmin) ++a;
+    if (cb == cmin) ++b;
+    ++n;
+  }
+  if (!pass) ptrb[rp + 1] = n;
+}
+
 // setup: elements per row (pass 0, out = counts) / fill (pass 1) of the
 // column-pair format from a CSR with sorted columns; one thread per row
 __global__ void csr2_build_kernel(int rows, const int* __restrict__ ptr, const int* __restrict__ idx,
