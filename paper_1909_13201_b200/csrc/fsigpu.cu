@@ -1499,14 +1499,11 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
       L.AP.lpr = std::max(2, L.AP.lpr / 2);
       L.AP.unroll = 8;
     } else if (d.n < 65536 && !pair_ap) {
-      // in-graph sweeps: config 0 (20k rows, 35 entries per row) 4.5 -> 4.3-4.4 us
-      // at 8 lanes with pairs; the 3D hierarchy (31k rows) 18.5 -> 13 us at
-      // 8-16 lanes x 4 pairs
-      const double want = (double)L.AP.nnz / std::max(1, d.n) / 4.0;
-      int l = 8;
-      while (l < 32 && want > l * 1.41421356) l *= 2;
-      L.AP.lpr = l;
-      L.AP.unroll = (double)L.AP.nnz / std::max(1, d.n) > 40.0 ? 24 : 22;
+      // in-graph sweeps: config 0 (20k rows, 56 entries per row) 4.5 -> 4.3 us at
+      // 8 lanes x 2 pairs (16 lanes: 6.0 us); the 3D hierarchy (31k rows, longer
+      // rows) 8 lanes x 4 pairs
+      L.AP.lpr = 8;
+      L.AP.unroll = (double)L.AP.nnz / std::max(1, d.n) > 64.0 ? 24 : 22;
     } else if (pair_ap) {
       // HBM-bound levels: the A*P half as 16-byte pairs (cold sweeps on the
       // config-2 hierarchy, profiles/r01_tune_cfg2full_ap.txt: L4 227 -> 190
