@@ -810,6 +810,24 @@ struct Level {
 static void launch_prolong_resid(const Level& L, const double* ec, const unsigned char* cmask_coarse,
                                  const double* r_pre, double* r, cudaStream_t s) {
   const int grid = ceil_div((long long)L.n * L.AP.lpr, 256);
+  if (L.AP.blocks22 && L.AP.lpr >= 2) {
+    const int grid2 = ceil_div((long long)(L.n / 2) * L.AP.lpr, 256);
+#define FSI_PR22(LP)                                                                                              \
+  launch_k(prolong_resid22_kernel<LP, 2>, dim3(grid2), dim3(256), 0, s, L.n / 2, (const int*)L.P.ptr.p,          \
+           (const int*)L.P.idx.p, (const double*)L.P.val.p, (const int*)L.AP.ptrb.p, (const int*)L.AP.idxb.p,     \
+           (const double2*)L.AP.valb.p, ec, cmask_coarse, (const unsigned char*)L.cmask.p, L.x, r_pre, r,         \
+           cur_stamp(1))
+    switch (L.AP.lpr) {
+      case 2: FSI_PR22(2); break;
+      case 4: FSI_PR22(4); break;
+      case 8: FSI_PR22(8); break;
+      case 16: FSI_PR22(16); break;
+      default: FSI_PR22(32); break;
+    }
+#undef FSI_PR22
+    FSI_CHECK_LAUNCH();
+    return;
+  }
   if (L.AP.pairs && L.AP.lpr >= 2) {
 #define FSI_PR2(LP, UA)                                                                                         \
   launch_k(prolong_resid2_kernel<LP, UA>, dim3(grid), dim3(256), 0, s, L.n, (const int*)L.P.ptr.p,             \
@@ -1516,11 +1534,21 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
     }
     // column-pair format of A*P on the large levels (keeps the lane count, 2 elements per batch)
     {
-      const int keep_lpr = L.AP.lpr;
+      const int keep_lpr = L.AP.lpr, keep_unroll = L.AP.unroll;
+      // 2 x 2 blocks of A*P on the HBM-bound levels (config 2 in-graph: 1.25M rows
+      // 174 -> 159 us, 313k rows 48 -> 39 us; on config 0's 20k rows 3.7 -> 4.5 us, so not there)
       L.AP.build_pairs(s);
-      if (L.AP.pairs) {
+      L.AP.build_blocks22(s);
+      if (L.AP.blocks22) {
         L.AP.lpr = keep_lpr;
         L.AP.unroll = 4;
+      } else if (L.AP.pairs && d.n >= 65536) {
+        L.AP.lpr = keep_lpr;
+        L.AP.unroll = 4;
+      } else {
+        L.AP.pairs = false;
+        L.AP.lpr = keep_lpr;
+        L.AP.unroll = keep_unroll;
       }
     }
   }

@@ -839,6 +839,126 @@ __global__ void __launch_bounds__(256) prolong_resid2_kernel(int rows, const int
   stamp_end(stamp);
 }
 
+// The same for a ROW PAIR (2 rp, 2 rp + 1) with A*P as 2 x 2 blocks
+// (bsr22_kernel's format): one index and one 16-byte gather of the coarse
+// iterate per four entries. LPR lanes per row pair; the two P rows stay
+// scalar (lanes 0 / 1 own the two rows' epilogues).
+template <int LPR, int UA>
+__global__ void __launch_bounds__(256) prolong_resid22_kernel(int row_pairs, const int* __restrict__ pp,
+                                                              const int* __restrict__ pi, const double* __restrict__ pv,
+                                                              const int* __restrict__ ap, const int* __restrict__ ai,
+                                                              const double2* __restrict__ av, const double* ec,
+                                                              const unsigned char* __restrict__ cmask_coarse,
+                                                              const unsigned char* __restrict__ cmask, double* x,
+                                                              const double* r_pre, double* r, unsigned long long* stamp) {
+  stamp_fold(stamp);
+  constexpr int UP = (9 + LPR - 1) / LPR > 1 ? (9 + LPR - 1) / LPR : 1;
+  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int rp = (int)(gt / LPR);
+  const int lane = threadIdx.x & (LPR - 1);
+  const bool ok = rp < row_pairs;
+  pdl_trigger();
+  int p0 = 0, p1 = 0, p2 = 0, a0 = 0, a1 = 0;
+  if (ok) {
+    p0 = __ldg(pp + 2 * rp);
+    p1 = __ldg(pp + 2 * rp + 1);
+    p2 = __ldg(pp + 2 * rp + 2);
+    a0 = __ldg(ap + rp);
+    a1 = __ldg(ap + rp + 1);
+  }
+  unsigned char cm = 1;
+  if (ok && lane < 2) cm = __ldg(cmask + 2 * rp + lane);
+  int ca[UP], cb[UP], c2[UA];
+  double va[UP], vb[UP];
+  double2 v0[UA], v1[UA];
+#pragma unroll
+  for (int u = 0; u < UP; ++u) {
+    const int ka = p0 + lane + u * LPR, kb = p1 + lane + u * LPR;
+    ca[u] = ka < p1 ? __ldg(pi + ka) : -1;
+    va[u] = ka < p1 ? __ldg(pv + ka) : 0.0;
+    cb[u] = kb < p2 ? __ldg(pi + kb) : -1;
+    vb[u] = kb < p2 ? __ldg(pv + kb) : 0.0;
+  }
+  int ka2 = a0 + lane;
+  auto load2 = [&](int kb) {
+#pragma unroll
+    for (int u = 0; u < UA; ++u) {
+      const int k = kb + u * LPR;
+      const bool in = k < a1;
+      c2[u] = in ? __ldg(ai + k) : -1;
+      v0[u] = in ? __ldg(av + 2 * (size_t)k) : make_double2(0.0, 0.0);
+      v1[u] = in ? __ldg(av + 2 * (size_t)k + 1) : make_double2(0.0, 0.0);
+    }
+  };
+  load2(ka2);
+  pdl_wait();
+  stamp_start(stamp);
+  double xo = 0.0, rpre = 0.0;
+  if (ok && lane < 2) {
+    xo = x[2 * rp + lane];
+    rpre = r_pre[2 * rp + lane];
+  }
+  auto gather = [&](int cc) -> double {
+    return cc >= 0 ? ((cmask_coarse && __ldg(cmask_coarse + cc)) ? 0.0 : __ldg(ec + cc)) : 0.0;
+  };
+  auto gather2 = [&](int cc) -> double2 {
+    if (cc < 0) return make_double2(0.0, 0.0);
+    double2 e = __ldg(reinterpret_cast<const double2*>(ec) + cc);
+    if (cmask_coarse) {
+      const uchar2 m = __ldg(reinterpret_cast<const uchar2*>(cmask_coarse) + cc);
+      if (m.x) e.x = 0.0;
+      if (m.y) e.y = 0.0;
+    }
+    return e;
+  };
+  double s1a = 0.0, s1b = 0.0, s2a = 0.0, s2b = 0.0;
+  {
+    double xa[UP], xb[UP];
+#pragma unroll
+    for (int u = 0; u < UP; ++u) {
+      xa[u] = gather(ca[u]);
+      xb[u] = gather(cb[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < UP; ++u) {
+      s1a = fma(va[u], xa[u], s1a);
+      s1b = fma(vb[u], xb[u], s1b);
+    }
+  }
+  for (int k = p0 + lane + UP * LPR; k < p1; k += LPR) s1a = fma(__ldg(pv + k), gather(__ldg(pi + k)), s1a);
+  for (int k = p1 + lane + UP * LPR; k < p2; k += LPR) s1b = fma(__ldg(pv + k), gather(__ldg(pi + k)), s1b);
+  for (; ka2 < a1; ka2 += UA * LPR) {
+    double2 xv[UA], w0[UA], w1[UA];
+#pragma unroll
+    for (int u = 0; u < UA; ++u) {
+      xv[u] = gather2(c2[u]);
+      w0[u] = v0[u];
+      w1[u] = v1[u];
+    }
+    if (ka2 + UA * LPR < a1) load2(ka2 + UA * LPR);
+#pragma unroll
+    for (int u = 0; u < UA; ++u) {
+      s2a = fma(w0[u].x, xv[u].x, s2a);
+      s2a = fma(w0[u].y, xv[u].y, s2a);
+      s2b = fma(w1[u].x, xv[u].x, s2b);
+      s2b = fma(w1[u].y, xv[u].y, s2b);
+    }
+  }
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) {
+    s1a += __shfl_xor_sync(kFull, s1a, o, LPR);
+    s1b += __shfl_xor_sync(kFull, s1b, o, LPR);
+    s2a += __shfl_xor_sync(kFull, s2a, o, LPR);
+    s2b += __shfl_xor_sync(kFull, s2b, o, LPR);
+  }
+  if (ok && lane < 2) {
+    const int row = 2 * rp + lane;
+    if (!cm) x[row] = xo + (lane ? s1b : s1a);
+    r[row] = rpre - (lane ? s2b : s2a);
+  }
+  stamp_end(stamp);
+}
+
 // prolong_resid_kernel with the A*P half streamed as 16-byte pairs (int2
 // columns, double2 values; see csr_pair_kernel), UA pairs per lane per
 // batch. The P half and the first A*P batch are still fetched together.
