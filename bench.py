@@ -456,6 +456,7 @@ def run_ours(args, ws, rank, local):
             names[f"restrict@L{lvl}"] = ("transfer", lvl, 0)
             names[f"prolong_resid@L{lvl}"] = ("transfer", lvl, 1)
         names["coarse@L0"] = ("coarse", 0, 0)
+        names["arnoldi_A_outer_spmv_when_split"] = ("spmv", -1, 0)
         names["arnoldi_A_spmv_dots"] = ("arnoldi", -1, 0)
         names["arnoldi_B_update_dots_norm"] = ("arnoldi", -1, 1)
         names["arnoldi_C_update_normalize"] = ("arnoldi", -1, 2)

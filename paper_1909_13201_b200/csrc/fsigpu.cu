@@ -1809,7 +1809,14 @@ struct Gmres {
       ProfScope ps(FSIGPU_K_SPMV, T.A.bytes(false) + 8.0 * n * 3, s);
       // 128-row tiles, 8 lanes per row (1024 threads), grid-stride over
       // tiles; large systems: 32-row tiles on 256-thread CTAs
-      if (kk.fuse_small)
+      if (kk.fuse_small && T.A.blocks22 && !std::getenv("FSIGPU_ARNOLDI_FUSED")) {
+        // large systems with the operator as 2 x 2 blocks: the SpMV as its own
+        // launch (bsr22_kernel), then the dots and the Z[j] copy
+        g_prof.level = -1;
+        T.A.launch(GatherPlain{kk.zbuf}, EpiScaled{kk.scale, kk.w}, s);
+        launch_k(k_dots_copy, dim3(gs), dim3(kDotsThreads), 0, s, kk);
+        counted();
+      } else if (kk.fuse_small)
         launch_k(k_spmv_dots_s, dim3(gs), dim3(kFuseThreadsS), 0, s, kk);
       else if (gs == ceil_div(n, kFuseRows))
         launch_k(k_spmv_dots_1<8>, dim3(gs), dim3(kFuseThreads), 0, s, kk);

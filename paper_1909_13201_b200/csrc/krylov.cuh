@@ -635,6 +635,41 @@ __global__ void __launch_bounds__(kFuseThreadsS) k_spmv_dots_s(KBufs k) {
   stamp_end(k.stamp ? k.stamp + 0 : nullptr);
 }
 
+// Second half of (A) when the outer SpMV runs as its own launch (large
+// systems whose operator is held as 2 x 2 blocks: bsr22_kernel streams it at a
+// higher rate than the fused kernel's row loop): the partials of h1 = V^T w in
+// (A)'s layout, and Z[j] = z_j. Rows grid-stride, one row per thread per pass.
+constexpr int kDotsThreads = 256;
+__global__ void __launch_bounds__(kDotsThreads) k_dots_copy(KBufs k) {
+  stamp_fold(k.stamp ? k.stamp + 0 : nullptr);
+  pdl_trigger();
+  pdl_wait();
+  stamp_start(k.stamp ? k.stamp + 0 : nullptr);
+  __shared__ double sm[kPartLd * (kDotsThreads / 32)];
+  const int j = k.st->j;
+  const int nv = j + 1;
+  double acc[kRegRestart];
+#pragma unroll
+  for (int v = 0; v < kRegRestart; ++v) acc[v] = 0.0;
+  const double* __restrict__ V = k.V;
+  const double* __restrict__ W = k.w;
+  const double* __restrict__ Zb = k.zbuf;
+  double* __restrict__ zj = k.Z + (size_t)j * k.n;
+  const size_t n = (size_t)k.n;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x) {
+    double vr[kRegRestart];
+#pragma unroll
+    for (int v = 0; v < kRegRestart; ++v) vr[v] = v < nv ? __ldg(V + (size_t)v * n + r) : 0.0;
+    const double wr = W[r];
+    zj[r] = Zb[r];
+#pragma unroll
+    for (int v = 0; v < kRegRestart; ++v)
+      if (v < nv) acc[v] = fma(vr[v], wr, acc[v]);
+  }
+  cta_reduce_t32<kDotsThreads>(acc, 0.0, nv, sm, k.partial + (size_t)blockIdx.x * kPartLd);
+  stamp_end(k.stamp ? k.stamp + 0 : nullptr);
+}
+
 // (B) h1 = sum of (A)'s partials (every CTA); w -= V h1 ; partial2 <- V^T w
 //     and ||w||^2 (h2 and the norm are finished by the CTAs of (C)).
 // PF: the first row's operands are loaded before the h1 reduction (small

@@ -56,6 +56,7 @@ for lvl in range(top, -1, -1):
     names[f"restrict@L{lvl}"] = ("transfer", lvl, 0)
     names[f"prolong_resid@L{lvl}"] = ("transfer", lvl, 1)
 names["coarse@L0"] = ("coarse", 0, 0)
+names["outer SpMV (split A)"] = ("spmv", -1, 0)
 names["arnoldi A"] = ("arnoldi", -1, 0)
 names["arnoldi B"] = ("arnoldi", -1, 1)
 names["arnoldi C"] = ("arnoldi", -1, 2)
