@@ -640,6 +640,38 @@ __global__ void __launch_bounds__(kFuseThreadsS) k_spmv_dots_s(KBufs k) {
 // higher rate than the fused kernel's row loop): the partials of h1 = V^T w in
 // (A)'s layout, and Z[j] = z_j. Rows grid-stride, one row per thread per pass.
 constexpr int kDotsThreads = 256;
+// NV: compile-time bound on the vectors; RP rows per thread per pass, so a
+// thread keeps NV x RP loads in flight whatever the Krylov column (with one
+// row per thread the first columns of a cycle move a few bytes per thread
+// and the kernel ran at 3.1 TB/s on config 2).
+template <int NV, int RP>
+__device__ __forceinline__ void dots_copy_rows(const KBufs& k, int nv, int j, double (&acc)[kRegRestart]) {
+  const double* __restrict__ V = k.V;
+  const double* __restrict__ W = k.w;
+  const double* __restrict__ Zb = k.zbuf;
+  double* __restrict__ zj = k.Z + (size_t)j * k.n;
+  const size_t n = (size_t)k.n;
+  const int stride = gridDim.x * blockDim.x;
+  for (int r0 = blockIdx.x * blockDim.x + threadIdx.x; r0 < k.n; r0 += RP * stride) {
+    double vr[RP][NV], wr[RP], zr[RP];
+#pragma unroll
+    for (int q = 0; q < RP; ++q) {
+      const int r = r0 + q * stride;
+      const bool in = r < k.n;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) vr[q][v] = (in && v < nv) ? __ldg(V + (size_t)v * n + r) : 0.0;
+      wr[q] = in ? W[r] : 0.0;
+      zr[q] = in ? Zb[r] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < RP; ++q) {
+      const int r = r0 + q * stride;
+      if (r < k.n) zj[r] = zr[q];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) acc[v] = fma(vr[q][v], wr[q], acc[v]);
+    }
+  }
+}
 __global__ void __launch_bounds__(kDotsThreads) k_dots_copy(KBufs k) {
   stamp_fold(k.stamp ? k.stamp + 0 : nullptr);
   pdl_trigger();
@@ -651,21 +683,10 @@ __global__ void __launch_bounds__(kDotsThreads) k_dots_copy(KBufs k) {
   double acc[kRegRestart];
 #pragma unroll
   for (int v = 0; v < kRegRestart; ++v) acc[v] = 0.0;
-  const double* __restrict__ V = k.V;
-  const double* __restrict__ W = k.w;
-  const double* __restrict__ Zb = k.zbuf;
-  double* __restrict__ zj = k.Z + (size_t)j * k.n;
-  const size_t n = (size_t)k.n;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k.n; r += gridDim.x * blockDim.x) {
-    double vr[kRegRestart];
-#pragma unroll
-    for (int v = 0; v < kRegRestart; ++v) vr[v] = v < nv ? __ldg(V + (size_t)v * n + r) : 0.0;
-    const double wr = W[r];
-    zj[r] = Zb[r];
-#pragma unroll
-    for (int v = 0; v < kRegRestart; ++v)
-      if (v < nv) acc[v] = fma(vr[v], wr, acc[v]);
-  }
+  if (nv <= 4) dots_copy_rows<4, 8>(k, nv, j, acc);
+  else if (nv <= 8) dots_copy_rows<8, 4>(k, nv, j, acc);
+  else if (nv <= 16) dots_copy_rows<16, 2>(k, nv, j, acc);
+  else dots_copy_rows<kRegRestart, 1>(k, nv, j, acc);
   cta_reduce_t32<kDotsThreads>(acc, 0.0, nv, sm, k.partial + (size_t)blockIdx.x * kPartLd);
   stamp_end(k.stamp ? k.stamp + 0 : nullptr);
 }
