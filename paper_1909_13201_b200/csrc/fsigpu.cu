@@ -1809,7 +1809,7 @@ struct Gmres {
       ProfScope ps(FSIGPU_K_SPMV, T.A.bytes(false) + 8.0 * n * 3, s);
       // 128-row tiles, 8 lanes per row (1024 threads), grid-stride over
       // tiles; large systems: 32-row tiles on 256-thread CTAs
-      if (kk.fuse_small && T.A.blocks22 && !std::getenv("FSIGPU_ARNOLDI_FUSED")) {
+      if (kk.fuse_small && T.A.blocks22) {
         // large systems with the operator as 2 x 2 blocks: the SpMV as its own
         // launch (bsr22_kernel), then the dots and the Z[j] copy
         g_prof.level = -1;
@@ -1827,7 +1827,7 @@ struct Gmres {
       // (B) on parts_b CTAs; (C) on parts_b row CTAs + 1 Givens CTA
       ProfScope ps(FSIGPU_K_ARNOLDI, 8.0 * n * 4, s);
       if (kk.fuse_small) {  // large systems: rows streamed through cp.async stages, (C) on its own grid
-        launch_k(k_update_dots_norm_cp, dim3(kk.parts_b), dim3(kArnThreads), kStageSmem, s, kk);
+        launch_k(k_update_dots_norm_mr, dim3(kk.parts_b), dim3(kArnThreads), 0, s, kk);
         launch_k(k_update_normalize<false>, dim3(kk.parts_c + 1), dim3(kArnThreads), 0, s, kk);
       } else {
         launch_k(k_update_dots_norm<true>, dim3(kk.parts_b), dim3(kArnThreads), 0, s, kk);
@@ -2672,13 +2672,10 @@ int fsigpu_gmres_create(fsigpu_gmg g, const double* frame_scale, int restart, fs
       FSI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
       const bool big = ceil_div(n, kFuseRows) > 8 * sms || force_big();
       if (big) {
-        FSI_CUDA(cudaFuncSetAttribute(k_update_dots_norm_cp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)kStageSmem));
-        FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_dots_norm_cp, kArnThreads, kStageSmem));
+        FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_dots_norm_mr, kArnThreads, 0));
         kb.parts_b = std::max(1, std::min(ceil_div(n, kArnThreads), sms * std::min(std::max(occ, 1), 16)));
-        // (C) stays on registers: at 80 registers it runs 6 CTAs per SM
-        // (50.6 us on the config-2 fine level) against 3 for a 70 KB staged
-        // variant (61.5 us)
+        // (C): its own grid at its resident CTA count (168 registers with the
+        // multi-row loop of normalize_rows)
         int occ_c = 0;
         FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, k_update_normalize<false>, kArnThreads, 0));
         kb.parts_c = std::max(1, std::min(ceil_div(n, kArnThreads), sms * std::max(occ_c, 1) - 1));

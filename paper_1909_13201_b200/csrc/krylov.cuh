@@ -775,69 +775,103 @@ __global__ void __launch_bounds__(kArnThreads) k_update_dots_norm(KBufs k) {
   stamp_end(k.stamp ? k.stamp + 4 : nullptr);
 }
 
-// Large-n variants of (B) and (C): each thread streams its rows' operands
-// (the nv basis entries, w, and for (C) the frame scale) into its own
-// shared-memory slots with 8-byte cp.async, one row ahead (two stages), so
-// the next row's loads are in flight while the current row's dependent FMA
-// chain runs, without holding them in registers. A thread reads back only
-// what it copied itself, so cp.async.wait_group alone orders the stages.
-// Slots: stage s, value q, thread t at stg[(s * kStageVals + q) * kArnThreads + t].
-constexpr int kStageVals = kRegRestart + 2;
-constexpr size_t kStageSmem = 2 * kStageVals * kArnThreads * sizeof(double);
-
-__device__ __forceinline__ void stage_row(const KBufs& k, double* stg, int st, int r, int nv, bool with_scale) {
-  const int t = threadIdx.x;
-  if (r < k.n) {
-    double* base = stg + (size_t)st * kStageVals * kArnThreads + t;
-    for (int v = 0; v < nv; ++v) cp_async8(base + (size_t)v * kArnThreads, k.V + (size_t)v * k.n + r);
-    cp_async8(base + (size_t)kRegRestart * kArnThreads, k.w + r);
-    if (with_scale) cp_async8(base + (size_t)kPartLd * kArnThreads, k.scale + r);
+// Large-n (B) with NV x RP loads in flight per thread (see dots_copy_rows):
+// RP rows per thread per pass, each row's operands in registers. It replaced a
+// cp.async-staged variant with one row in flight ahead (config 2 in-graph: 62 ->
+// 41 us = 4.3 TB/s; (C) with the same row loop 62 -> 44 us).
+template <int NV, int RP>
+__device__ __forceinline__ void update_dots_rows(const KBufs& k, int nv, const double* hs,
+                                                 double (&acc)[kRegRestart], double& n2) {
+  const double* __restrict__ V = k.V;
+  double* __restrict__ W = k.w;
+  const size_t n = (size_t)k.n;
+  const int stride = gridDim.x * blockDim.x;
+  for (int r0 = blockIdx.x * blockDim.x + threadIdx.x; r0 < k.n; r0 += RP * stride) {
+    double vr[RP][NV], wr[RP];
+#pragma unroll
+    for (int q = 0; q < RP; ++q) {
+      const int r = r0 + q * stride;
+      const bool in = r < k.n;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) vr[q][v] = (in && v < nv) ? __ldg(V + (size_t)v * n + r) : 0.0;
+      wr[q] = in ? W[r] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < RP; ++q) {
+      const int r = r0 + q * stride;
+      double w1 = wr[q];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) w1 = fma(-hs[v], vr[q][v], w1);  // hs[v] = 0 beyond nv
+      if (r < k.n) W[r] = w1;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) acc[v] = fma(vr[q][v], w1, acc[v]);
+      n2 = fma(w1, w1, n2);
+    }
   }
-  cp_async_commit();
 }
-
-__global__ void __launch_bounds__(kArnThreads) k_update_dots_norm_cp(KBufs k) {
+__global__ void __launch_bounds__(kArnThreads) k_update_dots_norm_mr(KBufs k) {
   stamp_fold(k.stamp ? k.stamp + 4 : nullptr);
   pdl_trigger();
   pdl_wait();
   stamp_start(k.stamp ? k.stamp + 4 : nullptr);
-  extern __shared__ __align__(16) double stg[];
   __shared__ double sm[kPartLd * (kArnThreads / 32)];
   __shared__ double hs[kRegRestart + 1];
   __shared__ double red[kPartLd * kSumSlices];
   const int j = k.st->j;
   const int nv = j + 1;
-  const int t = threadIdx.x;
-  const int stride = gridDim.x * blockDim.x;
-  int r = blockIdx.x * blockDim.x + t;
-  stage_row(k, stg, 0, r, nv, false);  // overlaps the h1 reduction
+  if (threadIdx.x <= kRegRestart) hs[threadIdx.x] = 0.0;
+  __syncthreads();
   sum_partials<kArnThreads>(k.partial, k.parts_a, nv, hs, red);
   if (blockIdx.x == 0) {
-    if (t < nv) k.st->h1[t] = hs[t];
-    if (t == 0) k.st->jc = j + 1;
+    if (threadIdx.x < nv) k.st->h1[threadIdx.x] = hs[threadIdx.x];
+    if (threadIdx.x == 0) k.st->jc = j + 1;
   }
   double acc[kRegRestart];
 #pragma unroll
   for (int v = 0; v < kRegRestart; ++v) acc[v] = 0.0;
   double n2 = 0.0;
-  double* __restrict__ W = k.w;
-  for (int it = 0; r < k.n; ++it, r += stride) {
-    stage_row(k, stg, (it + 1) & 1, r + stride, nv, false);
-    cp_async_wait<1>();
-    const double* row = stg + (size_t)(it & 1) * kStageVals * kArnThreads + t;
-    double wr = row[(size_t)kRegRestart * kArnThreads];
-#pragma unroll
-    for (int v = 0; v < kRegRestart; ++v)
-      if (v < nv) wr = fma(-hs[v], row[(size_t)v * kArnThreads], wr);
-    W[r] = wr;
-#pragma unroll
-    for (int v = 0; v < kRegRestart; ++v)
-      if (v < nv) acc[v] = fma(row[(size_t)v * kArnThreads], wr, acc[v]);
-    n2 = fma(wr, wr, n2);
-  }
-  cp_async_wait<0>();
+  if (nv <= 4) update_dots_rows<4, 8>(k, nv, hs, acc, n2);
+  else if (nv <= 8) update_dots_rows<8, 4>(k, nv, hs, acc, n2);
+  else if (nv <= 16) update_dots_rows<16, 2>(k, nv, hs, acc, n2);
+  else update_dots_rows<kRegRestart, 1>(k, nv, hs, acc, n2);
   cta_reduce_t32<kArnThreads>(acc, n2, nv, sm, k.partial2 + (size_t)blockIdx.x * kPartLd);
   stamp_end(k.stamp ? k.stamp + 4 : nullptr);
+}
+
+// Row loop of the large-n (C) with NV x RP loads in flight per thread.
+template <int NV, int RP>
+__device__ __forceinline__ void normalize_rows(const KBufs& k, int nv, int nb, const double* hs, double hn,
+                                               bool lucky, double* __restrict__ VJ) {
+  const double* __restrict__ V = k.V;
+  const double* __restrict__ W = k.w;
+  const double* __restrict__ S = k.scale;
+  double* __restrict__ UB = k.ubuf;
+  const size_t n = (size_t)k.n;
+  const int stride = nb * blockDim.x;
+  for (int r0 = blockIdx.x * blockDim.x + threadIdx.x; r0 < k.n; r0 += RP * stride) {
+    double vr[RP][NV], wr[RP], sc[RP];
+#pragma unroll
+    for (int q = 0; q < RP; ++q) {
+      const int r = r0 + q * stride;
+      const bool in = r < k.n;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) vr[q][v] = (in && v < nv) ? __ldg(V + (size_t)v * n + r) : 0.0;
+      wr[q] = in ? W[r] : 0.0;
+      sc[q] = in ? S[r] : 1.0;
+    }
+#pragma unroll
+    for (int q = 0; q < RP; ++q) {
+      const int r = r0 + q * stride;
+      double w1 = wr[q];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) w1 = fma(-hs[v], vr[q][v], w1);
+      if (r < k.n && !lucky) {
+        const double vv = w1 / hn;
+        VJ[r] = vv;
+        UB[r] = vv / sc[q];
+      }
+    }
+  }
 }
 
 // (C) every CTA sums (B)'s partials into h2 and ||w||^2 and forms
@@ -931,28 +965,16 @@ __global__ void __launch_bounds__(kArnThreads) k_update_normalize(KBufs k) {
       }
     }
   } else {
-    // restrict-qualified views (see k_update_dots_norm): the stores of v_{j+1}
-    // and u do not alias V, w or scale, so row loads run ahead of them
-    const double* __restrict__ V = k.V;
-    const double* __restrict__ W = k.w;
-    const double* __restrict__ S = k.scale;
-    double* __restrict__ VJ = vj;
-    double* __restrict__ UB = k.ubuf;
-    const size_t n = (size_t)k.n;
-    for (int r = PF ? r0 + nb * blockDim.x : (rows_cta ? r0 : k.n); r < k.n; r += nb * blockDim.x) {
-      double vr[kRegRestart];
-#pragma unroll
-      for (int v = 0; v < kRegRestart; ++v) vr[v] = v < nv ? __ldg(V + (size_t)v * n + r) : 0.0;
-      double wr = W[r];
-      const double sc = S[r];
-#pragma unroll
-      for (int v = 0; v < kRegRestart; ++v)
-        if (v < nv) wr = fma(-hs[v], vr[v], wr);
-      if (!lucky) {
-        const double vv = wr / hn;
-        VJ[r] = vv;
-        UB[r] = vv / sc;
-      }
+    // large systems: NV x RP loads in flight per thread (normalize_rows);
+    // hs[] beyond nv must read as 0 for the fixed-length FMA chains
+    if (rows_cta) {
+      __syncthreads();
+      if (threadIdx.x + nv <= kRegRestart) hs[nv + threadIdx.x] = 0.0;
+      __syncthreads();
+      if (nv <= 4) normalize_rows<4, 8>(k, nv, nb, hs, hn, lucky, vj);
+      else if (nv <= 8) normalize_rows<8, 4>(k, nv, nb, hs, hn, lucky, vj);
+      else if (nv <= 16) normalize_rows<16, 2>(k, nv, nb, hs, hn, lucky, vj);
+      else normalize_rows<kRegRestart, 1>(k, nv, nb, hs, hn, lucky, vj);
     }
   }
   stamp_end(k.stamp ? k.stamp + 8 : nullptr);
