@@ -272,6 +272,8 @@ struct Csr {
     // matter and the wider loads cost occupancy (config 0 in-graph: fine FS
     // 6.5 -> 6.9 us, fine residual 3.5 -> 4.5 us with pairs; config 2: 1.25M rows
     // FS 692 -> 669 us, residual 220 -> 195 us, 20k rows FS 13.9 -> 14.9 us)
+    const char* fb = std::getenv("FSIGPU_FORCE_BIG");  // the parity tests take the large-level formats on small fixtures
+    if (fb && fb[0] == '1') any_size = true;
     if ((rows < 65536 && !any_size) || !rows || (cols & 1) || pairs_disabled()) return;
     ptr2.alloc((size_t)rows + 1);
     ptr2.zero(s);
@@ -449,8 +451,9 @@ enum BlockMode { kModeLU = 0, kModeInverse = 1, kModeAssembled = 2 };
 static std::atomic<int> g_default_mode{kModeAssembled};
 
 // FSIGPU_FORCE_BIG=1: take the large-system kernel variants at any size
-// (k_spmv_dots_s, the cp.async Arnoldi stages, paired SpMV / A*P loads), so
-// the parity tests cover them on the small committed fixtures.
+// (k_spmv_dots_s or the split (A), the multi-row Arnoldi updates, paired
+// loads, the column-pair / 2 x 2 block formats), so the parity tests cover
+// them on the small committed fixtures.
 static bool force_big() {
   const char* e = std::getenv("FSIGPU_FORCE_BIG");
   return e && e[0] == '1';
@@ -1243,7 +1246,7 @@ static void assemble_fs(Level& L, const fsigpu_level_desc& d, const std::vector<
     const int keep_lpr = L.FS.lpr, keep_unroll = L.FS.unroll;
     L.FS.build_pairs(s, L.n >= 16384);
     L.FS.build_blocks22(s);
-    if (!L.FS.blocks22 && L.n < 65536) {  // plain CSR with its own launch shape
+    if (!L.FS.blocks22 && L.n < 65536 && !force_big()) {  // plain CSR with its own launch shape
       L.FS.pairs = false;
       L.FS.lpr = keep_lpr;
       L.FS.unroll = keep_unroll;
@@ -1542,7 +1545,7 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
       if (L.AP.blocks22) {
         L.AP.lpr = keep_lpr;
         L.AP.unroll = 4;
-      } else if (L.AP.pairs && d.n >= 65536) {
+      } else if (L.AP.pairs && (d.n >= 65536 || force_big())) {
         L.AP.lpr = keep_lpr;
         L.AP.unroll = 4;
       } else {

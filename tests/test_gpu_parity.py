@@ -484,13 +484,23 @@ def test_paired_load_kernels(cfg0, unroll):
     assert res.converged and abs(res.iterations - int(g["gmres_add/iterations"][0])) <= 1
 
 
-def test_large_system_kernel_variants(cfg0, monkeypatch):
-    """FSIGPU_FORCE_BIG=1 takes the kernels config 2 runs on (k_spmv_dots_s,
-    the cp.async Arnoldi stages, paired SpMV and A*P loads) on config 0:
-    V-cycle against the reference's golden output, GMRES iterations within
-    +-1 and the final relative residual within 1e-8 of the reference's."""
+@pytest.mark.parametrize("fmt", ["blocks22", "pairs", "csr"])
+def test_large_system_kernel_variants(cfg0, monkeypatch, fmt):
+    """FSIGPU_FORCE_BIG=1 takes the kernels config 2 runs on, on config 0:
+    the FS operator, A and A*P as 2 x 2 blocks (bsr22_kernel,
+    prolong_resid22_kernel, Arnoldi (A) split into SpMV + k_dots_copy), as
+    column pairs (csr2_kernel, prolong_resid2_kernel) or as CSR with paired
+    loads (k_spmv_dots_s), and the multi-row Arnoldi updates. V-cycle against
+    the reference's golden output, GMRES iterations within +-1 and the final
+    relative residual within 1e-8 of the reference's."""
     monkeypatch.setenv("FSIGPU_FORCE_BIG", "1")
+    if fmt == "pairs":
+        monkeypatch.setenv("FSIGPU_BLOCKS22", "0")
+    elif fmt == "csr":
+        monkeypatch.setenv("FSIGPU_COLUMN_PAIRS", "0")
     G = fsigpu.GmgPreconditioner(cfg0.levels)
+    top = len(cfg0.levels) - 1
+    assert rel(G.fs_apply(top, cfg0.golden["golden/fs_r"]), cfg0.golden["golden/fs_z_add"]) <= 1e-12
     g = cfg0.golden
     assert rel(G.apply(g["golden/vcycle_r"]), g["golden/vcycle_z_add"]) <= 1e-9
     cfg = fsigpu.KrylovConfig(restart=30, max_iters=2000, rel_tol=1e-10, abs_tol=1e-300)
