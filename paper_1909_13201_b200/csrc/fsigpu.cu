@@ -357,7 +357,10 @@ struct Csr {
     if (!rows) return;
     const long long threads = (long long)rows * lpr;
     const int grid = ceil_div(threads, 256);
-    if (blocks22 && lpr >= 2) {
+    // the pair / block kernels gather x as double2: a caller-supplied vector
+    // that is only 8-byte aligned takes the CSR kernels
+    const bool x16 = (reinterpret_cast<uintptr_t>(g.x) & 15) == 0;
+    if (blocks22 && lpr >= 2 && x16) {
       const int grid2 = ceil_div((long long)(rows / 2) * lpr, 256);
 #define FSI_BSR(LP, UU) launch_k(bsr22_kernel<LP, G, E, UU>, dim3(grid2), dim3(256), 0, s, rows / 2, (const int*)ptrb.p, (const int*)idxb.p, (const double2*)valb.p, g, e, cur_stamp(0))
       switch (lpr) {
@@ -372,7 +375,7 @@ struct Csr {
       counted();
       return;
     }
-    if (pairs && lpr >= 2) {
+    if (pairs && lpr >= 2 && x16) {
       // column-pair format: batches of 2 (unroll 4 / 22) or 4 (unroll 8 / 24) elements per lane
 #define FSI_CSR2(LP, UU) launch_k(csr2_kernel<LP, G, E, UU>, dim3(grid), dim3(256), 0, s, rows, (const int*)ptr2.p, (const int*)idx2.p, (const double2*)val2.p, g, e, cur_stamp(0))
       if (unroll == 8 || unroll == 24) {

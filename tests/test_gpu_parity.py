@@ -919,3 +919,26 @@ def test_device_clock_stamps(cfg0):
         fsigpu.Stamps.enable(False)
     again = S.solve(P.b, cfg)
     assert again.iterations == base.iterations and np.array_equal(again.x, base.x)
+
+
+def test_apply_dev_with_8_byte_aligned_vectors(cfg0):
+    """The 2 x 2 block / column-pair kernels gather the input vector as
+    double2; device pointers that are only 8-byte aligned (a view at an odd
+    element offset) must still work (they take the CSR kernels) and give the
+    same V-cycle to rounding."""
+    import torch
+    P = cfg0
+    G = fsigpu.GmgPreconditioner(P.levels)
+    n = P.b.shape[0]
+    r = torch.from_numpy(P.golden["golden/vcycle_r"]).cuda()
+    z = torch.zeros(n, dtype=torch.float64, device="cuda")
+    G.apply_dev(r.data_ptr(), z.data_ptr())
+    torch.cuda.synchronize()
+    buf_r = torch.zeros(n + 1, dtype=torch.float64, device="cuda")
+    buf_z = torch.zeros(n + 1, dtype=torch.float64, device="cuda")
+    buf_r[1:] = r
+    assert buf_r[1:].data_ptr() % 16 == 8
+    G.apply_dev(buf_r[1:].data_ptr(), buf_z[1:].data_ptr())
+    torch.cuda.synchronize()
+    assert rel(buf_z[1:].cpu().numpy(), z.cpu().numpy()) <= 1e-13
+    assert rel(z.cpu().numpy(), P.golden["golden/vcycle_z_add"]) <= 1e-9
