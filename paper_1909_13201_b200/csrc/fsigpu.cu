@@ -341,6 +341,8 @@ struct Csr {
       while (l < 32 && want > l * 1.41421356) l *= 2;
       lpr = l;
       unroll = 4;
+    } else if (lpr < 4) {
+      lpr = 4;  // A on config 2: 1.25M rows 151 -> 145 us, 313k rows 44 -> 38 us (4 lanes per row pair)
     }
   }
   static bool pairs_disabled() {
@@ -363,12 +365,22 @@ struct Csr {
     if (blocks22 && lpr >= 2 && x16) {
       const int grid2 = ceil_div((long long)(rows / 2) * lpr, 256);
 #define FSI_BSR(LP, UU) launch_k(bsr22_kernel<LP, G, E, UU>, dim3(grid2), dim3(256), 0, s, rows / 2, (const int*)ptrb.p, (const int*)idxb.p, (const double2*)valb.p, g, e, cur_stamp(0))
-      switch (lpr) {
-        case 2: FSI_BSR(2, 2); break;
-        case 4: FSI_BSR(4, 2); break;
-        case 8: FSI_BSR(8, 2); break;
-        case 16: FSI_BSR(16, 2); break;
-        default: FSI_BSR(32, 2); break;
+      if (unroll == 8 || unroll == 24) {  // batches of 4 blocks per lane
+        switch (lpr) {
+          case 2: FSI_BSR(2, 4); break;
+          case 4: FSI_BSR(4, 4); break;
+          case 8: FSI_BSR(8, 4); break;
+          case 16: FSI_BSR(16, 4); break;
+          default: FSI_BSR(32, 4); break;
+        }
+      } else {
+        switch (lpr) {
+          case 2: FSI_BSR(2, 2); break;
+          case 4: FSI_BSR(4, 2); break;
+          case 8: FSI_BSR(8, 2); break;
+          case 16: FSI_BSR(16, 2); break;
+          default: FSI_BSR(32, 2); break;
+        }
       }
 #undef FSI_BSR
       FSI_CHECK_LAUNCH();
@@ -1546,7 +1558,7 @@ static void build_level(Gmg& g, int l, const fsigpu_level_desc& d, cudaStream_t 
       L.AP.build_pairs(s);
       L.AP.build_blocks22(s);
       if (L.AP.blocks22) {
-        L.AP.lpr = keep_lpr;
+        L.AP.lpr = std::max(keep_lpr, 4);  // 1.25M rows: 159 -> 148 us at 4 lanes per row pair
         L.AP.unroll = 4;
       } else if (L.AP.pairs && (d.n >= 65536 || force_big())) {
         L.AP.lpr = keep_lpr;
