@@ -466,7 +466,7 @@ enum BlockMode { kModeLU = 0, kModeInverse = 1, kModeAssembled = 2 };
 static std::atomic<int> g_default_mode{kModeAssembled};
 
 // FSIGPU_FORCE_BIG=1: take the large-system kernel variants at any size
-// (k_spmv_dots_s or the split (A), the multi-row Arnoldi updates, paired
+// (the split (A), the multi-row Arnoldi updates, paired
 // loads, the column-pair / 2 x 2 block formats), so the parity tests cover
 // them on the small committed fixtures.
 static bool force_big() {
@@ -1825,18 +1825,15 @@ struct Gmres {
     const int gs = kk.parts_a;
     {
       ProfScope ps(FSIGPU_K_SPMV, T.A.bytes(false) + 8.0 * n * 3, s);
-      // 128-row tiles, 8 lanes per row (1024 threads), grid-stride over
-      // tiles; large systems: 32-row tiles on 256-thread CTAs
-      if (kk.fuse_small && T.A.blocks22) {
-        // large systems with the operator as 2 x 2 blocks: the SpMV as its own
-        // launch (bsr22_kernel), then the dots and the Z[j] copy
+      // small systems: 128-row tiles, 8 lanes per row (1024 threads), grid-stride over tiles
+      if (kk.fuse_small) {
+        // large systems: the SpMV as its own launch (bsr22_kernel when A is held
+        // as 2 x 2 blocks, else the CSR kernels), then the dots and the Z[j] copy
         g_prof.level = -1;
         T.A.launch(GatherPlain{kk.zbuf}, EpiScaled{kk.scale, kk.w}, s);
         launch_k(k_dots_copy, dim3(gs), dim3(kDotsThreads), 0, s, kk);
         counted();
-      } else if (kk.fuse_small)
-        launch_k(k_spmv_dots_s, dim3(gs), dim3(kFuseThreadsS), 0, s, kk);
-      else if (gs == ceil_div(n, kFuseRows))
+      } else if (gs == ceil_div(n, kFuseRows))
         launch_k(k_spmv_dots_1<8>, dim3(gs), dim3(kFuseThreads), 0, s, kk);
       else
         launch_k(k_spmv_dots<8>, dim3(gs), dim3(kFuseThreads), 0, s, kk);
@@ -1844,7 +1841,7 @@ struct Gmres {
     {
       // (B) on parts_b CTAs; (C) on parts_b row CTAs + 1 Givens CTA
       ProfScope ps(FSIGPU_K_ARNOLDI, 8.0 * n * 4, s);
-      if (kk.fuse_small) {  // large systems: rows streamed through cp.async stages, (C) on its own grid
+      if (kk.fuse_small) {  // large systems: multi-row register loops, (C) on its own grid
         launch_k(k_update_dots_norm_mr, dim3(kk.parts_b), dim3(kArnThreads), 0, s, kk);
         launch_k(k_update_normalize<false>, dim3(kk.parts_c + 1), dim3(kArnThreads), 0, s, kk);
       } else {
@@ -2673,12 +2670,11 @@ int fsigpu_gmres_create(fsigpu_gmg g, const double* frame_scale, int restart, fs
       FSI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
       FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_dots<8>, kFuseThreads, 0));
       // small systems keep one 128-row tile per CTA (config 0: 157 tiles);
-      // large ones run k_spmv_dots_s on up to 4 resident CTAs per SM
+      // large ones run (A) as SpMV + k_dots_copy
       const int tiles = ceil_div(n, kFuseRows);
       kb.fuse_small = tiles > 8 * sms || force_big();
       if (kb.fuse_small) {
-        FSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_dots_s, kFuseThreadsS, 0));
-        kb.parts_a = sms * std::min(std::max(occ, 1), 4);
+        kb.parts_a = sms * 4;  // grid of k_dots_copy (rows grid-stride): the partial rows (B) sums
       } else {
         kb.parts_a = tiles <= 8 * sms ? tiles : sms * std::max(occ, 1);
       }

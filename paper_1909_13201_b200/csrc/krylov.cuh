@@ -67,7 +67,7 @@ struct KBufs {
   double* partial;      // grid x (kRegRestart+1)
   double* partial2;     // second partial buffer of the fused Arnoldi step
   int parts_a;          // CTAs of k_spmv_dots (rows of partial it writes)
-  int fuse_small;       // (A) runs as k_spmv_dots_s (large n)
+  int fuse_small;       // large n: (A) runs as SpMV + k_dots_copy
   int parts_b;          // CTAs of k_update_dots_norm (rows of partial2)
   int parts_c;          // row CTAs of k_update_normalize (+1 Givens CTA)
   double* partialw;     // restart > 32 (krylov_wide.cuh): chunks x parts_w x kPartLd
@@ -570,75 +570,13 @@ __device__ __forceinline__ void sum_partials(const double* __restrict__ part, in
   __syncthreads();
 }
 
-// Large-n variant of (A): 256-thread CTAs on 32-row tiles (8 lanes per
-// row, one pass), several CTAs per SM, grid-stride over tiles with the grid
-// at the resident CTA count. With one 1024-thread CTA per SM (k_spmv_dots)
-// every SM worked on a single tile at a time, so each tile's dependent
-// pointer -> index -> gather rounds were exposed (config-2 fine level: 272
-// us for 1.23 GB). Warp w owns the dots of vectors w, w+8, w+16, w+24.
-constexpr int kFuseThreadsS = 256;
-constexpr int kFuseRowsS = 32;
-__global__ void __launch_bounds__(kFuseThreadsS) k_spmv_dots_s(KBufs k) {
-  stamp_fold(k.stamp ? k.stamp + 0 : nullptr);
-  pdl_trigger();
-  pdl_wait();
-  stamp_start(k.stamp ? k.stamp + 0 : nullptr);
-  __shared__ double ws[kFuseRowsS];
-  const int j = k.st->j;
-  const int nv = j + 1;
-  const int t = threadIdx.x;
-  const int warp = t >> 5, lane = t & 31;
-  constexpr int LPR = 8;
-  constexpr int NQ = kRegRestart / (kFuseThreadsS / 32);  // vectors per warp
-  const int ntiles = (k.n + kFuseRowsS - 1) / kFuseRowsS;
-  double s[NQ];
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) s[q] = 0.0;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int r0 = tile * kFuseRowsS;
-    const int rowv = r0 + lane;
-    double vv[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      const int v = warp + 8 * q;
-      vv[q] = (v < nv && rowv < k.n) ? k.V[(size_t)v * k.n + rowv] : 0.0;
-    }
-    const bool zc = t < kFuseRowsS && r0 + t < k.n;
-    const double zj = zc ? k.zbuf[r0 + t] : 0.0;
-    const int rl = t / LPR;
-    const int row = r0 + rl;
-    const bool ok = row < k.n;
-    const bool head = ok && (t & (LPR - 1)) == 0;
-    const double sc = head ? k.scale[row] : 0.0;
-    const double sr = fused_row<LPR>(k, ok ? row : -1, t & (LPR - 1));
-    if (head) {
-      const double w = sc * sr;
-      k.w[row] = w;
-      ws[rl] = w;
-    }
-    if (zc) k.Z[(size_t)j * k.n + r0 + t] = zj;
-    if (t < kFuseRowsS && r0 + t >= k.n) ws[t] = 0.0;
-    __syncthreads();
-    const double wl = ws[lane];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) s[q] = fma(vv[q], wl, s[q]);
-    __syncthreads();  // ws is rewritten by the next tile
-  }
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    double x = s[q];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
-    const int v = warp + 8 * q;
-    if (lane == 0 && v < nv) k.partial[(size_t)blockIdx.x * kPartLd + v] = x;
-  }
-  stamp_end(k.stamp ? k.stamp + 0 : nullptr);
-}
-
-// Second half of (A) when the outer SpMV runs as its own launch (large
-// systems whose operator is held as 2 x 2 blocks: bsr22_kernel streams it at a
-// higher rate than the fused kernel's row loop): the partials of h1 = V^T w in
-// (A)'s layout, and Z[j] = z_j. Rows grid-stride, one row per thread per pass.
+// Large systems run (A) as two launches: the outer SpMV through the level
+// operator's own kernel (bsr22_kernel when A is held as 2 x 2 blocks, else the
+// CSR kernels) with the w = diag(s) A z epilogue, then this kernel: the
+// partials of h1 = V^T w in (A)'s layout, and Z[j] = z_j. The fused large-n
+// kernel it replaced (256-thread CTAs on 32-row tiles with the row loop inside)
+// ran at 246 us on config 2 against 145 + 43 us, and at 115 us on the 3D
+// system against 88 + 12 us. Rows grid-stride.
 constexpr int kDotsThreads = 256;
 // NV: compile-time bound on the vectors; RP rows per thread per pass, so a
 // thread keeps NV x RP loads in flight whatever the Krylov column (with one

@@ -490,7 +490,7 @@ def test_large_system_kernel_variants(cfg0, monkeypatch, fmt):
     the FS operator, A and A*P as 2 x 2 blocks (bsr22_kernel,
     prolong_resid22_kernel, Arnoldi (A) split into SpMV + k_dots_copy), as
     column pairs (csr2_kernel, prolong_resid2_kernel) or as CSR with paired
-    loads (k_spmv_dots_s), and the multi-row Arnoldi updates. V-cycle against
+    loads, and the multi-row Arnoldi updates. V-cycle against
     the reference's golden output, GMRES iterations within +-1 and the final
     relative residual within 1e-8 of the reference's."""
     monkeypatch.setenv("FSIGPU_FORCE_BIG", "1")
