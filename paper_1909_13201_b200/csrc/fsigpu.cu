@@ -332,6 +332,12 @@ struct Csr {
     FSI_CHECK_LAUNCH();
     FSI_CUDA(cudaStreamSynchronize(s));
     blocks22 = true;
+    // the column pairs were only the intermediate: free them (3.4 GB for the
+    // fine FS operator of config 2)
+    pairs = false;
+    ptr2.release();
+    idx2.release();
+    val2.release();
     // launch shape of bsr22_kernel (in-graph sweeps): the HBM-bound levels keep
     // the pair format's lane count; L2-resident levels take ~3 blocks per lane
     // (config 0 fine FS: 32 lanes 5.4 us, 8 lanes 22 us)
